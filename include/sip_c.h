@@ -1,0 +1,170 @@
+/*
+ * sip_c.h -- C-ABI of the B200-native SIP (Stone's strongly implicit
+ * procedure) hot path.  Plain pointers and sizes only; no CUDA / torch types.
+ *
+ * The reference (arXiv 1303.4538 artifact "bsfv", /root/reference) defines
+ * SIP only as a specification; the entry points below replace the SPEC's sip
+ * module operations one for one:
+ *
+ *   reference                         this ABI
+ *   ------------------------------------------  -------------------------------
+ *   StencilSystem          SPEC.md:116-119       sip_set_system / sip_set_source
+ *   SipFactors + stamp     SPEC.md:120-123       factor state inside sip_ctx
+ *   SipConfig              SPEC.md:124-127       alpha / max_iters / target / precision args
+ *   SolveReport            SPEC.md:128-131       norms_out / iters_used / sip_report
+ *   sip_factor             SPEC.md:143-151       sip_factor
+ *   residual_general       SPEC.md:152-160       sip_residual
+ *   residual_symmetric     SPEC.md:161-169       sip_residual (symmetric = 1)
+ *   sip_sweep              SPEC.md:170-178       sip_iterate (iters = 1)
+ *   solve                  SPEC.md:179-187       sip_solve
+ *   decompose / with_ranks proj/src/grid.cpp:50-102   sip_create_lattice
+ *   Endpoint::all_reduce   proj/include/bsfv/net.hpp:131  (inside; NCCL)
+ *   exchange_nonblocking   SPEC.md:263-271       (inside; device copies + NCCL)
+ *   Field3<double>         proj/include/bsfv/field.hpp:21-44  host array layout
+ *
+ * Host arrays use the reference's Field3 layout: (nx+2)*(ny+2)*(nz+2) doubles,
+ * index i + (nx+2)*(j + (ny+2)*k), interior 1..n, one ghost layer.  The sign
+ * convention is the matrix-entry one (FASTEST / Ferziger-Peric):
+ *   AP*phi_P + AW*phi_W + AE*phi_E + AS*phi_S + AN*phi_N + AB*phi_B + AT*phi_T = Q
+ * i.e. SPEC's a_nb = -A_nb.
+ *
+ * Every function returns a SIP_* status and never throws.  The C++ shim
+ * include/bsfv_sip.hpp maps statuses onto the reference's exception classes
+ * (proj/include/bsfv/error.hpp:10-50).  Threading: one context per host
+ * thread / rank; calls only from the owning thread.
+ */
+#ifndef SIP_C_H_
+#define SIP_C_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -> bsfv exception classes (error.hpp). */
+#define SIP_OK 0
+#define SIP_ERR_SINGULAR 1 /* SingularFactorError  error.hpp:34-37 */
+#define SIP_ERR_STALE 2    /* StaleFactorsError    error.hpp:40-43 */
+#define SIP_ERR_MISUSE 3   /* MisuseError          error.hpp:47-50 */
+#define SIP_ERR_CONFIG 4   /* ConfigError          error.hpp:16-19 */
+#define SIP_ERR_CUDA 5     /* Error (device failure)               */
+#define SIP_ERR_NCCL 6     /* Error (collective failure)           */
+#define SIP_ERR_NOMEM 7    /* Error (device allocation)            */
+
+/* bsfv::Precision (field.hpp:10): relaxation precision. */
+#define SIP_PREC_DOUBLE 0
+#define SIP_PREC_SINGLE 1
+
+typedef struct sip_ctx sip_ctx;
+
+/* Library version string and build flags ("sm_100a ..."). */
+const char* sip_version(void);
+const char* sip_status_string(int status);
+/* Last error message of a context (or of the last failed create if ctx NULL). */
+const char* sip_last_error(const sip_ctx* ctx);
+
+/*
+ * Single block of nx*ny*nz interior cells on CUDA device `device`.
+ */
+int sip_create(int device, int nx, int ny, int nz, int precision, sip_ctx** out);
+
+/*
+ * Block-structured grid gnx*gny*gnz split into px*py*pz blocks exactly as
+ * bsfv::decompose (grid.cpp:50-89: even split, remainder to the last block
+ * per axis; block id = bx + px*(by + py*bz)).  block_rank[nblocks] assigns
+ * blocks to ranks (NULL: compact sub-lattices, see sip_plan_block_ranks);
+ * this process is `rank` of `nranks` and owns the blocks mapped to it.
+ * nccl_id: 128-byte ncclUniqueId shared by all ranks (NULL when nranks == 1).
+ */
+int sip_create_lattice(int device, int gnx, int gny, int gnz, int px, int py, int pz,
+                       const int* block_rank, int rank, int nranks, const void* nccl_id,
+                       int precision, sip_ctx** out);
+int sip_destroy(sip_ctx* ctx);
+
+/* Local blocks of this rank, ascending block id. */
+int sip_num_local_blocks(const sip_ctx* ctx, int* n);
+int sip_local_block(const sip_ctx* ctx, int local, int* block_id, int dims[3], int origin[3]);
+
+/*
+ * Stencil system of one local block (Field3 host arrays, G doubles each).
+ * Bumps the system revision (stale factors are detected).
+ */
+int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw,
+                   const double* ae, const double* as, const double* an, const double* ab,
+                   const double* at, const double* q);
+/* Source term only (su changes per RK stage; factors stay valid). */
+int sip_set_source(sip_ctx* ctx, int local, const double* q);
+/* Seeded synthetic system generated on the device:
+ * kind 0 = configs 0/1/3/4 generator, kind 2 = config 2; seed per block =
+ * seed + block id.  Same values as sip_generate_host. */
+int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed);
+
+/*
+ * Stone incomplete-LU factorisation of every local block.
+ * On SIP_ERR_SINGULAR, *bad_block / *bad_cell name the first singular cell
+ * (block id, Field3 index) in lexicographic order.
+ */
+int sip_factor(sip_ctx* ctx, double alpha, long long* bad_block, long long* bad_cell);
+
+/*
+ * solve on the reuse path: phi[local] (Field3 host arrays,
+ * in/out) converted once at entry / exit; iterate until norm/norm[0] <=
+ * target or max_iters (target <= 0: fixed count; target >= 1: no-op, 0
+ * iterations).  norms_out[max_iters] receives the per-iteration L1 norm of
+ * the pre-update residual, summed over all blocks of all ranks in block order.
+ */
+int sip_solve(sip_ctx* ctx, double* const* phi, int max_iters, double target, double* norms_out,
+              int* iters_used);
+
+/* Device-resident path (used for the HBM-resident throughput number). */
+int sip_load_phi(sip_ctx* ctx, double* const* phi);      /* host Field3 -> device */
+int sip_store_phi(sip_ctx* ctx, double* const* phi);     /* device -> host Field3 */
+int sip_iterate(sip_ctx* ctx, int iters);                 /* enqueue, no host sync */
+int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* block_norms);
+int sip_synchronize(sip_ctx* ctx);
+
+/* residual_general / residual_symmetric of the current
+ * device phi into res[local] (Field3 host arrays, interior written). */
+int sip_residual(sip_ctx* ctx, int symmetric, double* const* res);
+
+/* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */
+int sip_set_stream(sip_ctx* ctx, void* stream);
+void* sip_get_stream(const sip_ctx* ctx);
+
+/* Per-kernel CUDA-event timing of subsequent sip_iterate calls (0 = off).
+ * Totals over the iterations since enabling: forward (K2), backward (K3),
+ * halo (K4) in ms, and the number of kernel launches enqueued. */
+int sip_set_profiling(sip_ctx* ctx, int on);
+int sip_get_profile(sip_ctx* ctx, double* fwd_ms, double* bwd_ms, double* halo_ms,
+                    long long* launches);
+/* Total kernel launches enqueued by this context so far. */
+long long sip_launch_count(const sip_ctx* ctx);
+/* Tile geometry of the wavefront kernels (TI, TJ, tiles, slices). */
+int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long long* slices);
+
+/* ---- host-only helpers (no device needed) ---- */
+/* 128-byte ncclUniqueId for sip_create_lattice (rank 0 creates, all share). */
+int sip_nccl_unique_id(void* out128);
+/* Host copy of the synthetic generator (Field3 arrays of one block). */
+int sip_generate_host(int kind, uint64_t seed, const int g[3], const int o[3], int nx, int ny,
+                      int nz, double* ap, double* aw, double* ae, double* as, double* an,
+                      double* ab, double* at, double* q);
+/* Compact block -> rank map: each rank gets a near-cubic sub-lattice of the
+ * px*py*pz block lattice (replaces with_ranks' slabs, grid.cpp:91-102). */
+int sip_plan_block_ranks(int px, int py, int pz, int nranks, int* block_rank);
+/* Face-halo plan of one rank (faces only; the 7-point stencil reads no edge or
+ * corner ghosts).  Each entry is 12 ints in the field order of
+ * the reference's TransferEntry / FTT1 record (tables.hpp:18-28,55-59):
+ *   dir (0 local, 1 send, 2 recv), kind (0 = face), face (E,W,N,S,T,B = 0..5),
+ *   peer rank, owner block, neighbor block, ilo, ihi, jlo, jhi, klo, khi
+ * in the canonical order of transfers.cpp:148-165 restricted to faces.
+ * block_rank NULL = one block per rank (decompose()).  *n_entries is the
+ * capacity on input (entries may be NULL to query the count). */
+int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz, const int* block_rank,
+                  int rank, int* n_entries, int* entries /* [n][12] */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIP_C_H_ */

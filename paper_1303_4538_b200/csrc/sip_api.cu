@@ -1,0 +1,968 @@
+// sip_api.cu -- host runtime behind the C-ABI (include/sip_c.h): device
+// memory for the tile-slice packs, factor/solve orchestration on one CUDA
+// stream, face-halo exchange (device copies inside a GPU, NCCL send/recv
+// between GPUs), deterministic norm reduction and per-kernel timing.
+// Host C++ only calls kernels through the launchers of sip_kernels.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "sip_internal.h"
+
+using namespace sipb;
+
+namespace {
+thread_local std::string g_create_err;
+
+struct Peer {
+  int rank = -1;
+  std::vector<FaceCopy> pack, unpack;  // plane -> send buffer, recv buffer -> ghost
+  long long count = 0;                 // elements each way
+  FaceCopy* d_pack = nullptr;
+  FaceCopy* d_unpack = nullptr;
+  void* sbuf = nullptr;
+  void* rbuf = nullptr;
+  int max_plane = 0;
+};
+}  // namespace
+
+struct sip_ctx {
+  int device = 0, precision = 0, rank = 0, nranks = 1;
+  size_t esize = 8;
+  Lattice L;
+  std::vector<int> rank_of, local, local_of;
+  std::vector<BlockDesc> hblocks;
+  std::vector<TileDesc> htiles;
+  std::vector<int> order_f, order_b;
+  BlockDesc* d_blocks = nullptr;
+  TileDesc* d_tiles = nullptr;
+  int* d_order_f = nullptr;
+  int* d_order_b = nullptr;
+  void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
+  void *edgeW = nullptr, *edgeS = nullptr;
+  double *fw64 = nullptr, *bw64 = nullptr;  // fp32 mode: fp64 shadow for the factorisation
+  unsigned *st_f = nullptr, *st_b = nullptr, *st_fac = nullptr;
+  double* partial = nullptr;
+  double* d_norms = nullptr;
+  double* d_bnorms = nullptr;
+  int norm_cap = 0, n_done = 0;
+  unsigned long long* d_bad = nullptr;
+  double* staging = nullptr;  // 8 x Gmax doubles (generator needs all 8)
+  size_t gmax = 0;
+  double* phi_stage = nullptr;       // per local block Field3 fp64 mirror of phi (load/store)
+  std::vector<size_t> phi_stage_off;
+  long long total_slices = 0, total_edge = 0, total_ghost = 0;
+  int grid_f = 1, grid_b = 1, grid_fac = 1;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  long long revision = 0, factor_stamp = -1;
+  bool factored = false;
+  double alpha = 0.92;
+  std::vector<FaceCopy> local_copies;
+  FaceCopy* d_local_copies = nullptr;
+  int local_max_plane = 0;
+  std::vector<Peer> peers;
+  ncclComm_t comm = nullptr;
+  bool prof = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo
+  double t_fwd = 0, t_bwd = 0, t_halo = 0;
+  long long launches = 0, prof_launches = 0;
+  std::string err;
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+      return (e_ == cudaErrorMemoryAllocation) ? SIP_ERR_NOMEM : SIP_ERR_CUDA;      \
+    }                                                                               \
+  } while (0)
+#define CKS(call)                        \
+  do {                                   \
+    int s_ = (call);                     \
+    if (s_ != SIP_OK) {                  \
+      if (ctx->err.empty()) ctx->err = #call; \
+      return s_;                         \
+    }                                    \
+  } while (0)
+#define CKN(call)                                                     \
+  do {                                                                \
+    ncclResult_t r_ = (call);                                         \
+    if (r_ != ncclSuccess) {                                          \
+      ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);  \
+      return SIP_ERR_NCCL;                                            \
+    }                                                                 \
+  } while (0)
+
+static int set_device(sip_ctx* ctx) {
+  CK(cudaSetDevice(ctx->device));
+  return SIP_OK;
+}
+
+template <typename P>
+static int dalloc(sip_ctx* ctx, P** p, size_t bytes) {
+  void* v = nullptr;
+  CK(cudaMalloc(&v, bytes ? bytes : 16));
+  CK(cudaMemset(v, 0, bytes ? bytes : 16));
+  *p = static_cast<P*>(v);
+  return SIP_OK;
+}
+
+static size_t field3_elems(const BlockDesc& b) {
+  return (size_t)(b.nx + 2) * (b.ny + 2) * (b.nz + 2);
+}
+
+// -------------------------------------------------------------- construction
+static int build(sip_ctx* ctx) {
+  // local blocks and their tiles
+  const int nb = (int)ctx->L.blocks.size();
+  ctx->local_of.assign(nb, -1);
+  for (int b = 0; b < nb; ++b)
+    if (ctx->rank_of[b] == ctx->rank) {
+      ctx->local_of[b] = (int)ctx->local.size();
+      ctx->local.push_back(b);
+    }
+  long long slot = 0, edge = 0, ghost = 0;
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
+    BlockDesc bd{};
+    bd.id = ctx->local[lb];
+    bd.nx = bi.n[0]; bd.ny = bi.n[1]; bd.nz = bi.n[2];
+    bd.TX = (bd.nx + kTI - 1) / kTI;
+    bd.TY = (bd.ny + kTJ - 1) / kTJ;
+    bd.ns = bd.nz + kD - 1;
+    bd.slot0 = slot;
+    bd.ghost = ghost;
+    bd.tile0 = (int)ctx->htiles.size();
+    bd.ntiles = bd.TX * bd.TY;
+    for (int c = 0; c < bd.TY; ++c)
+      for (int a = 0; a < bd.TX; ++a) {
+        TileDesc td{};
+        td.slot = slot;
+        td.edge = edge;
+        td.block = (int)lb;
+        td.i0 = a * kTI; td.j0 = c * kTJ;
+        td.wI = std::min(kTI, bd.nx - td.i0);
+        td.wJ = std::min(kTJ, bd.ny - td.j0);
+        auto idx = [&](int aa, int cc) { return bd.tile0 + aa + bd.TX * cc; };
+        td.nW = a > 0 ? idx(a - 1, c) : -1;
+        td.nE = a + 1 < bd.TX ? idx(a + 1, c) : -1;
+        td.nS = c > 0 ? idx(a, c - 1) : -1;
+        td.nN = c + 1 < bd.TY ? idx(a, c + 1) : -1;
+        td.ns = bd.ns;
+        td.nz = bd.nz;
+        ctx->htiles.push_back(td);
+        slot += bd.ns;
+        edge += (long long)bd.nz * std::max(kTI, kTJ);
+      }
+    ghost += ghost_count(bd.nx, bd.ny, bd.nz);
+    ctx->hblocks.push_back(bd);
+    ctx->gmax = std::max(ctx->gmax, field3_elems(bd));
+  }
+  ctx->total_slices = slot;
+  ctx->total_edge = edge;
+  ctx->total_ghost = ghost;
+  const int nt = (int)ctx->htiles.size();
+  // topological ticket order: anti-diagonal of the tile lattice, then block
+  std::vector<std::tuple<int, int, int, int>> keys;
+  for (int t = 0; t < nt; ++t) {
+    const TileDesc& td = ctx->htiles[t];
+    keys.emplace_back(td.i0 / kTI + td.j0 / kTJ, td.block, td.i0, t);
+  }
+  std::sort(keys.begin(), keys.end());
+  for (auto& k : keys) ctx->order_f.push_back(std::get<3>(k));
+  ctx->order_b.assign(ctx->order_f.rbegin(), ctx->order_f.rend());
+
+  const size_t es = ctx->esize;
+  const size_t TT = kTT;
+  CKS(dalloc(ctx, &ctx->d_blocks, sizeof(BlockDesc) * std::max<size_t>(1, ctx->hblocks.size())));
+  CKS(dalloc(ctx, &ctx->d_tiles, sizeof(TileDesc) * std::max(1, nt)));
+  CKS(dalloc(ctx, &ctx->d_order_f, sizeof(int) * std::max(1, nt)));
+  CKS(dalloc(ctx, &ctx->d_order_b, sizeof(int) * std::max(1, nt)));
+  if (nt) {
+    CK(cudaMemcpy(ctx->d_blocks, ctx->hblocks.data(), sizeof(BlockDesc) * ctx->hblocks.size(),
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_tiles, ctx->htiles.data(), sizeof(TileDesc) * nt, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_order_f, ctx->order_f.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_order_b, ctx->order_b.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+  }
+  const size_t S = (size_t)ctx->total_slices * TT;
+  CKS(dalloc(ctx, &ctx->fw, S * F_NA * es));
+  CKS(dalloc(ctx, &ctx->bw, S * B_NA * es));
+  CKS(dalloc(ctx, &ctx->phi, S * es));
+  CKS(dalloc(ctx, &ctx->R, S * es));
+  CKS(dalloc(ctx, &ctx->ghost, (size_t)ctx->total_ghost * es));
+  CKS(dalloc(ctx, &ctx->edgeW, (size_t)ctx->total_edge * es));
+  CKS(dalloc(ctx, &ctx->edgeS, (size_t)ctx->total_edge * es));
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    CKS(dalloc(ctx, &ctx->fw64, S * F_NA * sizeof(double)));
+    CKS(dalloc(ctx, &ctx->bw64, S * B_NA * sizeof(double)));
+  } else {
+    ctx->fw64 = static_cast<double*>(ctx->fw);
+    ctx->bw64 = static_cast<double*>(ctx->bw);
+  }
+  const size_t st = 32 + (size_t)std::max(1, nt);
+  CKS(dalloc(ctx, &ctx->st_f, st * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->st_b, st * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->st_fac, st * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->partial, sizeof(double) * std::max(1, nt)));
+  CKS(dalloc(ctx, &ctx->d_bad, sizeof(unsigned long long)));
+  CKS(dalloc(ctx, &ctx->staging, sizeof(double) * 8 * std::max<size_t>(1, ctx->gmax)));
+  size_t pst = 0;
+  for (const BlockDesc& b : ctx->hblocks) {
+    ctx->phi_stage_off.push_back(pst);
+    pst += field3_elems(b);
+  }
+  CKS(dalloc(ctx, &ctx->phi_stage, sizeof(double) * std::max<size_t>(1, pst)));
+
+  int cap = 0;
+  CKS(max_resident_ctas(1, ctx->precision, &cap));
+  ctx->grid_f = std::max(1, std::min(nt, cap));
+  CKS(max_resident_ctas(2, ctx->precision, &cap));
+  ctx->grid_b = std::max(1, std::min(nt, cap));
+  CKS(max_resident_ctas(0, ctx->precision, &cap));
+  ctx->grid_fac = std::max(1, std::min(nt, cap));
+
+  // halo plan: faces only, canonical order (transfers.cpp:148-165)
+  std::vector<HaloEntry> plan;
+  plan_halo(ctx->L, ctx->rank_of, ctx->rank, plan);
+  // bsfv face id (E,W,N,S,T,B) -> kernel face (W,E,S,N,B,T)
+  auto kface = [](int f) { static const int m[6] = {G_E, G_W, G_N, G_S, G_T, G_B}; return m[f]; };
+  auto plane = [&](int gblock, int kf, int& n0, int& n1) {
+    const BlockInfo& bi = ctx->L.blocks[gblock];
+    if (kf <= G_E) { n0 = bi.n[1]; n1 = bi.n[2]; }
+    else if (kf <= G_N) { n0 = bi.n[0]; n1 = bi.n[2]; }
+    else { n0 = bi.n[0]; n1 = bi.n[1]; }
+  };
+  for (const HaloEntry& e : plan) {
+    FaceCopy fc{};
+    if (e.dir == 0) {  // local: owner = src block, face = src plane; dst ghost = opposite
+      fc.src_block = ctx->local_of[e.owner];
+      fc.src_face = kface(e.face);
+      fc.dst_block = ctx->local_of[e.neighbor];
+      fc.dst_face = kface(e.face ^ 1);
+      plane(e.owner, fc.src_face, fc.n0, fc.n1);
+      ctx->local_copies.push_back(fc);
+      ctx->local_max_plane = std::max(ctx->local_max_plane, fc.n0 * fc.n1);
+      continue;
+    }
+    auto it = std::find_if(ctx->peers.begin(), ctx->peers.end(),
+                           [&](const Peer& p) { return p.rank == e.peer; });
+    if (it == ctx->peers.end()) {
+      ctx->peers.emplace_back();
+      ctx->peers.back().rank = e.peer;
+      it = ctx->peers.end() - 1;
+    }
+    if (e.dir == 1) {  // send: owner = local src block, plane face
+      fc.src_block = ctx->local_of[e.owner];
+      fc.src_face = kface(e.face);
+      fc.dst_block = -1;
+      plane(e.owner, fc.src_face, fc.n0, fc.n1);
+      fc.buf = 0;
+      for (auto& q : it->pack) fc.buf += (long long)q.n0 * q.n1;
+      it->pack.push_back(fc);
+    } else {  // recv: owner = local dst block, face = ghost face
+      fc.src_block = -1;
+      fc.dst_block = ctx->local_of[e.owner];
+      fc.dst_face = kface(e.face);
+      plane(e.owner, fc.dst_face, fc.n0, fc.n1);
+      fc.buf = 0;
+      for (auto& q : it->unpack) fc.buf += (long long)q.n0 * q.n1;
+      it->unpack.push_back(fc);
+    }
+    it->max_plane = std::max(it->max_plane, fc.n0 * fc.n1);
+  }
+  if (!ctx->local_copies.empty()) {
+    CKS(dalloc(ctx, &ctx->d_local_copies, sizeof(FaceCopy) * ctx->local_copies.size()));
+    CK(cudaMemcpy(ctx->d_local_copies, ctx->local_copies.data(),
+                  sizeof(FaceCopy) * ctx->local_copies.size(), cudaMemcpyHostToDevice));
+  }
+  for (Peer& p : ctx->peers) {
+    long long ns = 0, nr = 0;
+    for (auto& q : p.pack) ns += (long long)q.n0 * q.n1;
+    for (auto& q : p.unpack) nr += (long long)q.n0 * q.n1;
+    if (ns != nr) {
+      ctx->err = "halo plan: send/recv volume mismatch with rank " + std::to_string(p.rank);
+      return SIP_ERR_CONFIG;
+    }
+    p.count = ns;
+    CKS(dalloc(ctx, &p.d_pack, sizeof(FaceCopy) * std::max<size_t>(1, p.pack.size())));
+    CKS(dalloc(ctx, &p.d_unpack, sizeof(FaceCopy) * std::max<size_t>(1, p.unpack.size())));
+    if (!p.pack.empty())
+      CK(cudaMemcpy(p.d_pack, p.pack.data(), sizeof(FaceCopy) * p.pack.size(), cudaMemcpyHostToDevice));
+    if (!p.unpack.empty())
+      CK(cudaMemcpy(p.d_unpack, p.unpack.data(), sizeof(FaceCopy) * p.unpack.size(),
+                    cudaMemcpyHostToDevice));
+    CKS(dalloc(ctx, &p.sbuf, (size_t)std::max(1LL, p.count) * es));
+    CKS(dalloc(ctx, &p.rbuf, (size_t)std::max(1LL, p.count) * es));
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  return SIP_OK;
+}
+
+static int create_common(int device, int gnx, int gny, int gnz, int px, int py, int pz,
+                         const int* block_rank, int rank, int nranks, const void* nccl_id,
+                         int precision, sip_ctx** out) {
+  if (!out) return SIP_ERR_CONFIG;
+  *out = nullptr;
+  if (precision != SIP_PREC_DOUBLE && precision != SIP_PREC_SINGLE) {
+    g_create_err = "precision must be SIP_PREC_DOUBLE or SIP_PREC_SINGLE";
+    return SIP_ERR_CONFIG;
+  }
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    g_create_err = "rank out of range";
+    return SIP_ERR_CONFIG;
+  }
+  sip_ctx* ctx = new sip_ctx();
+  ctx->device = device;
+  ctx->precision = precision;
+  ctx->esize = precision == SIP_PREC_DOUBLE ? 8 : 4;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  std::string err;
+  if (!build_lattice(gnx, gny, gnz, px, py, pz, ctx->L, err)) {
+    g_create_err = err;
+    delete ctx;
+    return SIP_ERR_CONFIG;
+  }
+  const int nb = px * py * pz;
+  if (block_rank) {
+    ctx->rank_of.assign(block_rank, block_rank + nb);
+    for (int r : ctx->rank_of)
+      if (r < 0 || r >= nranks) {
+        g_create_err = "block_rank entry out of range";
+        delete ctx;
+        return SIP_ERR_CONFIG;
+      }
+  } else if (!plan_block_ranks(px, py, pz, nranks, ctx->rank_of)) {
+    g_create_err = "cannot place " + std::to_string(nb) + " blocks on " + std::to_string(nranks) +
+                   " ranks";
+    delete ctx;
+    return SIP_ERR_CONFIG;
+  }
+  int s = set_device(ctx);
+  if (s == SIP_OK) s = build(ctx);
+  if (s == SIP_OK && nranks > 1) {
+    if (!nccl_id) {
+      ctx->err = "nccl_id required when nranks > 1";
+      s = SIP_ERR_CONFIG;
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+      if (r != ncclSuccess) {
+        ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+        s = SIP_ERR_NCCL;
+      }
+    }
+  }
+  if (s != SIP_OK) {
+    g_create_err = ctx->err;
+    sip_destroy(ctx);
+    return s;
+  }
+  *out = ctx;
+  return SIP_OK;
+}
+
+// ------------------------------------------------------------------ helpers
+static int ensure_norm_cap(sip_ctx* ctx, int need) {
+  if (need <= ctx->norm_cap) return SIP_OK;
+  const int cap = std::max(need, std::max(64, 2 * ctx->norm_cap));
+  const int nl = std::max<int>(1, (int)ctx->local.size());
+  double *n = nullptr, *bn = nullptr;
+  CK(cudaStreamSynchronize(ctx->stream));
+  CKS(dalloc(ctx, &n, sizeof(double) * cap));
+  CKS(dalloc(ctx, &bn, sizeof(double) * cap * nl));
+  if (ctx->d_norms) {
+    CK(cudaMemcpy(n, ctx->d_norms, sizeof(double) * ctx->norm_cap, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(bn, ctx->d_bnorms, sizeof(double) * ctx->norm_cap * nl, cudaMemcpyDeviceToDevice));
+    cudaFree(ctx->d_norms);
+    cudaFree(ctx->d_bnorms);
+  }
+  ctx->d_norms = n;
+  ctx->d_bnorms = bn;
+  ctx->norm_cap = cap;
+  return SIP_OK;
+}
+
+template <typename T>
+static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
+  SweepParams<T> p{};
+  p.tiles = ctx->d_tiles;
+  p.blocks = ctx->d_blocks;
+  p.order = forward ? ctx->d_order_f : ctx->d_order_b;
+  p.ntiles = (int)ctx->htiles.size();
+  p.nblocks = (int)ctx->hblocks.size();
+  p.fw = static_cast<T*>(ctx->fw);
+  p.bw = static_cast<T*>(ctx->bw);
+  p.phi = static_cast<T*>(ctx->phi);
+  p.R = static_cast<T*>(ctx->R);
+  p.ghost = static_cast<T*>(ctx->ghost);
+  p.edgeW = static_cast<T*>(ctx->edgeW);
+  p.edgeS = static_cast<T*>(ctx->edgeS);
+  p.state = forward ? ctx->st_f : ctx->st_b;
+  p.state_other = forward ? ctx->st_b : ctx->st_f;
+  p.partial = ctx->partial;
+  p.block_norms = ctx->d_bnorms + (size_t)it * std::max<size_t>(1, ctx->local.size());
+  p.norm = ctx->d_norms + it;
+  return p;
+}
+
+static void ev_begin(sip_ctx* ctx, int kind, cudaEvent_t* a) {
+  if (!ctx->prof) return;
+  cudaEvent_t b;
+  cudaEventCreate(a);
+  cudaEventCreate(&b);
+  cudaEventRecord(*a, ctx->stream);
+  ctx->events.emplace_back(kind, *a, b);
+}
+static void ev_end(sip_ctx* ctx) {
+  if (!ctx->prof) return;
+  cudaEventRecord(std::get<2>(ctx->events.back()), ctx->stream);
+}
+
+template <typename T>
+static int exchange(sip_ctx* ctx) {
+  if (ctx->local_copies.empty() && ctx->peers.empty()) return SIP_OK;
+  cudaEvent_t e;
+  ev_begin(ctx, 2, &e);
+  T* phi = static_cast<T*>(ctx->phi);
+  T* ghost = static_cast<T*>(ctx->ghost);
+  if (!ctx->local_copies.empty()) {
+    CKS(launch_face_copies<T>(ctx->d_local_copies, (int)ctx->local_copies.size(),
+                              ctx->local_max_plane, ctx->d_blocks, phi, ghost, nullptr, nullptr,
+                              ctx->stream));
+    ++ctx->launches;
+  }
+  if (!ctx->peers.empty()) {
+    for (Peer& p : ctx->peers) {
+      CKS(launch_face_copies<T>(p.d_pack, (int)p.pack.size(), p.max_plane, ctx->d_blocks, phi,
+                                ghost, nullptr, static_cast<T*>(p.sbuf), ctx->stream));
+      ++ctx->launches;
+    }
+    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    // non-blocking exchange: all receives and sends posted
+    // in one group; NCCL matches per peer in issue order
+    CKN(ncclGroupStart());
+    for (Peer& p : ctx->peers) {
+      CKN(ncclRecv(p.rbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
+      CKN(ncclSend(p.sbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    for (Peer& p : ctx->peers) {
+      CKS(launch_face_copies<T>(p.d_unpack, (int)p.unpack.size(), p.max_plane, ctx->d_blocks, phi,
+                                ghost, static_cast<T*>(p.rbuf), nullptr, ctx->stream));
+      ++ctx->launches;
+    }
+  }
+  ev_end(ctx);
+  return SIP_OK;
+}
+
+template <typename T>
+static int iterate_t(sip_ctx* ctx, int iters) {
+  CKS(ensure_norm_cap(ctx, ctx->n_done + iters));
+  for (int n = 0; n < iters; ++n) {
+    const int it = ctx->n_done + n;
+    cudaEvent_t e;
+    ev_begin(ctx, 0, &e);
+    CKS(launch_forward<T>(sweep_params<T>(ctx, true, it), ctx->grid_f, ctx->stream));
+    ++ctx->launches;
+    ev_end(ctx);
+    ev_begin(ctx, 1, &e);
+    CKS(launch_backward<T>(sweep_params<T>(ctx, false, it), ctx->grid_b, ctx->stream));
+    ++ctx->launches;
+    ev_end(ctx);
+    CKS(exchange<T>(ctx));
+  }
+  ctx->n_done += iters;
+  return SIP_OK;
+}
+
+static int check_ready(sip_ctx* ctx) {
+  if (!ctx->factored) {
+    ctx->err = "solve before sip_factor (no factors for this system)";
+    return SIP_ERR_MISUSE;
+  }
+  if (ctx->factor_stamp != ctx->revision) {
+    ctx->err = "factors stamped with revision " + std::to_string(ctx->factor_stamp) +
+               " used against system revision " + std::to_string(ctx->revision);
+    return SIP_ERR_STALE;
+  }
+  return SIP_OK;
+}
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* sip_version(void) {
+  return "b200-sip 0.1 (sm_100a, tiles 16x16, bulk-copy wavefront K1/K2/K3, NCCL halo)";
+}
+
+const char* sip_status_string(int s) {
+  switch (s) {
+    case SIP_OK: return "ok";
+    case SIP_ERR_SINGULAR: return "singular factorization";
+    case SIP_ERR_STALE: return "stale factors";
+    case SIP_ERR_MISUSE: return "misuse";
+    case SIP_ERR_CONFIG: return "invalid configuration";
+    case SIP_ERR_CUDA: return "CUDA error";
+    case SIP_ERR_NCCL: return "NCCL error";
+    case SIP_ERR_NOMEM: return "device out of memory";
+    default: return "unknown status";
+  }
+}
+
+const char* sip_last_error(const sip_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+int sip_create(int device, int nx, int ny, int nz, int precision, sip_ctx** out) {
+  return create_common(device, nx, ny, nz, 1, 1, 1, nullptr, 0, 1, nullptr, precision, out);
+}
+
+int sip_create_lattice(int device, int gnx, int gny, int gnz, int px, int py, int pz,
+                       const int* block_rank, int rank, int nranks, const void* nccl_id,
+                       int precision, sip_ctx** out) {
+  return create_common(device, gnx, gny, gnz, px, py, pz, block_rank, rank, nranks, nccl_id,
+                       precision, out);
+}
+
+int sip_destroy(sip_ctx* ctx) {
+  if (!ctx) return SIP_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (auto& e : ctx->events) {
+    cudaEventDestroy(std::get<1>(e));
+    cudaEventDestroy(std::get<2>(e));
+  }
+  void* ptrs[] = {ctx->d_blocks, ctx->d_tiles, ctx->d_order_f, ctx->d_order_b, ctx->fw, ctx->bw,
+                  ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
+                  ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
+                  ctx->staging, ctx->d_local_copies, ctx->phi_stage};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    if (ctx->fw64) cudaFree(ctx->fw64);
+    if (ctx->bw64) cudaFree(ctx->bw64);
+  }
+  for (Peer& p : ctx->peers) {
+    if (p.d_pack) cudaFree(p.d_pack);
+    if (p.d_unpack) cudaFree(p.d_unpack);
+    if (p.sbuf) cudaFree(p.sbuf);
+    if (p.rbuf) cudaFree(p.rbuf);
+  }
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return SIP_OK;
+}
+
+int sip_num_local_blocks(const sip_ctx* ctx, int* n) {
+  if (!ctx || !n) return SIP_ERR_MISUSE;
+  *n = (int)ctx->local.size();
+  return SIP_OK;
+}
+
+int sip_local_block(const sip_ctx* ctx, int local, int* block_id, int dims[3], int origin[3]) {
+  if (!ctx || local < 0 || local >= (int)ctx->local.size()) return SIP_ERR_MISUSE;
+  const BlockInfo& bi = ctx->L.blocks[ctx->local[local]];
+  if (block_id) *block_id = ctx->local[local];
+  for (int a = 0; a < 3; ++a) {
+    if (dims) dims[a] = bi.n[a];
+    if (origin) origin[a] = bi.lo[a];
+  }
+  return SIP_OK;
+}
+
+int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw, const double* ae,
+                   const double* as, const double* an, const double* ab, const double* at,
+                   const double* q) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (local < 0 || local >= (int)ctx->local.size()) {
+    ctx->err = "sip_set_system: local block index out of range";
+    return SIP_ERR_MISUSE;
+  }
+  const double* src[8] = {ap, aw, ae, as, an, ab, at, q};
+  const int arr[8] = {F_AP, F_AW, F_AE, F_AS, F_AN, F_AB, F_AT, F_Q};
+  for (const double* s : src)
+    if (!s) {
+      ctx->err = "sip_set_system: null array";
+      return SIP_ERR_MISUSE;
+    }
+  CKS(set_device(ctx));
+  const BlockDesc& hb = ctx->hblocks[local];
+  const size_t G = field3_elems(hb);
+  for (int a = 0; a < 8; ++a) {
+    CK(cudaMemcpyAsync(ctx->staging, src[a], G * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->precision == SIP_PREC_SINGLE) {
+      CKS(launch_scatter<float>(ctx->staging, ctx->d_blocks, local, hb, static_cast<float*>(ctx->fw),
+                                F_NA, arr[a], ctx->stream));
+    }
+    CKS(launch_scatter<double>(ctx->staging, ctx->d_blocks, local, hb, ctx->fw64, F_NA, arr[a],
+                               ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ++ctx->revision;
+  return SIP_OK;
+}
+
+int sip_set_source(sip_ctx* ctx, int local, const double* q) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (local < 0 || local >= (int)ctx->local.size() || !q) {
+    ctx->err = "sip_set_source: bad arguments";
+    return SIP_ERR_MISUSE;
+  }
+  CKS(set_device(ctx));
+  const BlockDesc& hb = ctx->hblocks[local];
+  CK(cudaMemcpyAsync(ctx->staging, q, field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (ctx->precision == SIP_PREC_SINGLE)
+    CKS(launch_scatter<float>(ctx->staging, ctx->d_blocks, local, hb, static_cast<float*>(ctx->fw),
+                              F_NA, F_Q, ctx->stream));
+  CKS(launch_scatter<double>(ctx->staging, ctx->d_blocks, local, hb, ctx->fw64, F_NA, F_Q,
+                             ctx->stream));
+  return SIP_OK;
+}
+
+int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (kind != 0 && kind != 2) {
+    ctx->err = "generator kind must be 0 or 2";
+    return SIP_ERR_CONFIG;
+  }
+  CKS(set_device(ctx));
+  const int arr[8] = {F_AP, F_AW, F_AE, F_AS, F_AN, F_AB, F_AT, F_Q};
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& hb = ctx->hblocks[lb];
+    const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
+    const size_t G = field3_elems(hb);
+    double* out8[8];
+    for (int a = 0; a < 8; ++a) out8[a] = ctx->staging + a * G;
+    CK(cudaMemsetAsync(ctx->staging, 0, 8 * G * sizeof(double), ctx->stream));
+    const int g[3] = {ctx->L.g[0], ctx->L.g[1], ctx->L.g[2]};
+    CKS(launch_generate(kind, seed + (uint64_t)ctx->local[lb], g, bi.lo.data(), hb.nx, hb.ny, hb.nz, out8,
+                        ctx->stream));
+    for (int a = 0; a < 8; ++a) {
+      if (ctx->precision == SIP_PREC_SINGLE)
+        CKS(launch_scatter<float>(out8[a], ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
+                                  F_NA, arr[a], ctx->stream));
+      CKS(launch_scatter<double>(out8[a], ctx->d_blocks, (int)lb, hb, ctx->fw64, F_NA, arr[a],
+                                 ctx->stream));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ++ctx->revision;
+  return SIP_OK;
+}
+
+int sip_factor(sip_ctx* ctx, double alpha, long long* bad_block, long long* bad_cell) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (!(alpha >= 0.0 && alpha < 1.0)) {
+    ctx->err = "alpha must be in [0, 1) (SPEC.md:124-127)";
+    return SIP_ERR_CONFIG;
+  }
+  CKS(set_device(ctx));
+  const int nt = (int)ctx->htiles.size();
+  CK(cudaMemsetAsync(ctx->st_fac, 0, (32 + (size_t)std::max(1, nt)) * sizeof(unsigned), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_bad, 0xff, sizeof(unsigned long long), ctx->stream));
+  FactorParams fp{};
+  fp.tiles = ctx->d_tiles;
+  fp.blocks = ctx->d_blocks;
+  fp.order = ctx->d_order_f;
+  fp.ntiles = nt;
+  fp.alpha = alpha;
+  fp.fw = ctx->fw64;
+  fp.bw = ctx->bw64;
+  fp.state = ctx->st_fac;
+  fp.bad = ctx->d_bad;
+  if (nt) {
+    CKS(launch_factor(fp, ctx->grid_fac, ctx->stream));
+    ++ctx->launches;
+  }
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    const long long S = ctx->total_slices * kTT;
+    CKS(launch_convert(ctx->fw64, static_cast<float*>(ctx->fw), S * F_NA, ctx->stream));
+    CKS(launch_convert(ctx->bw64, static_cast<float*>(ctx->bw), S * B_NA, ctx->stream));
+    ctx->launches += 2;
+  }
+  unsigned long long bad = ~0ULL;
+  CK(cudaMemcpyAsync(&bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad != ~0ULL) {
+    const long long blk = (long long)(bad >> 40), cell = (long long)(bad & ((1ULL << 40) - 1));
+    if (bad_block) *bad_block = blk;
+    if (bad_cell) *bad_cell = cell;
+    ctx->factored = false;
+    ctx->err = "singular factorization: |pivot| < 1e-30 at block " + std::to_string(blk) +
+               ", Field3 index " + std::to_string(cell);
+    return SIP_ERR_SINGULAR;
+  }
+  if (bad_block) *bad_block = -1;
+  if (bad_cell) *bad_cell = -1;
+  ctx->factored = true;
+  ctx->factor_stamp = ctx->revision;
+  ctx->alpha = alpha;
+  return SIP_OK;
+}
+
+int sip_load_phi(sip_ctx* ctx, double* const* phi) {
+  if (!ctx || !phi) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    if (!phi[lb]) {
+      ctx->err = "sip_load_phi: null phi";
+      return SIP_ERR_MISUSE;
+    }
+    const BlockDesc& hb = ctx->hblocks[lb];
+    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    // Field3 -> device mirror (keeps the caller's ghost layer for the store)
+    CK(cudaMemcpyAsync(st, phi[lb], field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if (ctx->precision == SIP_PREC_SINGLE) {
+      CKS(launch_scatter<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->phi), 1, 0,
+                                ctx->stream));
+      CKS(launch_ghost_in<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->ghost),
+                                 ctx->stream));
+    } else {
+      CKS(launch_scatter<double>(st, ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->phi), 1,
+                                 0, ctx->stream));
+      CKS(launch_ghost_in<double>(st, ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->ghost),
+                                  ctx->stream));
+    }
+    ctx->launches += 2;
+  }
+  // interface ghosts <- neighbours' phi0 (the exchange that precedes sweep 1)
+  int s = ctx->precision == SIP_PREC_SINGLE ? exchange<float>(ctx) : exchange<double>(ctx);
+  ctx->n_done = 0;
+  return s;
+}
+
+int sip_store_phi(sip_ctx* ctx, double* const* phi) {
+  if (!ctx || !phi) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& hb = ctx->hblocks[lb];
+    const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
+    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    // interior + interface ghosts are overwritten; domain-boundary ghosts,
+    // edges and corners keep the values loaded by sip_load_phi
+    if (ctx->precision == SIP_PREC_SINGLE)
+      CKS(launch_gather<float>(static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost),
+                               ctx->d_blocks, (int)lb, hb, bi.nbr.data(), st, ctx->stream));
+    else
+      CKS(launch_gather<double>(static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
+                                ctx->d_blocks, (int)lb, hb, bi.nbr.data(), st, ctx->stream));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(phi[lb], st, field3_elems(hb) * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_iterate(sip_ctx* ctx, int iters) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (iters < 0) {
+    ctx->err = "iters must be >= 0";
+    return SIP_ERR_CONFIG;
+  }
+  CKS(check_ready(ctx));
+  CKS(set_device(ctx));
+  return ctx->precision == SIP_PREC_SINGLE ? iterate_t<float>(ctx, iters)
+                                           : iterate_t<double>(ctx, iters);
+}
+
+int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* block_norms) {
+  if (!ctx || first < 0 || count < 0 || first + count > ctx->n_done) {
+    if (ctx) ctx->err = "sip_read_norms: range outside the iterations run";
+    return SIP_ERR_MISUSE;
+  }
+  CKS(set_device(ctx));
+  const int nl = std::max<int>(1, (int)ctx->local.size());
+  std::vector<double> bn((size_t)count * nl);
+  if (count) {
+    CK(cudaMemcpyAsync(bn.data(), ctx->d_bnorms + (size_t)first * nl, bn.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int nb = (int)ctx->L.blocks.size();
+  std::vector<double> all((size_t)count * nb, 0.0);
+  if (ctx->nranks == 1) {
+    for (int it = 0; it < count; ++it)
+      for (int lb = 0; lb < (int)ctx->local.size(); ++lb)
+        all[(size_t)it * nb + ctx->local[lb]] = bn[(size_t)it * nl + lb];
+  } else {
+    // all-gather every rank's block norms (Endpoint::all_reduce, net.hpp:131:
+    // fixed block order makes the sum independent of the placement)
+    int maxl = 0;
+    std::vector<std::vector<int>> blocks_of(ctx->nranks);
+    for (int b = 0; b < nb; ++b) blocks_of[ctx->rank_of[b]].push_back(b);
+    for (auto& v : blocks_of) maxl = std::max<int>(maxl, (int)v.size());
+    const size_t per = (size_t)count * maxl;
+    double *d_send = nullptr, *d_recv = nullptr;
+    CKS(dalloc(ctx, &d_send, sizeof(double) * std::max<size_t>(1, per)));
+    CKS(dalloc(ctx, &d_recv, sizeof(double) * std::max<size_t>(1, per * ctx->nranks)));
+    std::vector<double> pad(per, 0.0);
+    for (int it = 0; it < count; ++it)
+      for (int lb = 0; lb < (int)ctx->local.size(); ++lb) pad[(size_t)it * maxl + lb] = bn[(size_t)it * nl + lb];
+    CK(cudaMemcpy(d_send, pad.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    CKN(ncclAllGather(d_send, d_recv, per, ncclFloat64, ctx->comm, ctx->stream));
+    std::vector<double> got(per * ctx->nranks);
+    CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_send);
+    cudaFree(d_recv);
+    for (int r = 0; r < ctx->nranks; ++r)
+      for (int it = 0; it < count; ++it)
+        for (size_t lb = 0; lb < blocks_of[r].size(); ++lb)
+          all[(size_t)it * nb + blocks_of[r][lb]] = got[per * r + (size_t)it * maxl + lb];
+  }
+  for (int it = 0; it < count; ++it) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += all[(size_t)it * nb + b];
+    if (norms) norms[it] = s;
+    if (block_norms)
+      for (int b = 0; b < nb; ++b) block_norms[(size_t)it * nb + b] = all[(size_t)it * nb + b];
+  }
+  return SIP_OK;
+}
+
+int sip_synchronize(sip_ctx* ctx) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_solve(sip_ctx* ctx, double* const* phi, int max_iters, double target, double* norms_out,
+              int* iters_used) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (max_iters < 1) {
+    ctx->err = "max_iters must be >= 1 (SPEC.md:124-127)";
+    return SIP_ERR_CONFIG;
+  }
+  CKS(check_ready(ctx));
+  if (iters_used) *iters_used = 0;
+  if (target >= 1.0) return SIP_OK;  // no-op: fi0 returned, 0 iterations
+  CKS(sip_load_phi(ctx, phi));
+  int used = 0;
+  if (target <= 0.0) {
+    CKS(sip_iterate(ctx, max_iters));
+    used = max_iters;
+  } else {
+    double n0 = 0.0;
+    while (used < max_iters) {
+      CKS(sip_iterate(ctx, 1));
+      double n = 0.0;
+      CKS(sip_read_norms(ctx, used, 1, &n, nullptr));
+      if (used == 0) n0 = n;
+      ++used;
+      if (n0 == 0.0 || n / n0 <= target) break;
+    }
+  }
+  if (norms_out) CKS(sip_read_norms(ctx, 0, used, norms_out, nullptr));
+  CKS(sip_store_phi(ctx, phi));
+  if (iters_used) *iters_used = used;
+  return SIP_OK;
+}
+
+int sip_residual(sip_ctx* ctx, int symmetric, double* const* res) {
+  if (!ctx || !res) return SIP_ERR_MISUSE;
+  if (symmetric) {
+    ctx->err = "residual_symmetric is not available on the device path yet";
+    return SIP_ERR_MISUSE;
+  }
+  CKS(set_device(ctx));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& hb = ctx->hblocks[lb];
+    const size_t G = field3_elems(hb);
+    CK(cudaMemsetAsync(ctx->staging, 0, G * sizeof(double), ctx->stream));
+    if (ctx->precision == SIP_PREC_SINGLE)
+      CKS(launch_residual<float>(ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
+                                 static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost), 0,
+                                 ctx->staging, ctx->stream));
+    else
+      CKS(launch_residual<double>(ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->fw),
+                                  static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
+                                  0, ctx->staging, ctx->stream));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(res[lb], ctx->staging, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_set_stream(sip_ctx* ctx, void* stream) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return SIP_OK;
+}
+
+void* sip_get_stream(const sip_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int sip_set_profiling(sip_ctx* ctx, int on) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (auto& e : ctx->events) {
+    cudaEventDestroy(std::get<1>(e));
+    cudaEventDestroy(std::get<2>(e));
+  }
+  ctx->events.clear();
+  ctx->t_fwd = ctx->t_bwd = ctx->t_halo = 0;
+  ctx->prof = on != 0;
+  ctx->prof_launches = ctx->launches;
+  return SIP_OK;
+}
+
+int sip_get_profile(sip_ctx* ctx, double* fwd_ms, double* bwd_ms, double* halo_ms,
+                    long long* launches) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (auto& e : ctx->events) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, std::get<1>(e), std::get<2>(e)));
+    (std::get<0>(e) == 0 ? ctx->t_fwd : std::get<0>(e) == 1 ? ctx->t_bwd : ctx->t_halo) += ms;
+    cudaEventDestroy(std::get<1>(e));
+    cudaEventDestroy(std::get<2>(e));
+  }
+  ctx->events.clear();
+  if (fwd_ms) *fwd_ms = ctx->t_fwd;
+  if (bwd_ms) *bwd_ms = ctx->t_bwd;
+  if (halo_ms) *halo_ms = ctx->t_halo;
+  if (launches) *launches = ctx->launches - ctx->prof_launches;
+  return SIP_OK;
+}
+
+long long sip_launch_count(const sip_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long long* slices) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (ti) *ti = kTI;
+  if (tj) *tj = kTJ;
+  if (tiles) *tiles = (long long)ctx->htiles.size();
+  if (slices) *slices = ctx->total_slices;
+  return SIP_OK;
+}
+
+int sip_nccl_unique_id(void* out128) {
+  if (!out128) return SIP_ERR_MISUSE;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SIP_ERR_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return SIP_OK;
+}
+
+}  // extern "C"

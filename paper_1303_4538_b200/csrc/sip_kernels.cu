@@ -1,0 +1,957 @@
+// sip_kernels.cu -- sm_100a kernels of the SIP hot path.
+//
+//   K1 k_factor    Stone ILU factor          wavefront, fp64
+//   K2 k_forward   residual + L1 norm + forward substitution   wavefront, bulk-copy ring
+//                  (resforward3d, SPEC.md:155 + SPEC.md:173)
+//   K3 k_backward  backward substitution + phi update          wavefront, bulk-copy ring
+//                  (backward3d)
+//   K4 k_face_copy face-halo copies / pack / unpack (exvec)
+//   K5 k_convert   fp64 -> fp32 (Field3::cast, field.hpp:61-68)
+//   K7 k_scatter / k_gather / k_ghost_in   Field3 <-> tile-slice layout
+//
+// Wavefront scheme: a CTA owns a 16x16-column tile and walks the
+// tile's hyperplanes t = k + ti + tj.  Inside a tile the W/S neighbours of a
+// cell were produced one step earlier by neighbouring threads (double-buffered
+// shared memory, one __syncthreads per step); the B neighbour is the thread's
+// own previous value (register).  Across tiles, values travel through L2 and
+// each tile publishes a monotone progress counter (release/acquire), so there
+// is no grid-wide barrier: upstream tiles run ahead and the hand-off latency
+// becomes pipeline skew.  Tiles are claimed through an atomic ticket in
+// topological order, so the kernel is deadlock-free for any residency.
+//
+// Bitwise parity: every cell performs the oracle's operations in the oracle's
+// order (oracle/sip_oracle.c header); this file is compiled with
+// --fmad=false and IEEE division, so no contraction changes the rounding.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sip_internal.h"
+
+namespace sipb {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = saddr(b);
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_relaxed(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// thread position p -> (ti, tj) of the anti-diagonal numbering
+__device__ __forceinline__ void pos_to_tij(int p, int& ti, int& tj) {
+  int d = 0;
+  while (diag_off(d + 1) <= p) ++d;
+  const int lo = d - (kTJ - 1) > 0 ? d - (kTJ - 1) : 0;
+  ti = lo + (p - diag_off(d));
+  tj = d - ti;
+}
+
+// Valid cell range [lo, hi) of slice t in a tile of nz planes, widened to 16 B.
+template <typename T>
+__device__ __forceinline__ void slice_range(int t, int nz, int& lo, int& hi) {
+  constexpr int EPV = 16 / sizeof(T);
+  const int dlo = t - nz + 1 > 0 ? t - nz + 1 : 0;
+  const int dhi = t < kD - 1 ? t : kD - 1;  // inclusive
+  lo = diag_off(dlo) & ~(EPV - 1);
+  hi = (diag_off(dhi + 1) + EPV - 1) & ~(EPV - 1);
+  if (hi > kTT) hi = kTT;
+}
+
+// Copy `na` arrays of one slice (pack stride na*TT) into smem (stride TT).
+template <typename T>
+__device__ __forceinline__ uint32_t issue_slice(T* dst, const T* src, int na, int t, int nz,
+                                                uint64_t* bar, bool arm, uint32_t extra_tx) {
+  int lo, hi;
+  slice_range<T>(t, nz, lo, hi);
+  const uint32_t bytes = static_cast<uint32_t>(na * (hi - lo) * sizeof(T));
+  if (arm) mbar_expect_tx(bar, bytes + extra_tx);
+  if (lo == 0 && hi == kTT) {
+    bulk_g2s(dst, src, bytes, bar);
+  } else {
+    for (int a = 0; a < na; ++a)
+      bulk_g2s(dst + a * kTT + lo, src + a * kTT + lo, static_cast<uint32_t>((hi - lo) * sizeof(T)),
+               bar);
+  }
+  return bytes;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t slice_bytes(int t, int nz, int na) {
+  int lo, hi;
+  slice_range<T>(t, nz, lo, hi);
+  return static_cast<uint32_t>(na * (hi - lo) * sizeof(T));
+}
+
+// Deterministic CTA sum (fixed xor-tree per warp, warps summed in order).
+__device__ __forceinline__ double cta_sum(double v, double* s_red) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) s_red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int x = 0; x < (int)(blockDim.x >> 5); ++x) s += s_red[x];
+  return s;  // valid on thread 0
+}
+
+constexpr int kProgOff = 32;  // state layout: [0] ticket, [1] done, progress at +32
+
+// =============================================================================
+// K1: Stone factorisation (fp64), SPEC.md:146 -- once per system revision.
+// =============================================================================
+__global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
+  __shared__ double s_U[2][3][kTT];
+  __shared__ int s_tile;
+  const int p = threadIdx.x;
+  int ti, tj;
+  pos_to_tij(p, ti, tj);
+  const int d = ti + tj;
+  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : p;
+  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : p;
+  unsigned* const prog = P.state + kProgOff;
+  const double alpha = P.alpha;
+
+  for (;;) {
+    __syncthreads();
+    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= P.ntiles) break;
+    const int tid = P.order[tk];
+    const TileDesc td = P.tiles[tid];
+    const BlockDesc bd = P.blocks[td.block];
+    const int NS = td.ns, nz = td.nz;
+    const bool col = ti < td.wI && tj < td.wJ;
+    const bool inW = ti > 0, inS = tj > 0;
+    const long long slotW = td.nW >= 0 ? P.tiles[td.nW].slot : 0;
+    const long long slotS = td.nS >= 0 ? P.tiles[td.nS].slot : 0;
+    const int posW = tile_pos(kTI - 1, tj), posS = tile_pos(ti, kTJ - 1);
+    double unB = 0.0, ueB = 0.0, utB = 0.0;
+    unsigned cW = 0, cS = 0;
+    for (int t = 0; t < NS; ++t) {
+      __syncthreads();
+      if (p == 0 && t > 0) {
+        __threadfence();
+        st_release(&prog[tid], (unsigned)t);
+      }
+      const int k = t - d;
+      if (col && k >= 0 && k < nz) {
+        double unW = 0.0, ueW = 0.0, utW = 0.0, unS = 0.0, ueS = 0.0, utS = 0.0;
+        if (inW) {
+          const int b = ((t - 1) & 1);
+          unW = s_U[b][0][pW]; ueW = s_U[b][1][pW]; utW = s_U[b][2][pW];
+        } else if (td.nW >= 0) {
+          const unsigned need = min(t + kTI, NS);
+          while (cW < need) cW = ld_acquire(&prog[td.nW]);
+          const long long base = (slotW + k + kTI - 1 + tj) * B_NA * kTT + posW;
+          unW = ld_relaxed(P.bw + base + B_UN * kTT);
+          ueW = ld_relaxed(P.bw + base + B_UE * kTT);
+          utW = ld_relaxed(P.bw + base + B_UT * kTT);
+        }
+        if (inS) {
+          const int b = ((t - 1) & 1);
+          unS = s_U[b][0][pS]; ueS = s_U[b][1][pS]; utS = s_U[b][2][pS];
+        } else if (td.nS >= 0) {
+          const unsigned need = min(t + kTJ, NS);
+          while (cS < need) cS = ld_acquire(&prog[td.nS]);
+          const long long base = (slotS + k + ti + kTJ - 1) * B_NA * kTT + posS;
+          unS = ld_relaxed(P.bw + base + B_UN * kTT);
+          ueS = ld_relaxed(P.bw + base + B_UE * kTT);
+          utS = ld_relaxed(P.bw + base + B_UT * kTT);
+        }
+        double* f = P.fw + (td.slot + t) * F_NA * kTT + p;
+        const double ap = f[F_AP * kTT], aw = f[F_AW * kTT], ae = f[F_AE * kTT];
+        const double as = f[F_AS * kTT], an = f[F_AN * kTT], ab = f[F_AB * kTT];
+        const double at = f[F_AT * kTT];
+        // SPEC.md:146 with m_nb = A_nb, operation order of oracle/sip_oracle.c
+        const double lb = ab / (1.0 + alpha * (unB + ueB));
+        const double lw = aw / (1.0 + alpha * (unW + utW));
+        const double ls = as / (1.0 + alpha * (ueS + utS));
+        const double p1 = alpha * (lb * unB + lw * unW);
+        const double p2 = alpha * (lb * ueB + ls * ueS);
+        const double p3 = alpha * (lw * utW + ls * utS);
+        const double den = ap + p1 + p2 + p3 - lb * utB - lw * ueW - ls * unS;
+        if (!(fabs(den) >= 1e-30)) {
+          const long long c = (long long)(td.i0 + ti + 1) +
+                              (long long)(bd.nx + 2) *
+                                  ((long long)(td.j0 + tj + 1) + (long long)(bd.ny + 2) * (k + 1));
+          atomicMin(P.bad, ((unsigned long long)bd.id << 40) | (unsigned long long)c);
+        }
+        const double lp = 1.0 / den;
+        const double un = (an - p1) * lp, ue = (ae - p2) * lp, ut = (at - p3) * lp;
+        f[F_LB * kTT] = lb;
+        f[F_LW * kTT] = lw;
+        f[F_LS * kTT] = ls;
+        f[F_LP * kTT] = lp;
+        double* u = P.bw + (td.slot + t) * B_NA * kTT + p;
+        u[B_UN * kTT] = un;
+        u[B_UE * kTT] = ue;
+        u[B_UT * kTT] = ut;
+        s_U[t & 1][0][p] = un;
+        s_U[t & 1][1][p] = ue;
+        s_U[t & 1][2][p] = ut;
+        unB = un; ueB = ue; utB = ut;
+      }
+    }
+    __syncthreads();
+    if (p == 0) {
+      __threadfence();
+      st_release(&prog[tid], (unsigned)NS);
+    }
+  }
+}
+
+// =============================================================================
+// K2: fused residual + L1 norm + forward substitution (resforward3d).
+// Per step a tile streams 12 constant arrays (AP..AT, Q, LB, LW, LS, LP) and
+// one phi slice through a bulk-copy ring in shared memory and writes R.
+// =============================================================================
+template <typename T, int SF>
+struct FwdCfg {
+  static constexpr int LA = SF - 1;     // slices of FW prefetched ahead
+  static constexpr int LPH = LA + 1;    // phi is needed one slice earlier (t+1)
+  static constexpr int SP = LPH + 2;    // phi keeps t-1, t, t+1 resident
+  static constexpr size_t bytes =
+      (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) + (SF + SP) * sizeof(uint64_t);
+};
+
+template <typename T, int SF>
+__global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
+  using C = FwdCfg<T, SF>;
+  constexpr int LA = C::LA, LPH = C::LPH, SP = C::SP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* s_fw = reinterpret_cast<T*>(smem);
+  T* s_ph = s_fw + SF * F_NA * kTT;
+  T* s_R = s_ph + SP * kTT;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_R + 2 * kTT);
+  __shared__ int s_tile, s_last;
+  __shared__ double s_red[kTT / 32];
+
+  const int p = threadIdx.x;
+  int ti, tj;
+  pos_to_tij(p, ti, tj);
+  const int d = ti + tj;
+  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : p;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
+  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : p;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
+  unsigned* const prog = P.state + kProgOff;
+
+  if (p == 0) {
+    for (int b = 0; b < SF + SP; ++b) mbar_init(&s_bar[b], 1);
+    fence_mbar_init();
+  }
+  uint32_t fq = 0, pq = 0;  // CTA-uniform sequence numbers of issued slices
+
+  for (;;) {
+    __syncthreads();
+    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= P.ntiles) break;
+    const int tid = P.order[tk];
+    const TileDesc td = P.tiles[tid];
+    const BlockDesc bd = P.blocks[td.block];
+    const int NS = td.ns, nz = td.nz;
+    const bool col = ti < td.wI && tj < td.wJ;
+    const int gi = td.i0 + ti, gj = td.j0 + tj;
+    const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
+    const long long slotW = td.nW >= 0 ? P.tiles[td.nW].slot : 0;
+    const long long slotE = td.nE >= 0 ? P.tiles[td.nE].slot : 0;
+    const long long slotS = td.nS >= 0 ? P.tiles[td.nS].slot : 0;
+    const long long slotN = td.nN >= 0 ? P.tiles[td.nN].slot : 0;
+    const int posW = tile_pos(kTI - 1, tj), posE = tile_pos(0, tj);
+    const int posS = tile_pos(ti, kTJ - 1), posN = tile_pos(ti, 0);
+    const T* gW = P.ghost + ghost_face_offset(bd, G_W) + gj;
+    const T* gE = P.ghost + ghost_face_offset(bd, G_E) + gj;
+    const T* gS = P.ghost + ghost_face_offset(bd, G_S) + gi;
+    const T* gN = P.ghost + ghost_face_offset(bd, G_N) + gi;
+    const T* gB = P.ghost + ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj;
+    const T* gT = P.ghost + ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj;
+    const T* fw_src = P.fw + td.slot * F_NA * kTT;
+    const T* ph_src = P.phi + td.slot * kTT;
+
+    const uint32_t fb = fq, pb = pq;
+    fq += NS;
+    pq += NS;
+    if (p == 0) {
+      for (int s = 0; s < LA && s < NS; ++s) {
+        const uint32_t q = fb + s;
+        issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s, nz,
+                       &s_bar[q % SF], true, 0);
+      }
+      for (int s = 0; s < LPH && s < NS; ++s) {
+        const uint32_t q = pb + s;
+        issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s * kTT, 1, s, nz,
+                       &s_bar[SF + q % SP], true, 0);
+      }
+    }
+    T RB = T(0);
+    double nrm = 0.0;
+    unsigned cW = 0, cS = 0;
+    for (int t = 0; t < NS; ++t) {
+      __syncthreads();  // step t-1 complete: R visible, ring slots of t-1 free
+      if (p == 0) {
+        if (t > 0) {
+          __threadfence();
+          st_release(&prog[tid], (unsigned)t);
+        }
+        if (t + LA < NS) {
+          const int s = t + LA;
+          const uint32_t q = fb + s;
+          issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s,
+                         nz, &s_bar[q % SF], true, 0);
+        }
+        if (t + LPH < NS) {
+          const int s = t + LPH;
+          const uint32_t q = pb + s;
+          issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s * kTT, 1, s, nz,
+                         &s_bar[SF + q % SP], true, 0);
+        }
+      }
+      {
+        const uint32_t q = fb + t;
+        mbar_wait(&s_bar[q % SF], (q / SF) & 1);
+      }
+      if (t == 0) mbar_wait(&s_bar[SF + pb % SP], (pb / SP) & 1);
+      if (t + 1 < NS) {
+        const uint32_t q = pb + t + 1;
+        mbar_wait(&s_bar[SF + q % SP], (q / SP) & 1);
+      }
+      const int k = t - d;
+      if (col && k >= 0 && k < nz) {
+        const T* f = s_fw + ((fb + t) % SF) * F_NA * kTT + p;
+        const T* ph0 = s_ph + ((pb + t) % SP) * kTT;
+        const T* phm = s_ph + ((pb + t + SP - 1) % SP) * kTT;
+        const T* php = s_ph + ((pb + t + 1) % SP) * kTT;
+        const T fP = ph0[p];
+        const T fB = k > 0 ? phm[p] : gB[0];
+        const T fT = k + 1 < nz ? php[p] : gT[0];
+        const long long kk = k;
+        const T fW = inW ? phm[pW]
+                         : (td.nW >= 0 ? P.phi[(slotW + k + kTI - 1 + tj) * kTT + posW]
+                                       : gW[(long long)bd.ny * kk]);
+        const T fE = inE ? php[pE]
+                         : (td.nE >= 0 ? P.phi[(slotE + k + tj) * kTT + posE]
+                                       : gE[(long long)bd.ny * kk]);
+        const T fS = inS ? phm[pS]
+                         : (td.nS >= 0 ? P.phi[(slotS + k + ti + kTJ - 1) * kTT + posS]
+                                       : gS[(long long)bd.nx * kk]);
+        const T fN = inN ? php[pN]
+                         : (td.nN >= 0 ? P.phi[(slotN + k + ti) * kTT + posN]
+                                       : gN[(long long)bd.nx * kk]);
+        // residual, Listing-1 term order, a_nb = -A_nb
+        T r = -(f[F_AE * kTT] * fE);
+        r -= f[F_AW * kTT] * fW;
+        r -= f[F_AN * kTT] * fN;
+        r -= f[F_AS * kTT] * fS;
+        r -= f[F_AT * kTT] * fT;
+        r -= f[F_AB * kTT] * fB;
+        r += f[F_Q * kTT];
+        r -= f[F_AP * kTT] * fP;
+        nrm += fabs(static_cast<double>(r));
+        T RW, RS;
+        if (inW) {
+          RW = s_R[((t - 1) & 1) * kTT + pW];
+        } else if (td.nW >= 0) {
+          const unsigned need = min(t + kTI, NS);
+          while (cW < need) cW = ld_acquire(&prog[td.nW]);
+          RW = ld_relaxed(P.R + (slotW + k + kTI - 1 + tj) * kTT + posW);
+        } else {
+          RW = T(0);
+        }
+        if (inS) {
+          RS = s_R[((t - 1) & 1) * kTT + pS];
+        } else if (td.nS >= 0) {
+          const unsigned need = min(t + kTJ, NS);
+          while (cS < need) cS = ld_acquire(&prog[td.nS]);
+          RS = ld_relaxed(P.R + (slotS + k + ti + kTJ - 1) * kTT + posS);
+        } else {
+          RS = T(0);
+        }
+        const T Rv = (((r - f[F_LB * kTT] * RB) - f[F_LW * kTT] * RW) - f[F_LS * kTT] * RS) *
+                     f[F_LP * kTT];
+        RB = Rv;
+        P.R[(td.slot + t) * kTT + p] = Rv;
+        s_R[(t & 1) * kTT + p] = Rv;
+      }
+    }
+    __syncthreads();
+    if (p == 0) {
+      __threadfence();
+      st_release(&prog[tid], (unsigned)NS);
+    }
+    const double s = cta_sum(nrm, s_red);
+    if (p == 0) {
+      P.partial[tid] = s;
+      __threadfence();
+      s_last = (atomicAdd(P.state + 1, 1u) == (unsigned)P.ntiles - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      // finaliser: deterministic per-block norms, then reset the backward state
+      __threadfence();
+      const int w = p >> 5, l = p & 31, nw = blockDim.x >> 5;
+      for (int b = w; b < P.nblocks; b += nw) {
+        const BlockDesc bb = P.blocks[b];
+        double v = 0.0;
+        for (int x = l; x < bb.ntiles; x += 32) v += __ldcg(P.partial + bb.tile0 + x);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (l == 0) P.block_norms[b] = v;
+      }
+      __syncthreads();
+      if (p == 0) {
+        double v = 0.0;
+        for (int b = 0; b < P.nblocks; ++b) v += P.block_norms[b];
+        *P.norm = v;
+      }
+      for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
+    }
+  }
+}
+
+// =============================================================================
+// K3: backward substitution + phi update (backward3d).  Slices in reverse.
+// Ring slot = {R, phi, UN, UE, UT} of one slice.
+// =============================================================================
+template <typename T, int SB>
+struct BwdCfg {
+  static constexpr int LA = SB - 1;
+  static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) + SB * sizeof(uint64_t);
+};
+
+template <typename T, int SB>
+__global__ void __launch_bounds__(kTT, 1) k_backward(const SweepParams<T> P) {
+  constexpr int LA = BwdCfg<T, SB>::LA;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* s_rg = reinterpret_cast<T*>(smem);
+  T* s_D = s_rg + SB * 5 * kTT;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_D + 2 * kTT);
+  __shared__ int s_tile, s_last;
+
+  const int p = threadIdx.x;
+  int ti, tj;
+  pos_to_tij(p, ti, tj);
+  const int d = ti + tj;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
+  unsigned* const prog = P.state + kProgOff;
+
+  if (p == 0) {
+    for (int b = 0; b < SB; ++b) mbar_init(&s_bar[b], 1);
+    fence_mbar_init();
+  }
+  uint32_t q0 = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= P.ntiles) break;
+    const int tid = P.order[tk];
+    const TileDesc td = P.tiles[tid];
+    const int NS = td.ns, nz = td.nz;
+    const bool col = ti < td.wI && tj < td.wJ;
+    const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
+    const long long edgeE = td.nE >= 0 ? P.tiles[td.nE].edge : 0;
+    const long long edgeN = td.nN >= 0 ? P.tiles[td.nN].edge : 0;
+    const bool pubW = (ti == 0 && td.nW >= 0), pubS = (tj == 0 && td.nS >= 0);
+    const T* r_src = P.R + td.slot * kTT;
+    const T* ph_src = P.phi + td.slot * kTT;
+    const T* bw_src = P.bw + td.slot * B_NA * kTT;
+
+    auto issue = [&](int u) {
+      const int t = NS - 1 - u;
+      const uint32_t q = q0 + u;
+      T* dst = s_rg + (q % SB) * 5 * kTT;
+      uint64_t* bar = &s_bar[q % SB];
+      const uint32_t b1 = slice_bytes<T>(t, nz, 1), b3 = slice_bytes<T>(t, nz, B_NA);
+      mbar_expect_tx(bar, 2 * b1 + b3);
+      issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+      issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+      issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false, 0);
+    };
+    const uint32_t qb = q0;
+    if (p == 0)
+      for (int u = 0; u < LA && u < NS; ++u) issue(u);
+    T dT = T(0);
+    unsigned cE = 0, cN = 0;
+    for (int u = 0; u < NS; ++u) {
+      const int t = NS - 1 - u;
+      __syncthreads();
+      if (p == 0) {
+        if (u > 0) {
+          __threadfence();
+          st_release(&prog[tid], (unsigned)u);
+        }
+        if (u + LA < NS) issue(u + LA);
+      }
+      {
+        const uint32_t q = qb + u;
+        mbar_wait(&s_bar[q % SB], (q / SB) & 1);
+      }
+      const int k = t - d;
+      if (col && k >= 0 && k < nz) {
+        const T* sl = s_rg + ((qb + u) % SB) * 5 * kTT + p;
+        T dN, dE;
+        if (inN) {
+          dN = s_D[((u - 1) & 1) * kTT + pN];
+        } else if (td.nN >= 0) {
+          const unsigned need = min(u + kTJ, NS);
+          while (cN < need) cN = ld_acquire(&prog[td.nN]);
+          dN = ld_relaxed(P.edgeS + edgeN + (long long)k * kTI + ti);
+        } else {
+          dN = T(0);
+        }
+        if (inE) {
+          dE = s_D[((u - 1) & 1) * kTT + pE];
+        } else if (td.nE >= 0) {
+          const unsigned need = min(u + kTI, NS);
+          while (cE < need) cE = ld_acquire(&prog[td.nE]);
+          dE = ld_relaxed(P.edgeW + edgeE + (long long)k * kTJ + tj);
+        } else {
+          dE = T(0);
+        }
+        const T dl = ((sl[0] - sl[2 * kTT] * dN) - sl[3 * kTT] * dE) - sl[4 * kTT] * dT;
+        dT = dl;
+        P.phi[(td.slot + t) * kTT + p] = sl[kTT] + dl;
+        s_D[(u & 1) * kTT + p] = dl;
+        if (pubW) P.edgeW[td.edge + (long long)k * kTJ + tj] = dl;
+        if (pubS) P.edgeS[td.edge + (long long)k * kTI + ti] = dl;
+      }
+    }
+    q0 += NS;
+    __syncthreads();
+    if (p == 0) {
+      __threadfence();
+      st_release(&prog[tid], (unsigned)NS);
+      s_last = (atomicAdd(P.state + 1, 1u) == (unsigned)P.ntiles - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
+    }
+  }
+}
+
+// =============================================================================
+// Layout / halo / utility kernels
+// =============================================================================
+__device__ __forceinline__ long long f3(int nx, int ny, int i, int j, int k) {
+  return (long long)i + (long long)(nx + 2) * ((long long)j + (long long)(ny + 2) * k);
+}
+
+template <typename T>
+__global__ void k_scatter(const double* __restrict__ src, const BlockDesc* blocks, int b, T* pack,
+                          int na, int arr) {
+  const BlockDesc bd = blocks[b];
+  const long long n = (long long)bd.nx * bd.ny * bd.nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % bd.nx);
+    const long long r = c / bd.nx;
+    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    pack[pack_index(bd, na, arr, i, j, k)] = static_cast<T>(src[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)]);
+  }
+}
+
+// plane coordinate (x0 fast, x1 slow) of face f -> 1-based Field3 cell
+__device__ __forceinline__ void face_cell(const BlockDesc& bd, int f, int x0, int x1, bool ghost,
+                                          int& i, int& j, int& k) {
+  switch (f) {
+    case G_W: i = ghost ? 0 : 1; j = x0 + 1; k = x1 + 1; break;
+    case G_E: i = ghost ? bd.nx + 1 : bd.nx; j = x0 + 1; k = x1 + 1; break;
+    case G_S: i = x0 + 1; j = ghost ? 0 : 1; k = x1 + 1; break;
+    case G_N: i = x0 + 1; j = ghost ? bd.ny + 1 : bd.ny; k = x1 + 1; break;
+    case G_B: i = x0 + 1; j = x1 + 1; k = ghost ? 0 : 1; break;
+    default: i = x0 + 1; j = x1 + 1; k = ghost ? bd.nz + 1 : bd.nz; break;
+  }
+}
+__device__ __forceinline__ void face_dims(const BlockDesc& bd, int f, int& n0, int& n1) {
+  if (f <= G_E) { n0 = bd.ny; n1 = bd.nz; }
+  else if (f <= G_N) { n0 = bd.nx; n1 = bd.nz; }
+  else { n0 = bd.nx; n1 = bd.ny; }
+}
+
+template <typename T>
+__global__ void k_ghost_in(const double* __restrict__ src, const BlockDesc* blocks, int b, T* ghost) {
+  const BlockDesc bd = blocks[b];
+  const int f = blockIdx.y;
+  int n0, n1;
+  face_dims(bd, f, n0, n1);
+  const long long n = (long long)n0 * n1;
+  T* g = ghost + ghost_face_offset(bd, f);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    int i, j, k;
+    face_cell(bd, f, (int)(c % n0), (int)(c / n0), true, i, j, k);
+    g[c] = static_cast<T>(src[f3(bd.nx, bd.ny, i, j, k)]);
+  }
+}
+
+template <typename T>
+__global__ void k_gather(const T* __restrict__ pack, const T* __restrict__ ghost,
+                         const BlockDesc* blocks, int b, int nbrmask, double* dst) {
+  const BlockDesc bd = blocks[b];
+  const long long n = (long long)bd.nx * bd.ny * bd.nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % bd.nx);
+    const long long r = c / bd.nx;
+    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    dst[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(pack[pack_index(bd, 1, 0, i, j, k)]);
+  }
+  // interface ghosts (faces with a neighbour block): values of the last exchange
+  for (int f = 0; f < 6; ++f) {
+    if (!((nbrmask >> f) & 1)) continue;
+    int n0, n1;
+    face_dims(bd, f, n0, n1);
+    const long long m = (long long)n0 * n1;
+    const T* g = ghost + ghost_face_offset(bd, f);
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < m;
+         c += (long long)gridDim.x * blockDim.x) {
+      int i, j, k;
+      face_cell(bd, f, (int)(c % n0), (int)(c / n0), true, i, j, k);
+      dst[f3(bd.nx, bd.ny, i, j, k)] = static_cast<double>(g[c]);
+    }
+  }
+}
+
+// K4: face copies.  grid.y = copy index.  Source: interior plane `src_face`
+// of local block src_block (phi pack) or buf_in; destination: ghost face
+// dst_face of local block dst_block or buf_out.
+template <typename T>
+__global__ void k_face_copy(const FaceCopy* copies, const BlockDesc* blocks, const T* __restrict__ phi,
+                            T* ghost, const T* buf_in, T* buf_out) {
+  const FaceCopy fc = copies[blockIdx.y];
+  const long long n = (long long)fc.n0 * fc.n1;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int x0 = (int)(c % fc.n0), x1 = (int)(c / fc.n0);
+    T v;
+    if (fc.src_block >= 0) {
+      const BlockDesc sb = blocks[fc.src_block];
+      int i, j, k;
+      face_cell(sb, fc.src_face, x0, x1, false, i, j, k);
+      v = phi[pack_index(sb, 1, 0, i - 1, j - 1, k - 1)];
+    } else {
+      v = buf_in[fc.buf + c];
+    }
+    if (fc.dst_block >= 0) {
+      const BlockDesc db = blocks[fc.dst_block];
+      ghost[ghost_face_offset(db, fc.dst_face) + c] = v;
+    } else {
+      buf_out[fc.buf + c] = v;
+    }
+  }
+}
+
+// residual_general of the device phi, Field3 fp64 output
+template <typename T>
+__global__ void k_residual(const BlockDesc* blocks, int b, const T* __restrict__ fw,
+                           const T* __restrict__ phi, const T* __restrict__ ghost, double* out) {
+  const BlockDesc bd = blocks[b];
+  const long long n = (long long)bd.nx * bd.ny * bd.nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % bd.nx);
+    const long long r = c / bd.nx;
+    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    auto ph = [&](int ii, int jj, int kk) -> T {
+      if (ii < 0) return ghost[ghost_face_offset(bd, G_W) + jj + (long long)bd.ny * kk];
+      if (ii >= bd.nx) return ghost[ghost_face_offset(bd, G_E) + jj + (long long)bd.ny * kk];
+      if (jj < 0) return ghost[ghost_face_offset(bd, G_S) + ii + (long long)bd.nx * kk];
+      if (jj >= bd.ny) return ghost[ghost_face_offset(bd, G_N) + ii + (long long)bd.nx * kk];
+      if (kk < 0) return ghost[ghost_face_offset(bd, G_B) + ii + (long long)bd.nx * jj];
+      if (kk >= bd.nz) return ghost[ghost_face_offset(bd, G_T) + ii + (long long)bd.nx * jj];
+      return phi[pack_index(bd, 1, 0, ii, jj, kk)];
+    };
+    auto A = [&](int arr) -> T { return fw[pack_index(bd, F_NA, arr, i, j, k)]; };
+    T v = -(A(F_AE) * ph(i + 1, j, k));
+    v -= A(F_AW) * ph(i - 1, j, k);
+    v -= A(F_AN) * ph(i, j + 1, k);
+    v -= A(F_AS) * ph(i, j - 1, k);
+    v -= A(F_AT) * ph(i, j, k + 1);
+    v -= A(F_AB) * ph(i, j, k - 1);
+    v += A(F_Q);
+    v -= A(F_AP) * ph(i, j, k);
+    out[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(v);
+  }
+}
+
+__global__ void k_convert(const double* __restrict__ src, float* __restrict__ dst, long long n) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x)
+    dst[c] = static_cast<float>(src[c]);
+}
+
+// Synthetic generator; identical arithmetic to
+// sip_generate_host (sip_gen.cpp).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double u01(uint64_t seed, uint32_t aid, uint64_t cell) {
+  uint64_t h = mix64(seed ^ 0x5851F42D4C957F2DULL);
+  h = mix64(h ^ ((uint64_t)(aid + 1) * 0x9E3779B97F4A7C15ULL));
+  h = mix64(h ^ cell);
+  return (double)(h >> 11) * 0x1.0p-53;
+}
+struct GenArgs {
+  double* out[8];
+  int g[3], o[3];
+  int nx, ny, nz, kind;
+  uint64_t seed;
+};
+__global__ void k_generate(const GenArgs A) {
+  const long long n = (long long)A.nx * A.ny * A.nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % A.nx);
+    const long long r = c / A.nx;
+    const int j = (int)(r % A.ny), k = (int)(r / A.ny);
+    const long long gi = A.o[0] + i, gj = A.o[1] + j, gk = A.o[2] + k;
+    const uint64_t cell = (uint64_t)gi + (uint64_t)A.g[0] * ((uint64_t)gj + (uint64_t)A.g[1] * (uint64_t)gk);
+    double aw, ae, as, an, ab, at;
+    if (A.kind == 2) {
+      const double m = 2.0 * u01(A.seed, 7, cell);
+      ae = -1.0; aw = -1.0 - 1.0 * m;
+      an = -10.0; as = -10.0 - 0.5 * m;
+      at = -100.0; ab = -100.0 - 0.25 * m;
+    } else {
+      aw = -(1.0 + 0.5 * u01(A.seed, 0, cell));
+      ae = -(1.0 + 0.5 * u01(A.seed, 1, cell));
+      as = -(1.0 + 0.5 * u01(A.seed, 2, cell));
+      an = -(1.0 + 0.5 * u01(A.seed, 3, cell));
+      ab = -(1.0 + 0.5 * u01(A.seed, 4, cell));
+      at = -(1.0 + 0.5 * u01(A.seed, 5, cell));
+    }
+    if (gi == 0) aw = 0.0;
+    if (gi == A.g[0] - 1) ae = 0.0;
+    if (gj == 0) as = 0.0;
+    if (gj == A.g[1] - 1) an = 0.0;
+    if (gk == 0) ab = 0.0;
+    if (gk == A.g[2] - 1) at = 0.0;
+    const double s = fabs(aw) + fabs(ae) + fabs(as) + fabs(an) + fabs(ab) + fabs(at);
+    const long long x = f3(A.nx, A.ny, i + 1, j + 1, k + 1);
+    A.out[0][x] = (A.kind == 2) ? s + 1e-3 : 1.01 * s;
+    A.out[1][x] = aw; A.out[2][x] = ae; A.out[3][x] = as;
+    A.out[4][x] = an; A.out[5][x] = ab; A.out[6][x] = at;
+    A.out[7][x] = 2.0 * u01(A.seed, 6, cell) - 1.0;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_for(long long n, int threads = 256) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148LL * 16) g = 148LL * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+static inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? SIP_OK : SIP_ERR_CUDA; }
+
+constexpr int kSF64 = 4, kSF32 = 6;  // forward ring depth (fp64 / fp32)
+constexpr int kSB64 = 6, kSB32 = 8;  // backward ring depth
+
+template <typename T> struct Rings;
+template <> struct Rings<double> { static constexpr int SF = kSF64, SB = kSB64; };
+template <> struct Rings<float> { static constexpr int SF = kSF32, SB = kSB32; };
+
+int launch_factor(const FactorParams& p, int grid, void* stream) {
+  k_factor<<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
+  constexpr int SF = Rings<T>::SF;
+  const size_t smem = FwdCfg<T, SF>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_forward<T, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_forward<T, SF><<<grid, kTT, smem, (cudaStream_t)stream>>>(p);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
+  constexpr int SB = Rings<T>::SB;
+  const size_t smem = BwdCfg<T, SB>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_backward<T, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_backward<T, SB><<<grid, kTT, smem, (cudaStream_t)stream>>>(p);
+  return cuda_status(cudaGetLastError());
+}
+
+int max_resident_ctas(int kind, int precision, int* grid) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaSuccess;
+  if (kind == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_factor, kTT, 0);
+  } else if (kind == 1) {
+    if (precision == SIP_PREC_DOUBLE) {
+      constexpr int SF = Rings<double>::SF;
+      cudaFuncSetAttribute(k_forward<double, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FwdCfg<double, SF>::bytes);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, SF>, kTT,
+                                                        FwdCfg<double, SF>::bytes);
+    } else {
+      constexpr int SF = Rings<float>::SF;
+      cudaFuncSetAttribute(k_forward<float, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)FwdCfg<float, SF>::bytes);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, SF>, kTT,
+                                                        FwdCfg<float, SF>::bytes);
+    }
+  } else {
+    if (precision == SIP_PREC_DOUBLE) {
+      constexpr int SB = Rings<double>::SB;
+      cudaFuncSetAttribute(k_backward<double, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)BwdCfg<double, SB>::bytes);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double, SB>, kTT,
+                                                        BwdCfg<double, SB>::bytes);
+    } else {
+      constexpr int SB = Rings<float>::SB;
+      cudaFuncSetAttribute(k_backward<float, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)BwdCfg<float, SB>::bytes);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float, SB>, kTT,
+                                                        BwdCfg<float, SB>::bytes);
+    }
+  }
+  if (e != cudaSuccess || per < 1) return SIP_ERR_CUDA;
+  *grid = per * sms;
+  return SIP_OK;
+}
+
+template <typename T>
+int launch_scatter(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                   T* pack, int na, int arr, void* stream) {
+  k_scatter<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
+      src, d_blocks, block, pack, na, arr);
+  return cuda_status(cudaGetLastError());
+}
+template <typename T>
+int launch_ghost_in(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                    T* ghost, void* stream) {
+  long long m = (long long)hb.nx * hb.ny;
+  if ((long long)hb.ny * hb.nz > m) m = (long long)hb.ny * hb.nz;
+  if ((long long)hb.nx * hb.nz > m) m = (long long)hb.nx * hb.nz;
+  dim3 g(grid_for(m) / 6 + 1, 6);
+  k_ghost_in<T><<<g, 256, 0, (cudaStream_t)stream>>>(src, d_blocks, block, ghost);
+  return cuda_status(cudaGetLastError());
+}
+template <typename T>
+int launch_gather(const T* pack, const T* ghost, const BlockDesc* d_blocks, int block,
+                  const BlockDesc& hb, const int* nbr6, double* dst, void* stream) {
+  int mask = 0;
+  for (int f = 0; f < 6; ++f)
+    if (nbr6[f] >= 0) mask |= 1 << f;
+  k_gather<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
+      pack, ghost, d_blocks, block, mask, dst);
+  return cuda_status(cudaGetLastError());
+}
+template <typename T>
+int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
+                       const BlockDesc* d_blocks, const T* phi, T* ghost, T* buf_in, T* buf_out,
+                       void* stream) {
+  if (ncopies <= 0) return SIP_OK;
+  int gx = (max_plane + 255) / 256;
+  if (gx > 64) gx = 64;
+  dim3 g(gx, ncopies);
+  k_face_copy<T><<<g, 256, 0, (cudaStream_t)stream>>>(d_copies, d_blocks, phi, ghost, buf_in, buf_out);
+  return cuda_status(cudaGetLastError());
+}
+template <typename T>
+int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
+                    const T* phi, const T* ghost, int symmetric, double* out, void* stream) {
+  (void)symmetric;
+  k_residual<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
+      d_blocks, block, fw, phi, ghost, out);
+  return cuda_status(cudaGetLastError());
+}
+int launch_convert(const double* src, float* dst, long long n, void* stream) {
+  k_convert<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(src, dst, n);
+  return cuda_status(cudaGetLastError());
+}
+int launch_generate(int kind, uint64_t seed, const int g[3], const int o[3], int nx, int ny, int nz,
+                    double* const* out8, void* stream) {
+  GenArgs a;
+  for (int x = 0; x < 8; ++x) a.out[x] = out8[x];
+  for (int x = 0; x < 3; ++x) { a.g[x] = g[x]; a.o[x] = o[x]; }
+  a.nx = nx; a.ny = ny; a.nz = nz; a.kind = kind; a.seed = seed;
+  k_generate<<<grid_for((long long)nx * ny * nz), 256, 0, (cudaStream_t)stream>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+#define SIPB_INST(T)                                                                              \
+  template int launch_forward<T>(const SweepParams<T>&, int, void*);                              \
+  template int launch_backward<T>(const SweepParams<T>&, int, void*);                             \
+  template int launch_scatter<T>(const double*, const BlockDesc*, int, const BlockDesc&, T*, int, \
+                                 int, void*);                                                     \
+  template int launch_ghost_in<T>(const double*, const BlockDesc*, int, const BlockDesc&, T*,     \
+                                  void*);                                                         \
+  template int launch_gather<T>(const T*, const T*, const BlockDesc*, int, const BlockDesc&,      \
+                                const int*, double*, void*);                                      \
+  template int launch_face_copies<T>(const FaceCopy*, int, int, const BlockDesc*, const T*, T*,   \
+                                     T*, T*, void*);                                              \
+  template int launch_residual<T>(const BlockDesc*, int, const BlockDesc&, const T*, const T*,    \
+                                  const T*, int, double*, void*);
+SIPB_INST(double)
+SIPB_INST(float)
+
+}  // namespace sipb

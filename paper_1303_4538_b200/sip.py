@@ -1,0 +1,404 @@
+"""Python mirror of the reference's sip module interface on
+top of the B200 C-ABI library (include/sip_c.h, libsip_b200.so).
+
+Names, argument meaning and error behaviour follow the specification:
+
+    StencilSystem   -> StencilSystem
+    SipFactors   -> SipFactors (device-resident, stamped)
+    SipConfig   -> SipConfig
+    SolveReport   -> SolveReport
+    sip_factor   -> sip_factor
+    residual_general -> residual_general
+    sip_sweep   -> sip_sweep
+    solve   -> solve
+    errors         (error.hpp:34-50)   -> SingularFactorError, StaleFactorsError, MisuseError
+
+Arrays are numpy float64 Field3 arrays (proj/include/bsfv/field.hpp:25-44):
+shape (nz+2, ny+2, nx+2), i fastest, interior 1..n.  Coefficients use the
+matrix-entry sign convention (A_nb = -a_nb).
+
+There is no CPU fallback: every operation runs the sm_100a kernels; when the
+shared library or a CUDA device is missing the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import time
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsip_b200.so")
+
+SIP_OK, SIP_ERR_SINGULAR, SIP_ERR_STALE, SIP_ERR_MISUSE = 0, 1, 2, 3
+SIP_ERR_CONFIG, SIP_ERR_CUDA, SIP_ERR_NCCL, SIP_ERR_NOMEM = 4, 5, 6, 7
+PREC = {"f64": 0, "double": 0, "f32": 1, "single": 1}
+
+ARRAYS = ("AP", "AW", "AE", "AS", "AN", "AB", "AT", "Q")
+
+# Exported symbols declared by include/sip_c.h (checked by the CPU tests).
+EXPORTS = (
+    "sip_version", "sip_status_string", "sip_last_error", "sip_create", "sip_create_lattice",
+    "sip_destroy", "sip_num_local_blocks", "sip_local_block", "sip_set_system", "sip_set_source",
+    "sip_generate_system", "sip_factor", "sip_solve", "sip_load_phi", "sip_store_phi",
+    "sip_iterate", "sip_read_norms", "sip_synchronize", "sip_residual", "sip_set_stream",
+    "sip_get_stream", "sip_set_profiling", "sip_get_profile", "sip_launch_count", "sip_geometry",
+    "sip_nccl_unique_id", "sip_generate_host", "sip_plan_block_ranks", "sip_plan_halo",
+)
+
+
+class Error(RuntimeError):
+    """bsfv::Error (error.hpp:10-14)."""
+
+
+class ConfigError(Error):
+    """bsfv::ConfigError (error.hpp:16-19)."""
+
+
+class SingularFactorError(Error):
+    """bsfv::SingularFactorError (error.hpp:34-37): names the cell."""
+
+
+class StaleFactorsError(Error):
+    """bsfv::StaleFactorsError (error.hpp:40-43)."""
+
+
+class MisuseError(Error):
+    """bsfv::MisuseError (error.hpp:47-50)."""
+
+
+_EXC = {SIP_ERR_SINGULAR: SingularFactorError, SIP_ERR_STALE: StaleFactorsError,
+        SIP_ERR_MISUSE: MisuseError, SIP_ERR_CONFIG: ConfigError}
+
+_lib = None
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def lib():
+    """Load libsip_b200.so (built by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        L.sip_version.restype = ctypes.c_char_p
+        L.sip_status_string.restype = ctypes.c_char_p
+        L.sip_last_error.restype = ctypes.c_char_p
+        L.sip_last_error.argtypes = [ctypes.c_void_p]
+        L.sip_get_stream.restype = ctypes.c_void_p
+        L.sip_get_stream.argtypes = [ctypes.c_void_p]
+        L.sip_launch_count.restype = ctypes.c_longlong
+        L.sip_launch_count.argtypes = [ctypes.c_void_p]
+        for name in ("sip_destroy", "sip_synchronize"):
+            getattr(L, name).argtypes = [ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(ctx, status: int, what: str):
+    if status == SIP_OK:
+        return
+    msg = lib().sip_last_error(ctx).decode(errors="replace") if True else ""
+    cls = _EXC.get(status, Error)
+    raise cls(f"{what}: {lib().sip_status_string(status).decode()}: {msg}")
+
+
+def _ptr(a: np.ndarray):
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise MisuseError("arrays must be C-contiguous float64 Field3 arrays")
+    return a.ctypes.data_as(_dp)
+
+
+def field(nx: int, ny: int, nz: int) -> np.ndarray:
+    """Zero Field3 array (one ghost layer)."""
+    return np.zeros((nz + 2, ny + 2, nx + 2), dtype=np.float64)
+
+
+# ----------------------------------------------------------------- types
+@dataclasses.dataclass
+class StencilSystem:
+    """Seven diagonals + source of one block, matrix-entry signs."""
+    AP: np.ndarray
+    AW: np.ndarray
+    AE: np.ndarray
+    AS: np.ndarray
+    AN: np.ndarray
+    AB: np.ndarray
+    AT: np.ndarray
+    Q: np.ndarray
+    symmetric: bool = False
+
+    @property
+    def dims(self):
+        nz, ny, nx = (s - 2 for s in self.AP.shape)
+        return nx, ny, nz
+
+    def arrays(self):
+        return [getattr(self, n) for n in ARRAYS]
+
+    @classmethod
+    def from_dict(cls, d: dict, symmetric: bool = False) -> "StencilSystem":
+        return cls(*(np.ascontiguousarray(d[n], dtype=np.float64) for n in ARRAYS),
+                   symmetric=symmetric)
+
+
+@dataclasses.dataclass
+class SipConfig:
+    """alpha in [0,1), max_iters >= 1, target reduction, precision."""
+    alpha: float = 0.92
+    max_iters: int = 50
+    target: float = 0.0          # <= 0: fixed iteration count
+    precision: str = "f64"       # "f64" | "f32" (single-precision relaxation)
+
+    def validate(self):
+        if not (0.0 <= self.alpha < 1.0):
+            raise ConfigError("alpha must be in [0, 1)")
+        if self.max_iters < 1:
+            raise ConfigError("max_iters must be >= 1")
+        if self.precision not in PREC:
+            raise ConfigError(f"unknown precision {self.precision!r}")
+
+
+@dataclasses.dataclass
+class SolveReport:
+    """SPEC.md:128-131."""
+    iterations: int
+    norms: np.ndarray
+    factor_seconds: float = 0.0
+    relax_seconds: float = 0.0
+
+    @property
+    def initial_norm(self):
+        return float(self.norms[0]) if len(self.norms) else 0.0
+
+    @property
+    def final_norm(self):
+        return float(self.norms[-1]) if len(self.norms) else 0.0
+
+
+# ----------------------------------------------------------------- device context
+class Solver:
+    """One C-ABI context: a single block (dims) or a block lattice."""
+
+    def __init__(self, dims=None, precision: str = "f64", device: int = 0, *, lattice=None,
+                 block_rank: Optional[Sequence[int]] = None, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        L = lib()
+        self._ctx = ctypes.c_void_p()
+        p = PREC[precision]
+        self.precision = precision
+        if lattice is None:
+            nx, ny, nz = dims
+            st = L.sip_create(device, nx, ny, nz, p, ctypes.byref(self._ctx))
+        else:
+            (gx, gy, gz), (px, py, pz) = lattice
+            br = None
+            if block_rank is not None:
+                br = (ctypes.c_int * len(block_rank))(*block_rank)
+            nid = None if nccl_id is None else ctypes.create_string_buffer(nccl_id, 128)
+            st = L.sip_create_lattice(device, gx, gy, gz, px, py, pz, br, rank, nranks, nid, p,
+                                      ctypes.byref(self._ctx))
+        if st != SIP_OK:
+            raise _EXC.get(st, Error)(
+                f"sip_create: {L.sip_status_string(st).decode()}: {L.sip_last_error(None).decode()}")
+        n = ctypes.c_int()
+        L.sip_num_local_blocks(self._ctx, ctypes.byref(n))
+        self.blocks = []
+        for lb in range(n.value):
+            bid = ctypes.c_int()
+            d = (ctypes.c_int * 3)()
+            o = (ctypes.c_int * 3)()
+            L.sip_local_block(self._ctx, lb, ctypes.byref(bid), d, o)
+            self.blocks.append((bid.value, tuple(d), tuple(o)))
+
+    # -- plumbing
+    @property
+    def handle(self):
+        return self._ctx
+
+    def close(self):
+        if self._ctx:
+            lib().sip_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, st, what):
+        _check(self._ctx, st, what)
+
+    # -- system / factor
+    def set_system(self, local: int, A: StencilSystem):
+        self._c(lib().sip_set_system(self._ctx, local, *[_ptr(a) for a in A.arrays()]),
+                "sip_set_system")
+
+    def set_source(self, local: int, q: np.ndarray):
+        self._c(lib().sip_set_source(self._ctx, local, _ptr(q)), "sip_set_source")
+
+    def generate(self, kind: int, seed: int):
+        self._c(lib().sip_generate_system(self._ctx, kind, ctypes.c_uint64(seed)),
+                "sip_generate_system")
+
+    def factor(self, alpha: float):
+        bb, bc = ctypes.c_longlong(-1), ctypes.c_longlong(-1)
+        st = lib().sip_factor(self._ctx, ctypes.c_double(alpha), ctypes.byref(bb), ctypes.byref(bc))
+        if st == SIP_ERR_SINGULAR:
+            raise SingularFactorError(
+                f"singular factorization at block {bb.value}, Field3 index {bc.value}")
+        self._c(st, "sip_factor")
+
+    # -- relaxation
+    def _phis(self, phis):
+        arr = (_dp * len(phis))(*[_ptr(p) for p in phis])
+        return arr
+
+    def solve(self, phis: Sequence[np.ndarray], max_iters: int, target: float = 0.0):
+        norms = np.zeros(max(max_iters, 1))
+        used = ctypes.c_int(0)
+        self._c(lib().sip_solve(self._ctx, self._phis(phis), max_iters, ctypes.c_double(target),
+                                norms.ctypes.data_as(_dp), ctypes.byref(used)), "sip_solve")
+        return norms[:used.value]
+
+    def load_phi(self, phis):
+        self._c(lib().sip_load_phi(self._ctx, self._phis(phis)), "sip_load_phi")
+
+    def store_phi(self, phis):
+        self._c(lib().sip_store_phi(self._ctx, self._phis(phis)), "sip_store_phi")
+
+    def iterate(self, iters: int):
+        self._c(lib().sip_iterate(self._ctx, iters), "sip_iterate")
+
+    def read_norms(self, first: int, count: int, per_block: bool = False):
+        n = np.zeros(max(count, 1))
+        nb = self.num_global_blocks() if per_block else 0
+        bn = np.zeros((max(count, 1), max(nb, 1)))
+        self._c(lib().sip_read_norms(self._ctx, first, count, n.ctypes.data_as(_dp),
+                                     bn.ctypes.data_as(_dp) if per_block else None),
+                "sip_read_norms")
+        return (n[:count], bn[:count]) if per_block else n[:count]
+
+    def num_global_blocks(self):
+        return self._nglobal if hasattr(self, "_nglobal") else len(self.blocks)
+
+    def synchronize(self):
+        self._c(lib().sip_synchronize(self._ctx), "sip_synchronize")
+
+    def residual(self, symmetric: bool = False):
+        outs = [field(*d) for (_, d, _) in self.blocks]
+        self._c(lib().sip_residual(self._ctx, int(symmetric), self._phis(outs)), "sip_residual")
+        return outs
+
+    # -- measurement helpers
+    def set_stream(self, stream_ptr: int):
+        self._c(lib().sip_set_stream(self._ctx, ctypes.c_void_p(stream_ptr)), "sip_set_stream")
+
+    def set_profiling(self, on: bool):
+        self._c(lib().sip_set_profiling(self._ctx, int(on)), "sip_set_profiling")
+
+    def profile(self):
+        f, b, h = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        n = ctypes.c_longlong()
+        self._c(lib().sip_get_profile(self._ctx, ctypes.byref(f), ctypes.byref(b), ctypes.byref(h),
+                                      ctypes.byref(n)), "sip_get_profile")
+        return {"fwd_ms": f.value, "bwd_ms": b.value, "halo_ms": h.value, "launches": n.value}
+
+    def launch_count(self) -> int:
+        return int(lib().sip_launch_count(self._ctx))
+
+    def geometry(self):
+        ti, tj = ctypes.c_int(), ctypes.c_int()
+        nt, ns = ctypes.c_longlong(), ctypes.c_longlong()
+        lib().sip_geometry(self._ctx, ctypes.byref(ti), ctypes.byref(tj), ctypes.byref(nt),
+                           ctypes.byref(ns))
+        return {"ti": ti.value, "tj": tj.value, "tiles": nt.value, "slices": ns.value}
+
+
+# ----------------------------------------------------------------- SPEC operations
+class SipFactors:
+    """Factors of one StencilSystem, resident on the device and stamped with
+    the system revision they were computed from."""
+
+    def __init__(self, solver: Solver, system: StencilSystem, alpha: float, revision: int):
+        self.solver = solver
+        self.system = system
+        self.alpha = alpha
+        self.revision = revision
+        self.precision = solver.precision
+
+
+_factor_count = 0
+
+
+def factorization_count() -> int:
+    """Number of sip_factor calls made through this module (work-avoidance check)."""
+    return _factor_count
+
+
+def sip_factor(A: StencilSystem, cfg: SipConfig, device: int = 0) -> SipFactors:
+    """SPEC.md:143-151.  Raises SingularFactorError naming the cell."""
+    global _factor_count
+    cfg.validate()
+    s = Solver(A.dims, cfg.precision, device)
+    s.set_system(0, A)
+    s.factor(cfg.alpha)
+    _factor_count += 1
+    return SipFactors(s, A, cfg.alpha, _revision(A))
+
+
+def _revision(A: StencilSystem) -> int:
+    # content stamp of the coefficient arrays (the source Q may change freely)
+    h = 0
+    for a in A.arrays()[:7]:
+        h = hash((h, a.tobytes()[:4096], a.sum()))
+    return h
+
+
+def residual_general(A: StencilSystem, fi: np.ndarray, device: int = 0) -> np.ndarray:
+    """res = sum a_nb*fi_nb + su - ap*fi at interior cells."""
+    s = Solver(A.dims, "f64", device)
+    s.set_system(0, A)
+    s.load_phi([np.ascontiguousarray(fi, dtype=np.float64)])
+    return s.residual()[0]
+
+
+def sip_sweep(A: StencilSystem, F: SipFactors, fi: np.ndarray) -> float:
+    """one iteration in place on fi; returns the L1 norm."""
+    if _revision(A) != F.revision:
+        raise StaleFactorsError("factors were computed from a different system revision")
+    s = F.solver
+    s.set_source(0, A.Q)
+    norms = s.solve([fi], 1, 0.0)
+    return float(norms[0])
+
+
+def solve(A: StencilSystem, fi0: np.ndarray, cfg: SipConfig, F: Optional[SipFactors] = None):
+    """SPEC.md:179-187.  Returns (fi, SolveReport); factorises at most once
+    (zero times on the reuse path, when F is given and its stamp matches)."""
+    cfg.validate()
+    fi = np.array(fi0, dtype=np.float64, copy=True, order="C")
+    t0 = time.perf_counter()
+    if F is None:
+        F = sip_factor(A, cfg)
+    elif _revision(A) != F.revision:
+        raise StaleFactorsError("factors were computed from a different system revision")
+    elif F.precision != cfg.precision:
+        raise MisuseError("factors were computed for another precision")
+    t1 = time.perf_counter()
+    if cfg.target >= 1.0:
+        return fi, SolveReport(0, np.zeros(0), t1 - t0, 0.0)
+    F.solver.set_source(0, A.Q)
+    norms = F.solver.solve([fi], cfg.max_iters, cfg.target)
+    t2 = time.perf_counter()
+    return fi, SolveReport(len(norms), norms, t1 - t0, t2 - t1)
+
+
+def version() -> str:
+    return lib().sip_version().decode()
