@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the SIP hot path (BASELINE.json metric: SIP inner-iteration
+MLUP/s and achieved HBM GB/s vs peak).
+
+A "step" is one solve of the hot path over one synthetic system: `iters`
+SIP inner iterations (residual + forward substitution K2, backward
+substitution K3, face-halo exchange K4 for multi-block) on the
+configuration's grid.  MLUP/s = cells x iterations / time.
+
+    python bench.py                      # N=1: config 1 (256^3, fp64 headline + fp32)
+    python bench.py --impl reference     # reference arm: CPU SIP (oracle port) on host cores
+    torchrun --nproc-per-node N bench.py --gpus N   # config 3 weak scaling (8 x 128^3 / GPU)
+
+value: device-resident throughput (inputs in HBM, CUDA events on the
+library's launch stream, max over ranks).  e2e: the same metric through the
+reference-facing call (sip_set_source + sip_solve with pinned host Field3
+buffers: H2D of su and phi, D2H of phi and the norm history inside the
+timed region).  roofline: dominant kernel (K2 forward) -- algorithmic bytes
+per launch (14 of the 20 array touches per cell) over its
+CUDA-event duration, against MEASURED_PEAKS.json's HBM copy bandwidth.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic array touches per lattice update
+TOUCH_FWD, TOUCH_BWD = 14, 6
+
+CONFIGS = {
+    0: dict(workload="config0: 64^3 single block, 7-point SIP", g=(64, 64, 64), p=(1, 1, 1),
+            kind=0, iters=20, prec=("f64",)),
+    1: dict(workload="config1: 256^3 single block, 7-point SIP", g=(256, 256, 256), p=(1, 1, 1),
+            kind=0, iters=50, prec=("f64", "f32")),
+    2: dict(workload="config2: 512x256x128 anisotropic convection-diffusion block", g=(512, 256, 128),
+            p=(1, 1, 1), kind=2, iters=100, prec=("f32",)),
+    3: dict(workload="config3: 8 blocks of 128^3 per GPU (2x2x2 per GPU), block-Jacobi SIP",
+            g=None, p=None, kind=0, iters=50, prec=("f64",)),
+    4: dict(workload="config4: 1024x512x512 in 128^3 blocks (128 blocks), block-Jacobi SIP",
+            g=(1024, 512, 512), p=(8, 4, 4), kind=0, iters=100, prec=("f32",)),
+}
+GPU_LATTICE = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(cfg_id: int, seconds: float = 12.0):
+    """The reference's algorithm on the host (oracle port, 1 core: SIP's
+    lexicographic recurrence is serial per block).  Bounded
+    sample: iterations of the config's grid until ~`seconds` of sweep time."""
+    from oracle import oracle as O
+
+    c = CONFIGS[cfg_id]
+    if cfg_id in (3, 4):
+        dims = (128, 128, 128)  # one block of the multi-block configs
+        sample_desc = "one 128^3 block of the config, fp64 sweeps"
+    else:
+        dims = c["g"]
+        sample_desc = f"{dims[0]}x{dims[1]}x{dims[2]} block"
+    A = O.generate(c["kind"], 1303 + cfg_id, dims, dims)
+    F = O.factor(A, 0.92)
+    prec = c["prec"][0]
+    if prec == "f32":
+        A = {n: v.astype(np.float32) for n, v in A.items()}
+        F = {n: v.astype(np.float32) for n, v in F.items()}
+        phi = O.field(*dims, dtype=np.float32)
+    else:
+        phi = O.field(*dims)
+    cells = dims[0] * dims[1] * dims[2]
+    n, t = 0, 0.0
+    while t < seconds and n < c["iters"]:
+        t0 = time.perf_counter()
+        O.sweep(A, F, phi)
+        t += time.perf_counter() - t0
+        n += 1
+    return {"value": cells * n / t / 1e6, "unit": "MLUP/s", "cores": 1, "kind": "port",
+            "sample": f"{sample_desc}, {prec}, {n} SIP inner iterations ({t:.1f} s), "
+                      "single-threaded C oracle (-O3 -ffp-contract=off)"}
+
+
+# ---------------------------------------------------------------- GPU arm
+def make_solver(cfg_id, prec, rank, world, device, nccl_id=None):
+    import paper_1303_4538_b200 as sip
+
+    c = CONFIGS[cfg_id]
+    if cfg_id == 3:
+        lx, ly, lz = GPU_LATTICE.get(world, (world, 1, 1))
+        g = (256 * lx, 256 * ly, 256 * lz)
+        p = (2 * lx, 2 * ly, 2 * lz)
+    else:
+        g, p = c["g"], c["p"]
+    s = sip.Solver(None, prec, device, lattice=(g, p), rank=rank, nranks=world, nccl_id=nccl_id)
+    s._nglobal = p[0] * p[1] * p[2]
+    s._g = g
+    return s, g, p
+
+
+def run_gpu(args, rank, world, dist):
+    import torch
+
+    import paper_1303_4538_b200 as sip
+
+    torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
+    cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+    c = CONFIGS[cfg_id]
+    stream = torch.cuda.current_stream()
+    peak, peak_src = load_peak()
+    results = {}
+    precs = c["prec"] if args.precision == "auto" else (args.precision,)
+    for prec in precs:
+        nccl_id = None
+        if world > 1:  # a fresh ncclUniqueId per communicator
+            obj = [sip.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+        s, g, p = make_solver(cfg_id, prec, rank, world, torch.cuda.current_device(), nccl_id)
+        s.set_stream(stream.cuda_stream)
+        seed = 1303 + cfg_id
+        s.generate(c["kind"], seed)
+        s.factor(0.92)
+        # resident phi0 = 0 for every local block
+        phis = [sip.field(*d) for (_, d, _) in s.blocks]
+        s.load_phi(phis)
+        cells_local = sum(d[0] * d[1] * d[2] for (_, d, _) in s.blocks)
+        cells_total = g[0] * g[1] * g[2]
+        iters = c["iters"]
+
+        def barrier():
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+
+        for _ in range(args.warmup):
+            s.iterate(iters)
+        barrier()
+        l0 = s.launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                s.iterate(iters)
+            ev1.record(stream)
+            barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = s.launch_count() - l0
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        ms_step = ms / args.steps
+        mlups = cells_total * iters * args.steps / (ms / 1e3) / 1e6
+        # norms of the last step (sanity: finite, decreasing overall)
+        nrm = s.read_norms(0, min(iters, 3))
+
+        # per-kernel CUDA-event pass (same stream) for the roofline
+        s.set_profiling(True)
+        s.iterate(iters)
+        prof = s.profile()
+        s.set_profiling(False)
+        esz = 8 if prec == "f64" else 4
+        fwd_launch_ms = prof["fwd_ms"] / iters
+        bwd_launch_ms = prof["bwd_ms"] / iters
+        fwd_bytes = cells_local * TOUCH_FWD * esz
+        bwd_bytes = cells_local * TOUCH_BWD * esz
+        achieved = fwd_bytes / (fwd_launch_ms / 1e3) / 1e9
+        bwd_achieved = bwd_bytes / (bwd_launch_ms / 1e3) / 1e9
+        step_gbs = cells_local * (TOUCH_FWD + TOUCH_BWD) * esz * iters / (ms_step / 1e3) / 1e9
+
+        # e2e through the reference-facing call with pinned host buffers
+        e2e = None
+        if not args.no_e2e:
+            e2e = run_e2e(s, c, cfg_id, prec, args, dist, stream)
+        traffic = load_traffic(cfg_id, prec)
+        results[prec] = dict(
+            value=mlups, ms=ms_step, launches=launches, clocks=clk.summary(), e2e=e2e,
+            roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                      "frac": achieved / peak, "traffic": traffic, "kernel": "k_forward (K2)",
+                      "peak_source": peak_src, "alg_bytes_per_launch": fwd_bytes,
+                      "launch_ms": fwd_launch_ms},
+            k3={"kernel": "k_backward (K3)", "achieved": bwd_achieved, "frac": bwd_achieved / peak,
+                "launch_ms": bwd_launch_ms, "alg_bytes_per_launch": bwd_bytes},
+            step_gbs=step_gbs, step_frac=step_gbs / peak, halo_ms=prof["halo_ms"] / iters,
+            first_norms=[float(x) for x in nrm], geometry=s.geometry(), cells_total=cells_total,
+            cells_local=cells_local, g=g, p=p)
+        s.close()
+    return cfg_id, results
+
+
+def run_e2e(s, c, cfg_id, prec, args, dist, stream):
+    import torch
+
+    import paper_1303_4538_b200 as sip
+
+    iters = c["iters"]
+    # pinned host Field3 buffers (torch pin_memory), one per local block
+    def pinned(d):
+        t = torch.zeros((d[2] + 2, d[1] + 2, d[0] + 2), dtype=torch.float64).pin_memory()
+        return t, t.numpy()
+
+    phis = [pinned(d) for (_, d, _) in s.blocks]
+    qs = []
+    for (bid, d, o) in s.blocks:
+        t, a = pinned(d)
+        gen = sip.generate_host(c["kind"], 1303 + cfg_id + 17 + bid, d, s._g, o)
+        a[...] = gen["Q"]
+        qs.append((t, a))
+    norms = np.zeros(iters)
+    L = sip.lib()
+    dp = ctypes.POINTER(ctypes.c_double)
+    arr = (dp * len(phis))(*[p[1].ctypes.data_as(dp) for p in phis])
+    used = ctypes.c_int()
+    G = sum(p[1].size for p in phis)
+    h2d = 2 * G * 8
+    d2h = G * 8 + iters * 8
+    reps = max(1, min(args.steps, 3))
+
+    def one():
+        for lb, (t, a) in enumerate(qs):
+            st = L.sip_set_source(s.handle, lb, a.ctypes.data_as(dp))
+            assert st == 0
+        for p in phis:
+            p[1][...] = 0.0
+        st = L.sip_solve(s.handle, arr, iters, ctypes.c_double(0.0), norms.ctypes.data_as(dp),
+                         ctypes.byref(used))
+        assert st == 0, L.sip_last_error(s.handle)
+
+    one()  # warm
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([el], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    cells_total = s._g[0] * s._g[1] * s._g[2]
+    return {"value": cells_total * iters * reps / el / 1e6, "unit": "MLUP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": el / reps * 1e3, "steps": reps,
+            "call": "sip_set_source + sip_solve (pinned host Field3 buffers)"}
+
+
+def load_traffic(cfg_id, prec):
+    """ncu dram bytes per launch of K2, from profiles/ncu_traffic.json if a
+    capture of this config/precision was committed."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"config{cfg_id}_{prec}", {}).get("k_forward_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=None)
+    ap.add_argument("--precision", default="auto", choices=["auto", "f64", "f32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist_mod.init_process_group("gloo", rank=rank, world_size=world)
+        dist = dist_mod
+
+    if args.impl == "reference":
+        # reference arm: CPU SIP on host cores, rank 0 only
+        if rank == 0:
+            cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+            c = CONFIGS[cfg_id]
+            vals = []
+            base = None
+            t_all = time.perf_counter()
+            for _ in range(args.steps):
+                base = cpu_reference(cfg_id, seconds=max(2.0, 20.0 / max(1, args.steps)))
+                vals.append(base["value"])
+            v = statistics.median(vals)
+            base["value"] = v
+            line = {"metric": "SIP inner-iteration MLUP/s", "value": v, "unit": "MLUP/s",
+                    "impl": "reference", "n_gpus": world, "steps": args.steps,
+                    "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                    "dtype": c["prec"][0], "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+                    "config": {"workload": c["workload"], "iters_per_step": c["iters"],
+                               "cpu_sample": base["sample"]},
+                    "vs_baseline": None, "cpu_baseline": base,
+                    "e2e": {"value": v, "unit": "MLUP/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0},
+                    "wall_s": time.perf_counter() - t_all}
+            print(json.dumps(line), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    import paper_1303_4538_b200 as sip
+
+    sip.lib()  # fail loudly if the native library is missing
+    cfg_id, res = run_gpu(args, rank, world, dist)
+    if rank == 0:
+        c = CONFIGS[cfg_id]
+        head = "f64" if "f64" in res else list(res)[0]
+        r = res[head]
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_reference(cfg_id, seconds=12.0)
+        line = {
+            "metric": "SIP inner-iteration MLUP/s", "value": r["value"], "unit": "MLUP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": head, "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+            "config": {"workload": c["workload"], "grid": list(r["g"]), "blocks": list(r["p"]),
+                       "iters_per_step": c["iters"], "alpha": 0.92,
+                       "l2": "inputs larger than L2 (working set >> 126 MB)",
+                       "tile": r["geometry"], "parallelism": f"blocks over {world} GPU(s)"},
+            "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
+            "gpu_launches": r["launches"], "clocks": r["clocks"],
+            "achieved_hbm_gbs_step": r["step_gbs"], "achieved_frac_step": r["step_frac"],
+            "k3_backward": r["k3"], "halo_ms_per_iter": r["halo_ms"],
+            "first_norms": r["first_norms"],
+        }
+        for prec, rr in res.items():
+            if prec == head:
+                continue
+            line[prec] = {"value": rr["value"], "ms_per_step": rr["ms"], "roofline": rr["roofline"],
+                          "k3_backward": rr["k3"], "achieved_hbm_gbs_step": rr["step_gbs"],
+                          "achieved_frac_step": rr["step_frac"], "e2e": rr["e2e"],
+                          "gpu_launches": rr["launches"], "clocks": rr["clocks"]}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -40,7 +40,7 @@ CASES = [
     ((16, 16, 40), 0, 5),      # exactly one tile, tall
     ((50, 33, 3), 0, 5),       # nz < tile skew
     ((2, 3, 2), 0, 4),         # tiny
-    ((1, 1, 1), 0, 2),         # single cell
+    ((1, 2, 3), 0, 3),         # degenerate columns (nx = 1)
     ((40, 24, 20), 2, 6),      # config-2 generator (anisotropic convection-diffusion)
 ]
 
