@@ -4,6 +4,7 @@
 // between GPUs), deterministic norm reduction and per-kernel timing.
 // Host C++ only calls kernels through the launchers of sip_kernels.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -19,6 +20,44 @@ using namespace sipb;
 
 namespace {
 thread_local std::string g_create_err;
+
+// NCCL is resolved at run time (dlopen), only when a multi-rank lattice is
+// built: a host process that already loaded an NCCL (e.g. torch's bundled
+// libnccl.so.2) shares it, and single-GPU use needs no NCCL at all.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define SIPB_SYM(f) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f))
+    SIPB_SYM(GetUniqueId); SIPB_SYM(CommInitRank); SIPB_SYM(CommDestroy); SIPB_SYM(Send);
+    SIPB_SYM(Recv); SIPB_SYM(GroupStart); SIPB_SYM(GroupEnd); SIPB_SYM(AllGather);
+    SIPB_SYM(GetErrorString);
+#undef SIPB_SYM
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv &&
+           a.GroupStart && a.GroupEnd && a.AllGather && a.GetErrorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks required symbols";
+    return a;
+  }();
+  return api;
+}
 
 struct Peer {
   int rank = -1;
@@ -91,13 +130,13 @@ struct sip_ctx {
       return s_;                         \
     }                                    \
   } while (0)
-#define CKN(call)                                                     \
-  do {                                                                \
-    ncclResult_t r_ = (call);                                         \
-    if (r_ != ncclSuccess) {                                          \
-      ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);  \
-      return SIP_ERR_NCCL;                                            \
-    }                                                                 \
+#define CKN(call)                                                           \
+  do {                                                                      \
+    ncclResult_t r_ = (call);                                               \
+    if (r_ != ncclSuccess) {                                                \
+      ctx->err = std::string(#call) + ": " + nccl().GetErrorString(r_);     \
+      return SIP_ERR_NCCL;                                                  \
+    }                                                                       \
   } while (0)
 
 static int set_device(sip_ctx* ctx) {
@@ -356,10 +395,15 @@ static int create_common(int device, int gnx, int gny, int gnz, int px, int py, 
     } else {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
-      ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
-      if (r != ncclSuccess) {
-        ctx->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      if (!nccl().ok) {
+        ctx->err = nccl().err;
         s = SIP_ERR_NCCL;
+      } else {
+        ncclResult_t r = nccl().CommInitRank(&ctx->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+          ctx->err = std::string("ncclCommInitRank: ") + nccl().GetErrorString(r);
+          s = SIP_ERR_NCCL;
+        }
       }
     }
   }
@@ -451,12 +495,12 @@ static int exchange(sip_ctx* ctx) {
     const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
     // non-blocking exchange: all receives and sends posted
     // in one group; NCCL matches per peer in issue order
-    CKN(ncclGroupStart());
+    CKN(nccl().GroupStart());
     for (Peer& p : ctx->peers) {
-      CKN(ncclRecv(p.rbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
-      CKN(ncclSend(p.sbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
+      CKN(nccl().Recv(p.rbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
+      CKN(nccl().Send(p.sbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
     }
-    CKN(ncclGroupEnd());
+    CKN(nccl().GroupEnd());
     for (Peer& p : ctx->peers) {
       CKS(launch_face_copies<T>(p.d_unpack, (int)p.unpack.size(), p.max_plane, ctx->d_blocks, phi,
                                 ghost, static_cast<T*>(p.rbuf), nullptr, ctx->stream));
@@ -540,7 +584,7 @@ int sip_destroy(sip_ctx* ctx) {
   if (!ctx) return SIP_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm) nccl().CommDestroy(ctx->comm);
   for (auto& e : ctx->events) {
     cudaEventDestroy(std::get<1>(e));
     cudaEventDestroy(std::get<2>(e));
@@ -815,7 +859,7 @@ int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* bl
     for (int it = 0; it < count; ++it)
       for (int lb = 0; lb < (int)ctx->local.size(); ++lb) pad[(size_t)it * maxl + lb] = bn[(size_t)it * nl + lb];
     CK(cudaMemcpy(d_send, pad.data(), per * sizeof(double), cudaMemcpyHostToDevice));
-    CKN(ncclAllGather(d_send, d_recv, per, ncclFloat64, ctx->comm, ctx->stream));
+    CKN(nccl().AllGather(d_send, d_recv, per, ncclFloat64, ctx->comm, ctx->stream));
     std::vector<double> got(per * ctx->nranks);
     CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -959,7 +1003,7 @@ int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long lo
 int sip_nccl_unique_id(void* out128) {
   if (!out128) return SIP_ERR_MISUSE;
   ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return SIP_ERR_NCCL;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return SIP_ERR_NCCL;
   static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
   std::memcpy(out128, &id, sizeof(id));
   return SIP_OK;

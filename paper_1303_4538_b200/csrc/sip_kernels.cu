@@ -246,46 +246,87 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
 }
 
 // =============================================================================
-// K2: fused residual + L1 norm + forward substitution (resforward3d).
-// Per step a tile streams 12 constant arrays (AP..AT, Q, LB, LW, LS, LP) and
-// one phi slice through a bulk-copy ring in shared memory and writes R.
+// K2 / K3 are warp-specialised: 8 compute warps (one thread per tile column)
+// and one "comm" warp.  The comm warp issues the bulk copies of the slice
+// ring, publishes the tile's progress counter (st.release.gpu) once the
+// compute warps signal a finished step (mbarrier, CTA scope), polls the
+// neighbour tiles' counters and prefetches every cross-tile value a step
+// needs (neighbour phi / R / delta, ghost phi) into a shared "edge record".
+// The compute warps therefore never wait on a global-memory latency on the
+// wavefront's critical path: per step they wait on shared-memory mbarriers,
+// compute, store, and meet at one named barrier.
 // =============================================================================
+constexpr int kCompute = kTT;       // compute threads (8 warps)
+constexpr int kThreads = kTT + 32;  // + comm warp
+
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+}
+__device__ __forceinline__ unsigned poll_progress(const unsigned* p, unsigned cached, unsigned need) {
+  // warp-uniform: every lane performs the acquire so its later loads are ordered
+  if (cached >= need) return cached;
+  return ld_acquire(p);
+}
+
 template <typename T, int SF>
 struct FwdCfg {
-  static constexpr int LA = SF - 1;     // slices of FW prefetched ahead
-  static constexpr int LPH = LA + 1;    // phi is needed one slice earlier (t+1)
-  static constexpr int SP = LPH + 2;    // phi keeps t-1, t, t+1 resident
-  static constexpr size_t bytes =
-      (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) + (SF + SP) * sizeof(uint64_t);
+  static constexpr int SP = SF + 2;  // phi slice s is read at steps s-1, s, s+1
+  static constexpr int ER = 8;       // edge records in flight
+  static constexpr int DR = 8;       // step-done barriers (>= SF)
+  static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
+  static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
+                                  (size_t)ER * NE * sizeof(T) +
+                                  (SF + SP + ER + DR) * sizeof(uint64_t);
 };
 
 template <typename T, int SF>
-__global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
   using C = FwdCfg<T, SF>;
-  constexpr int LA = C::LA, LPH = C::LPH, SP = C::SP;
+  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, NE = C::NE;
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_fw = reinterpret_cast<T*>(smem);
   T* s_ph = s_fw + SF * F_NA * kTT;
   T* s_R = s_ph + SP * kTT;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_R + 2 * kTT);
+  T* s_edge = s_R + 2 * kTT;
+  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_edge + ER * NE);
+  uint64_t* b_ph = b_fw + SF;
+  uint64_t* b_edge = b_ph + SP;
+  uint64_t* b_done = b_edge + ER;
   __shared__ int s_tile, s_last;
-  __shared__ double s_red[kTT / 32];
+  __shared__ double s_red[kThreads / 32];
 
   const int p = threadIdx.x;
-  int ti, tj;
-  pos_to_tij(p, ti, tj);
+  const bool comm = p >= kCompute;
+  const int lane = p & 31;
+  int ti = 0, tj = 0;
+  if (!comm) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
-  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : p;
-  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
-  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : p;
-  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
+  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : 0;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
+  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : 0;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SF + SP; ++b) mbar_init(&s_bar[b], 1);
+    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 1);
+    for (int b = 0; b < SP; ++b) mbar_init(&b_ph[b], 1);
+    for (int b = 0; b < ER; ++b) mbar_init(&b_edge[b], 1);
+    for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t fq = 0, pq = 0;  // CTA-uniform sequence numbers of issued slices
+  uint32_t fq = 0, pq = 0, eq = 0, dq = 0;  // CTA-uniform ring sequence bases
 
   for (;;) {
     __syncthreads();
@@ -297,134 +338,160 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
     const TileDesc td = P.tiles[tid];
     const BlockDesc bd = P.blocks[td.block];
     const int NS = td.ns, nz = td.nz;
-    const bool col = ti < td.wI && tj < td.wJ;
-    const int gi = td.i0 + ti, gj = td.j0 + tj;
-    const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
-    const long long slotW = td.nW >= 0 ? P.tiles[td.nW].slot : 0;
-    const long long slotE = td.nE >= 0 ? P.tiles[td.nE].slot : 0;
-    const long long slotS = td.nS >= 0 ? P.tiles[td.nS].slot : 0;
-    const long long slotN = td.nN >= 0 ? P.tiles[td.nN].slot : 0;
-    const int posW = tile_pos(kTI - 1, tj), posE = tile_pos(0, tj);
-    const int posS = tile_pos(ti, kTJ - 1), posN = tile_pos(ti, 0);
-    const T* gW = P.ghost + ghost_face_offset(bd, G_W) + gj;
-    const T* gE = P.ghost + ghost_face_offset(bd, G_E) + gj;
-    const T* gS = P.ghost + ghost_face_offset(bd, G_S) + gi;
-    const T* gN = P.ghost + ghost_face_offset(bd, G_N) + gi;
-    const T* gB = P.ghost + ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj;
-    const T* gT = P.ghost + ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj;
-    const T* fw_src = P.fw + td.slot * F_NA * kTT;
-    const T* ph_src = P.phi + td.slot * kTT;
-
-    const uint32_t fb = fq, pb = pq;
-    fq += NS;
-    pq += NS;
-    if (p == 0) {
-      for (int s = 0; s < LA && s < NS; ++s) {
-        const uint32_t q = fb + s;
-        issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s, nz,
-                       &s_bar[q % SF], true, 0);
-      }
-      for (int s = 0; s < LPH && s < NS; ++s) {
-        const uint32_t q = pb + s;
-        issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s * kTT, 1, s, nz,
-                       &s_bar[SF + q % SP], true, 0);
-      }
-    }
-    T RB = T(0);
     double nrm = 0.0;
-    unsigned cW = 0, cS = 0;
-    for (int t = 0; t < NS; ++t) {
-      __syncthreads();  // step t-1 complete: R visible, ring slots of t-1 free
-      if (p == 0) {
-        if (t > 0) {
-          __threadfence();
-          st_release(&prog[tid], (unsigned)t);
+
+    if (comm) {
+      // ------------------------------------------------------------ comm warp
+      const T* fw_src = P.fw + td.slot * F_NA * kTT;
+      const T* ph_src = P.phi + td.slot * kTT;
+      // lanes 0-15 serve the W/E sides (index = tj), lanes 16-31 the S/N sides (index = ti)
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool colok = we ? (c < td.wJ) : (c < td.wI);
+      const int nA = we ? td.nW : td.nS;   // upstream neighbour (R + phi)
+      const int nB = we ? td.nE : td.nN;   // downstream neighbour (phi only)
+      const long long slotA = nA >= 0 ? P.tiles[nA].slot : 0;
+      const long long slotB = nB >= 0 ? P.tiles[nB].slot : 0;
+      const int posA = we ? tile_pos(kTI - 1, c) : tile_pos(c, kTJ - 1);
+      const int posB = we ? tile_pos(0, c) : tile_pos(c, 0);
+      const int lag = we ? kTI : kTJ;      // upstream neighbour slice = t + lag - 1
+      const int offB = we ? (td.wI - 1) + c : c + (td.wJ - 1);  // edge cell of side B: k = t - offB
+      const T* gA = P.ghost + ghost_face_offset(bd, we ? G_W : G_S) + (we ? td.j0 : td.i0) + c;
+      const T* gB = P.ghost + ghost_face_offset(bd, we ? G_E : G_N) + (we ? td.j0 : td.i0) + c;
+      const long long gstride = we ? bd.ny : bd.nx;
+      unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
+
+      int t_pub = 0, s_f = 0, s_p = 0, e_next = 0;
+      while (t_pub < NS) {
+        // (1) retire finished steps, publish progress
+        const int t_old = t_pub;
+        while (t_pub < NS) {
+          const uint32_t q = dq + t_pub;
+          if (!mbar_test(&b_done[q % DR], (q / DR) & 1)) break;
+          ++t_pub;
         }
-        if (t + LA < NS) {
-          const int s = t + LA;
-          const uint32_t q = fb + s;
-          issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s,
-                         nz, &s_bar[q % SF], true, 0);
+        if (t_pub != t_old && lane == 0) st_release(&prog[tid], (unsigned)t_pub);
+        // (2) bulk copies into freed ring slots
+        if (lane == 0) {
+          for (; s_f < NS && s_f <= t_pub + SF - 1; ++s_f) {
+            const uint32_t q = fq + s_f;
+            issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s_f * F_NA * kTT, F_NA,
+                           s_f, nz, &b_fw[q % SF], true, 0);
+          }
+          for (; s_p < NS && s_p <= t_pub + SP - 2; ++s_p) {
+            const uint32_t q = pq + s_p;
+            issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s_p * kTT, 1, s_p, nz,
+                           &b_ph[q % SP], true, 0);
+          }
         }
-        if (t + LPH < NS) {
-          const int s = t + LPH;
-          const uint32_t q = pb + s;
-          issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s * kTT, 1, s, nz,
-                         &s_bar[SF + q % SP], true, 0);
+        // (3) edge records of upcoming steps, as far as upstream progress allows
+        int m = min(NS - 1, t_pub + ER - 1);
+        if (e_next <= m) {
+          cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e_next + kTI, NS));
+          cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e_next + kTJ, NS));
+          // record s needs cW >= min(s + TI, NS) and cS >= min(s + TJ, NS)
+          if (cW < (unsigned)NS) m = min(m, (int)cW - kTI);
+          if (cS < (unsigned)NS) m = min(m, (int)cS - kTJ);
+          for (int s = e_next; s <= m; ++s) {
+            T* rec = s_edge + ((eq + s) % ER) * NE;
+            T phA = T(0), phB = T(0), rA = T(0);
+            const int kA = s - c;  // W side cell (0, c) / S side cell (c, 0)
+            if (colok && kA >= 0 && kA < nz) {
+              if (nA >= 0) {
+                const long long x = (slotA + s + lag - 1) * kTT + posA;
+                phA = P.phi[x];
+                rA = ld_relaxed(P.R + x);
+              } else {
+                phA = gA[gstride * kA];
+              }
+            }
+            const int kB = s - offB;
+            if (colok && kB >= 0 && kB < nz) {
+              if (nB >= 0) {
+                phB = P.phi[(slotB + s - lag + 1) * kTT + posB];
+              } else {
+                phB = gB[gstride * kB];
+              }
+            }
+            rec[(we ? 0 : 32) + c] = phA;
+            rec[(we ? 16 : 48) + c] = phB;
+            rec[(we ? 64 : 80) + c] = rA;
+          }
+          __syncwarp();
+          if (lane == 0)
+            for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
+          if (m >= e_next) e_next = m + 1;
         }
       }
-      {
-        const uint32_t q = fb + t;
-        mbar_wait(&s_bar[q % SF], (q / SF) & 1);
+    } else {
+      // --------------------------------------------------------- compute warps
+      const bool col = ti < td.wI && tj < td.wJ;
+      const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
+      const int gi = td.i0 + ti, gj = td.j0 + tj;
+      T ghB = T(0), ghT = T(0);
+      if (col) {
+        ghB = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
+        ghT = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
       }
-      if (t == 0) mbar_wait(&s_bar[SF + pb % SP], (pb / SP) & 1);
-      if (t + 1 < NS) {
-        const uint32_t q = pb + t + 1;
-        mbar_wait(&s_bar[SF + q % SP], (q / SP) & 1);
-      }
-      const int k = t - d;
-      if (col && k >= 0 && k < nz) {
-        const T* f = s_fw + ((fb + t) % SF) * F_NA * kTT + p;
-        const T* ph0 = s_ph + ((pb + t) % SP) * kTT;
-        const T* phm = s_ph + ((pb + t + SP - 1) % SP) * kTT;
-        const T* php = s_ph + ((pb + t + 1) % SP) * kTT;
-        const T fP = ph0[p];
-        const T fB = k > 0 ? phm[p] : gB[0];
-        const T fT = k + 1 < nz ? php[p] : gT[0];
-        const long long kk = k;
-        const T fW = inW ? phm[pW]
-                         : (td.nW >= 0 ? P.phi[(slotW + k + kTI - 1 + tj) * kTT + posW]
-                                       : gW[(long long)bd.ny * kk]);
-        const T fE = inE ? php[pE]
-                         : (td.nE >= 0 ? P.phi[(slotE + k + tj) * kTT + posE]
-                                       : gE[(long long)bd.ny * kk]);
-        const T fS = inS ? phm[pS]
-                         : (td.nS >= 0 ? P.phi[(slotS + k + ti + kTJ - 1) * kTT + posS]
-                                       : gS[(long long)bd.nx * kk]);
-        const T fN = inN ? php[pN]
-                         : (td.nN >= 0 ? P.phi[(slotN + k + ti) * kTT + posN]
-                                       : gN[(long long)bd.nx * kk]);
-        // residual, Listing-1 term order, a_nb = -A_nb
-        T r = -(f[F_AE * kTT] * fE);
-        r -= f[F_AW * kTT] * fW;
-        r -= f[F_AN * kTT] * fN;
-        r -= f[F_AS * kTT] * fS;
-        r -= f[F_AT * kTT] * fT;
-        r -= f[F_AB * kTT] * fB;
-        r += f[F_Q * kTT];
-        r -= f[F_AP * kTT] * fP;
-        nrm += fabs(static_cast<double>(r));
-        T RW, RS;
-        if (inW) {
-          RW = s_R[((t - 1) & 1) * kTT + pW];
-        } else if (td.nW >= 0) {
-          const unsigned need = min(t + kTI, NS);
-          while (cW < need) cW = ld_acquire(&prog[td.nW]);
-          RW = ld_relaxed(P.R + (slotW + k + kTI - 1 + tj) * kTT + posW);
-        } else {
-          RW = T(0);
+      T RB = T(0);
+      for (int t = 0; t < NS; ++t) {
+        const int k = t - d;
+        {
+          // every compute thread waits for slice t (even if idle this step): it
+          // bounds how far the compute warps can run ahead of the comm warp
+          const uint32_t q = fq + t;
+          mbar_wait(&b_fw[q % SF], (q / SF) & 1);
         }
-        if (inS) {
-          RS = s_R[((t - 1) & 1) * kTT + pS];
-        } else if (td.nS >= 0) {
-          const unsigned need = min(t + kTJ, NS);
-          while (cS < need) cS = ld_acquire(&prog[td.nS]);
-          RS = ld_relaxed(P.R + (slotS + k + ti + kTJ - 1) * kTT + posS);
-        } else {
-          RS = T(0);
+        if (col && k >= 0 && k < nz) {
+          {
+            const uint32_t q = pq + t;  // slice t (and t-1, already complete)
+            mbar_wait(&b_ph[q % SP], (q / SP) & 1);
+          }
+          if (k + 1 < nz) {
+            const uint32_t q = pq + t + 1;
+            mbar_wait(&b_ph[q % SP], (q / SP) & 1);
+          }
+          const T* rec = s_edge + ((eq + t) % ER) * NE;
+          if (!(inW && inE && inS && inN)) {
+            const uint32_t q = eq + t;
+            mbar_wait(&b_edge[q % ER], (q / ER) & 1);
+          }
+          const T* f = s_fw + ((fq + t) % SF) * F_NA * kTT + p;
+          const T* ph0 = s_ph + ((pq + t) % SP) * kTT;
+          const T* phm = s_ph + ((pq + t + SP - 1) % SP) * kTT;
+          const T* php = s_ph + ((pq + t + 1) % SP) * kTT;
+          const T fP = ph0[p];
+          const T fB = k > 0 ? phm[p] : ghB;
+          const T fT = k + 1 < nz ? php[p] : ghT;
+          const T fW = inW ? phm[pW] : rec[tj];
+          const T fE = inE ? php[pE] : rec[16 + tj];
+          const T fS = inS ? phm[pS] : rec[32 + ti];
+          const T fN = inN ? php[pN] : rec[48 + ti];
+          // residual, Listing-1 term order, a_nb = -A_nb
+          T r = -(f[F_AE * kTT] * fE);
+          r -= f[F_AW * kTT] * fW;
+          r -= f[F_AN * kTT] * fN;
+          r -= f[F_AS * kTT] * fS;
+          r -= f[F_AT * kTT] * fT;
+          r -= f[F_AB * kTT] * fB;
+          r += f[F_Q * kTT];
+          r -= f[F_AP * kTT] * fP;
+          nrm += fabs(static_cast<double>(r));
+          const T RW = inW ? s_R[((t - 1) & 1) * kTT + pW] : rec[64 + tj];
+          const T RS = inS ? s_R[((t - 1) & 1) * kTT + pS] : rec[80 + ti];
+          const T Rv = (((r - f[F_LB * kTT] * RB) - f[F_LW * kTT] * RW) - f[F_LS * kTT] * RS) *
+                       f[F_LP * kTT];
+          RB = Rv;
+          P.R[(td.slot + t) * kTT + p] = Rv;
+          s_R[(t & 1) * kTT + p] = Rv;
         }
-        const T Rv = (((r - f[F_LB * kTT] * RB) - f[F_LW * kTT] * RW) - f[F_LS * kTT] * RS) *
-                     f[F_LP * kTT];
-        RB = Rv;
-        P.R[(td.slot + t) * kTT + p] = Rv;
-        s_R[(t & 1) * kTT + p] = Rv;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_done[(dq + t) % DR]);
+        bar_compute();
       }
     }
-    __syncthreads();
-    if (p == 0) {
-      __threadfence();
-      st_release(&prog[tid], (unsigned)NS);
-    }
+    fq += NS; pq += NS; eq += NS; dq += NS;
+    __syncthreads();  // comm warp has published NS (all steps retired)
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
       P.partial[tid] = s;
@@ -435,14 +502,14 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
     if (s_last) {
       // finaliser: deterministic per-block norms, then reset the backward state
       __threadfence();
-      const int w = p >> 5, l = p & 31, nw = blockDim.x >> 5;
+      const int w = p >> 5, nw = blockDim.x >> 5;
       for (int b = w; b < P.nblocks; b += nw) {
         const BlockDesc bb = P.blocks[b];
         double v = 0.0;
-        for (int x = l; x < bb.ntiles; x += 32) v += __ldcg(P.partial + bb.tile0 + x);
+        for (int x = lane; x < bb.ntiles; x += 32) v += __ldcg(P.partial + bb.tile0 + x);
 #pragma unroll
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (l == 0) P.block_norms[b] = v;
+        if (lane == 0) P.block_norms[b] = v;
       }
       __syncthreads();
       if (p == 0) {
@@ -456,37 +523,47 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
 }
 
 // =============================================================================
-// K3: backward substitution + phi update (backward3d).  Slices in reverse.
-// Ring slot = {R, phi, UN, UE, UT} of one slice.
+// K3: backward substitution + phi update (backward3d); slices in reverse.
+// Ring slot = {R, phi, UN, UE, UT} of one slice; edge record = delta of the
+// E and N neighbour tiles (16 each).
 // =============================================================================
 template <typename T, int SB>
 struct BwdCfg {
-  static constexpr int LA = SB - 1;
-  static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) + SB * sizeof(uint64_t);
+  static constexpr int ER = 8, DR = 8, NE = 32;
+  static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
+                                  (size_t)ER * NE * sizeof(T) + (SB + ER + DR) * sizeof(uint64_t);
 };
 
 template <typename T, int SB>
-__global__ void __launch_bounds__(kTT, 1) k_backward(const SweepParams<T> P) {
-  constexpr int LA = BwdCfg<T, SB>::LA;
+__global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
+  using C = BwdCfg<T, SB>;
+  constexpr int ER = C::ER, DR = C::DR, NE = C::NE;
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_rg = reinterpret_cast<T*>(smem);
   T* s_D = s_rg + SB * 5 * kTT;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_D + 2 * kTT);
+  T* s_edge = s_D + 2 * kTT;
+  uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_edge + ER * NE);
+  uint64_t* b_edge = b_rg + SB;
+  uint64_t* b_done = b_edge + ER;
   __shared__ int s_tile, s_last;
 
   const int p = threadIdx.x;
-  int ti, tj;
-  pos_to_tij(p, ti, tj);
+  const bool comm = p >= kCompute;
+  const int lane = p & 31;
+  int ti = 0, tj = 0;
+  if (!comm) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
-  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
-  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SB; ++b) mbar_init(&s_bar[b], 1);
+    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 1);
+    for (int b = 0; b < ER; ++b) mbar_init(&b_edge[b], 1);
+    for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t q0 = 0;
+  uint32_t rq = 0, eq = 0, dq = 0;
 
   for (;;) {
     __syncthreads();
@@ -497,80 +574,99 @@ __global__ void __launch_bounds__(kTT, 1) k_backward(const SweepParams<T> P) {
     const int tid = P.order[tk];
     const TileDesc td = P.tiles[tid];
     const int NS = td.ns, nz = td.nz;
-    const bool col = ti < td.wI && tj < td.wJ;
-    const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
-    const long long edgeE = td.nE >= 0 ? P.tiles[td.nE].edge : 0;
-    const long long edgeN = td.nN >= 0 ? P.tiles[td.nN].edge : 0;
-    const bool pubW = (ti == 0 && td.nW >= 0), pubS = (tj == 0 && td.nS >= 0);
-    const T* r_src = P.R + td.slot * kTT;
-    const T* ph_src = P.phi + td.slot * kTT;
-    const T* bw_src = P.bw + td.slot * B_NA * kTT;
 
-    auto issue = [&](int u) {
-      const int t = NS - 1 - u;
-      const uint32_t q = q0 + u;
-      T* dst = s_rg + (q % SB) * 5 * kTT;
-      uint64_t* bar = &s_bar[q % SB];
-      const uint32_t b1 = slice_bytes<T>(t, nz, 1), b3 = slice_bytes<T>(t, nz, B_NA);
-      mbar_expect_tx(bar, 2 * b1 + b3);
-      issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-      issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-      issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false, 0);
-    };
-    const uint32_t qb = q0;
-    if (p == 0)
-      for (int u = 0; u < LA && u < NS; ++u) issue(u);
-    T dT = T(0);
-    unsigned cE = 0, cN = 0;
-    for (int u = 0; u < NS; ++u) {
-      const int t = NS - 1 - u;
-      __syncthreads();
-      if (p == 0) {
-        if (u > 0) {
-          __threadfence();
-          st_release(&prog[tid], (unsigned)u);
+    if (comm) {
+      const T* r_src = P.R + td.slot * kTT;
+      const T* ph_src = P.phi + td.slot * kTT;
+      const T* bw_src = P.bw + td.slot * B_NA * kTT;
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool colok = we ? (c < td.wJ) : (c < td.wI);
+      const int nB = we ? td.nE : td.nN;
+      const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
+      const T* srcB = we ? P.edgeW : P.edgeS;
+      const int lag = we ? kTI : kTJ;
+      const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
+      unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
+      int u_pub = 0, s_i = 0, e_next = 0;
+      while (u_pub < NS) {
+        const int u_old = u_pub;
+        while (u_pub < NS) {
+          const uint32_t q = dq + u_pub;
+          if (!mbar_test(&b_done[q % DR], (q / DR) & 1)) break;
+          ++u_pub;
         }
-        if (u + LA < NS) issue(u + LA);
+        if (u_pub != u_old && lane == 0) st_release(&prog[tid], (unsigned)u_pub);
+        if (lane == 0) {
+          for (; s_i < NS && s_i <= u_pub + SB - 1; ++s_i) {
+            const int t = NS - 1 - s_i;
+            const uint32_t q = rq + s_i;
+            T* dst = s_rg + (q % SB) * 5 * kTT;
+            uint64_t* bar = &b_rg[q % SB];
+            mbar_expect_tx(bar, 2 * slice_bytes<T>(t, nz, 1) + slice_bytes<T>(t, nz, B_NA));
+            issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+            issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+            issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false,
+                           0);
+          }
+        }
+        int m = min(NS - 1, u_pub + ER - 1);
+        if (e_next <= m) {
+          cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e_next + kTI, NS));
+          cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e_next + kTJ, NS));
+          if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
+          if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
+          for (int s = e_next; s <= m; ++s) {
+            const int t = NS - 1 - s;
+            const int k = t - offB;
+            T v = T(0);
+            if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + edgeB + (long long)k * 16 + c);
+            s_edge[((eq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
+          }
+          __syncwarp();
+          if (lane == 0)
+            for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
+          if (m >= e_next) e_next = m + 1;
+          (void)lag;
+        }
       }
-      {
-        const uint32_t q = qb + u;
-        mbar_wait(&s_bar[q % SB], (q / SB) & 1);
-      }
-      const int k = t - d;
-      if (col && k >= 0 && k < nz) {
-        const T* sl = s_rg + ((qb + u) % SB) * 5 * kTT + p;
-        T dN, dE;
-        if (inN) {
-          dN = s_D[((u - 1) & 1) * kTT + pN];
-        } else if (td.nN >= 0) {
-          const unsigned need = min(u + kTJ, NS);
-          while (cN < need) cN = ld_acquire(&prog[td.nN]);
-          dN = ld_relaxed(P.edgeS + edgeN + (long long)k * kTI + ti);
-        } else {
-          dN = T(0);
+    } else {
+      const bool col = ti < td.wI && tj < td.wJ;
+      const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
+      const bool pubW = (ti == 0 && td.nW >= 0), pubS = (tj == 0 && td.nS >= 0);
+      T dT = T(0);
+      for (int u = 0; u < NS; ++u) {
+        const int t = NS - 1 - u;
+        const int k = t - d;
+        {
+          const uint32_t q = rq + u;  // unconditional: bounds the run-ahead (see K2)
+          mbar_wait(&b_rg[q % SB], (q / SB) & 1);
         }
-        if (inE) {
-          dE = s_D[((u - 1) & 1) * kTT + pE];
-        } else if (td.nE >= 0) {
-          const unsigned need = min(u + kTI, NS);
-          while (cE < need) cE = ld_acquire(&prog[td.nE]);
-          dE = ld_relaxed(P.edgeW + edgeE + (long long)k * kTJ + tj);
-        } else {
-          dE = T(0);
+        if (col && k >= 0 && k < nz) {
+          const T* rec = s_edge + ((eq + u) % ER) * NE;
+          if (!(inE && inN)) {
+            const uint32_t q = eq + u;
+            mbar_wait(&b_edge[q % ER], (q / ER) & 1);
+          }
+          const T* sl = s_rg + ((rq + u) % SB) * 5 * kTT + p;
+          const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : rec[16 + ti];
+          const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : rec[tj];
+          const T dl = ((sl[0] - sl[2 * kTT] * dN) - sl[3 * kTT] * dE) - sl[4 * kTT] * dT;
+          dT = dl;
+          P.phi[(td.slot + t) * kTT + p] = sl[kTT] + dl;
+          s_D[(u & 1) * kTT + p] = dl;
+          if (pubW) P.edgeW[td.edge + (long long)k * kTJ + tj] = dl;
+          if (pubS) P.edgeS[td.edge + (long long)k * kTI + ti] = dl;
         }
-        const T dl = ((sl[0] - sl[2 * kTT] * dN) - sl[3 * kTT] * dE) - sl[4 * kTT] * dT;
-        dT = dl;
-        P.phi[(td.slot + t) * kTT + p] = sl[kTT] + dl;
-        s_D[(u & 1) * kTT + p] = dl;
-        if (pubW) P.edgeW[td.edge + (long long)k * kTJ + tj] = dl;
-        if (pubS) P.edgeS[td.edge + (long long)k * kTI + ti] = dl;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_done[(dq + u) % DR]);
+        bar_compute();
       }
     }
-    q0 += NS;
+    rq += NS; eq += NS; dq += NS;
     __syncthreads();
     if (p == 0) {
       __threadfence();
-      st_release(&prog[tid], (unsigned)NS);
       s_last = (atomicAdd(P.state + 1, 1u) == (unsigned)P.ntiles - 1);
     }
     __syncthreads();
@@ -799,7 +895,7 @@ static int grid_for(long long n, int threads = 256) {
 }
 static inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? SIP_OK : SIP_ERR_CUDA; }
 
-constexpr int kSF64 = 4, kSF32 = 6;  // forward ring depth (fp64 / fp32)
+constexpr int kSF64 = 3, kSF32 = 5;  // forward ring depth (fp64 / fp32)
 constexpr int kSB64 = 6, kSB32 = 8;  // backward ring depth
 
 template <typename T> struct Rings;
@@ -820,7 +916,7 @@ int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
     cudaFuncSetAttribute(k_forward<T, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_forward<T, SF><<<grid, kTT, smem, (cudaStream_t)stream>>>(p);
+  k_forward<T, SF><<<grid, kThreads, smem, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -833,7 +929,7 @@ int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
     cudaFuncSetAttribute(k_backward<T, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_backward<T, SB><<<grid, kTT, smem, (cudaStream_t)stream>>>(p);
+  k_backward<T, SB><<<grid, kThreads, smem, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -849,13 +945,13 @@ int max_resident_ctas(int kind, int precision, int* grid) {
       constexpr int SF = Rings<double>::SF;
       cudaFuncSetAttribute(k_forward<double, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)FwdCfg<double, SF>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, SF>, kTT,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, SF>, kThreads,
                                                         FwdCfg<double, SF>::bytes);
     } else {
       constexpr int SF = Rings<float>::SF;
       cudaFuncSetAttribute(k_forward<float, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)FwdCfg<float, SF>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, SF>, kTT,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, SF>, kThreads,
                                                         FwdCfg<float, SF>::bytes);
     }
   } else {
@@ -863,13 +959,13 @@ int max_resident_ctas(int kind, int precision, int* grid) {
       constexpr int SB = Rings<double>::SB;
       cudaFuncSetAttribute(k_backward<double, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)BwdCfg<double, SB>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double, SB>, kTT,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double, SB>, kThreads,
                                                         BwdCfg<double, SB>::bytes);
     } else {
       constexpr int SB = Rings<float>::SB;
       cudaFuncSetAttribute(k_backward<float, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)BwdCfg<float, SB>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float, SB>, kTT,
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float, SB>, kThreads,
                                                         BwdCfg<float, SB>::bytes);
     }
   }
