@@ -143,6 +143,13 @@ long long sip_launch_count(const sip_ctx* ctx);
 /* Tile geometry of the wavefront kernels (TI, TJ, tiles, slices). */
 int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long long* slices);
 
+/* ---- debugging / test helpers (not part of the reference interface) ---- */
+/* One forward sweep (K2) on the current device phi (writes R). */
+int sip_debug_forward(sip_ctx* ctx);
+/* Gather a device pack of one local block into a Field3 array: which = 0 phi,
+ * 1 R, 2..13 forward pack (AP,AW,AE,AS,AN,AB,AT,Q,LB,LW,LS,LP), 14..16 UN,UE,UT. */
+int sip_debug_field(sip_ctx* ctx, int local, int which, double* out);
+
 /* ---- host-only helpers (no device needed) ---- */
 /* 128-byte ncclUniqueId for sip_create_lattice (rank 0 creates, all share). */
 int sip_nccl_unique_id(void* out128);

@@ -117,6 +117,16 @@ def sweep(A: dict, F: dict, phi: np.ndarray) -> float:
               _p(work))
 
 
+def forward(A: dict, F: dict, phi: np.ndarray) -> np.ndarray:
+    """Residual + forward substitution only: returns R (fp64)."""
+    nz, ny, nx = (s - 2 for s in A["AP"].shape)
+    work = field(nx, ny, nz)
+    lib().orc_forward_d.restype = ctypes.c_double
+    lib().orc_forward_d(nx, ny, nz, *[_p(A[n]) for n in ARRAYS], *[_p(F[n]) for n in FACTORS[:4]],
+                        _p(phi), _p(work))
+    return work
+
+
 def solve(A: dict, phi: np.ndarray, alpha: float, iters: int, precision: str = "f64"):
     """Factor + `iters` SIP iterations; phi updated in place.  Returns norms."""
     nz, ny, nx = (s - 2 for s in A["AP"].shape)

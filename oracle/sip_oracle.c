@@ -244,6 +244,33 @@ double orc_sweep_d(int nx, int ny, int nz, const double* AP, const double* AW, c
   return norm;
 }
 
+/* Residual + forward substitution only (R left in work); returns the norm. */
+double orc_forward_d(int nx, int ny, int nz, const double* AP, const double* AW, const double* AE,
+                     const double* AS, const double* AN, const double* AB, const double* AT,
+                     const double* Q, const double* LB, const double* LW, const double* LS,
+                     const double* LP, const double* phi, double* work) {
+  const size_t sj = nx + 2, sk = (size_t)(nx + 2) * (ny + 2);
+  size_t G = (size_t)(nx + 2) * (ny + 2) * (nz + 2);
+  memset(work, 0, G * 8);
+  double norm = 0.0;
+  for (int k = 1; k <= nz; ++k)
+    for (int j = 1; j <= ny; ++j)
+      for (int i = 1; i <= nx; ++i) {
+        size_t c = IDX(i, j, k);
+        double r = -(AE[c] * phi[c + 1]);
+        r -= AW[c] * phi[c - 1];
+        r -= AN[c] * phi[c + sj];
+        r -= AS[c] * phi[c - sj];
+        r -= AT[c] * phi[c + sk];
+        r -= AB[c] * phi[c - sk];
+        r += Q[c];
+        r -= AP[c] * phi[c];
+        norm += fabs(r);
+        work[c] = (((r - LB[c] * work[c - sk]) - LW[c] * work[c - 1]) - LS[c] * work[c - sj]) * LP[c];
+      }
+  return norm;
+}
+
 /* Same iteration with every relaxation array in fp32. */
 double orc_sweep_f(int nx, int ny, int nz, const float* AP, const float* AW, const float* AE,
                    const float* AS, const float* AN, const float* AB, const float* AT,

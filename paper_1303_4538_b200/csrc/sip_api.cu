@@ -9,9 +9,11 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "sip_internal.h"
@@ -267,6 +269,12 @@ static int build(sip_ctx* ctx) {
   ctx->grid_b = std::max(1, std::min(nt, cap));
   CKS(max_resident_ctas(0, ctx->precision, &cap));
   ctx->grid_fac = std::max(1, std::min(nt, cap));
+  if (const char* g = getenv("SIPB_GRID")) {  // debugging: cap the persistent grid
+    const int gg = std::max(1, atoi(g));
+    ctx->grid_f = std::min(ctx->grid_f, gg);
+    ctx->grid_b = std::min(ctx->grid_b, gg);
+    ctx->grid_fac = std::min(ctx->grid_fac, gg);
+  }
 
   // halo plan: faces only, canonical order (transfers.cpp:148-165)
   std::vector<HaloEntry> plan;
@@ -997,6 +1005,78 @@ int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long lo
   if (tj) *tj = kTJ;
   if (tiles) *tiles = (long long)ctx->htiles.size();
   if (slices) *slices = ctx->total_slices;
+  return SIP_OK;
+}
+
+// ---- debugging / test helpers (not part of the reference interface) ----
+// Runs one forward sweep (K2) only, on the current device phi.
+int sip_debug_forward(sip_ctx* ctx) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  CKS(check_ready(ctx));
+  CKS(set_device(ctx));
+  CKS(ensure_norm_cap(ctx, ctx->n_done + 1));
+  const size_t st = (32 + std::max<size_t>(1, ctx->htiles.size())) * sizeof(unsigned);
+  CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
+  if (ctx->precision == SIP_PREC_SINGLE)
+    CKS(launch_forward<float>(sweep_params<float>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
+  else
+    CKS(launch_forward<double>(sweep_params<double>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
+  CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
+  CK(cudaMemsetAsync(ctx->st_b, 0, st, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+// Gathers a device pack (0 = phi, 1 = R, 2..13 = forward pack arrays
+// AP..LP, 14..16 = UN/UE/UT) of one local block into a Field3 array.
+int sip_debug_field(sip_ctx* ctx, int local, int which, double* out) {
+  if (!ctx || !out || local < 0 || local >= (int)ctx->local.size()) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  const BlockDesc& hb = ctx->hblocks[local];
+  const size_t G = field3_elems(hb);
+  const int none[6] = {-1, -1, -1, -1, -1, -1};
+  CK(cudaMemsetAsync(ctx->staging, 0, G * sizeof(double), ctx->stream));
+  // gather reads pack index (na = 1, arr = 0); offset the base pointer for other packs
+  auto run = [&](auto* base, int na, int arr) -> int {
+    using T = std::remove_pointer_t<decltype(base)>;
+    return launch_gather_any<T>(base, na, arr, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
+  };
+  int rc;
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    float* phi = static_cast<float*>(ctx->phi);
+    float* R = static_cast<float*>(ctx->R);
+    float* fw = static_cast<float*>(ctx->fw);
+    float* bw = static_cast<float*>(ctx->bw);
+    rc = which == 0 ? run(phi, 1, 0) : which == 1 ? run(R, 1, 0)
+         : which < 14 ? run(fw, F_NA, which - 2) : run(bw, B_NA, which - 14);
+  } else {
+    double* phi = static_cast<double*>(ctx->phi);
+    double* R = static_cast<double*>(ctx->R);
+    double* fw = static_cast<double*>(ctx->fw);
+    double* bw = static_cast<double*>(ctx->bw);
+    rc = which == 0 ? run(phi, 1, 0) : which == 1 ? run(R, 1, 0)
+         : which < 14 ? run(fw, F_NA, which - 2) : run(bw, B_NA, which - 14);
+  }
+  (void)none;
+  CKS(rc);
+  CK(cudaMemcpyAsync(out, ctx->staging, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+// Raw copy of the cross-tile edge buffers (which = 0: edgeW, 1: edgeS) as doubles.
+int sip_debug_edges(sip_ctx* ctx, int which, double* out, long long* count) {
+  if (!ctx || !count) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  const long long n = ctx->total_edge;
+  if (out) {
+    std::vector<char> tmp((size_t)n * ctx->esize);
+    CK(cudaMemcpy(tmp.data(), which ? ctx->edgeS : ctx->edgeW, tmp.size(), cudaMemcpyDeviceToHost));
+    for (long long x = 0; x < n; ++x)
+      out[x] = ctx->esize == 8 ? reinterpret_cast<double*>(tmp.data())[x]
+                               : (double)reinterpret_cast<float*>(tmp.data())[x];
+  }
+  *count = n;
   return SIP_OK;
 }
 

@@ -184,6 +184,9 @@ int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
 template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
                     const T* phi, const T* ghost, int symmetric, double* out, void* stream);
+template <typename T>
+int launch_gather_any(const T* pack, int na, int arr, const BlockDesc* d_blocks, int block,
+                      const BlockDesc& hb, double* dst, void* stream);
 int launch_convert(const double* src, float* dst, long long n, void* stream);
 int launch_generate(int kind, uint64_t seed, const int g[3], const int o[3], int nx, int ny, int nz,
                     double* const* out8, void* stream);

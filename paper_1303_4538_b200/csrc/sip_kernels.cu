@@ -70,6 +70,9 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ double ld_relaxed(const double* p) {
   double v;
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
@@ -274,10 +277,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
   asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
 }
+// Warp-collective poll of a neighbour's progress counter.  Every lane performs
+// its own acquire (so its later loads are ordered) and the warp takes the
+// minimum, so all lanes agree on a value each of them has acquired.  Lanes of
+// a warp may execute independently (Volta+ scheduling): decisions taken from
+// memory must be made uniform explicitly.
 __device__ __forceinline__ unsigned poll_progress(const unsigned* p, unsigned cached, unsigned need) {
-  // warp-uniform: every lane performs the acquire so its later loads are ordered
   if (cached >= need) return cached;
-  return ld_acquire(p);
+  return __reduce_min_sync(0xffffffffu, ld_acquire(p));
+}
+// Warp-collective test of a step-done barrier: complete only if every lane
+// observed completion (each such lane holds its own acquire).
+__device__ __forceinline__ bool warp_test(uint64_t* b, uint32_t parity) {
+  return __all_sync(0xffffffffu, mbar_test(b, parity));
 }
 
 template <typename T, int SF>
@@ -286,21 +298,23 @@ struct FwdCfg {
   static constexpr int ER = 8;       // edge records in flight
   static constexpr int DR = 8;       // step-done barriers (>= SF)
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
+  static constexpr int OR = 8;       // outgoing edge records (>= SF)
   static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
-                                  (size_t)ER * NE * sizeof(T) +
+                                  (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SF + SP + ER + DR) * sizeof(uint64_t);
 };
 
 template <typename T, int SF>
 __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
   using C = FwdCfg<T, SF>;
-  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, NE = C::NE;
+  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_fw = reinterpret_cast<T*>(smem);
   T* s_ph = s_fw + SF * F_NA * kTT;
   T* s_R = s_ph + SP * kTT;
   T* s_edge = s_R + 2 * kTT;
-  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_edge + ER * NE);
+  T* s_out = s_edge + ER * NE;  // [OR][32]: R of the E column (tj) and N row (16 + ti)
+  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_out + OR * 32);
   uint64_t* b_ph = b_fw + SF;
   uint64_t* b_edge = b_ph + SP;
   uint64_t* b_done = b_edge + ER;
@@ -352,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const int nB = we ? td.nE : td.nN;   // downstream neighbour (phi only)
       const long long slotA = nA >= 0 ? P.tiles[nA].slot : 0;
       const long long slotB = nB >= 0 ? P.tiles[nB].slot : 0;
+      const long long edgeA = nA >= 0 ? P.tiles[nA].edge : 0;
       const int posA = we ? tile_pos(kTI - 1, c) : tile_pos(c, kTJ - 1);
       const int posB = we ? tile_pos(0, c) : tile_pos(c, 0);
       const int lag = we ? kTI : kTJ;      // upstream neighbour slice = t + lag - 1
@@ -361,16 +376,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const long long gstride = we ? bd.ny : bd.nx;
       unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
 
+      // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
+      const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
+      const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
+      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
       int t_pub = 0, s_f = 0, s_p = 0, e_next = 0;
       while (t_pub < NS) {
-        // (1) retire finished steps, publish progress
+        // (1) retire finished steps: forward their edge R to global, then
+        //     publish progress with a warp-wide gpu fence (release pattern)
         const int t_old = t_pub;
         while (t_pub < NS) {
           const uint32_t q = dq + t_pub;
-          if (!mbar_test(&b_done[q % DR], (q / DR) & 1)) break;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          const int k = t_pub - outoff;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t_pub % OR) * 32 + lane];
           ++t_pub;
         }
-        if (t_pub != t_old && lane == 0) st_release(&prog[tid], (unsigned)t_pub);
+        if (t_pub != t_old) {
+          __syncwarp();
+          __threadfence();
+          if (lane == 0) st_relaxed_u32(&prog[tid], (unsigned)t_pub);
+        }
         // (2) bulk copies into freed ring slots
         if (lane == 0) {
           for (; s_f < NS && s_f <= t_pub + SF - 1; ++s_f) {
@@ -398,9 +424,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
             const int kA = s - c;  // W side cell (0, c) / S side cell (c, 0)
             if (colok && kA >= 0 && kA < nz) {
               if (nA >= 0) {
-                const long long x = (slotA + s + lag - 1) * kTT + posA;
-                phA = P.phi[x];
-                rA = ld_relaxed(P.R + x);
+                phA = P.phi[(slotA + s + lag - 1) * kTT + posA];
+                rA = ld_relaxed((we ? P.edgeW : P.edgeS) + edgeA + (long long)kA * 16 + c);
               } else {
                 phA = gA[gstride * kA];
               }
@@ -437,25 +462,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       for (int t = 0; t < NS; ++t) {
         const int k = t - d;
         {
-          // every compute thread waits for slice t (even if idle this step): it
-          // bounds how far the compute warps can run ahead of the comm warp
+          // every compute thread waits for slice t and edge record t, even if
+          // idle this step: that bounds how far the compute warps can run ahead
+          // of the comm warp, so an mbarrier is never waited on a phase that is
+          // two behind (which try_wait would report as complete)
           const uint32_t q = fq + t;
           mbar_wait(&b_fw[q % SF], (q / SF) & 1);
+          const uint32_t r = eq + t;
+          mbar_wait(&b_edge[r % ER], (r / ER) & 1);
         }
         if (col && k >= 0 && k < nz) {
           {
             const uint32_t q = pq + t;  // slice t (and t-1, already complete)
             mbar_wait(&b_ph[q % SP], (q / SP) & 1);
           }
-          if (k + 1 < nz) {
+          if (t + 1 < NS) {  // slice t+1 holds phi(k+1) and the E / N neighbours at k
             const uint32_t q = pq + t + 1;
             mbar_wait(&b_ph[q % SP], (q / SP) & 1);
           }
           const T* rec = s_edge + ((eq + t) % ER) * NE;
-          if (!(inW && inE && inS && inN)) {
-            const uint32_t q = eq + t;
-            mbar_wait(&b_edge[q % ER], (q / ER) & 1);
-          }
           const T* f = s_fw + ((fq + t) % SF) * F_NA * kTT + p;
           const T* ph0 = s_ph + ((pq + t) % SP) * kTT;
           const T* phm = s_ph + ((pq + t + SP - 1) % SP) * kTT;
@@ -484,6 +509,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           RB = Rv;
           P.R[(td.slot + t) * kTT + p] = Rv;
           s_R[(t & 1) * kTT + p] = Rv;
+          if (ti == kTI - 1) s_out[(t % OR) * 32 + tj] = Rv;
+          if (tj == kTJ - 1) s_out[(t % OR) * 32 + 16 + ti] = Rv;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_done[(dq + t) % DR]);
@@ -529,20 +556,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 // =============================================================================
 template <typename T, int SB>
 struct BwdCfg {
-  static constexpr int ER = 8, DR = 8, NE = 32;
+  static constexpr int ER = 8, DR = 8, NE = 32, OR = 8;  // OR >= SB
   static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
-                                  (size_t)ER * NE * sizeof(T) + (SB + ER + DR) * sizeof(uint64_t);
+                                  (size_t)(ER * NE + OR * 32) * sizeof(T) +
+                                  (SB + ER + DR) * sizeof(uint64_t);
 };
 
 template <typename T, int SB>
 __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
   using C = BwdCfg<T, SB>;
-  constexpr int ER = C::ER, DR = C::DR, NE = C::NE;
+  constexpr int ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
+  static_assert(OR >= SB, "outgoing edge ring must cover the slice ring");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_rg = reinterpret_cast<T*>(smem);
   T* s_D = s_rg + SB * 5 * kTT;
   T* s_edge = s_D + 2 * kTT;
-  uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_edge + ER * NE);
+  T* s_out = s_edge + ER * NE;  // [OR][32]: delta of the W column (tj) and S row (16 + ti)
+  uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
   uint64_t* b_edge = b_rg + SB;
   uint64_t* b_done = b_edge + ER;
   __shared__ int s_tile, s_last;
@@ -588,15 +618,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const int lag = we ? kTI : kTJ;
       const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
       unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
+      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
+      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
+      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
       int u_pub = 0, s_i = 0, e_next = 0;
       while (u_pub < NS) {
         const int u_old = u_pub;
         while (u_pub < NS) {
           const uint32_t q = dq + u_pub;
-          if (!mbar_test(&b_done[q % DR], (q / DR) & 1)) break;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          const int k = (NS - 1 - u_pub) - c;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u_pub % OR) * 32 + lane];
           ++u_pub;
         }
-        if (u_pub != u_old && lane == 0) st_release(&prog[tid], (unsigned)u_pub);
+        if (u_pub != u_old) {
+          __syncwarp();
+          __threadfence();
+          if (lane == 0) st_relaxed_u32(&prog[tid], (unsigned)u_pub);
+        }
         if (lane == 0) {
           for (; s_i < NS && s_i <= u_pub + SB - 1; ++s_i) {
             const int t = NS - 1 - s_i;
@@ -633,7 +672,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     } else {
       const bool col = ti < td.wI && tj < td.wJ;
       const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
-      const bool pubW = (ti == 0 && td.nW >= 0), pubS = (tj == 0 && td.nS >= 0);
       T dT = T(0);
       for (int u = 0; u < NS; ++u) {
         const int t = NS - 1 - u;
@@ -641,13 +679,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         {
           const uint32_t q = rq + u;  // unconditional: bounds the run-ahead (see K2)
           mbar_wait(&b_rg[q % SB], (q / SB) & 1);
+          const uint32_t r = eq + u;
+          mbar_wait(&b_edge[r % ER], (r / ER) & 1);
         }
         if (col && k >= 0 && k < nz) {
           const T* rec = s_edge + ((eq + u) % ER) * NE;
-          if (!(inE && inN)) {
-            const uint32_t q = eq + u;
-            mbar_wait(&b_edge[q % ER], (q / ER) & 1);
-          }
           const T* sl = s_rg + ((rq + u) % SB) * 5 * kTT + p;
           const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : rec[16 + ti];
           const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : rec[tj];
@@ -655,8 +691,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           dT = dl;
           P.phi[(td.slot + t) * kTT + p] = sl[kTT] + dl;
           s_D[(u & 1) * kTT + p] = dl;
-          if (pubW) P.edgeW[td.edge + (long long)k * kTJ + tj] = dl;
-          if (pubS) P.edgeS[td.edge + (long long)k * kTI + ti] = dl;
+          if (ti == 0) s_out[(u % OR) * 32 + tj] = dl;
+          if (tj == 0) s_out[(u % OR) * 32 + 16 + ti] = dl;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_done[(dq + u) % DR]);
@@ -757,6 +793,20 @@ __global__ void k_gather(const T* __restrict__ pack, const T* __restrict__ ghost
       face_cell(bd, f, (int)(c % n0), (int)(c / n0), true, i, j, k);
       dst[f3(bd.nx, bd.ny, i, j, k)] = static_cast<double>(g[c]);
     }
+  }
+}
+
+template <typename T>
+__global__ void k_gather_any(const T* __restrict__ pack, int na, int arr, const BlockDesc* blocks,
+                             int b, double* dst) {
+  const BlockDesc bd = blocks[b];
+  const long long n = (long long)bd.nx * bd.ny * bd.nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % bd.nx);
+    const long long r = c / bd.nx;
+    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    dst[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(pack[pack_index(bd, na, arr, i, j, k)]);
   }
 }
 
@@ -1020,6 +1070,18 @@ int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, c
       d_blocks, block, fw, phi, ghost, out);
   return cuda_status(cudaGetLastError());
 }
+template <typename T>
+int launch_gather_any(const T* pack, int na, int arr, const BlockDesc* d_blocks, int block,
+                      const BlockDesc& hb, double* dst, void* stream) {
+  k_gather_any<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
+      pack, na, arr, d_blocks, block, dst);
+  return cuda_status(cudaGetLastError());
+}
+template int launch_gather_any<double>(const double*, int, int, const BlockDesc*, int,
+                                       const BlockDesc&, double*, void*);
+template int launch_gather_any<float>(const float*, int, int, const BlockDesc*, int,
+                                      const BlockDesc&, double*, void*);
+
 int launch_convert(const double* src, float* dst, long long n, void* stream) {
   k_convert<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(src, dst, n);
   return cuda_status(cudaGetLastError());
