@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "sip_internal.h"
 
@@ -51,17 +52,47 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(saddr(bar))
       : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+// Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
+// (__trap -> the launch fails with an error instead of hanging the GPU).
+constexpr unsigned long long kWatchdogNs = 4000000000ULL;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void watchdog_fire(int where) {
+  printf("sip watchdog: block %d thread %d stalled at site %d\n", blockIdx.x, threadIdx.x, where);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int where = 0) {
   const uint32_t a = saddr(b);
   uint32_t ok;
+  unsigned long long t0 = 0;
+  int n = 0;
   do {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(a), "r"(parity)
         : "memory");
+    if (!ok && ((++n & 255) == 0)) {
+      if (t0 == 0) t0 = gtime();
+      else if (gtime() - t0 > kWatchdogNs) watchdog_fire(where);
+    }
   } while (!ok);
 }
+// Idle-loop watchdog of the service warps (reset whenever work was done).
+struct Watchdog {
+  unsigned long long t0 = 0;
+  int n = 0;
+  __device__ __forceinline__ void progress() { t0 = 0; n = 0; }
+  __device__ __forceinline__ void idle(int where) {
+    if ((++n & 255) == 0) {
+      if (t0 == 0) t0 = gtime();
+      else if (gtime() - t0 > kWatchdogNs) watchdog_fire(where);
+    }
+  }
+};
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -189,7 +220,11 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
           unW = s_U[b][0][pW]; ueW = s_U[b][1][pW]; utW = s_U[b][2][pW];
         } else if (td.nW >= 0) {
           const unsigned need = min(t + kTI, NS);
-          while (cW < need) cW = ld_acquire(&prog[td.nW]);
+          Watchdog wd;
+          while (cW < need) {
+            cW = ld_acquire(&prog[td.nW]);
+            wd.idle(1);
+          }
           const long long base = (slotW + k + kTI - 1 + tj) * B_NA * kTT + posW;
           unW = ld_relaxed(P.bw + base + B_UN * kTT);
           ueW = ld_relaxed(P.bw + base + B_UE * kTT);
@@ -200,7 +235,11 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
           unS = s_U[b][0][pS]; ueS = s_U[b][1][pS]; utS = s_U[b][2][pS];
         } else if (td.nS >= 0) {
           const unsigned need = min(t + kTJ, NS);
-          while (cS < need) cS = ld_acquire(&prog[td.nS]);
+          Watchdog wd;
+          while (cS < need) {
+            cS = ld_acquire(&prog[td.nS]);
+            wd.idle(2);
+          }
           const long long base = (slotS + k + ti + kTJ - 1) * B_NA * kTT + posS;
           unS = ld_relaxed(P.bw + base + B_UN * kTT);
           ueS = ld_relaxed(P.bw + base + B_UE * kTT);
@@ -250,17 +289,26 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
 
 // =============================================================================
 // K2 / K3 are warp-specialised: 8 compute warps (one thread per tile column)
-// and one "comm" warp.  The comm warp issues the bulk copies of the slice
-// ring, publishes the tile's progress counter (st.release.gpu) once the
-// compute warps signal a finished step (mbarrier, CTA scope), polls the
-// neighbour tiles' counters and prefetches every cross-tile value a step
-// needs (neighbour phi / R / delta, ghost phi) into a shared "edge record".
-// The compute warps therefore never wait on a global-memory latency on the
-// wavefront's critical path: per step they wait on shared-memory mbarriers,
-// compute, store, and meet at one named barrier.
+// plus two service warps.
+//   loader warp: retires finished steps and refills the slice ring with bulk
+//                copies (cp.async.bulk -> shared, mbarrier complete_tx), and
+//                keeps an L2 prefetch front (cp.async.bulk.prefetch.L2) kPF
+//                slices ahead, so ring refills hit L2 even on the wavefront's
+//                latency-bound critical path.  Shared-memory work only.
+//   linker warp: forwards the tile's outgoing edge values (copied by the
+//                compute warps into a shared out-record) to global memory,
+//                publishes the tile's progress counter (fence.acq_rel.gpu +
+//                relaxed store = release pattern), polls the upstream tiles'
+//                counters and prefetches every cross-tile value a step needs
+//                (neighbour phi / R / delta, ghost phi) into a shared
+//                "edge record".
+// The compute warps never wait on a global-memory latency: per step they wait
+// on shared-memory mbarriers, compute, store, and meet at one named barrier.
 // =============================================================================
 constexpr int kCompute = kTT;       // compute threads (8 warps)
-constexpr int kThreads = kTT + 32;  // + comm warp
+constexpr int kThreads = kTT + 64;  // + loader warp + linker warp
+constexpr int kLoaderWarp = kTT / 32, kLinkerWarp = kTT / 32 + 1;
+constexpr int kPF = 12;             // L2 prefetch distance (slices) beyond the ring
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
@@ -277,6 +325,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
   asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_release_cta_s(int* p, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr(p)) : "memory");
+  return v;
+}
+
 // Warp-collective poll of a neighbour's progress counter.  Every lane performs
 // its own acquire (so its later loads are ordered) and the warp takes the
 // minimum, so all lanes agree on a value each of them has acquired.  Lanes of
@@ -296,9 +357,9 @@ template <typename T, int SF>
 struct FwdCfg {
   static constexpr int SP = SF + 2;  // phi slice s is read at steps s-1, s, s+1
   static constexpr int ER = 8;       // edge records in flight
-  static constexpr int DR = 8;       // step-done barriers (>= SF)
+  static constexpr int OR = 8;       // outgoing edge records
+  static constexpr int DR = 16;      // step-done barriers (> OR + SF)
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
-  static constexpr int OR = 8;       // outgoing edge records (>= SF)
   static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SF + SP + ER + DR) * sizeof(uint64_t);
@@ -308,6 +369,7 @@ template <typename T, int SF>
 __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
   using C = FwdCfg<T, SF>;
   constexpr int SP = C::SP, ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
+  static_assert(DR > OR + SF, "done ring must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_fw = reinterpret_cast<T*>(smem);
   T* s_ph = s_fw + SF * F_NA * kTT;
@@ -318,14 +380,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   uint64_t* b_ph = b_fw + SF;
   uint64_t* b_edge = b_ph + SP;
   uint64_t* b_done = b_edge + ER;
-  __shared__ int s_tile, s_last;
+  __shared__ int s_tile, s_last, s_linked;
   __shared__ double s_red[kThreads / 32];
 
   const int p = threadIdx.x;
-  const bool comm = p >= kCompute;
-  const int lane = p & 31;
+  const int warp = p >> 5, lane = p & 31;
   int ti = 0, tj = 0;
-  if (!comm) pos_to_tij(p, ti, tj);
+  if (warp < kLoaderWarp) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
   const int pW = ti > 0 ? tile_pos(ti - 1, tj) : 0;
   const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
@@ -344,7 +405,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 
   for (;;) {
     __syncthreads();
-    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    if (p == 0) {
+      s_tile = atomicAdd(P.state, 1u);
+      s_linked = 0;
+    }
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -354,10 +418,46 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     const int NS = td.ns, nz = td.nz;
     double nrm = 0.0;
 
-    if (comm) {
-      // ------------------------------------------------------------ comm warp
+    if (warp == kLoaderWarp) {
+      // ------------------------------------------------------------ loader
       const T* fw_src = P.fw + td.slot * F_NA * kTT;
       const T* ph_src = P.phi + td.slot * kTT;
+      int t_pub = 0, s_f = 0, s_p = 0, s_l2 = 0;
+      Watchdog wd;
+      while (s_f < NS || s_p < NS) {
+        const int before = s_f + s_p + t_pub;
+        while (t_pub < NS) {
+          const uint32_t q = dq + t_pub;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          ++t_pub;
+        }
+        const int linked = ld_acquire_cta_s(&s_linked);
+        // compute step x needs FW slice x and phi slice x+1; it may not get
+        // OR steps ahead of the linker (out-record ring)
+        const int lim = min(t_pub + SF - 1, linked + OR - 1);
+        if (lane == 0) {
+          for (; s_f < NS && s_f <= lim; ++s_f) {
+            const uint32_t q = fq + s_f;
+            issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s_f * F_NA * kTT, F_NA,
+                           s_f, nz, &b_fw[q % SF], true, 0);
+          }
+          for (; s_p < NS && s_p <= min(t_pub + SP - 2, lim + 1); ++s_p) {
+            const uint32_t q = pq + s_p;
+            issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s_p * kTT, 1, s_p, nz,
+                           &b_ph[q % SP], true, 0);
+          }
+          if (s_l2 < s_f) s_l2 = s_f;
+          for (; s_l2 < NS && s_l2 < s_f + kPF; ++s_l2) {
+            prefetch_l2(fw_src + (long long)s_l2 * F_NA * kTT, F_NA * kTT * sizeof(T));
+            prefetch_l2(ph_src + (long long)s_l2 * kTT, kTT * sizeof(T));
+          }
+        }
+        s_f = __shfl_sync(0xffffffffu, s_f, 0);
+        s_p = __shfl_sync(0xffffffffu, s_p, 0);
+        if (s_f + s_p + t_pub != before) wd.progress(); else wd.idle(11);
+      }
+    } else if (warp == kLinkerWarp) {
+      // ------------------------------------------------------------ linker
       // lanes 0-15 serve the W/E sides (index = tj), lanes 16-31 the S/N sides (index = ti)
       const bool we = lane < 16;
       const int c = lane & 15;
@@ -373,45 +473,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const int offB = we ? (td.wI - 1) + c : c + (td.wJ - 1);  // edge cell of side B: k = t - offB
       const T* gA = P.ghost + ghost_face_offset(bd, we ? G_W : G_S) + (we ? td.j0 : td.i0) + c;
       const T* gB = P.ghost + ghost_face_offset(bd, we ? G_E : G_N) + (we ? td.j0 : td.i0) + c;
+      const T* eA = (we ? P.edgeW : P.edgeS) + edgeA + c;
       const long long gstride = we ? bd.ny : bd.nx;
       unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
-
       // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
       const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
       const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
       T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
-      int t_pub = 0, s_f = 0, s_p = 0, e_next = 0;
-      while (t_pub < NS) {
+      int t_lk = 0, e_next = 0;
+      Watchdog wd;
+      while (t_lk < NS) {
+        const int before = t_lk + e_next;
         // (1) retire finished steps: forward their edge R to global, then
-        //     publish progress with a warp-wide gpu fence (release pattern)
-        const int t_old = t_pub;
-        while (t_pub < NS) {
-          const uint32_t q = dq + t_pub;
+        //     publish progress (release pattern)
+        const int t_old = t_lk;
+        while (t_lk < NS) {
+          const uint32_t q = dq + t_lk;
           if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          const int k = t_pub - outoff;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t_pub % OR) * 32 + lane];
-          ++t_pub;
+          const int k = t_lk - outoff;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t_lk % OR) * 32 + lane];
+          ++t_lk;
         }
-        if (t_pub != t_old) {
+        if (t_lk != t_old) {
           __syncwarp();
-          __threadfence();
-          if (lane == 0) st_relaxed_u32(&prog[tid], (unsigned)t_pub);
-        }
-        // (2) bulk copies into freed ring slots
-        if (lane == 0) {
-          for (; s_f < NS && s_f <= t_pub + SF - 1; ++s_f) {
-            const uint32_t q = fq + s_f;
-            issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s_f * F_NA * kTT, F_NA,
-                           s_f, nz, &b_fw[q % SF], true, 0);
-          }
-          for (; s_p < NS && s_p <= t_pub + SP - 2; ++s_p) {
-            const uint32_t q = pq + s_p;
-            issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s_p * kTT, 1, s_p, nz,
-                           &b_ph[q % SP], true, 0);
+          fence_gpu();
+          if (lane == 0) {
+            st_relaxed_u32(&prog[tid], (unsigned)t_lk);
+            st_release_cta_s(&s_linked, t_lk);
           }
         }
-        // (3) edge records of upcoming steps, as far as upstream progress allows
-        int m = min(NS - 1, t_pub + ER - 1);
+        // (2) edge records of upcoming steps, as far as upstream progress allows
+        int m = min(NS - 1, t_lk + ER - 1);
         if (e_next <= m) {
           cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e_next + kTI, NS));
           cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e_next + kTJ, NS));
@@ -425,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
             if (colok && kA >= 0 && kA < nz) {
               if (nA >= 0) {
                 phA = P.phi[(slotA + s + lag - 1) * kTT + posA];
-                rA = ld_relaxed((we ? P.edgeW : P.edgeS) + edgeA + (long long)kA * 16 + c);
+                rA = ld_relaxed(eA + (long long)kA * 16);
               } else {
                 phA = gA[gstride * kA];
               }
@@ -447,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
             for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
           if (m >= e_next) e_next = m + 1;
         }
+        if (t_lk + e_next != before) wd.progress(); else wd.idle(12);
       }
     } else {
       // --------------------------------------------------------- compute warps
@@ -464,21 +557,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         {
           // every compute thread waits for slice t and edge record t, even if
           // idle this step: that bounds how far the compute warps can run ahead
-          // of the comm warp, so an mbarrier is never waited on a phase that is
-          // two behind (which try_wait would report as complete)
+          // of the service warps, so an mbarrier is never waited on a phase two
+          // behind (which try_wait would report as complete)
           const uint32_t q = fq + t;
-          mbar_wait(&b_fw[q % SF], (q / SF) & 1);
+          mbar_wait(&b_fw[q % SF], (q / SF) & 1, 21);
           const uint32_t r = eq + t;
-          mbar_wait(&b_edge[r % ER], (r / ER) & 1);
+          mbar_wait(&b_edge[r % ER], (r / ER) & 1, 22);
         }
         if (col && k >= 0 && k < nz) {
           {
-            const uint32_t q = pq + t;  // slice t (and t-1, already complete)
-            mbar_wait(&b_ph[q % SP], (q / SP) & 1);
+            const uint32_t q = pq + t;  // slice t (t-1 completed earlier)
+            mbar_wait(&b_ph[q % SP], (q / SP) & 1, 23);
           }
           if (t + 1 < NS) {  // slice t+1 holds phi(k+1) and the E / N neighbours at k
             const uint32_t q = pq + t + 1;
-            mbar_wait(&b_ph[q % SP], (q / SP) & 1);
+            mbar_wait(&b_ph[q % SP], (q / SP) & 1, 24);
           }
           const T* rec = s_edge + ((eq + t) % ER) * NE;
           const T* f = s_fw + ((fq + t) % SF) * F_NA * kTT + p;
@@ -518,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       }
     }
     fq += NS; pq += NS; eq += NS; dq += NS;
-    __syncthreads();  // comm warp has published NS (all steps retired)
+    __syncthreads();  // linker has published NS (all steps retired)
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
       P.partial[tid] = s;
@@ -529,8 +622,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     if (s_last) {
       // finaliser: deterministic per-block norms, then reset the backward state
       __threadfence();
-      const int w = p >> 5, nw = blockDim.x >> 5;
-      for (int b = w; b < P.nblocks; b += nw) {
+      const int nw = blockDim.x >> 5;
+      for (int b = warp; b < P.nblocks; b += nw) {
         const BlockDesc bb = P.blocks[b];
         double v = 0.0;
         for (int x = lane; x < bb.ntiles; x += 32) v += __ldcg(P.partial + bb.tile0 + x);
@@ -556,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 // =============================================================================
 template <typename T, int SB>
 struct BwdCfg {
-  static constexpr int ER = 8, DR = 8, NE = 32, OR = 8;  // OR >= SB
+  static constexpr int ER = 8, NE = 32, OR = 8, DR = 24;
   static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SB + ER + DR) * sizeof(uint64_t);
@@ -566,7 +659,7 @@ template <typename T, int SB>
 __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
   using C = BwdCfg<T, SB>;
   constexpr int ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
-  static_assert(OR >= SB, "outgoing edge ring must cover the slice ring");
+  static_assert(DR > OR + SB, "done ring must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_rg = reinterpret_cast<T*>(smem);
   T* s_D = s_rg + SB * 5 * kTT;
@@ -575,13 +668,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
   uint64_t* b_edge = b_rg + SB;
   uint64_t* b_done = b_edge + ER;
-  __shared__ int s_tile, s_last;
+  __shared__ int s_tile, s_last, s_linked;
 
   const int p = threadIdx.x;
-  const bool comm = p >= kCompute;
-  const int lane = p & 31;
+  const int warp = p >> 5, lane = p & 31;
   int ti = 0, tj = 0;
-  if (!comm) pos_to_tij(p, ti, tj);
+  if (warp < kLoaderWarp) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
   const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
   const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
@@ -597,7 +689,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
 
   for (;;) {
     __syncthreads();
-    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    if (p == 0) {
+      s_tile = atomicAdd(P.state, 1u);
+      s_linked = 0;
+    }
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -605,39 +700,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     const TileDesc td = P.tiles[tid];
     const int NS = td.ns, nz = td.nz;
 
-    if (comm) {
+    if (warp == kLoaderWarp) {
       const T* r_src = P.R + td.slot * kTT;
       const T* ph_src = P.phi + td.slot * kTT;
       const T* bw_src = P.bw + td.slot * B_NA * kTT;
-      const bool we = lane < 16;
-      const int c = lane & 15;
-      const bool colok = we ? (c < td.wJ) : (c < td.wI);
-      const int nB = we ? td.nE : td.nN;
-      const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
-      const T* srcB = we ? P.edgeW : P.edgeS;
-      const int lag = we ? kTI : kTJ;
-      const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
-      unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
-      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
-      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
-      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
-      int u_pub = 0, s_i = 0, e_next = 0;
-      while (u_pub < NS) {
-        const int u_old = u_pub;
+      int u_pub = 0, s_i = 0, s_l2 = 0;
+      Watchdog wd;
+      while (s_i < NS) {
+        const int before = s_i + u_pub;
         while (u_pub < NS) {
           const uint32_t q = dq + u_pub;
           if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          const int k = (NS - 1 - u_pub) - c;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u_pub % OR) * 32 + lane];
           ++u_pub;
         }
-        if (u_pub != u_old) {
-          __syncwarp();
-          __threadfence();
-          if (lane == 0) st_relaxed_u32(&prog[tid], (unsigned)u_pub);
-        }
+        const int linked = ld_acquire_cta_s(&s_linked);
+        const int lim = min(u_pub + SB - 1, linked + OR - 1);
         if (lane == 0) {
-          for (; s_i < NS && s_i <= u_pub + SB - 1; ++s_i) {
+          for (; s_i < NS && s_i <= lim; ++s_i) {
             const int t = NS - 1 - s_i;
             const uint32_t q = rq + s_i;
             T* dst = s_rg + (q % SB) * 5 * kTT;
@@ -648,26 +727,67 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
             issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false,
                            0);
           }
+          if (s_l2 < s_i) s_l2 = s_i;
+          for (; s_l2 < NS && s_l2 < s_i + kPF; ++s_l2) {
+            const int t = NS - 1 - s_l2;
+            prefetch_l2(r_src + (long long)t * kTT, kTT * sizeof(T));
+            prefetch_l2(ph_src + (long long)t * kTT, kTT * sizeof(T));
+            prefetch_l2(bw_src + (long long)t * B_NA * kTT, B_NA * kTT * sizeof(T));
+          }
         }
-        int m = min(NS - 1, u_pub + ER - 1);
+        s_i = __shfl_sync(0xffffffffu, s_i, 0);
+        if (s_i + u_pub != before) wd.progress(); else wd.idle(13);
+      }
+    } else if (warp == kLinkerWarp) {
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool colok = we ? (c < td.wJ) : (c < td.wI);
+      const int nB = we ? td.nE : td.nN;
+      const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
+      const T* srcB = (we ? P.edgeW : P.edgeS) + edgeB + c;
+      const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
+      unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
+      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
+      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
+      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
+      int u_lk = 0, e_next = 0;
+      Watchdog wd;
+      while (u_lk < NS) {
+        const int before = u_lk + e_next;
+        const int u_old = u_lk;
+        while (u_lk < NS) {
+          const uint32_t q = dq + u_lk;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          const int k = (NS - 1 - u_lk) - c;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u_lk % OR) * 32 + lane];
+          ++u_lk;
+        }
+        if (u_lk != u_old) {
+          __syncwarp();
+          fence_gpu();
+          if (lane == 0) {
+            st_relaxed_u32(&prog[tid], (unsigned)u_lk);
+            st_release_cta_s(&s_linked, u_lk);
+          }
+        }
+        int m = min(NS - 1, u_lk + ER - 1);
         if (e_next <= m) {
           cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e_next + kTI, NS));
           cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e_next + kTJ, NS));
           if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
           if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
           for (int s = e_next; s <= m; ++s) {
-            const int t = NS - 1 - s;
-            const int k = t - offB;
+            const int k = (NS - 1 - s) - offB;
             T v = T(0);
-            if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + edgeB + (long long)k * 16 + c);
+            if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + (long long)k * 16);
             s_edge[((eq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
           }
           __syncwarp();
           if (lane == 0)
             for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
           if (m >= e_next) e_next = m + 1;
-          (void)lag;
         }
+        if (u_lk + e_next != before) wd.progress(); else wd.idle(14);
       }
     } else {
       const bool col = ti < td.wI && tj < td.wJ;
@@ -678,9 +798,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         const int k = t - d;
         {
           const uint32_t q = rq + u;  // unconditional: bounds the run-ahead (see K2)
-          mbar_wait(&b_rg[q % SB], (q / SB) & 1);
+          mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);
           const uint32_t r = eq + u;
-          mbar_wait(&b_edge[r % ER], (r / ER) & 1);
+          mbar_wait(&b_edge[r % ER], (r / ER) & 1, 32);
         }
         if (col && k >= 0 && k < nz) {
           const T* rec = s_edge + ((eq + u) % ER) * NE;
