@@ -113,6 +113,8 @@ struct sip_ctx {
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo
   double t_fwd = 0, t_bwd = 0, t_halo = 0;
   long long launches = 0, prof_launches = 0;
+  unsigned long long* trace = nullptr;  // debug: per-tile timestamps of the last F/B sweeps
+  int trace_tile = 0;
   std::string err;
 };
 
@@ -465,6 +467,8 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
   p.partial = ctx->partial;
   p.block_norms = ctx->d_bnorms + (size_t)it * std::max<size_t>(1, ctx->local.size());
   p.norm = ctx->d_norms + it;
+  p.trace = ctx->trace ? ctx->trace + (forward ? 0 : 4 * ctx->htiles.size()) : nullptr;
+  p.trace_tile = ctx->trace_tile;
   return p;
 }
 
@@ -600,7 +604,7 @@ int sip_destroy(sip_ctx* ctx) {
   void* ptrs[] = {ctx->d_blocks, ctx->d_tiles, ctx->d_order_f, ctx->d_order_b, ctx->fw, ctx->bw,
                   ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
                   ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
-                  ctx->staging, ctx->d_local_copies, ctx->phi_stage};
+                  ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->precision == SIP_PREC_SINGLE) {
@@ -1077,6 +1081,28 @@ int sip_debug_edges(sip_ctx* ctx, int which, double* out, long long* count) {
                                : (double)reinterpret_cast<float*>(tmp.data())[x];
   }
   *count = n;
+  return SIP_OK;
+}
+
+// Per-tile timestamps (ns) of the most recent forward and backward sweep:
+// out[2][ntiles][4] = {start, end, smid, cta}.  Enabled by the first call.
+int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
+  if (!ctx || !ntiles) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  const size_t nt = ctx->htiles.size();
+  *ntiles = (long long)nt;
+  if (!ctx->trace) {
+    // table [2][nt][4] + per-step record of one tile (forward: 4 x slices)
+    const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
+    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 4 * ns)));
+    if (const char* tt = getenv("SIPB_TRACE_TILE")) ctx->trace_tile = atoi(tt);
+    return SIP_OK;
+  }
+  if (out) {
+    const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 4 * ns), cudaMemcpyDeviceToHost));
+  }
   return SIP_OK;
 }
 

@@ -148,6 +148,8 @@ struct SweepParams {
   double* partial;        // [ntiles] tile norm partials
   double* block_norms;    // [nblocks] row of this iteration (forward only)
   double* norm;           // scalar slot of this iteration (forward only)
+  unsigned long long* trace;  // optional [ntiles][4]: start ns, end ns, smid, cta (debug)
+  int trace_tile;             // debug: tile whose per-step times are recorded after the table
 };
 
 struct FactorParams {

@@ -417,6 +417,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     const BlockDesc bd = P.blocks[td.block];
     const int NS = td.ns, nz = td.nz;
     double nrm = 0.0;
+    if (P.trace && p == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      P.trace[4 * tid + 0] = gtime();
+      P.trace[4 * tid + 2] = smid;
+      P.trace[4 * tid + 3] = blockIdx.x;
+    }
 
     if (warp == kLoaderWarp) {
       // ------------------------------------------------------------ loader
@@ -559,10 +566,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           // idle this step: that bounds how far the compute warps can run ahead
           // of the service warps, so an mbarrier is never waited on a phase two
           // behind (which try_wait would report as complete)
+          unsigned long long* tr =
+              (P.trace && p == 0 && tid == P.trace_tile) ? P.trace + 8 * P.ntiles + 4 * t : nullptr;
+          if (tr) tr[0] = gtime();
           const uint32_t q = fq + t;
           mbar_wait(&b_fw[q % SF], (q / SF) & 1, 21);
+          if (tr) tr[1] = gtime();
           const uint32_t r = eq + t;
           mbar_wait(&b_edge[r % ER], (r / ER) & 1, 22);
+          if (tr) tr[2] = gtime();
         }
         if (col && k >= 0 && k < nz) {
           {
@@ -612,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     }
     fq += NS; pq += NS; eq += NS; dq += NS;
     __syncthreads();  // linker has published NS (all steps retired)
+    if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
       P.partial[tid] = s;
@@ -699,6 +712,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     const int tid = P.order[tk];
     const TileDesc td = P.tiles[tid];
     const int NS = td.ns, nz = td.nz;
+    if (P.trace && p == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      P.trace[4 * tid + 0] = gtime();
+      P.trace[4 * tid + 2] = smid;
+      P.trace[4 * tid + 3] = blockIdx.x;
+    }
 
     if (warp == kLoaderWarp) {
       const T* r_src = P.R + td.slot * kTT;
@@ -821,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     }
     rq += NS; eq += NS; dq += NS;
     __syncthreads();
+    if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     if (p == 0) {
       __threadfence();
       s_last = (atomicAdd(P.state + 1, 1u) == (unsigned)P.ntiles - 1);
