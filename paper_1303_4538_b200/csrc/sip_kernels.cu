@@ -306,8 +306,9 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
 // on shared-memory mbarriers, compute, store, and meet at one named barrier.
 // =============================================================================
 constexpr int kCompute = kTT;       // compute threads (8 warps)
-constexpr int kThreads = kTT + 64;  // + loader warp + linker warp
+constexpr int kThreads = kTT + 96;  // + loader, publisher / linker, fetcher warps
 constexpr int kLoaderWarp = kTT / 32, kLinkerWarp = kTT / 32 + 1;
+constexpr int kPublisherWarp = kLinkerWarp, kFetcherWarp = kTT / 32 + 2;
 constexpr int kPF = 12;             // L2 prefetch distance (slices) beyond the ring
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
@@ -355,31 +356,42 @@ __device__ __forceinline__ bool warp_test(uint64_t* b, uint32_t parity) {
 
 template <typename T, int SF>
 struct FwdCfg {
-  static constexpr int SP = SF + 2;  // phi slice s is read at steps s-1, s, s+1
-  static constexpr int ER = 8;       // edge records in flight
+  static constexpr int SP = SF + 2;  // phi slice s is read while preparing steps s-1, s, s+1
+  static constexpr int ER = SF;      // edge records share the slot barrier of their step
   static constexpr int OR = 8;       // outgoing edge records
-  static constexpr int DR = 16;      // step-done barriers (> OR + SF)
+  static constexpr int EB = 16;      // "step prepared" (slot empty) barriers
+  static constexpr int DR = 16;      // "step done" barriers
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
   static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SF + SP + ER + DR) * sizeof(uint64_t);
+                                  (SF + EB + DR) * sizeof(uint64_t);
 };
 
+// Step pipeline of one compute thread (K2):
+//   prep(x):  wait for slice x / edge record x, evaluate the residual of step x
+//             and pre = r - LB*R_B (everything that does not depend on the
+//             in-tile neighbours of step x-1), then signal "slice x consumed";
+//   step(t):  after the named barrier, R = ((pre - LW*R_W) - LS*R_S) * LP,
+//             store, signal "step t done", prep(t+1), barrier.
+// The recurrence's critical path per step is thus two shared loads, four
+// dependent flops and one barrier; the operation order per cell is exactly
+// the oracle's (pre is the oracle's first subtraction).
 template <typename T, int SF>
 __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
   using C = FwdCfg<T, SF>;
-  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
-  static_assert(DR > OR + SF, "done ring must cover the run-ahead");
+  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, EB = C::EB, NE = C::NE, OR = C::OR;
+  static_assert(EB > SF + 1 && EB > ER && DR > OR + SF, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_fw = reinterpret_cast<T*>(smem);
   T* s_ph = s_fw + SF * F_NA * kTT;
   T* s_R = s_ph + SP * kTT;
   T* s_edge = s_R + 2 * kTT;
   T* s_out = s_edge + ER * NE;  // [OR][32]: R of the E column (tj) and N row (16 + ti)
+  // b_fw[x % SF] completes when FW slice x, phi slice x+1 (and, for x = 0,
+  // phi slice 0) have landed AND the fetcher has written edge record x
   uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_out + OR * 32);
-  uint64_t* b_ph = b_fw + SF;
-  uint64_t* b_edge = b_ph + SP;
-  uint64_t* b_done = b_edge + ER;
+  uint64_t* b_empty = b_fw + SF;
+  uint64_t* b_done = b_empty + EB;
   __shared__ int s_tile, s_last, s_linked;
   __shared__ double s_red[kThreads / 32];
 
@@ -395,13 +407,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 1);
-    for (int b = 0; b < SP; ++b) mbar_init(&b_ph[b], 1);
-    for (int b = 0; b < ER; ++b) mbar_init(&b_edge[b], 1);
+    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 2);  // loader (expect_tx) + fetcher
+    for (int b = 0; b < EB; ++b) mbar_init(&b_empty[b], kCompute / 32);
     for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t fq = 0, pq = 0, eq = 0, dq = 0;  // CTA-uniform ring sequence bases
+  uint32_t sq = 0;  // CTA-uniform step sequence base (all rings advance once per step)
 
   for (;;) {
     __syncthreads();
@@ -427,44 +438,86 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 
     if (warp == kLoaderWarp) {
       // ------------------------------------------------------------ loader
-      const T* fw_src = P.fw + td.slot * F_NA * kTT;
-      const T* ph_src = P.phi + td.slot * kTT;
-      int t_pub = 0, s_f = 0, s_p = 0, s_l2 = 0;
-      Watchdog wd;
-      while (s_f < NS || s_p < NS) {
-        const int before = s_f + s_p + t_pub;
-        while (t_pub < NS) {
-          const uint32_t q = dq + t_pub;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          ++t_pub;
+      if (lane == 0) {
+        const T* fw_src = P.fw + td.slot * F_NA * kTT;
+        const T* ph_src = P.phi + td.slot * kTT;
+        // step s's transaction: FW slice s + phi slice s+1 (+ phi slice 0 for s = 0)
+        auto fw = [&](int s) {
+          const uint32_t q = sq + s;
+          uint64_t* bar = &b_fw[q % SF];
+          uint32_t tx = slice_bytes<T>(s, nz, F_NA);
+          if (s + 1 < NS) tx += slice_bytes<T>(s + 1, nz, 1);
+          if (s == 0) tx += slice_bytes<T>(0, nz, 1);
+          mbar_expect_tx(bar, tx);
+          issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s,
+                         nz, bar, false, 0);
+          if (s + 1 < NS)
+            issue_slice<T>(s_ph + ((q + 1) % SP) * kTT, ph_src + (long long)(s + 1) * kTT, 1, s + 1,
+                           nz, bar, false, 0);
+          if (s == 0) issue_slice<T>(s_ph + (q % SP) * kTT, ph_src, 1, 0, nz, bar, false, 0);
+        };
+        int l2 = 0;
+        auto pf = [&](int upto) {
+          for (; l2 < NS && l2 <= upto; ++l2) {
+            int lo, hi;
+            slice_range<T>(l2, nz, lo, hi);
+            if (lo == 0 && hi == kTT) {
+              prefetch_l2(fw_src + (long long)l2 * F_NA * kTT, F_NA * kTT * sizeof(T));
+            } else {
+              for (int a = 0; a < F_NA; ++a)
+                prefetch_l2(fw_src + ((long long)l2 * F_NA + a) * kTT + lo, (hi - lo) * sizeof(T));
+            }
+            prefetch_l2(ph_src + (long long)l2 * kTT + lo, (hi - lo) * sizeof(T));
+          }
+        };
+        for (int s = 0; s < SF && s < NS; ++s) fw(s);
+        pf(SF + kPF);
+        Watchdog wd;
+        for (int x = 0; x < NS; ++x) {
+          const uint32_t q = sq + x;
+          mbar_wait(&b_empty[q % EB], (q / EB) & 1, 41);  // slice x consumed by prep(x)
+          const int s = x + SF;
+          if (s < NS) {
+            // compute step s writes out-record slot s % OR: the publisher must be past s - OR
+            while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(42);
+            fw(s);  // phi slice s+1 reuses the slot of phi slice s+1-SP = x-1, last read by prep(x)
+          }
+          pf(s + kPF);
         }
-        const int linked = ld_acquire_cta_s(&s_linked);
-        // compute step x needs FW slice x and phi slice x+1; it may not get
-        // OR steps ahead of the linker (out-record ring)
-        const int lim = min(t_pub + SF - 1, linked + OR - 1);
-        if (lane == 0) {
-          for (; s_f < NS && s_f <= lim; ++s_f) {
-            const uint32_t q = fq + s_f;
-            issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s_f * F_NA * kTT, F_NA,
-                           s_f, nz, &b_fw[q % SF], true, 0);
-          }
-          for (; s_p < NS && s_p <= min(t_pub + SP - 2, lim + 1); ++s_p) {
-            const uint32_t q = pq + s_p;
-            issue_slice<T>(s_ph + (q % SP) * kTT, ph_src + (long long)s_p * kTT, 1, s_p, nz,
-                           &b_ph[q % SP], true, 0);
-          }
-          if (s_l2 < s_f) s_l2 = s_f;
-          for (; s_l2 < NS && s_l2 < s_f + kPF; ++s_l2) {
-            prefetch_l2(fw_src + (long long)s_l2 * F_NA * kTT, F_NA * kTT * sizeof(T));
-            prefetch_l2(ph_src + (long long)s_l2 * kTT, kTT * sizeof(T));
-          }
-        }
-        s_f = __shfl_sync(0xffffffffu, s_f, 0);
-        s_p = __shfl_sync(0xffffffffu, s_p, 0);
-        if (s_f + s_p + t_pub != before) wd.progress(); else wd.idle(11);
       }
-    } else if (warp == kLinkerWarp) {
-      // ------------------------------------------------------------ linker
+    } else if (warp == kPublisherWarp) {
+      // --------------------------------------------------------- publisher
+      // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
+      const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
+      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
+      int t = 0;
+      while (t < NS) {
+        {
+          const uint32_t q = sq + t;
+          mbar_wait(&b_done[q % DR], (q / DR) & 1, 43);
+        }
+        int t_end = t + 1;
+        while (t_end < NS) {
+          const uint32_t q = sq + t_end;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          ++t_end;
+        }
+        for (; t < t_end; ++t) {
+          const int k = t - outoff;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t % OR) * 32 + lane];
+        }
+        __syncwarp();
+        fence_gpu();  // release pattern: edge values before the progress counter
+        if (lane == 0) {
+          st_relaxed_u32(&prog[tid], (unsigned)t);
+          st_release_cta_s(&s_linked, t);
+        }
+      }
+    } else if (warp == kFetcherWarp) {
+      // ----------------------------------------------------------- fetcher
       // lanes 0-15 serve the W/E sides (index = tj), lanes 16-31 the S/N sides (index = ti)
       const bool we = lane < 16;
       const int c = lane & 15;
@@ -483,72 +536,58 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const T* eA = (we ? P.edgeW : P.edgeS) + edgeA + c;
       const long long gstride = we ? bd.ny : bd.nx;
       unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
-      // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
-      const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
-      const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
-      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
-      int t_lk = 0, e_next = 0;
+      int e = 0, freed = 0;  // record s may be written once prep(s - ER) is done (freed > s - ER)
       Watchdog wd;
-      while (t_lk < NS) {
-        const int before = t_lk + e_next;
-        // (1) retire finished steps: forward their edge R to global, then
-        //     publish progress (release pattern)
-        const int t_old = t_lk;
-        while (t_lk < NS) {
-          const uint32_t q = dq + t_lk;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          const int k = t_lk - outoff;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t_lk % OR) * 32 + lane];
-          ++t_lk;
+      while (e < NS) {
+        while (freed < e + 1 && freed < NS) {  // slots of consumed records
+          const uint32_t q = sq + freed;
+          if (!warp_test(&b_empty[q % EB], (q / EB) & 1)) break;
+          ++freed;
         }
-        if (t_lk != t_old) {
-          __syncwarp();
-          fence_gpu();
-          if (lane == 0) {
-            st_relaxed_u32(&prog[tid], (unsigned)t_lk);
-            st_release_cta_s(&s_linked, t_lk);
-          }
-        }
-        // (2) edge records of upcoming steps, as far as upstream progress allows
-        int m = min(NS - 1, t_lk + ER - 1);
-        if (e_next <= m) {
-          cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e_next + kTI, NS));
-          cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e_next + kTJ, NS));
+        int m = min(NS - 1, freed + ER - 1);
+        if (m >= e) {
+          cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e + kTI, NS));
+          cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e + kTJ, NS));
           // record s needs cW >= min(s + TI, NS) and cS >= min(s + TJ, NS)
           if (cW < (unsigned)NS) m = min(m, (int)cW - kTI);
           if (cS < (unsigned)NS) m = min(m, (int)cS - kTJ);
-          for (int s = e_next; s <= m; ++s) {
-            T* rec = s_edge + ((eq + s) % ER) * NE;
-            T phA = T(0), phB = T(0), rA = T(0);
-            const int kA = s - c;  // W side cell (0, c) / S side cell (c, 0)
-            if (colok && kA >= 0 && kA < nz) {
-              if (nA >= 0) {
-                phA = P.phi[(slotA + s + lag - 1) * kTT + posA];
-                rA = ld_relaxed(eA + (long long)kA * 16);
-              } else {
-                phA = gA[gstride * kA];
-              }
-            }
-            const int kB = s - offB;
-            if (colok && kB >= 0 && kB < nz) {
-              if (nB >= 0) {
-                phB = P.phi[(slotB + s - lag + 1) * kTT + posB];
-              } else {
-                phB = gB[gstride * kB];
-              }
-            }
-            rec[(we ? 0 : 32) + c] = phA;
-            rec[(we ? 16 : 48) + c] = phB;
-            rec[(we ? 64 : 80) + c] = rA;
-          }
-          __syncwarp();
-          if (lane == 0)
-            for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
-          if (m >= e_next) e_next = m + 1;
         }
-        if (t_lk + e_next != before) wd.progress(); else wd.idle(12);
+        if (m < e) {
+          wd.idle(44);
+          __nanosleep(64);
+          continue;
+        }
+        wd.progress();
+        for (int s = e; s <= m; ++s) {
+          T* rec = s_edge + ((sq + s) % ER) * NE;
+          T phA = T(0), phB = T(0), rA = T(0);
+          const int kA = s - c;  // W side cell (0, c) / S side cell (c, 0)
+          if (colok && kA >= 0 && kA < nz) {
+            if (nA >= 0) {
+              phA = P.phi[(slotA + s + lag - 1) * kTT + posA];
+              rA = ld_relaxed(eA + (long long)kA * 16);
+            } else {
+              phA = gA[gstride * kA];
+            }
+          }
+          const int kB = s - offB;
+          if (colok && kB >= 0 && kB < nz) {
+            if (nB >= 0) {
+              phB = P.phi[(slotB + s - lag + 1) * kTT + posB];
+            } else {
+              phB = gB[gstride * kB];
+            }
+          }
+          rec[(we ? 0 : 32) + c] = phA;
+          rec[(we ? 16 : 48) + c] = phB;
+          rec[(we ? 64 : 80) + c] = rA;
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int s = e; s <= m; ++s) mbar_arrive(&b_fw[(sq + s) % SF]);
+        e = m + 1;
       }
-    } else {
+    } else if (warp < kLoaderWarp) {
       // --------------------------------------------------------- compute warps
       const bool col = ti < td.wI && tj < td.wJ;
       const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
@@ -558,38 +597,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         ghB = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
         ghT = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
       }
-      T RB = T(0);
-      for (int t = 0; t < NS; ++t) {
-        const int k = t - d;
-        {
-          // every compute thread waits for slice t and edge record t, even if
-          // idle this step: that bounds how far the compute warps can run ahead
-          // of the service warps, so an mbarrier is never waited on a phase two
-          // behind (which try_wait would report as complete)
-          unsigned long long* tr =
-              (P.trace && p == 0 && tid == P.trace_tile) ? P.trace + 8 * P.ntiles + 4 * t : nullptr;
-          if (tr) tr[0] = gtime();
-          const uint32_t q = fq + t;
-          mbar_wait(&b_fw[q % SF], (q / SF) & 1, 21);
-          if (tr) tr[1] = gtime();
-          const uint32_t r = eq + t;
-          mbar_wait(&b_edge[r % ER], (r / ER) & 1, 22);
-          if (tr) tr[2] = gtime();
-        }
-        if (col && k >= 0 && k < nz) {
-          {
-            const uint32_t q = pq + t;  // slice t (t-1 completed earlier)
-            mbar_wait(&b_ph[q % SP], (q / SP) & 1, 23);
-          }
-          if (t + 1 < NS) {  // slice t+1 holds phi(k+1) and the E / N neighbours at k
-            const uint32_t q = pq + t + 1;
-            mbar_wait(&b_ph[q % SP], (q / SP) & 1, 24);
-          }
-          const T* rec = s_edge + ((eq + t) % ER) * NE;
-          const T* f = s_fw + ((fq + t) % SF) * F_NA * kTT + p;
-          const T* ph0 = s_ph + ((pq + t) % SP) * kTT;
-          const T* phm = s_ph + ((pq + t + SP - 1) % SP) * kTT;
-          const T* php = s_ph + ((pq + t + 1) % SP) * kTT;
+      T RB = T(0);                                   // own R of the previous plane
+      T pre = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
+      T rwx = T(0), rsx = T(0);                      // cross-tile R_W / R_S of the prepared step
+      bool act = false;
+      unsigned long long* trp = nullptr;  // debug trace slots of the step being prepared
+      auto prep = [&](int x) {
+        const uint32_t q = sq + x;
+        if (trp) trp[0] = gtime();
+        // one wait covers FW slice x, phi slice x+1 and edge record x (phi
+        // slices x-1 and x arrived with the transactions of steps x-2 and x-1,
+        // which every compute thread has already waited for)
+        mbar_wait(&b_fw[q % SF], (q / SF) & 1, 21);
+        if (trp) trp[1] = gtime();
+        const int k = x - d;
+        act = col && k >= 0 && k < nz;
+        if (act) {
+          if (trp) trp[3] = gtime();
+          const T* rec = s_edge + (q % ER) * NE;
+          const T* f = s_fw + (q % SF) * F_NA * kTT + p;
+          const T* ph0 = s_ph + (q % SP) * kTT;
+          const T* phm = s_ph + ((q + SP - 1) % SP) * kTT;
+          const T* php = s_ph + ((q + 1) % SP) * kTT;
           const T fP = ph0[p];
           const T fB = k > 0 ? phm[p] : ghB;
           const T fT = k + 1 < nz ? php[p] : ghT;
@@ -607,10 +636,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           r += f[F_Q * kTT];
           r -= f[F_AP * kTT] * fP;
           nrm += fabs(static_cast<double>(r));
-          const T RW = inW ? s_R[((t - 1) & 1) * kTT + pW] : rec[64 + tj];
-          const T RS = inS ? s_R[((t - 1) & 1) * kTT + pS] : rec[80 + ti];
-          const T Rv = (((r - f[F_LB * kTT] * RB) - f[F_LW * kTT] * RW) - f[F_LS * kTT] * RS) *
-                       f[F_LP * kTT];
+          pre = r - f[F_LB * kTT] * RB;
+          lw = f[F_LW * kTT];
+          ls = f[F_LS * kTT];
+          lp = f[F_LP * kTT];
+          rwx = rec[64 + tj];
+          rsx = rec[80 + ti];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_empty[q % EB]);
+      };
+      const bool tracing = P.trace && p == 0 && tid == P.trace_tile;
+      if (tracing) trp = P.trace + 8 * P.ntiles;
+      prep(0);
+      for (int t = 0; t < NS; ++t) {
+        if (act) {
+          const T RW = inW ? s_R[((t - 1) & 1) * kTT + pW] : rwx;
+          const T RS = inS ? s_R[((t - 1) & 1) * kTT + pS] : rsx;
+          const T Rv = ((pre - lw * RW) - ls * RS) * lp;
           RB = Rv;
           P.R[(td.slot + t) * kTT + p] = Rv;
           s_R[(t & 1) * kTT + p] = Rv;
@@ -618,12 +661,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           if (tj == kTJ - 1) s_out[(t % OR) * 32 + 16 + ti] = Rv;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&b_done[(dq + t) % DR]);
+        if (lane == 0) mbar_arrive(&b_done[(sq + t) % DR]);
+        if (tracing) trp = P.trace + 8 * P.ntiles + 4 * (t + 1);
+        if (t + 1 < NS) prep(t + 1);
         bar_compute();
       }
     }
-    fq += NS; pq += NS; eq += NS; dq += NS;
-    __syncthreads();  // linker has published NS (all steps retired)
+    sq += NS;
+    __syncthreads();  // publisher has published NS (all steps retired)
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
@@ -658,29 +703,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 // =============================================================================
 // K3: backward substitution + phi update (backward3d); slices in reverse.
 // Ring slot = {R, phi, UN, UE, UT} of one slice; edge record = delta of the
-// E and N neighbour tiles (16 each).
+// E and N neighbour tiles (16 each).  Same warp roles and step pipeline as K2:
+// prep(x) loads the slot into registers and forms UT*dT; the critical step is
+// ((R - UN*dN) - UE*dE) - UT*dT after the barrier.
 // =============================================================================
 template <typename T, int SB>
 struct BwdCfg {
-  static constexpr int ER = 8, NE = 32, OR = 8, DR = 24;
+  static constexpr int ER = SB, NE = 32, OR = 8, EB = 16, DR = 24;
   static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SB + ER + DR) * sizeof(uint64_t);
+                                  (SB + EB + DR) * sizeof(uint64_t);
 };
 
 template <typename T, int SB>
 __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
   using C = BwdCfg<T, SB>;
-  constexpr int ER = C::ER, DR = C::DR, NE = C::NE, OR = C::OR;
-  static_assert(DR > OR + SB, "done ring must cover the run-ahead");
+  constexpr int ER = C::ER, DR = C::DR, EB = C::EB, NE = C::NE, OR = C::OR;
+  static_assert(EB > SB + 1 && DR > OR + SB, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_rg = reinterpret_cast<T*>(smem);
   T* s_D = s_rg + SB * 5 * kTT;
   T* s_edge = s_D + 2 * kTT;
   T* s_out = s_edge + ER * NE;  // [OR][32]: delta of the W column (tj) and S row (16 + ti)
+  // b_rg[u % SB] completes when slot u has landed AND edge record u is written
   uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
-  uint64_t* b_edge = b_rg + SB;
-  uint64_t* b_done = b_edge + ER;
+  uint64_t* b_empty = b_rg + SB;
+  uint64_t* b_done = b_empty + EB;
   __shared__ int s_tile, s_last, s_linked;
 
   const int p = threadIdx.x;
@@ -693,12 +741,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 1);
-    for (int b = 0; b < ER; ++b) mbar_init(&b_edge[b], 1);
+    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 2);  // loader (expect_tx) + fetcher
+    for (int b = 0; b < EB; ++b) mbar_init(&b_empty[b], kCompute / 32);
     for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t rq = 0, eq = 0, dq = 0;
+  uint32_t sq = 0;
 
   for (;;) {
     __syncthreads();
@@ -721,44 +769,81 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     }
 
     if (warp == kLoaderWarp) {
-      const T* r_src = P.R + td.slot * kTT;
-      const T* ph_src = P.phi + td.slot * kTT;
-      const T* bw_src = P.bw + td.slot * B_NA * kTT;
-      int u_pub = 0, s_i = 0, s_l2 = 0;
-      Watchdog wd;
-      while (s_i < NS) {
-        const int before = s_i + u_pub;
-        while (u_pub < NS) {
-          const uint32_t q = dq + u_pub;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          ++u_pub;
-        }
-        const int linked = ld_acquire_cta_s(&s_linked);
-        const int lim = min(u_pub + SB - 1, linked + OR - 1);
-        if (lane == 0) {
-          for (; s_i < NS && s_i <= lim; ++s_i) {
-            const int t = NS - 1 - s_i;
-            const uint32_t q = rq + s_i;
-            T* dst = s_rg + (q % SB) * 5 * kTT;
-            uint64_t* bar = &b_rg[q % SB];
-            mbar_expect_tx(bar, 2 * slice_bytes<T>(t, nz, 1) + slice_bytes<T>(t, nz, B_NA));
-            issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-            issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-            issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false,
-                           0);
+      if (lane == 0) {
+        const T* r_src = P.R + td.slot * kTT;
+        const T* ph_src = P.phi + td.slot * kTT;
+        const T* bw_src = P.bw + td.slot * B_NA * kTT;
+        auto slot = [&](int u) {
+          const int t = NS - 1 - u;
+          const uint32_t q = sq + u;
+          T* dst = s_rg + (q % SB) * 5 * kTT;
+          uint64_t* bar = &b_rg[q % SB];
+          mbar_expect_tx(bar, 2 * slice_bytes<T>(t, nz, 1) + slice_bytes<T>(t, nz, B_NA));
+          issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+          issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
+          issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false, 0);
+        };
+        int l2 = 0;
+        auto pf = [&](int upto) {
+          for (; l2 < NS && l2 <= upto; ++l2) {
+            const int t = NS - 1 - l2;
+            int lo, hi;
+            slice_range<T>(t, nz, lo, hi);
+            const uint32_t b1 = (hi - lo) * sizeof(T);
+            prefetch_l2(r_src + (long long)t * kTT + lo, b1);
+            prefetch_l2(ph_src + (long long)t * kTT + lo, b1);
+            if (lo == 0 && hi == kTT) {
+              prefetch_l2(bw_src + (long long)t * B_NA * kTT, B_NA * kTT * sizeof(T));
+            } else {
+              for (int a = 0; a < B_NA; ++a)
+                prefetch_l2(bw_src + ((long long)t * B_NA + a) * kTT + lo, b1);
+            }
           }
-          if (s_l2 < s_i) s_l2 = s_i;
-          for (; s_l2 < NS && s_l2 < s_i + kPF; ++s_l2) {
-            const int t = NS - 1 - s_l2;
-            prefetch_l2(r_src + (long long)t * kTT, kTT * sizeof(T));
-            prefetch_l2(ph_src + (long long)t * kTT, kTT * sizeof(T));
-            prefetch_l2(bw_src + (long long)t * B_NA * kTT, B_NA * kTT * sizeof(T));
+        };
+        for (int u = 0; u < SB && u < NS; ++u) slot(u);
+        pf(SB + kPF);
+        Watchdog wd;
+        for (int x = 0; x < NS; ++x) {
+          const uint32_t q = sq + x;
+          mbar_wait(&b_empty[q % EB], (q / EB) & 1, 51);
+          const int s = x + SB;
+          if (s < NS) {
+            while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(52);
+            slot(s);
           }
+          pf(s + kPF);
         }
-        s_i = __shfl_sync(0xffffffffu, s_i, 0);
-        if (s_i + u_pub != before) wd.progress(); else wd.idle(13);
       }
-    } else if (warp == kLinkerWarp) {
+    } else if (warp == kPublisherWarp) {
+      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
+      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
+      int u = 0;
+      while (u < NS) {
+        {
+          const uint32_t q = sq + u;
+          mbar_wait(&b_done[q % DR], (q / DR) & 1, 53);
+        }
+        int u_end = u + 1;
+        while (u_end < NS) {
+          const uint32_t q = sq + u_end;
+          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          ++u_end;
+        }
+        for (; u < u_end; ++u) {
+          const int k = (NS - 1 - u) - c;
+          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u % OR) * 32 + lane];
+        }
+        __syncwarp();
+        fence_gpu();
+        if (lane == 0) {
+          st_relaxed_u32(&prog[tid], (unsigned)u);
+          st_release_cta_s(&s_linked, u);
+        }
+      }
+    } else if (warp == kFetcherWarp) {
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool colok = we ? (c < td.wJ) : (c < td.wI);
@@ -767,79 +852,85 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const T* srcB = (we ? P.edgeW : P.edgeS) + edgeB + c;
       const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
       unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
-      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
-      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
-      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
-      int u_lk = 0, e_next = 0;
+      int e = 0, freed = 0;
       Watchdog wd;
-      while (u_lk < NS) {
-        const int before = u_lk + e_next;
-        const int u_old = u_lk;
-        while (u_lk < NS) {
-          const uint32_t q = dq + u_lk;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
-          const int k = (NS - 1 - u_lk) - c;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u_lk % OR) * 32 + lane];
-          ++u_lk;
+      while (e < NS) {
+        while (freed < e + 1 && freed < NS) {
+          const uint32_t q = sq + freed;
+          if (!warp_test(&b_empty[q % EB], (q / EB) & 1)) break;
+          ++freed;
         }
-        if (u_lk != u_old) {
-          __syncwarp();
-          fence_gpu();
-          if (lane == 0) {
-            st_relaxed_u32(&prog[tid], (unsigned)u_lk);
-            st_release_cta_s(&s_linked, u_lk);
-          }
-        }
-        int m = min(NS - 1, u_lk + ER - 1);
-        if (e_next <= m) {
-          cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e_next + kTI, NS));
-          cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e_next + kTJ, NS));
+        int m = min(NS - 1, freed + ER - 1);
+        if (m >= e) {
+          cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e + kTI, NS));
+          cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e + kTJ, NS));
           if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
           if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
-          for (int s = e_next; s <= m; ++s) {
-            const int k = (NS - 1 - s) - offB;
-            T v = T(0);
-            if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + (long long)k * 16);
-            s_edge[((eq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
-          }
-          __syncwarp();
-          if (lane == 0)
-            for (int s = e_next; s <= m; ++s) mbar_arrive(&b_edge[(eq + s) % ER]);
-          if (m >= e_next) e_next = m + 1;
         }
-        if (u_lk + e_next != before) wd.progress(); else wd.idle(14);
+        if (m < e) {
+          wd.idle(54);
+          __nanosleep(64);
+          continue;
+        }
+        wd.progress();
+        for (int s = e; s <= m; ++s) {
+          const int k = (NS - 1 - s) - offB;
+          T v = T(0);
+          if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + (long long)k * 16);
+          s_edge[((sq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int s = e; s <= m; ++s) mbar_arrive(&b_rg[(sq + s) % SB]);
+        e = m + 1;
       }
-    } else {
+    } else if (warp < kLoaderWarp) {
       const bool col = ti < td.wI && tj < td.wJ;
       const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
       T dT = T(0);
+      T rr = T(0), ph = T(0), un = T(0), ue = T(0), utdt = T(0), dnx = T(0), dex = T(0);
+      bool act = false;
+      int kk = 0;
+      auto prep = [&](int x) {
+        const uint32_t q = sq + x;
+        mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);
+        const int t = NS - 1 - x;
+        kk = t - d;
+        act = col && kk >= 0 && kk < nz;
+        if (act) {
+          const T* sl = s_rg + (q % SB) * 5 * kTT + p;
+          const T* rec = s_edge + (q % ER) * NE;
+          rr = sl[0];
+          ph = sl[kTT];
+          un = sl[2 * kTT];
+          ue = sl[3 * kTT];
+          utdt = sl[4 * kTT] * dT;
+          dnx = rec[16 + ti];
+          dex = rec[tj];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_empty[q % EB]);
+      };
+      prep(0);
       for (int u = 0; u < NS; ++u) {
         const int t = NS - 1 - u;
-        const int k = t - d;
-        {
-          const uint32_t q = rq + u;  // unconditional: bounds the run-ahead (see K2)
-          mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);
-          const uint32_t r = eq + u;
-          mbar_wait(&b_edge[r % ER], (r / ER) & 1, 32);
-        }
-        if (col && k >= 0 && k < nz) {
-          const T* rec = s_edge + ((eq + u) % ER) * NE;
-          const T* sl = s_rg + ((rq + u) % SB) * 5 * kTT + p;
-          const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : rec[16 + ti];
-          const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : rec[tj];
-          const T dl = ((sl[0] - sl[2 * kTT] * dN) - sl[3 * kTT] * dE) - sl[4 * kTT] * dT;
+        if (act) {
+          const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : dnx;
+          const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : dex;
+          const T dl = ((rr - un * dN) - ue * dE) - utdt;
           dT = dl;
-          P.phi[(td.slot + t) * kTT + p] = sl[kTT] + dl;
+          P.phi[(td.slot + t) * kTT + p] = ph + dl;
           s_D[(u & 1) * kTT + p] = dl;
           if (ti == 0) s_out[(u % OR) * 32 + tj] = dl;
           if (tj == 0) s_out[(u % OR) * 32 + 16 + ti] = dl;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&b_done[(dq + u) % DR]);
+        if (lane == 0) mbar_arrive(&b_done[(sq + u) % DR]);
+        if (u + 1 < NS) prep(u + 1);
         bar_compute();
       }
     }
-    rq += NS; eq += NS; dq += NS;
+    sq += NS;
     __syncthreads();
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     if (p == 0) {

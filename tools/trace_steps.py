@@ -1,4 +1,5 @@
-"""Per-step timing of one tile's forward sweep (SIPB_TRACE_TILE), config-1 sizes."""
+"""Per-step timing of one tile's forward sweep (SIPB_TRACE_TILE): for step x,
+trace[x] = {prep start, FW slice ready, edge record ready, phi ready}."""
 import ctypes, sys, os
 import numpy as np
 sys.path.insert(0, ".")
@@ -22,9 +23,11 @@ st = tr[8 * nt.value:].reshape(ns, 4).astype(np.int64)
 tile = int(os.environ.get("SIPB_TRACE_TILE", "0"))
 t0 = tab[0, :, 0].min()
 print(f"{g} {prec} tile {tile}: start {(tab[0,tile,0]-t0)/1e3:.1f} us end {(tab[0,tile,1]-t0)/1e3:.1f} us; fwd span {(tab[0,:,1].max()-t0)/1e3:.1f} us")
-a = (st[:, 0] - t0) / 1e3; b = (st[:, 1] - t0) / 1e3; c = (st[:, 2] - t0) / 1e3
+a, b, c, e = [(st[:, i] - t0) / 1e3 for i in range(4)]
 step = np.diff(a)
-print("step time us: median %.3f mean %.3f p90 %.3f max %.3f" % (np.median(step), step.mean(), np.percentile(step, 90), step.max()))
-print("wait FW (b-a) median %.3f mean %.3f ; wait edge (c-b) median %.3f mean %.3f" % (np.median(b - a), (b - a).mean(), np.median(c - b), (c - b).mean()))
-for t in list(range(0, 12)) + list(range(100, 106)) + list(range(ns - 4, ns)):
-    print(f"  t={t:3d} enter {a[t]:8.2f} fw {b[t]-a[t]:6.3f} edge {c[t]-b[t]:6.3f} next {a[t+1]-c[t] if t+1<ns else 0:6.3f}")
+ok = st[:, 3] > 0
+print("prep-to-prep us: median %.3f mean %.3f p90 %.3f" % (np.median(step), step.mean(), np.percentile(step, 90)))
+print("wait FW median %.3f mean %.3f | wait edge median %.3f mean %.3f | wait phi median %.3f mean %.3f (active steps)" % (
+    np.median(b - a), (b - a).mean(), np.median(c - b), (c - b).mean(), np.median((e - c)[ok]), (e - c)[ok].mean()))
+for t in list(range(0, 6)) + list(range(100, 104)):
+    print(f"  x={t:3d} start {a[t]:8.2f} fw {b[t]-a[t]:6.3f} edge {c[t]-b[t]:6.3f} phi {(e[t]-c[t]) if ok[t] else 0:6.3f} rest {a[t+1]-max(c[t], e[t]):6.3f}")
