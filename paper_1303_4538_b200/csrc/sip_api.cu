@@ -1094,14 +1094,14 @@ int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
   if (!ctx->trace) {
     // table [2][nt][4] + per-step record of one tile (forward: 4 x slices)
     const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
-    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 4 * ns)));
+    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 16 * ns)));
     if (const char* tt = getenv("SIPB_TRACE_TILE")) ctx->trace_tile = atoi(tt);
     return SIP_OK;
   }
   if (out) {
     const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 4 * ns), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 16 * ns), cudaMemcpyDeviceToHost));
   }
   return SIP_OK;
 }

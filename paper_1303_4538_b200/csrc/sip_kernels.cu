@@ -55,6 +55,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
 // (__trap -> the launch fails with an error instead of hanging the GPU).
 constexpr unsigned long long kWatchdogNs = 4000000000ULL;
+#define TRCLK() gtime()  // debug trace clock (globaltimer: comparable across SMs)
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -309,7 +310,7 @@ constexpr int kCompute = kTT;       // compute threads (8 warps)
 constexpr int kThreads = kTT + 96;  // + loader, publisher / linker, fetcher warps
 constexpr int kLoaderWarp = kTT / 32, kLinkerWarp = kTT / 32 + 1;
 constexpr int kPublisherWarp = kLinkerWarp, kFetcherWarp = kTT / 32 + 2;
-constexpr int kPF = 12;             // L2 prefetch distance (slices) beyond the ring
+constexpr int kPF = 0;              // L2 prefetch distance (slices; 0 = off: the TMA unit is the per-SM bottleneck)
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
@@ -357,14 +358,13 @@ __device__ __forceinline__ bool warp_test(uint64_t* b, uint32_t parity) {
 template <typename T, int SF>
 struct FwdCfg {
   static constexpr int SP = SF + 2;  // phi slice s is read while preparing steps s-1, s, s+1
-  static constexpr int ER = SF;      // edge records share the slot barrier of their step
+  static constexpr int ER = 16;      // edge records (deep ring; readiness rides on the slot barrier)
   static constexpr int OR = 8;       // outgoing edge records
-  static constexpr int EB = 16;      // "step prepared" (slot empty) barriers
-  static constexpr int DR = 16;      // "step done" barriers
+  static constexpr int EB = 32;      // step barriers E[x] (> ER + SF, > OR + SF + 1)
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
   static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SF + EB + DR) * sizeof(uint64_t);
+                                  (SF + EB) * sizeof(uint64_t);
 };
 
 // Step pipeline of one compute thread (K2):
@@ -379,8 +379,8 @@ struct FwdCfg {
 template <typename T, int SF>
 __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
   using C = FwdCfg<T, SF>;
-  constexpr int SP = C::SP, ER = C::ER, DR = C::DR, EB = C::EB, NE = C::NE, OR = C::OR;
-  static_assert(EB > SF + 1 && EB > ER && DR > OR + SF, "barrier rings must cover the run-ahead");
+  constexpr int SP = C::SP, ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
+  static_assert(EB > ER + SF && EB > OR + SF + 1, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_fw = reinterpret_cast<T*>(smem);
   T* s_ph = s_fw + SF * F_NA * kTT;
@@ -390,9 +390,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   // b_fw[x % SF] completes when FW slice x, phi slice x+1 (and, for x = 0,
   // phi slice 0) have landed AND the fetcher has written edge record x
   uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_out + OR * 32);
-  uint64_t* b_empty = b_fw + SF;
-  uint64_t* b_done = b_empty + EB;
-  __shared__ int s_tile, s_last, s_linked;
+  // E[x] (b_step[(eq + x) % EB], x = 0..NS): prep(x) is done -- slice x, phi
+  // slice x-1 and edge record x are consumed -- and step x-1 is complete
+  // (its R is in s_R / s_out).  One arrival per compute warp per step.
+  uint64_t* b_step = b_fw + SF;
+  __shared__ int s_tile, s_last, s_linked, s_fetched;
   __shared__ double s_red[kThreads / 32];
 
   const int p = threadIdx.x;
@@ -408,17 +410,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 
   if (p == 0) {
     for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 2);  // loader (expect_tx) + fetcher
-    for (int b = 0; b < EB; ++b) mbar_init(&b_empty[b], kCompute / 32);
-    for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
+    for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t sq = 0;  // CTA-uniform step sequence base (all rings advance once per step)
+  uint32_t sq = 0;  // CTA-uniform step sequence base (slot rings advance NS per tile)
+  uint32_t eq = 0;  // E ring base (advances NS + 1 per tile)
 
   for (;;) {
     __syncthreads();
     if (p == 0) {
       s_tile = atomicAdd(P.state, 1u);
       s_linked = 0;
+      s_fetched = 0;
     }
     __syncthreads();
     const int tk = s_tile;
@@ -458,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         };
         int l2 = 0;
         auto pf = [&](int upto) {
+          if (kPF == 0) return;
           for (; l2 < NS && l2 <= upto; ++l2) {
             int lo, hi;
             slice_range<T>(l2, nz, lo, hi);
@@ -470,17 +474,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
             prefetch_l2(ph_src + (long long)l2 * kTT + lo, (hi - lo) * sizeof(T));
           }
         };
-        for (int s = 0; s < SF && s < NS; ++s) fw(s);
-        pf(SF + kPF);
+        unsigned long long* ltr =
+            (P.trace && tid == P.trace_tile) ? P.trace + 8 * P.ntiles : nullptr;
         Watchdog wd;
+        // edge record s is announced on the same slot barrier as slice s
+        auto announce = [&](int s) {
+          while (ld_acquire_cta_s(&s_fetched) <= s) wd.idle(46);
+          if (ltr) ltr[16 * s + 10] = TRCLK();
+          mbar_arrive(&b_fw[(sq + s) % SF]);
+        };
+        for (int s = 0; s < SF && s < NS; ++s) {
+          if (ltr) ltr[16 * s + 8] = TRCLK();
+          fw(s);
+        }
+        for (int s = 0; s < SF && s < NS; ++s) announce(s);
+        pf(SF + kPF);
         for (int x = 0; x < NS; ++x) {
-          const uint32_t q = sq + x;
-          mbar_wait(&b_empty[q % EB], (q / EB) & 1, 41);  // slice x consumed by prep(x)
+          const uint32_t qe = eq + x;
+          mbar_wait(&b_step[qe % EB], (qe / EB) & 1, 41);  // slice x consumed by prep(x)
+          if (ltr) ltr[16 * x + 11] = TRCLK();
           const int s = x + SF;
           if (s < NS) {
             // compute step s writes out-record slot s % OR: the publisher must be past s - OR
             while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(42);
+            if (ltr) ltr[16 * s + 8] = TRCLK();
             fw(s);  // phi slice s+1 reuses the slot of phi slice s+1-SP = x-1, last read by prep(x)
+            announce(s);
           }
           pf(s + kPF);
         }
@@ -496,13 +515,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       int t = 0;
       while (t < NS) {
         {
-          const uint32_t q = sq + t;
-          mbar_wait(&b_done[q % DR], (q / DR) & 1, 43);
+          const uint32_t q = eq + t + 1;  // E[t+1]: step t complete
+          mbar_wait(&b_step[q % EB], (q / EB) & 1, 43);
         }
         int t_end = t + 1;
         while (t_end < NS) {
-          const uint32_t q = sq + t_end;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          const uint32_t q = eq + t_end + 1;
+          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++t_end;
         }
         for (; t < t_end; ++t) {
@@ -513,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         fence_gpu();  // release pattern: edge values before the progress counter
         if (lane == 0) {
           st_relaxed_u32(&prog[tid], (unsigned)t);
+          if (P.trace && tid == P.trace_tile) P.trace[8 * P.ntiles + 16 * (t - 1) + 12] = TRCLK();
           st_release_cta_s(&s_linked, t);
         }
       }
@@ -536,25 +556,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const T* eA = (we ? P.edgeW : P.edgeS) + edgeA + c;
       const long long gstride = we ? bd.ny : bd.nx;
       unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
-      int e = 0, freed = 0;  // record s may be written once prep(s - ER) is done (freed > s - ER)
+      // e: next record to fetch (global loads -> deep ring slot e % ER, reusable once
+      //    prep(e - ER) is done).  The loader announces fetched records on the
+      //    slot barrier of their step (s_fetched = records fetched so far).
+      int e = 0, freed = 0;
       Watchdog wd;
       while (e < NS) {
-        while (freed < e + 1 && freed < NS) {  // slots of consumed records
-          const uint32_t q = sq + freed;
-          if (!warp_test(&b_empty[q % EB], (q / EB) & 1)) break;
+        while (freed < NS) {  // prep(freed) done? (compute cannot pass the records: bounded)
+          const uint32_t q = eq + freed;
+          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
         }
-        int m = min(NS - 1, freed + ER - 1);
-        if (m >= e) {
+        // record slot s % ER is reused once prep(s - ER + 1) is done, i.e. after
+        // the critical step s - ER that still reads R_W / R_S from it
+        int m = min(NS - 1, freed + ER - 2);
+        if (e > m) {
+          wd.idle(45);
+          __nanosleep(32);
+          continue;
+        }
+        {
           cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e + kTI, NS));
           cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e + kTJ, NS));
           // record s needs cW >= min(s + TI, NS) and cS >= min(s + TJ, NS)
           if (cW < (unsigned)NS) m = min(m, (int)cW - kTI);
           if (cS < (unsigned)NS) m = min(m, (int)cS - kTJ);
+          if (lane == 0 && P.trace && tid == P.trace_tile)
+            for (int s2 = e; s2 <= m; ++s2) P.trace[8 * P.ntiles + 16 * s2 + 13] = TRCLK();
         }
         if (m < e) {
           wd.idle(44);
-          __nanosleep(64);
+          __nanosleep(32);
           continue;
         }
         wd.progress();
@@ -582,10 +614,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           rec[(we ? 16 : 48) + c] = phB;
           rec[(we ? 64 : 80) + c] = rA;
         }
-        __syncwarp();
-        if (lane == 0)
-          for (int s = e; s <= m; ++s) mbar_arrive(&b_fw[(sq + s) % SF]);
+        __syncwarp();  // record stores ordered before lane 0's release of s_fetched
+        if (lane == 0 && P.trace && tid == P.trace_tile)
+          for (int s = e; s <= m; ++s) P.trace[8 * P.ntiles + 16 * s + 9] = TRCLK();
         e = m + 1;
+        if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
     } else if (warp < kLoaderWarp) {
       // --------------------------------------------------------- compute warps
@@ -597,35 +630,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         ghB = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
         ghT = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
       }
-      T RB = T(0);                                   // own R of the previous plane
+      // Ring positions advance by one per step: keep them as rolling
+      // registers (SF and SP are not powers of two).
+      int fslot = sq % SF;
+      uint32_t fpar = (sq / SF) & 1;
+      int pc = sq % SP;  // phi slot of slice x while preparing step x
+      T RB = T(0);       // own R of the plane below (0 outside the block)
       T pre = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
-      T rwx = T(0), rsx = T(0);                      // cross-tile R_W / R_S of the prepared step
+      const T* srcRW = s_R;  // where the prepared step reads R_W / R_S after the barrier
+      const T* srcRS = s_R;
       bool act = false;
       unsigned long long* trp = nullptr;  // debug trace slots of the step being prepared
       auto prep = [&](int x) {
-        const uint32_t q = sq + x;
-        if (trp) trp[0] = gtime();
         // one wait covers FW slice x, phi slice x+1 and edge record x (phi
         // slices x-1 and x arrived with the transactions of steps x-2 and x-1,
         // which every compute thread has already waited for)
-        mbar_wait(&b_fw[q % SF], (q / SF) & 1, 21);
-        if (trp) trp[1] = gtime();
+        mbar_wait(&b_fw[fslot], fpar, 21);
+        if (trp) trp[3] = TRCLK();
         const int k = x - d;
         act = col && k >= 0 && k < nz;
+        const int pm = pc == 0 ? SP - 1 : pc - 1;
+        const int pp = pc + 1 == SP ? 0 : pc + 1;
         if (act) {
-          if (trp) trp[3] = gtime();
-          const T* rec = s_edge + (q % ER) * NE;
-          const T* f = s_fw + (q % SF) * F_NA * kTT + p;
-          const T* ph0 = s_ph + (q % SP) * kTT;
-          const T* phm = s_ph + ((q + SP - 1) % SP) * kTT;
-          const T* php = s_ph + ((q + 1) % SP) * kTT;
+          const T* rec = s_edge + ((sq + x) & (ER - 1)) * NE;
+          const T* f = s_fw + fslot * (F_NA * kTT) + p;
+          const T* ph0 = s_ph + pc * kTT;
+          const T* phm = s_ph + pm * kTT;
+          const T* php = s_ph + pp * kTT;
+          // branch-free operand selection: pick the shared address, then load
           const T fP = ph0[p];
-          const T fB = k > 0 ? phm[p] : ghB;
-          const T fT = k + 1 < nz ? php[p] : ghT;
-          const T fW = inW ? phm[pW] : rec[tj];
-          const T fE = inE ? php[pE] : rec[16 + tj];
-          const T fS = inS ? phm[pS] : rec[32 + ti];
-          const T fN = inN ? php[pN] : rec[48 + ti];
+          const T vB = phm[p], vT = php[p];
+          const T fB = k > 0 ? vB : ghB;
+          const T fT = k + 1 < nz ? vT : ghT;
+          const T fW = *(inW ? phm + pW : rec + tj);
+          const T fE = *(inE ? php + pE : rec + 16 + tj);
+          const T fS = *(inS ? phm + pS : rec + 32 + ti);
+          const T fN = *(inN ? php + pN : rec + 48 + ti);
           // residual, Listing-1 term order, a_nb = -A_nb
           T r = -(f[F_AE * kTT] * fE);
           r -= f[F_AW * kTT] * fW;
@@ -640,34 +680,52 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           lw = f[F_LW * kTT];
           ls = f[F_LS * kTT];
           lp = f[F_LP * kTT];
-          rwx = rec[64 + tj];
-          rsx = rec[80 + ti];
+          srcRW = rec + 64 + tj;  // replaced by s_R below for in-tile neighbours
+          srcRS = rec + 80 + ti;
         }
+        if (trp) trp[4] = TRCLK();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&b_empty[q % EB]);
+        if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
+        if (trp) trp[5] = TRCLK();
+        fslot = fslot + 1 == SF ? 0 : fslot + 1;
+        fpar ^= (fslot == 0);
+        pc = pp;
       };
       const bool tracing = P.trace && p == 0 && tid == P.trace_tile;
-      if (tracing) trp = P.trace + 8 * P.ntiles;
       prep(0);
       for (int t = 0; t < NS; ++t) {
+        if (tracing) {
+          trp = P.trace + 8 * P.ntiles + 16 * t;
+          trp[0] = TRCLK();
+        }
+        const bool was = act;
+        T Rv = T(0);
         if (act) {
-          const T RW = inW ? s_R[((t - 1) & 1) * kTT + pW] : rwx;
-          const T RS = inS ? s_R[((t - 1) & 1) * kTT + pS] : rsx;
-          const T Rv = ((pre - lw * RW) - ls * RS) * lp;
+          const T* sRm = s_R + ((t - 1) & 1) * kTT;
+          const T RW = *(inW ? sRm + pW : srcRW);
+          const T RS = *(inS ? sRm + pS : srcRS);
+          Rv = ((pre - lw * RW) - ls * RS) * lp;
           RB = Rv;
-          P.R[(td.slot + t) * kTT + p] = Rv;
           s_R[(t & 1) * kTT + p] = Rv;
           if (ti == kTI - 1) s_out[(t % OR) * 32 + tj] = Rv;
           if (tj == kTJ - 1) s_out[(t % OR) * 32 + 16 + ti] = Rv;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&b_done[(sq + t) % DR]);
-        if (tracing) trp = P.trace + 8 * P.ntiles + 4 * (t + 1);
-        if (t + 1 < NS) prep(t + 1);
+        if (trp) trp[1] = TRCLK();
+        if (trp) trp[2] = TRCLK();
+        if (t + 1 < NS) {
+          prep(t + 1);  // arrives E[t+1]: step t complete, step t+1 prepared
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b_step[(eq + NS) % EB]);
+        }
+        if (was) P.R[(td.slot + t) * kTT + p] = Rv;  // consumed only by K3 (next launch)
+        if (trp) trp[6] = TRCLK();
         bar_compute();
+        if (trp) trp[7] = TRCLK();
       }
     }
     sq += NS;
+    eq += NS + 1;
     __syncthreads();  // publisher has published NS (all steps retired)
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
@@ -709,17 +767,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 // =============================================================================
 template <typename T, int SB>
 struct BwdCfg {
-  static constexpr int ER = SB, NE = 32, OR = 8, EB = 16, DR = 24;
+  static constexpr int ER = 16, NE = 32, OR = 8, EB = 32;
   static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SB + EB + DR) * sizeof(uint64_t);
+                                  (SB + EB) * sizeof(uint64_t);
 };
 
 template <typename T, int SB>
 __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
   using C = BwdCfg<T, SB>;
-  constexpr int ER = C::ER, DR = C::DR, EB = C::EB, NE = C::NE, OR = C::OR;
-  static_assert(EB > SB + 1 && DR > OR + SB, "barrier rings must cover the run-ahead");
+  constexpr int ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
+  static_assert(EB > ER + SB && EB > OR + SB + 1, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
   T* s_rg = reinterpret_cast<T*>(smem);
   T* s_D = s_rg + SB * 5 * kTT;
@@ -727,9 +785,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   T* s_out = s_edge + ER * NE;  // [OR][32]: delta of the W column (tj) and S row (16 + ti)
   // b_rg[u % SB] completes when slot u has landed AND edge record u is written
   uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
-  uint64_t* b_empty = b_rg + SB;
-  uint64_t* b_done = b_empty + EB;
-  __shared__ int s_tile, s_last, s_linked;
+  uint64_t* b_step = b_rg + SB;  // E[x] as in K2
+  __shared__ int s_tile, s_last, s_linked, s_fetched;
 
   const int p = threadIdx.x;
   const int warp = p >> 5, lane = p & 31;
@@ -742,17 +799,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
 
   if (p == 0) {
     for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 2);  // loader (expect_tx) + fetcher
-    for (int b = 0; b < EB; ++b) mbar_init(&b_empty[b], kCompute / 32);
-    for (int b = 0; b < DR; ++b) mbar_init(&b_done[b], kCompute / 32);
+    for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
     fence_mbar_init();
   }
-  uint32_t sq = 0;
+  uint32_t sq = 0, eq = 0;
 
   for (;;) {
     __syncthreads();
     if (p == 0) {
       s_tile = atomicAdd(P.state, 1u);
       s_linked = 0;
+      s_fetched = 0;
     }
     __syncthreads();
     const int tk = s_tile;
@@ -785,6 +842,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         };
         int l2 = 0;
         auto pf = [&](int upto) {
+          if (kPF == 0) return;
           for (; l2 < NS && l2 <= upto; ++l2) {
             const int t = NS - 1 - l2;
             int lo, hi;
@@ -800,16 +858,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
             }
           }
         };
-        for (int u = 0; u < SB && u < NS; ++u) slot(u);
-        pf(SB + kPF);
         Watchdog wd;
+        auto announce = [&](int u) {  // edge record u rides on the slot barrier of step u
+          while (ld_acquire_cta_s(&s_fetched) <= u) wd.idle(56);
+          mbar_arrive(&b_rg[(sq + u) % SB]);
+        };
+        for (int u = 0; u < SB && u < NS; ++u) slot(u);
+        for (int u = 0; u < SB && u < NS; ++u) announce(u);
+        pf(SB + kPF);
         for (int x = 0; x < NS; ++x) {
           const uint32_t q = sq + x;
-          mbar_wait(&b_empty[q % EB], (q / EB) & 1, 51);
+          const uint32_t qe = eq + x;
+          mbar_wait(&b_step[qe % EB], (qe / EB) & 1, 51);
           const int s = x + SB;
           if (s < NS) {
             while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(52);
             slot(s);
+            announce(s);
           }
           pf(s + kPF);
         }
@@ -823,13 +888,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       int u = 0;
       while (u < NS) {
         {
-          const uint32_t q = sq + u;
-          mbar_wait(&b_done[q % DR], (q / DR) & 1, 53);
+          const uint32_t q = eq + u + 1;
+          mbar_wait(&b_step[q % EB], (q / EB) & 1, 53);
         }
         int u_end = u + 1;
         while (u_end < NS) {
-          const uint32_t q = sq + u_end;
-          if (!warp_test(&b_done[q % DR], (q / DR) & 1)) break;
+          const uint32_t q = eq + u_end + 1;
+          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++u_end;
         }
         for (; u < u_end; ++u) {
@@ -852,24 +917,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const T* srcB = (we ? P.edgeW : P.edgeS) + edgeB + c;
       const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
       unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
-      int e = 0, freed = 0;
+      int e = 0, freed = 0;  // as in K2: fetch ahead into the deep ring; the loader announces
       Watchdog wd;
       while (e < NS) {
-        while (freed < e + 1 && freed < NS) {
-          const uint32_t q = sq + freed;
-          if (!warp_test(&b_empty[q % EB], (q / EB) & 1)) break;
+        while (freed < NS) {
+          const uint32_t q = eq + freed;
+          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
         }
         int m = min(NS - 1, freed + ER - 1);
-        if (m >= e) {
-          cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e + kTI, NS));
-          cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e + kTJ, NS));
-          if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
-          if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
+        if (e > m) {
+          wd.idle(55);
+          __nanosleep(32);
+          continue;
         }
+        cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e + kTI, NS));
+        cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e + kTJ, NS));
+        if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
+        if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
         if (m < e) {
           wd.idle(54);
-          __nanosleep(64);
+          __nanosleep(32);
           continue;
         }
         wd.progress();
@@ -880,9 +948,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           s_edge[((sq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
         }
         __syncwarp();
-        if (lane == 0)
-          for (int s = e; s <= m; ++s) mbar_arrive(&b_rg[(sq + s) % SB]);
         e = m + 1;
+        if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
     } else if (warp < kLoaderWarp) {
       const bool col = ti < td.wI && tj < td.wJ;
@@ -909,28 +976,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           dex = rec[tj];
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&b_empty[q % EB]);
+        if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
       };
       prep(0);
       for (int u = 0; u < NS; ++u) {
         const int t = NS - 1 - u;
+        const bool was = act;
+        T phn = T(0);
         if (act) {
           const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : dnx;
           const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : dex;
           const T dl = ((rr - un * dN) - ue * dE) - utdt;
           dT = dl;
-          P.phi[(td.slot + t) * kTT + p] = ph + dl;
+          phn = ph + dl;
           s_D[(u & 1) * kTT + p] = dl;
           if (ti == 0) s_out[(u % OR) * 32 + tj] = dl;
           if (tj == 0) s_out[(u % OR) * 32 + 16 + ti] = dl;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&b_done[(sq + u) % DR]);
-        if (u + 1 < NS) prep(u + 1);
+        if (u + 1 < NS) {
+          prep(u + 1);  // arrives E[u+1]
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b_step[(eq + NS) % EB]);
+        }
+        if (was) P.phi[(td.slot + t) * kTT + p] = phn;
         bar_compute();
       }
     }
     sq += NS;
+    eq += NS + 1;
     __syncthreads();
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     if (p == 0) {

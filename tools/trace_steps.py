@@ -1,5 +1,7 @@
-"""Per-step timing of one tile's forward sweep (SIPB_TRACE_TILE): for step x,
-trace[x] = {prep start, FW slice ready, edge record ready, phi ready}."""
+"""Cycle breakdown of one tile's forward steps (SIPB_TRACE_TILE; clock64):
+compute thread 0: [0] step top [1] critical [2] - [3] prep wait done [4] prep compute
+[5] E arrive [6] prep end [7] after barrier; loader [8] slice issue [11] E(x) seen;
+fetcher [9] record fetched [10] record announced."""
 import ctypes, sys, os
 import numpy as np
 sys.path.insert(0, ".")
@@ -16,18 +18,30 @@ L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(2)
 ns = g[2] + 30
-tr = np.zeros(8 * nt.value + 4 * ns, dtype=np.uint64)
+tr = np.zeros(8 * nt.value + 16 * ns, dtype=np.uint64)
 L.sip_debug_trace(s.handle, tr.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
-tab = tr[:8 * nt.value].reshape(2, nt.value, 4).astype(np.int64)
-st = tr[8 * nt.value:].reshape(ns, 4).astype(np.int64)
+st = tr[8 * nt.value:].reshape(ns, 16).astype(np.int64)
 tile = int(os.environ.get("SIPB_TRACE_TILE", "0"))
-t0 = tab[0, :, 0].min()
-print(f"{g} {prec} tile {tile}: start {(tab[0,tile,0]-t0)/1e3:.1f} us end {(tab[0,tile,1]-t0)/1e3:.1f} us; fwd span {(tab[0,:,1].max()-t0)/1e3:.1f} us")
-a, b, c, e = [(st[:, i] - t0) / 1e3 for i in range(4)]
-step = np.diff(a)
-ok = st[:, 3] > 0
-print("prep-to-prep us: median %.3f mean %.3f p90 %.3f" % (np.median(step), step.mean(), np.percentile(step, 90)))
-print("wait FW median %.3f mean %.3f | wait edge median %.3f mean %.3f | wait phi median %.3f mean %.3f (active steps)" % (
-    np.median(b - a), (b - a).mean(), np.median(c - b), (c - b).mean(), np.median((e - c)[ok]), (e - c)[ok].mean()))
-for t in list(range(0, 6)) + list(range(100, 104)):
-    print(f"  x={t:3d} start {a[t]:8.2f} fw {b[t]-a[t]:6.3f} edge {c[t]-b[t]:6.3f} phi {(e[t]-c[t]) if ok[t] else 0:6.3f} rest {a[t+1]-max(c[t], e[t]):6.3f}")
+names = ["critical", "-", "prep-wait", "prep-compute", "E-arrive", "prep-tail", "barrier"]
+rows = st[1:ns - 1]
+print(f"{g} {prec} tile {tile}: cycles per step (median / mean) over {len(rows)} steps")
+tot = np.diff(st[:, 0])
+print("   step total     %7.0f %7.0f" % (np.median(tot), tot.mean()))
+for i, n in enumerate(names):
+    dlt = rows[:, i + 1] - rows[:, i]
+    print("   %-14s %7.0f %7.0f" % (n, np.median(dlt), dlt.mean()))
+# relative to the compute's prep-wait end of step x ([3] in the row of step x-1)
+base = st[:-1, 3]   # prep(x+1) wait done is stored in row x
+x = np.arange(1, ns)
+iss = st[x, 8]; fet = st[x, 9]; ann = st[x, 10]; ew = st[x - 1, 11]
+ready = base
+sel = slice(20, ns - 20)
+print("   slice issue -> prep ready   median %7.0f" % np.median((ready - iss)[sel]))
+print("   record fetched -> ready     median %7.0f" % np.median((ready - fet)[sel]))
+print("   record announced -> ready  median %7.0f" % np.median((ready - ann)[sel]))
+print("   loader saw E(x-1) -> issue(x+SF-1) median %7.0f" % np.median((st[x[sel] + 2, 8] - ew[sel])))
+b0 = st[100, 0]
+print("   raw timeline (cycles rel. to step 100 top):  top  prepwait  Earr  bar | loaderSawE(x) issue(x) | fetched(x) announced(x)")
+for t in range(100, 108):
+    r = st[t] - b0
+    print(f"   t={t}: {r[0]:7d} {r[3]:7d} {r[5]:7d} {r[7]:7d} | {r[11]:7d} {r[8]:7d} | {r[9]:8d} {r[10]:7d}")
