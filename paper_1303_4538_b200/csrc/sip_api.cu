@@ -87,6 +87,9 @@ struct sip_ctx {
   int* d_order_b = nullptr;
   void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
   void *edgeW = nullptr, *edgeS = nullptr;
+  unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
+  size_t tag_words = 0;                 // words per buffer
+  unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
   double *fw64 = nullptr, *bw64 = nullptr;  // fp32 mode: fp64 shadow for the factorisation
   unsigned *st_f = nullptr, *st_b = nullptr, *st_fac = nullptr;
   double* partial = nullptr;
@@ -243,6 +246,11 @@ static int build(sip_ctx* ctx) {
   CKS(dalloc(ctx, &ctx->ghost, (size_t)ctx->total_ghost * es));
   CKS(dalloc(ctx, &ctx->edgeW, (size_t)ctx->total_edge * es));
   CKS(dalloc(ctx, &ctx->edgeS, (size_t)ctx->total_edge * es));
+  ctx->tag_words = (size_t)std::max(1LL, ctx->total_edge) * (es / 4);
+  CKS(dalloc(ctx, &ctx->tags, 4 * ctx->tag_words * sizeof(unsigned long long)));
+  // tag 0xFFFFFFFF never matches a live (epoch, k) tag (k < 65535)
+  CK(cudaMemset(ctx->tags, 0xff, 4 * ctx->tag_words * sizeof(unsigned long long)));
+  CKS(dalloc(ctx, &ctx->epochs, 2 * sizeof(unsigned)));
   if (ctx->precision == SIP_PREC_SINGLE) {
     CKS(dalloc(ctx, &ctx->fw64, S * F_NA * sizeof(double)));
     CKS(dalloc(ctx, &ctx->bw64, S * B_NA * sizeof(double)));
@@ -462,6 +470,9 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
   p.ghost = static_cast<T*>(ctx->ghost);
   p.edgeW = static_cast<T*>(ctx->edgeW);
   p.edgeS = static_cast<T*>(ctx->edgeS);
+  p.tagA = ctx->tags + (forward ? 0 : 2) * ctx->tag_words;
+  p.tagB = ctx->tags + (forward ? 1 : 3) * ctx->tag_words;
+  p.epoch = ctx->epochs + (forward ? 0 : 1);
   p.state = forward ? ctx->st_f : ctx->st_b;
   p.state_other = forward ? ctx->st_b : ctx->st_f;
   p.partial = ctx->partial;
@@ -604,7 +615,8 @@ int sip_destroy(sip_ctx* ctx) {
   void* ptrs[] = {ctx->d_blocks, ctx->d_tiles, ctx->d_order_f, ctx->d_order_b, ctx->fw, ctx->bw,
                   ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
                   ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
-                  ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace};
+                  ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace,
+                  ctx->tags, ctx->epochs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->precision == SIP_PREC_SINGLE) {

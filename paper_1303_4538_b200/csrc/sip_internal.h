@@ -141,8 +141,16 @@ struct SweepParams {
   T* phi;
   T* R;
   T* ghost;
-  T* edgeW;  // backward delta of each tile's i = i0 column [edge + k*TJ + tj]
-  T* edgeS;  // backward delta of each tile's j = j0 row    [edge + k*TI + ti]
+  T* edgeW;  // (factor kernel only) unused by K2/K3
+  T* edgeS;
+  // Cross-tile edge values as self-validating tagged words (DESIGN.md
+  // "Cross-tile hand-off"): value bits + 32-bit tag (epoch << 16 | k), one
+  // 64-bit word per fp32 value, two per fp64 value; index (edge + k*16 + c).
+  //   K2: tagA = R of each tile's E column, tagB = R of its N row
+  //   K3: tagA = delta of each tile's W column, tagB = delta of its S row
+  unsigned long long* tagA;
+  unsigned long long* tagB;
+  unsigned* epoch;        // launch counter of this sweep kind (bumped by the finaliser)
   unsigned* state;        // this sweep: [0] ticket, [1] done, prog at state + 32
   unsigned* state_other;  // the other sweep's state, reset by our finaliser
   double* partial;        // [ntiles] tile norm partials

@@ -340,6 +340,35 @@ __device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
   return v;
 }
 
+// ---- tagged edge words: value bits + 32-bit tag, single-copy atomic 64-bit stores
+__device__ __forceinline__ uint32_t edge_tag(unsigned epoch, int k) {
+  return ((epoch & 0xFFFFu) << 16) | (uint32_t)(k & 0xFFFF);
+}
+__device__ __forceinline__ void put_tagged(unsigned long long* dst, float v, uint32_t tag) {
+  const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+}
+__device__ __forceinline__ void put_tagged(unsigned long long* dst, double v, uint32_t tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = ((unsigned long long)tag << 32) | (b >> 32);
+  const unsigned long long w1 = ((unsigned long long)tag << 32) | (b & 0xFFFFFFFFull);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ bool get_tagged(const unsigned long long* src, uint32_t tag, float& v) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(src) : "memory");
+  v = __uint_as_float((uint32_t)w);
+  return (uint32_t)(w >> 32) == tag;
+}
+__device__ __forceinline__ bool get_tagged(const unsigned long long* src, uint32_t tag, double& v) {
+  unsigned long long w0, w1;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(src) : "memory");
+  v = __longlong_as_double((long long)((w0 << 32) | (w1 & 0xFFFFFFFFull)));
+  return (uint32_t)(w0 >> 32) == tag && (uint32_t)(w1 >> 32) == tag;
+}
+template <typename T>
+constexpr int kTagWords = sizeof(T) / 4;  // 64-bit words per tagged value
+
 // Warp-collective poll of a neighbour's progress counter.  Every lane performs
 // its own acquire (so its later loads are ordered) and the warp takes the
 // minimum, so all lanes agree on a value each of them has acquired.  Lanes of
@@ -415,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   }
   uint32_t sq = 0;  // CTA-uniform step sequence base (slot rings advance NS per tile)
   uint32_t eq = 0;  // E ring base (advances NS + 1 per tile)
+  const unsigned epoch = *P.epoch;  // stable for this launch (bumped by the finaliser)
 
   for (;;) {
     __syncthreads();
@@ -507,11 +537,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     } else if (warp == kPublisherWarp) {
       // --------------------------------------------------------- publisher
       // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
+      // written as tagged words: the consumer validates each value by its tag,
+      // so no fence or progress counter is needed
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
       const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
-      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
+      unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
       int t = 0;
       while (t < NS) {
         {
@@ -526,12 +558,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         }
         for (; t < t_end; ++t) {
           const int k = t - outoff;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(t % OR) * 32 + lane];
+          if (outok && k >= 0 && k < nz)
+            put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(t % OR) * 32 + lane],
+                       edge_tag(epoch, k));
         }
         __syncwarp();
-        fence_gpu();  // release pattern: edge values before the progress counter
         if (lane == 0) {
-          st_relaxed_u32(&prog[tid], (unsigned)t);
           if (P.trace && tid == P.trace_tile) P.trace[8 * P.ntiles + 16 * (t - 1) + 12] = TRCLK();
           st_release_cta_s(&s_linked, t);
         }
@@ -553,71 +585,66 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const int offB = we ? (td.wI - 1) + c : c + (td.wJ - 1);  // edge cell of side B: k = t - offB
       const T* gA = P.ghost + ghost_face_offset(bd, we ? G_W : G_S) + (we ? td.j0 : td.i0) + c;
       const T* gB = P.ghost + ghost_face_offset(bd, we ? G_E : G_N) + (we ? td.j0 : td.i0) + c;
-      const T* eA = (we ? P.edgeW : P.edgeS) + edgeA + c;
+      const unsigned long long* eA = (we ? P.tagA : P.tagB) + (edgeA + c) * kTagWords<T>;
       const long long gstride = we ? bd.ny : bd.nx;
-      unsigned cW = td.nW >= 0 ? 0u : 0x7fffffffu, cS = td.nS >= 0 ? 0u : 0x7fffffffu;
-      // e: next record to fetch (global loads -> deep ring slot e % ER, reusable once
-      //    prep(e - ER) is done).  The loader announces fetched records on the
-      //    slot barrier of their step (s_fetched = records fetched so far).
+      // e: next record to fetch into deep-ring slot e % ER (reusable once
+      // prep(e - ER + 1) is done); the loader announces fetched records on the
+      // slot barrier of their step (s_fetched = records fetched so far)
       int e = 0, freed = 0;
       Watchdog wd;
+      constexpr int kB = 4;  // records polled per round trip
       while (e < NS) {
         while (freed < NS) {  // prep(freed) done? (compute cannot pass the records: bounded)
           const uint32_t q = eq + freed;
           if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
         }
-        // record slot s % ER is reused once prep(s - ER + 1) is done, i.e. after
-        // the critical step s - ER that still reads R_W / R_S from it
-        int m = min(NS - 1, freed + ER - 2);
+        const int m = min(NS - 1, freed + ER - 2);
         if (e > m) {
           wd.idle(45);
-          __nanosleep(32);
           continue;
         }
-        {
-          cW = poll_progress(&prog[td.nW >= 0 ? td.nW : 0], cW, (unsigned)min(e + kTI, NS));
-          cS = poll_progress(&prog[td.nS >= 0 ? td.nS : 0], cS, (unsigned)min(e + kTJ, NS));
-          // record s needs cW >= min(s + TI, NS) and cS >= min(s + TJ, NS)
-          if (cW < (unsigned)NS) m = min(m, (int)cW - kTI);
-          if (cS < (unsigned)NS) m = min(m, (int)cS - kTJ);
-          if (lane == 0 && P.trace && tid == P.trace_tile)
-            for (int s2 = e; s2 <= m; ++s2) P.trace[8 * P.ntiles + 16 * s2 + 13] = TRCLK();
+        // issue the loads of up to kB records at once, then accept the valid prefix
+        T phA[kB], phB[kB], rA[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const int s2 = e + j;
+          phA[j] = T(0); phB[j] = T(0); rA[j] = T(0); ok[j] = true;
+          if (s2 > m) continue;
+          const int kA = s2 - c;  // W side cell (0, c) / S side cell (c, 0)
+          if (colok && kA >= 0 && kA < nz) {
+            if (nA >= 0) {
+              phA[j] = P.phi[(slotA + s2 + lag - 1) * kTT + posA];
+              ok[j] = get_tagged(eA + (long long)kA * 16 * kTagWords<T>, edge_tag(epoch, kA), rA[j]);
+            } else {
+              phA[j] = gA[gstride * kA];
+            }
+          }
+          const int kB2 = s2 - offB;
+          if (colok && kB2 >= 0 && kB2 < nz)
+            phB[j] = nB >= 0 ? P.phi[(slotB + s2 - lag + 1) * kTT + posB] : gB[gstride * kB2];
         }
-        if (m < e) {
+        int n = 0;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          if (n == j && e + j <= m && __all_sync(0xffffffffu, ok[j])) {
+            T* rec = s_edge + ((sq + e + j) % ER) * NE;
+            rec[(we ? 0 : 32) + c] = phA[j];
+            rec[(we ? 16 : 48) + c] = phB[j];
+            rec[(we ? 64 : 80) + c] = rA[j];
+            n = j + 1;
+          }
+        }
+        if (n == 0) {
           wd.idle(44);
-          __nanosleep(32);
           continue;
         }
         wd.progress();
-        for (int s = e; s <= m; ++s) {
-          T* rec = s_edge + ((sq + s) % ER) * NE;
-          T phA = T(0), phB = T(0), rA = T(0);
-          const int kA = s - c;  // W side cell (0, c) / S side cell (c, 0)
-          if (colok && kA >= 0 && kA < nz) {
-            if (nA >= 0) {
-              phA = P.phi[(slotA + s + lag - 1) * kTT + posA];
-              rA = ld_relaxed(eA + (long long)kA * 16);
-            } else {
-              phA = gA[gstride * kA];
-            }
-          }
-          const int kB = s - offB;
-          if (colok && kB >= 0 && kB < nz) {
-            if (nB >= 0) {
-              phB = P.phi[(slotB + s - lag + 1) * kTT + posB];
-            } else {
-              phB = gB[gstride * kB];
-            }
-          }
-          rec[(we ? 0 : 32) + c] = phA;
-          rec[(we ? 16 : 48) + c] = phB;
-          rec[(we ? 64 : 80) + c] = rA;
-        }
         __syncwarp();  // record stores ordered before lane 0's release of s_fetched
         if (lane == 0 && P.trace && tid == P.trace_tile)
-          for (int s = e; s <= m; ++s) P.trace[8 * P.ntiles + 16 * s + 9] = TRCLK();
-        e = m + 1;
+          for (int s2 = e; s2 < e + n; ++s2) P.trace[8 * P.ntiles + 16 * s2 + 9] = TRCLK();
+        e += n;
         if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
     } else if (warp < kLoaderWarp) {
@@ -754,6 +781,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         *P.norm = v;
       }
       for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
+      if (p == 0) *P.epoch = epoch + 1;
     }
   }
 }
@@ -803,6 +831,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     fence_mbar_init();
   }
   uint32_t sq = 0, eq = 0;
+  const unsigned epoch = *P.epoch;
 
   for (;;) {
     __syncthreads();
@@ -884,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
-      T* outdst = (we ? P.edgeW : P.edgeS) + td.edge + c;
+      unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
       int u = 0;
       while (u < NS) {
         {
@@ -899,14 +928,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         }
         for (; u < u_end; ++u) {
           const int k = (NS - 1 - u) - c;
-          if (outok && k >= 0 && k < nz) outdst[(long long)k * 16] = s_out[(u % OR) * 32 + lane];
+          if (outok && k >= 0 && k < nz)
+            put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(u % OR) * 32 + lane],
+                       edge_tag(epoch, k));
         }
         __syncwarp();
-        fence_gpu();
-        if (lane == 0) {
-          st_relaxed_u32(&prog[tid], (unsigned)u);
-          st_release_cta_s(&s_linked, u);
-        }
+        if (lane == 0) st_release_cta_s(&s_linked, u);
       }
     } else if (warp == kFetcherWarp) {
       const bool we = lane < 16;
@@ -914,41 +941,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const bool colok = we ? (c < td.wJ) : (c < td.wI);
       const int nB = we ? td.nE : td.nN;
       const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
-      const T* srcB = (we ? P.edgeW : P.edgeS) + edgeB + c;
+      const unsigned long long* srcB = (we ? P.tagA : P.tagB) + (edgeB + c) * kTagWords<T>;
       const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
-      unsigned cE = td.nE >= 0 ? 0u : 0x7fffffffu, cN = td.nN >= 0 ? 0u : 0x7fffffffu;
-      int e = 0, freed = 0;  // as in K2: fetch ahead into the deep ring; the loader announces
+      int e = 0, freed = 0;  // as in K2: poll tagged deltas into the deep ring; the loader announces
       Watchdog wd;
+      constexpr int kB = 4;
       while (e < NS) {
         while (freed < NS) {
           const uint32_t q = eq + freed;
           if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
         }
-        int m = min(NS - 1, freed + ER - 1);
+        const int m = min(NS - 1, freed + ER - 2);
         if (e > m) {
           wd.idle(55);
-          __nanosleep(32);
           continue;
         }
-        cE = poll_progress(&prog[td.nE >= 0 ? td.nE : 0], cE, (unsigned)min(e + kTI, NS));
-        cN = poll_progress(&prog[td.nN >= 0 ? td.nN : 0], cN, (unsigned)min(e + kTJ, NS));
-        if (cE < (unsigned)NS) m = min(m, (int)cE - kTI);
-        if (cN < (unsigned)NS) m = min(m, (int)cN - kTJ);
-        if (m < e) {
+        T v[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const int s2 = e + j;
+          v[j] = T(0);
+          ok[j] = true;
+          if (s2 > m) continue;
+          const int k = (NS - 1 - s2) - offB;
+          if (nB >= 0 && colok && k >= 0 && k < nz)
+            ok[j] = get_tagged(srcB + (long long)k * 16 * kTagWords<T>, edge_tag(epoch, k), v[j]);
+        }
+        int n = 0;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          if (n == j && e + j <= m && __all_sync(0xffffffffu, ok[j])) {
+            s_edge[((sq + e + j) % ER) * NE + (we ? 0 : 16) + c] = v[j];
+            n = j + 1;
+          }
+        }
+        if (n == 0) {
           wd.idle(54);
-          __nanosleep(32);
           continue;
         }
         wd.progress();
-        for (int s = e; s <= m; ++s) {
-          const int k = (NS - 1 - s) - offB;
-          T v = T(0);
-          if (nB >= 0 && colok && k >= 0 && k < nz) v = ld_relaxed(srcB + (long long)k * 16);
-          s_edge[((sq + s) % ER) * NE + (we ? 0 : 16) + c] = v;
-        }
         __syncwarp();
-        e = m + 1;
+        e += n;
         if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
     } else if (warp < kLoaderWarp) {
@@ -1015,6 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     if (s_last) {
       __threadfence();
       for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
+      if (p == 0) *P.epoch = epoch + 1;
     }
   }
 }
