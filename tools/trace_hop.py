@@ -1,14 +1,15 @@
-"""Cross-tile hop latency: run the forward sweep tracing tile W, then tile T = W's
-east neighbour (globaltimer stamps).  For step s of T: W published progress
-s+16 at P_W[s+15]; T's fetcher saw it at F_T[s]; T's prep of step s ended at C_T[s]."""
-import ctypes, sys, os, subprocess
+"""Cross-tile hop latency (globaltimer): trace tile W, then its east neighbour
+T in a second identical run.  Per step s of T: W's publish of step s+15,
+T's fetch of record s, T's loader announce of record s, T's prep(s) done."""
+import ctypes, sys, os
 import numpy as np
 sys.path.insert(0, ".")
 import paper_1303_4538_b200 as sip
 g = (256, 256, 256)
+prec = sys.argv[2] if len(sys.argv) > 2 else "f64"
 def run(tile):
     os.environ["SIPB_TRACE_TILE"] = str(tile)
-    s = sip.Solver(None, "f64", 0, lattice=(g, (1, 1, 1)))
+    s = sip.Solver(None, prec, 0, lattice=(g, (1, 1, 1)))
     s._nglobal = 1
     s.generate(0, 1304)
     s.factor(0.92)
@@ -23,22 +24,14 @@ def run(tile):
     tab = tr[:8 * nt.value].reshape(2, nt.value, 4).astype(np.int64)
     st = tr[8 * nt.value:].reshape(ns, 16).astype(np.int64)
     s.close()
-    return tab, st
-W = int(sys.argv[1]) if len(sys.argv) > 1 else 17   # tile (1,1)
-T = W + 1                                            # tile (2,1)
-tabW, stW = run(W)
-tabT, stT = run(T)
-# align each run to its own kernel start (min tile start); runs differ, so compare
-# within-run quantities only, and W/T via the same reference
-t0W = tabW[0, :, 0].min(); t0T = tabT[0, :, 0].min()
-print("W start/end (us):", (tabW[0, W, 0] - t0W) / 1e3, (tabW[0, W, 1] - t0W) / 1e3)
-print("T start/end (us):", (tabT[0, T, 0] - t0T) / 1e3, (tabT[0, T, 1] - t0T) / 1e3)
-ns = stT.shape[0]
-pubW = (stW[:, 12] - t0W) / 1e3   # W published progress s+1 at pubW[s]
-fetT = (stT[:, 13] - t0T) / 1e3   # T's fetcher allowed record s
-prepT = (stT[:, 3] - t0T) / 1e3   # T: prep(s+1) wait done (row s)
-stepT = (stT[:, 0] - t0T) / 1e3
-for s in (20, 50, 100, 150, 200, 250):
-    print(f" s={s}: W pub(s+16) {pubW[s+15]:8.2f}  T fetch-allowed(s) {fetT[s]:8.2f}  T step(s) top {stepT[s]:8.2f}  T step period {stepT[s+1]-stepT[s]:.3f}")
-print("T step period median (us):", np.median(np.diff(stepT[20:-20])))
-print("W publish period median (us):", np.median(np.diff(pubW[20:-40])))
+    t0 = tab[0, :, 0].min()
+    return tab, (st - t0) / 1e3, t0
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 17
+T = W + 1
+tabW, sW, _ = run(W)
+tabT, sT, _ = run(T)
+print("W", W, "start/end", (tabW[0, W, 0] - tabW[0, :, 0].min()) / 1e3, (tabW[0, W, 1] - tabW[0, :, 0].min()) / 1e3)
+print("T", T, "start/end", (tabT[0, T, 0] - tabT[0, :, 0].min()) / 1e3, (tabT[0, T, 1] - tabT[0, :, 0].min()) / 1e3)
+print("  s   Wpub(s+15)  Tfetch(s)  Tannounce(s)  Tprepdone(s)  Tissue(s)")
+for s in (5, 10, 20, 40, 80, 120, 160, 200, 240, 270):
+    print(f"{s:4d} {sW[s+15,12]:10.2f} {sT[s,9]:10.2f} {sT[s,10]:12.2f} {sT[s-1,3]:12.2f} {sT[s,8]:10.2f}")

@@ -14,8 +14,10 @@ nt = ctypes.c_longlong()
 L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(3)
-tr = np.zeros((2, nt.value, 4), dtype=np.uint64)
-L.sip_debug_trace(s.handle, tr.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
+ns = n + 30
+buf = np.zeros(8 * nt.value + 16 * ns, dtype=np.uint64)  # table + per-step record (see sip_debug_trace)
+L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
+tr = buf[:8 * nt.value].reshape(2, nt.value, 4)
 TX = (n + 15) // 16
 for kind, name in ((0, "forward"), (1, "backward")):
     t = tr[kind].astype(np.int64)
