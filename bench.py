@@ -169,7 +169,11 @@ def run_gpu(args, rank, world, dist):
     torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
     cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
     c = CONFIGS[cfg_id]
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library launches on it and the CUDA
+    # events below are recorded on it (a NULL handle would mean "library's own
+    # stream" to sip_set_stream, invisible to events on torch's legacy stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     peak, peak_src = load_peak()
     results = {}
     precs = c["prec"] if args.precision == "auto" else (args.precision,)
@@ -246,6 +250,7 @@ def run_gpu(args, rank, world, dist):
             k3={"kernel": "k_backward (K3)", "achieved": bwd_achieved, "frac": bwd_achieved / peak,
                 "launch_ms": bwd_launch_ms, "alg_bytes_per_launch": bwd_bytes},
             step_gbs=step_gbs, step_frac=step_gbs / peak, halo_ms=prof["halo_ms"] / iters,
+            kernel_ms_per_iter=(prof["fwd_ms"] + prof["bwd_ms"] + prof["halo_ms"]) / iters,
             first_norms=[float(x) for x in nrm], geometry=s.geometry(), cells_total=cells_total,
             cells_local=cells_local, g=g, p=p)
         s.close()
@@ -396,6 +401,8 @@ def main():
             "gpu_launches": r["launches"], "clocks": r["clocks"],
             "achieved_hbm_gbs_step": r["step_gbs"], "achieved_frac_step": r["step_frac"],
             "k3_backward": r["k3"], "halo_ms_per_iter": r["halo_ms"],
+            "kernel_ms_per_iter": r["kernel_ms_per_iter"],
+            "timed_ms_per_iter": r["ms"] / c["iters"],
             "first_norms": r["first_norms"],
         }
         for prec, rr in res.items():
