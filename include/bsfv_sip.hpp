@@ -1,0 +1,189 @@
+// bsfv_sip.hpp -- header-only C++ shim that gives the reference's sip module
+// interface on top of the B200 C-ABI (sip_c.h).
+//
+// Drop-in use from the reference code base (proj/):
+//
+//   #include "bsfv/error.hpp"      // optional: throw the reference's own classes
+//   #include "bsfv/field.hpp"
+//   #define BSFV_SIP_USE_REFERENCE_ERRORS 1
+//   #include "bsfv_sip.hpp"
+//
+//   bsfv::b200::StencilSystemT<bsfv::FieldD> A{...};  // Field3<double> members
+//   ... fill A.ap, A.aw, ..., A.q ...
+//   bsfv::b200::SipConfig cfg;                     // alpha 0.92, max_iters, target
+//   auto F = bsfv::b200::sip_factor(A, cfg);       // SingularFactorError names the cell
+//   auto [fi, report] = bsfv::b200::solve(A, fi0, cfg, &F);
+//
+// The field type is a template parameter: anything with nx()/ny()/nz() and
+// data() over (nx+2)(ny+2)(nz+2) doubles in Field3 order
+// (proj/include/bsfv/field.hpp:21-44) works, including bsfv::FieldD itself.
+//
+// Error mapping (proj/include/bsfv/error.hpp:34-50):
+//   SIP_ERR_SINGULAR -> SingularFactorError, SIP_ERR_STALE -> StaleFactorsError,
+//   SIP_ERR_MISUSE -> MisuseError, SIP_ERR_CONFIG -> ConfigError, else Error.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sip_c.h"
+
+namespace bsfv {
+namespace b200 {
+
+#if defined(BSFV_SIP_USE_REFERENCE_ERRORS) && BSFV_SIP_USE_REFERENCE_ERRORS
+using Error = ::bsfv::Error;
+using ConfigError = ::bsfv::ConfigError;
+using SingularFactorError = ::bsfv::SingularFactorError;
+using StaleFactorsError = ::bsfv::StaleFactorsError;
+using MisuseError = ::bsfv::MisuseError;
+#else
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& w) : std::runtime_error(w) {}
+};
+class ConfigError : public Error {
+ public:
+  explicit ConfigError(const std::string& w) : Error(w) {}
+};
+class SingularFactorError : public Error {
+ public:
+  explicit SingularFactorError(const std::string& w) : Error(w) {}
+};
+class StaleFactorsError : public Error {
+ public:
+  explicit StaleFactorsError(const std::string& w) : Error(w) {}
+};
+class MisuseError : public Error {
+ public:
+  explicit MisuseError(const std::string& w) : Error(w) {}
+};
+#endif
+
+inline void check(int status, const sip_ctx* ctx, const char* what) {
+  if (status == SIP_OK) return;
+  const std::string msg = std::string(what) + ": " + ::sip_status_string(status) + ": " +
+                          ::sip_last_error(ctx);
+  switch (status) {
+    case SIP_ERR_SINGULAR: throw SingularFactorError(msg);
+    case SIP_ERR_STALE: throw StaleFactorsError(msg);
+    case SIP_ERR_MISUSE: throw MisuseError(msg);
+    case SIP_ERR_CONFIG: throw ConfigError(msg);
+    default: throw Error(msg);
+  }
+}
+
+/// SPEC.md:124-127
+struct SipConfig {
+  double alpha = 0.92;
+  int max_iters = 50;
+  double target = 0.0;  // <= 0: fixed iteration count
+  bool single_precision = false;
+};
+
+/// SPEC.md:128-131
+struct SolveReport {
+  int iterations = 0;
+  std::vector<double> norms;
+  double initial() const { return norms.empty() ? 0.0 : norms.front(); }
+  double final_norm() const { return norms.empty() ? 0.0 : norms.back(); }
+};
+
+/// StencilSystem over any Field3-compatible type; matrix
+/// entries (A_nb = -a_nb).
+template <class Field>
+struct StencilSystemT {
+  Field ap, aw, ae, as, an, ab, at, q;
+  long long revision = 0;  // bump after editing the coefficients
+};
+
+/// SipFactors: a device context holding the factors,
+/// stamped with the revision they were computed from.
+class SipFactors {
+ public:
+  SipFactors() = default;
+  SipFactors(sip_ctx* ctx, long long stamp, bool single) : ctx_(ctx), stamp_(stamp), single_(single) {}
+  SipFactors(const SipFactors&) = delete;
+  SipFactors& operator=(const SipFactors&) = delete;
+  SipFactors(SipFactors&& o) noexcept { *this = std::move(o); }
+  SipFactors& operator=(SipFactors&& o) noexcept {
+    std::swap(ctx_, o.ctx_);
+    stamp_ = o.stamp_;
+    single_ = o.single_;
+    return *this;
+  }
+  ~SipFactors() {
+    if (ctx_) ::sip_destroy(ctx_);
+  }
+  sip_ctx* ctx() const { return ctx_; }
+  long long stamp() const { return stamp_; }
+  bool single_precision() const { return single_; }
+
+ private:
+  sip_ctx* ctx_ = nullptr;
+  long long stamp_ = -1;
+  bool single_ = false;
+};
+
+/// sip_factor
+template <class Field>
+SipFactors sip_factor(const StencilSystemT<Field>& A, const SipConfig& cfg, int device = 0) {
+  sip_ctx* ctx = nullptr;
+  check(::sip_create(device, A.ap.nx(), A.ap.ny(), A.ap.nz(),
+                     cfg.single_precision ? SIP_PREC_SINGLE : SIP_PREC_DOUBLE, &ctx),
+        nullptr, "sip_create");
+  SipFactors F(ctx, A.revision, cfg.single_precision);  // owns ctx from here on
+  check(::sip_set_system(ctx, 0, A.ap.data(), A.aw.data(), A.ae.data(), A.as.data(), A.an.data(),
+                         A.ab.data(), A.at.data(), A.q.data()),
+        ctx, "sip_set_system");
+  long long bb = -1, bc = -1;
+  check(::sip_factor(ctx, cfg.alpha, &bb, &bc), ctx, "sip_factor");
+  return F;
+}
+
+/// solve on the reuse path (factors given) or with one
+/// factorisation at entry.  Returns (fi, report).
+template <class Field>
+std::pair<Field, SolveReport> solve(const StencilSystemT<Field>& A, const Field& fi0,
+                                    const SipConfig& cfg, SipFactors* F = nullptr,
+                                    int device = 0) {
+  SipFactors own;
+  if (!F) {
+    own = sip_factor(A, cfg, device);
+    F = &own;
+  } else if (F->stamp() != A.revision) {
+    throw StaleFactorsError("solve: factors stamped with revision " + std::to_string(F->stamp()) +
+                            " used against system revision " + std::to_string(A.revision));
+  } else if (F->single_precision() != cfg.single_precision) {
+    throw MisuseError("solve: factors were computed for another precision");
+  }
+  Field fi = fi0;
+  SolveReport rep;
+  if (cfg.target >= 1.0) return {fi, rep};
+  check(::sip_set_source(F->ctx(), 0, A.q.data()), F->ctx(), "sip_set_source");
+  rep.norms.assign(static_cast<size_t>(cfg.max_iters), 0.0);
+  double* phis[1] = {fi.data()};
+  int used = 0;
+  check(::sip_solve(F->ctx(), phis, cfg.max_iters, cfg.target, rep.norms.data(), &used), F->ctx(),
+        "sip_solve");
+  rep.norms.resize(static_cast<size_t>(used));
+  rep.iterations = used;
+  return {fi, rep};
+}
+
+/// sip_sweep: one inner iteration in place, returns the L1 norm.
+template <class Field>
+double sip_sweep(const StencilSystemT<Field>& A, SipFactors& F, Field& fi) {
+  if (F.stamp() != A.revision) throw StaleFactorsError("sip_sweep: stale factors");
+  check(::sip_set_source(F.ctx(), 0, A.q.data()), F.ctx(), "sip_set_source");
+  double norm = 0.0;
+  int used = 0;
+  double* phis[1] = {fi.data()};
+  check(::sip_solve(F.ctx(), phis, 1, 0.0, &norm, &used), F.ctx(), "sip_solve");
+  return norm;
+}
+
+}  // namespace b200
+}  // namespace bsfv

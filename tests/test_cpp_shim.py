@@ -1,0 +1,44 @@
+"""The C++ drop-in shim (include/bsfv_sip.hpp) compiles against the C-ABI
+library and maps statuses to the reference's exception classes."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIBDIR = os.path.join(ROOT, "paper_1303_4538_b200")
+
+
+def build(tmp_path):
+    exe = str(tmp_path / "shim_example")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "shim_example.cpp"), "-L", LIBDIR,
+                    "-lsip_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    return exe
+
+
+def test_shim_compiles_and_reports_missing_device(tmp_path):
+    exe = build(tmp_path)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present (covered by the gpu test)")
+    except Exception:
+        pass
+    r = subprocess.run([exe, "8"], capture_output=True, text=True)
+    assert r.returncode == 3 and "CUDA error" in r.stdout
+
+
+@pytest.mark.gpu
+def test_shim_solve_matches_oracle(gpu, tmp_path):
+    from oracle import oracle as O
+    exe = build(tmp_path)
+    for prec, flag in (("f64", "d"), ("f32", "s")):
+        r = subprocess.run([exe, "12", flag], capture_output=True, text=True, check=True)
+        lines = r.stdout.split()
+        assert lines[-2:] == ["stale", "ok"]
+        norms = np.array([float(x) for x in lines[:-2]])
+        A = O.generate(0, 1303, (12, 12, 12))
+        ref = O.solve(A, O.field(12, 12, 12), 0.92, 5, prec)
+        np.testing.assert_allclose(norms, ref, rtol=1e-12)
