@@ -55,7 +55,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
 // (__trap -> the launch fails with an error instead of hanging the GPU).
 constexpr unsigned long long kWatchdogNs = 4000000000ULL;
-#define TRCLK() gtime()  // debug trace clock (globaltimer: comparable across SMs)
+#define TRCLK() clock64()  // debug trace clock (SM cycles; use gtime() for cross-SM analysis)
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -331,8 +331,34 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// LSU-side L2 prefetch of one 128-byte line (does not use the TMA engine)
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+constexpr int kPFL = 6;  // steps of LSU L2 prefetch beyond the slice ring
 __device__ __forceinline__ void st_release_cta_s(int* p, int v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_cta_s(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+// Spin until *p >= need with cheap relaxed loads, then one CTA fence (the
+// relaxed load that observed the released value + fence = acquire pattern).
+__device__ __forceinline__ void wait_counter(const int* p, int need, int site) {
+  if (ld_relaxed_cta_s(p) < need) {
+    unsigned long long t0 = 0;
+    int n = 0;
+    while (ld_relaxed_cta_s(p) < need) {
+      if ((++n & 255) == 0) {
+        if (t0 == 0) t0 = gtime();
+        else if (gtime() - t0 > kWatchdogNs) watchdog_fire(site);
+      }
+    }
+  }
+  fence_cta();
 }
 __device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
   int v;
@@ -509,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         Watchdog wd;
         // edge record s is announced on the same slot barrier as slice s
         auto announce = [&](int s) {
-          while (ld_acquire_cta_s(&s_fetched) <= s) wd.idle(46);
+          wait_counter(&s_fetched, s + 1, 46);
           if (ltr) ltr[16 * s + 10] = TRCLK();
           mbar_arrive(&b_fw[(sq + s) % SF]);
         };
@@ -526,10 +552,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           const int s = x + SF;
           if (s < NS) {
             // compute step s writes out-record slot s % OR: the publisher must be past s - OR
-            while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(42);
+            wait_counter(&s_linked, s - OR + 1, 42);
             if (ltr) ltr[16 * s + 8] = TRCLK();
             fw(s);  // phi slice s+1 reuses the slot of phi slice s+1-SP = x-1, last read by prep(x)
+            if (ltr) ltr[16 * s + 14] = TRCLK();
             announce(s);
+            if (ltr) ltr[16 * s + 13] = TRCLK();
           }
           pf(s + kPF);
         }
@@ -668,6 +696,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const T* srcRS = s_R;
       bool act = false;
       unsigned long long* trp = nullptr;  // debug trace slots of the step being prepared
+      const T* fw_pf = P.fw + td.slot * F_NA * kTT;
+      const T* ph_pf = P.phi + td.slot * kTT;
       auto prep = [&](int x) {
         // one wait covers FW slice x, phi slice x+1 and edge record x (phi
         // slices x-1 and x arrived with the transactions of steps x-2 and x-1,
@@ -889,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         };
         Watchdog wd;
         auto announce = [&](int u) {  // edge record u rides on the slot barrier of step u
-          while (ld_acquire_cta_s(&s_fetched) <= u) wd.idle(56);
+          wait_counter(&s_fetched, u + 1, 56);
           mbar_arrive(&b_rg[(sq + u) % SB]);
         };
         for (int u = 0; u < SB && u < NS; ++u) slot(u);
@@ -901,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           mbar_wait(&b_step[qe % EB], (qe / EB) & 1, 51);
           const int s = x + SB;
           if (s < NS) {
-            while (ld_acquire_cta_s(&s_linked) < s - OR + 1) wd.idle(52);
+            wait_counter(&s_linked, s - OR + 1, 52);
             slot(s);
             announce(s);
           }
@@ -993,6 +1023,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       T rr = T(0), ph = T(0), un = T(0), ue = T(0), utdt = T(0), dnx = T(0), dex = T(0);
       bool act = false;
       int kk = 0;
+      const T* r_pf = P.R + td.slot * kTT;
+      const T* ph_pf = P.phi + td.slot * kTT;
+      const T* bw_pf = P.bw + td.slot * B_NA * kTT;
       auto prep = [&](int x) {
         const uint32_t q = sq + x;
         mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);
