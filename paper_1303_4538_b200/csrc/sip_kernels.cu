@@ -417,7 +417,9 @@ struct FwdCfg {
   static constexpr int OR = 8;       // outgoing edge records
   static constexpr int EB = 32;      // step barriers E[x] (> ER + SF, > OR + SF + 1)
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
-  static constexpr size_t bytes = (size_t)(SF * F_NA + SP + 2) * kTT * sizeof(T) +
+  // the forward pack is not staged in shared memory: each compute thread
+  // loads its own cell's 12 values with coalesced LDG one step ahead
+  static constexpr size_t bytes = (size_t)(SP + 2) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SF + EB) * sizeof(uint64_t);
 };
@@ -437,8 +439,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   constexpr int SP = C::SP, ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
   static_assert(EB > ER + SF && EB > OR + SF + 1, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
-  T* s_fw = reinterpret_cast<T*>(smem);
-  T* s_ph = s_fw + SF * F_NA * kTT;
+  T* s_ph = reinterpret_cast<T*>(smem);
   T* s_R = s_ph + SP * kTT;
   T* s_edge = s_R + 2 * kTT;
   T* s_out = s_edge + ER * NE;  // [OR][32]: R of the E column (tj) and N row (16 + ti)
@@ -500,16 +501,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       if (lane == 0) {
         const T* fw_src = P.fw + td.slot * F_NA * kTT;
         const T* ph_src = P.phi + td.slot * kTT;
-        // step s's transaction: FW slice s + phi slice s+1 (+ phi slice 0 for s = 0)
+        // step s's transaction: phi slice s+1 (+ phi slice 0 for s = 0); the
+        // forward pack is read by the compute threads with LDG
         auto fw = [&](int s) {
           const uint32_t q = sq + s;
           uint64_t* bar = &b_fw[q % SF];
-          uint32_t tx = slice_bytes<T>(s, nz, F_NA);
+          uint32_t tx = 0;
           if (s + 1 < NS) tx += slice_bytes<T>(s + 1, nz, 1);
           if (s == 0) tx += slice_bytes<T>(0, nz, 1);
           mbar_expect_tx(bar, tx);
-          issue_slice<T>(s_fw + (q % SF) * F_NA * kTT, fw_src + (long long)s * F_NA * kTT, F_NA, s,
-                         nz, bar, false, 0);
+          (void)fw_src;
           if (s + 1 < NS)
             issue_slice<T>(s_ph + ((q + 1) % SP) * kTT, ph_src + (long long)(s + 1) * kTT, 1, s + 1,
                            nz, bar, false, 0);
@@ -692,6 +693,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       int pc = sq % SP;  // phi slot of slice x while preparing step x
       T RB = T(0);       // own R of the plane below (0 outside the block)
       T pre = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
+      // this cell's 12 forward-pack values of the next step to prepare, loaded
+      // with coalesced read-only LDG one step ahead (no shared-memory staging)
+      T nf[F_NA];
+#pragma unroll
+      for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = T(0);
+      const T* fw_cell = P.fw + td.slot * F_NA * kTT + p;
+      auto ldg_next = [&](int xs) {
+        const int k2 = xs - d;
+        if (xs < NS && col && k2 >= 0 && k2 < nz) {
+          const T* src = fw_cell + (long long)xs * F_NA * kTT;
+#pragma unroll
+          for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = __ldg(src + a2 * kTT);
+        }
+      };
       const T* srcRW = s_R;  // where the prepared step reads R_W / R_S after the barrier
       const T* srcRS = s_R;
       bool act = false;
@@ -708,9 +723,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         act = col && k >= 0 && k < nz;
         const int pm = pc == 0 ? SP - 1 : pc - 1;
         const int pp = pc + 1 == SP ? 0 : pc + 1;
+        {  // keep the forward pack warm in L2 kPFL steps ahead (one 128-byte line per thread)
+          const int xs = x + kPFL;
+          constexpr int kLines = F_NA * kTT * (int)sizeof(T) / 128;
+          if (xs < NS && p < kLines)
+            prefetch_line_l2(reinterpret_cast<const char*>(fw_pf + (long long)xs * F_NA * kTT) + 128 * p);
+        }
         if (act) {
           const T* rec = s_edge + ((sq + x) & (ER - 1)) * NE;
-          const T* f = s_fw + fslot * (F_NA * kTT) + p;
+          const T* f = nf;
           const T* ph0 = s_ph + pc * kTT;
           const T* phm = s_ph + pm * kTT;
           const T* php = s_ph + pp * kTT;
@@ -724,22 +745,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           const T fS = *(inS ? phm + pS : rec + 32 + ti);
           const T fN = *(inN ? php + pN : rec + 48 + ti);
           // residual, Listing-1 term order, a_nb = -A_nb
-          T r = -(f[F_AE * kTT] * fE);
-          r -= f[F_AW * kTT] * fW;
-          r -= f[F_AN * kTT] * fN;
-          r -= f[F_AS * kTT] * fS;
-          r -= f[F_AT * kTT] * fT;
-          r -= f[F_AB * kTT] * fB;
-          r += f[F_Q * kTT];
-          r -= f[F_AP * kTT] * fP;
+          T r = -(f[F_AE] * fE);
+          r -= f[F_AW] * fW;
+          r -= f[F_AN] * fN;
+          r -= f[F_AS] * fS;
+          r -= f[F_AT] * fT;
+          r -= f[F_AB] * fB;
+          r += f[F_Q];
+          r -= f[F_AP] * fP;
           nrm += fabs(static_cast<double>(r));
-          pre = r - f[F_LB * kTT] * RB;
-          lw = f[F_LW * kTT];
-          ls = f[F_LS * kTT];
-          lp = f[F_LP * kTT];
+          pre = r - f[F_LB] * RB;
+          lw = f[F_LW];
+          ls = f[F_LS];
+          lp = f[F_LP];
           srcRW = rec + 64 + tj;  // replaced by s_R below for in-tile neighbours
           srcRS = rec + 80 + ti;
         }
+        ldg_next(x + 1);  // after the values above are consumed
         if (trp) trp[4] = TRCLK();
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
@@ -749,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         pc = pp;
       };
       const bool tracing = P.trace && p == 0 && tid == P.trace_tile;
+      ldg_next(0);
       prep(0);
       for (int t = 0; t < NS; ++t) {
         if (tracing) {
@@ -826,7 +849,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 template <typename T, int SB>
 struct BwdCfg {
   static constexpr int ER = 16, NE = 32, OR = 8, EB = 32;
-  static constexpr size_t bytes = (size_t)(SB * 5 + 2) * kTT * sizeof(T) +
+  // R, phi, UN, UE, UT are own-cell data: LDG'd by each compute thread one
+  // step ahead; shared memory holds only the delta exchange and edge records
+  static constexpr size_t bytes = (size_t)2 * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SB + EB) * sizeof(uint64_t);
 };
@@ -837,8 +862,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   constexpr int ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
   static_assert(EB > ER + SB && EB > OR + SB + 1, "barrier rings must cover the run-ahead");
   extern __shared__ __align__(128) unsigned char smem[];
-  T* s_rg = reinterpret_cast<T*>(smem);
-  T* s_D = s_rg + SB * 5 * kTT;
+  T* s_D = reinterpret_cast<T*>(smem);
   T* s_edge = s_D + 2 * kTT;
   T* s_out = s_edge + ER * NE;  // [OR][32]: delta of the W column (tj) and S row (16 + ti)
   // b_rg[u % SB] completes when slot u has landed AND edge record u is written
@@ -856,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 2);  // loader (expect_tx) + fetcher
+    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 1);  // loader: edge record announced
     for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
     fence_mbar_init();
   }
@@ -885,59 +909,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     }
 
     if (warp == kLoaderWarp) {
-      if (lane == 0) {
-        const T* r_src = P.R + td.slot * kTT;
-        const T* ph_src = P.phi + td.slot * kTT;
-        const T* bw_src = P.bw + td.slot * B_NA * kTT;
-        auto slot = [&](int u) {
-          const int t = NS - 1 - u;
-          const uint32_t q = sq + u;
-          T* dst = s_rg + (q % SB) * 5 * kTT;
-          uint64_t* bar = &b_rg[q % SB];
-          mbar_expect_tx(bar, 2 * slice_bytes<T>(t, nz, 1) + slice_bytes<T>(t, nz, B_NA));
-          issue_slice<T>(dst, r_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-          issue_slice<T>(dst + kTT, ph_src + (long long)t * kTT, 1, t, nz, bar, false, 0);
-          issue_slice<T>(dst + 2 * kTT, bw_src + (long long)t * B_NA * kTT, B_NA, t, nz, bar, false, 0);
-        };
-        int l2 = 0;
-        auto pf = [&](int upto) {
-          if (kPF == 0) return;
-          for (; l2 < NS && l2 <= upto; ++l2) {
-            const int t = NS - 1 - l2;
-            int lo, hi;
-            slice_range<T>(t, nz, lo, hi);
-            const uint32_t b1 = (hi - lo) * sizeof(T);
-            prefetch_l2(r_src + (long long)t * kTT + lo, b1);
-            prefetch_l2(ph_src + (long long)t * kTT + lo, b1);
-            if (lo == 0 && hi == kTT) {
-              prefetch_l2(bw_src + (long long)t * B_NA * kTT, B_NA * kTT * sizeof(T));
-            } else {
-              for (int a = 0; a < B_NA; ++a)
-                prefetch_l2(bw_src + ((long long)t * B_NA + a) * kTT + lo, b1);
-            }
-          }
-        };
-        Watchdog wd;
-        auto announce = [&](int u) {  // edge record u rides on the slot barrier of step u
-          wait_counter(&s_fetched, u + 1, 56);
-          mbar_arrive(&b_rg[(sq + u) % SB]);
-        };
-        for (int u = 0; u < SB && u < NS; ++u) slot(u);
-        for (int u = 0; u < SB && u < NS; ++u) announce(u);
-        pf(SB + kPF);
-        for (int x = 0; x < NS; ++x) {
-          const uint32_t q = sq + x;
-          const uint32_t qe = eq + x;
-          mbar_wait(&b_step[qe % EB], (qe / EB) & 1, 51);
-          const int s = x + SB;
-          if (s < NS) {
-            wait_counter(&s_linked, s - OR + 1, 52);
-            slot(s);
-            announce(s);
-          }
-          pf(s + kPF);
-        }
-      }
+      // K3 needs no loader: compute threads LDG their own cells, the fetcher
+      // announces edge records
     } else if (warp == kPublisherWarp) {
       // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
       const bool we = lane < 16;
@@ -973,14 +946,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
       const unsigned long long* srcB = (we ? P.tagA : P.tagB) + (edgeB + c) * kTagWords<T>;
       const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
-      int e = 0, freed = 0;  // as in K2: poll tagged deltas into the deep ring; the loader announces
+      // Poll tagged deltas into the deep ring (record s -> slot s % ER, reusable
+      // once prep(s - ER + 1) is done) and announce record s on b_rg[s % SB]
+      // once its previous phase is over (prep(s - SB) done).
+      int e = 0, a = 0, freed = 0;
       Watchdog wd;
       constexpr int kB = 4;
-      while (e < NS) {
+      while (a < NS) {
         while (freed < NS) {
           const uint32_t q = eq + freed;
           if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
+        }
+        // compute step s writes out-record slot s % OR: the publisher must be past s - OR
+        const int a_end = min(min(e, freed + SB), ld_relaxed_cta_s(&s_linked) + OR);
+        if (a_end > a) {
+          fence_cta();  // acquire the publisher's progress / order the record stores
+          __syncwarp();
+          if (lane == 0)
+            for (int s2 = a; s2 < a_end; ++s2) mbar_arrive(&b_rg[(sq + s2) % SB]);
+          a = a_end;
         }
         const int m = min(NS - 1, freed + ER - 2);
         if (e > m) {
@@ -1012,9 +997,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           continue;
         }
         wd.progress();
-        __syncwarp();
         e += n;
-        if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
     } else if (warp < kLoaderWarp) {
       const bool col = ti < td.wI && tj < td.wJ;
@@ -1023,29 +1006,53 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       T rr = T(0), ph = T(0), un = T(0), ue = T(0), utdt = T(0), dnx = T(0), dex = T(0);
       bool act = false;
       int kk = 0;
-      const T* r_pf = P.R + td.slot * kTT;
-      const T* ph_pf = P.phi + td.slot * kTT;
-      const T* bw_pf = P.bw + td.slot * B_NA * kTT;
+      const T* r_cell = P.R + td.slot * kTT + p;
+      const T* ph_cell = P.phi + td.slot * kTT + p;
+      const T* bw_cell = P.bw + td.slot * B_NA * kTT + p;
+      T nb[5] = {T(0), T(0), T(0), T(0), T(0)};  // R, phi, UN, UE, UT of the next step
+      auto ldg_next = [&](int xs) {
+        const int ts = NS - 1 - xs, k2 = ts - d;
+        if (xs < NS && col && k2 >= 0 && k2 < nz) {
+          nb[0] = __ldg(r_cell + (long long)ts * kTT);
+          nb[1] = __ldg(ph_cell + (long long)ts * kTT);
+          const T* u = bw_cell + (long long)ts * B_NA * kTT;
+          nb[2] = __ldg(u);
+          nb[3] = __ldg(u + kTT);
+          nb[4] = __ldg(u + 2 * kTT);
+        }
+      };
       auto prep = [&](int x) {
         const uint32_t q = sq + x;
-        mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);
+        {  // keep the next slices warm in L2 (one 128-byte line per thread, LSU path)
+          const int xs = x + kPFL;
+          constexpr int kL1 = kTT * (int)sizeof(T) / 128;
+          if (xs < NS && p < 5 * kL1) {
+            const int ts = NS - 1 - xs;
+            const char* base = p < kL1 ? reinterpret_cast<const char*>(r_cell - p + (long long)ts * kTT)
+                             : p < 2 * kL1 ? reinterpret_cast<const char*>(ph_cell - p + (long long)ts * kTT) - kL1 * 128
+                                           : reinterpret_cast<const char*>(bw_cell - p + (long long)ts * B_NA * kTT) - 2 * kL1 * 128;
+            prefetch_line_l2(base + 128 * p);
+          }
+        }
+        mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);  // edge record x announced
         const int t = NS - 1 - x;
         kk = t - d;
         act = col && kk >= 0 && kk < nz;
         if (act) {
-          const T* sl = s_rg + (q % SB) * 5 * kTT + p;
           const T* rec = s_edge + (q % ER) * NE;
-          rr = sl[0];
-          ph = sl[kTT];
-          un = sl[2 * kTT];
-          ue = sl[3 * kTT];
-          utdt = sl[4 * kTT] * dT;
+          rr = nb[0];
+          ph = nb[1];
+          un = nb[2];
+          ue = nb[3];
+          utdt = nb[4] * dT;
           dnx = rec[16 + ti];
           dex = rec[tj];
         }
+        ldg_next(x + 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
       };
+      ldg_next(0);
       prep(0);
       for (int u = 0; u < NS; ++u) {
         const int t = NS - 1 - u;
@@ -1320,8 +1327,8 @@ static int grid_for(long long n, int threads = 256) {
 }
 static inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? SIP_OK : SIP_ERR_CUDA; }
 
-constexpr int kSF64 = 3, kSF32 = 5;  // forward ring depth (fp64 / fp32)
-constexpr int kSB64 = 6, kSB32 = 8;  // backward ring depth
+constexpr int kSF64 = 6, kSF32 = 6;  // forward slot ring depth (phi slices + edge records)
+constexpr int kSB64 = 8, kSB32 = 8;  // backward record-announce ring depth
 
 template <typename T> struct Rings;
 template <> struct Rings<double> { static constexpr int SF = kSF64, SB = kSB64; };
