@@ -87,6 +87,7 @@ struct sip_ctx {
   int* d_order_b = nullptr;
   void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
   void *edgeW = nullptr, *edgeS = nullptr;
+  void* rec_phi = nullptr;  // [total_slices][64] static part of the K2 edge records
   unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
   size_t tag_words = 0;                 // words per buffer
   unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
@@ -246,6 +247,7 @@ static int build(sip_ctx* ctx) {
   CKS(dalloc(ctx, &ctx->ghost, (size_t)ctx->total_ghost * es));
   CKS(dalloc(ctx, &ctx->edgeW, (size_t)ctx->total_edge * es));
   CKS(dalloc(ctx, &ctx->edgeS, (size_t)ctx->total_edge * es));
+  CKS(dalloc(ctx, &ctx->rec_phi, (size_t)ctx->total_slices * 64 * es));
   ctx->tag_words = (size_t)std::max(1LL, ctx->total_edge) * (es / 4);
   CKS(dalloc(ctx, &ctx->tags, 4 * ctx->tag_words * sizeof(unsigned long long)));
   // tag 0xFFFFFFFF never matches a live (epoch, k) tag (k < 65535)
@@ -470,6 +472,7 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
   p.ghost = static_cast<T*>(ctx->ghost);
   p.edgeW = static_cast<T*>(ctx->edgeW);
   p.edgeS = static_cast<T*>(ctx->edgeS);
+  p.rec_phi = static_cast<T*>(ctx->rec_phi);
   p.tagA = ctx->tags + (forward ? 0 : 2) * ctx->tag_words;
   p.tagB = ctx->tags + (forward ? 1 : 3) * ctx->tag_words;
   p.epoch = ctx->epochs + (forward ? 0 : 1);
@@ -541,8 +544,9 @@ static int iterate_t(sip_ctx* ctx, int iters) {
     const int it = ctx->n_done + n;
     cudaEvent_t e;
     ev_begin(ctx, 0, &e);
+    CKS(launch_edge_phi<T>(sweep_params<T>(ctx, true, it), ctx->stream));
     CKS(launch_forward<T>(sweep_params<T>(ctx, true, it), ctx->grid_f, ctx->stream));
-    ++ctx->launches;
+    ctx->launches += 2;
     ev_end(ctx);
     ev_begin(ctx, 1, &e);
     CKS(launch_backward<T>(sweep_params<T>(ctx, false, it), ctx->grid_b, ctx->stream));
@@ -1033,10 +1037,13 @@ int sip_debug_forward(sip_ctx* ctx) {
   CKS(ensure_norm_cap(ctx, ctx->n_done + 1));
   const size_t st = (32 + std::max<size_t>(1, ctx->htiles.size())) * sizeof(unsigned);
   CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
-  if (ctx->precision == SIP_PREC_SINGLE)
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    CKS(launch_edge_phi<float>(sweep_params<float>(ctx, true, ctx->n_done), ctx->stream));
     CKS(launch_forward<float>(sweep_params<float>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
-  else
+  } else {
+    CKS(launch_edge_phi<double>(sweep_params<double>(ctx, true, ctx->n_done), ctx->stream));
     CKS(launch_forward<double>(sweep_params<double>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
+  }
   CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
   CK(cudaMemsetAsync(ctx->st_b, 0, st, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

@@ -143,6 +143,10 @@ struct SweepParams {
   T* ghost;
   T* edgeW;  // (factor kernel only) unused by K2/K3
   T* edgeS;
+  // K2: the static (old-phi / ghost) part of each step's edge record,
+  // [slot + s][64] = phiW, phiE, phiS, phiN (16 each); built by k_edge_phi
+  // after every halo exchange and bulk-copied with the step's phi slice
+  T* rec_phi;
   // Cross-tile edge values as self-validating tagged words (DESIGN.md
   // "Cross-tile hand-off"): value bits + 32-bit tag (epoch << 16 | k), one
   // 64-bit word per fp32 value, two per fp64 value; index (edge + k*16 + c).
@@ -178,6 +182,8 @@ template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream);
 template <typename T>
 int launch_backward(const SweepParams<T>& p, int grid, void* stream);
+template <typename T>
+int launch_edge_phi(const SweepParams<T>& p, void* stream);
 template <typename T>
 int launch_scatter(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
                    T* pack, int na, int arr, void* stream);

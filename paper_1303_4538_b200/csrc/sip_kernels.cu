@@ -55,7 +55,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
 // (__trap -> the launch fails with an error instead of hanging the GPU).
 constexpr unsigned long long kWatchdogNs = 4000000000ULL;
-#define TRCLK() clock64()  // debug trace clock (SM cycles; use gtime() for cross-SM analysis)
+#define TRCLK() clock64()
+// per-step cycle tracing of one tile (tools/trace_steps.py): debug builds only
+#ifdef SIPB_STEP_TRACE
+constexpr bool kStepTrace = true;
+#else
+constexpr bool kStepTrace = false;
+#endif  // debug trace clock (SM cycles; use gtime() for cross-SM analysis)
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -307,9 +313,9 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
 // on shared-memory mbarriers, compute, store, and meet at one named barrier.
 // =============================================================================
 constexpr int kCompute = kTT;       // compute threads (8 warps)
-constexpr int kThreads = kTT + 96;  // + loader, publisher / linker, fetcher warps
-constexpr int kLoaderWarp = kTT / 32, kLinkerWarp = kTT / 32 + 1;
-constexpr int kPublisherWarp = kLinkerWarp, kFetcherWarp = kTT / 32 + 2;
+constexpr int kThreads = kTT + 64;  // + publisher, fetcher warps
+constexpr int kComputeWarps = kTT / 32;
+constexpr int kPublisherWarp = kComputeWarps, kFetcherWarp = kComputeWarps + 1;
 constexpr int kPF = 0;              // L2 prefetch distance (slices; 0 = off: the TMA unit is the per-SM bottleneck)
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
@@ -327,12 +333,67 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
   asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
 }
+// Explicit 32-bit shared-window accesses: keep ring addresses in plain
+// registers (no generic->shared rematerialisation in the step loops).
+template <typename T>
+__device__ __forceinline__ T lds(uint32_t a);
+template <>
+__device__ __forceinline__ double lds<double>(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ float lds<float>(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int where) {
+  const unsigned long long t0 = gtime();
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (!ok && gtime() - t0 > kWatchdogNs) watchdog_fire(where);
+  } while (!ok);
+}
+// Fast path: one try_wait; the (rare) retry loop with its watchdog is out of line.
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity, int where) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  if (!ok) mbar_wait_slow(a, parity, where);
+}
+// advance a ring address by one slot (wrap-around without division)
+__device__ __forceinline__ uint32_t ring_next(uint32_t a, uint32_t base, uint32_t slot, uint32_t size) {
+  a += slot;
+  return a >= base + size ? a - size : a;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // LSU-side L2 prefetch of one 128-byte line (does not use the TMA engine)
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
+#ifdef SIPB_EXP_NOPF
+  return;
+#endif
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 constexpr int kPFL = 6;  // steps of LSU L2 prefetch beyond the slice ring
@@ -419,7 +480,7 @@ struct FwdCfg {
   static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
   // the forward pack is not staged in shared memory: each compute thread
   // loads its own cell's 12 values with coalesced LDG one step ahead
-  static constexpr size_t bytes = (size_t)(SP + 2) * kTT * sizeof(T) +
+  static constexpr size_t bytes = (size_t)(SP + 4) * kTT * sizeof(T) +
                                   (size_t)(ER * NE + OR * 32) * sizeof(T) +
                                   (SF + EB) * sizeof(uint64_t);
 };
@@ -443,20 +504,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   T* s_R = s_ph + SP * kTT;
   T* s_edge = s_R + 2 * kTT;
   T* s_out = s_edge + ER * NE;  // [OR][32]: R of the E column (tj) and N row (16 + ti)
-  // b_fw[x % SF] completes when FW slice x, phi slice x+1 (and, for x = 0,
-  // phi slice 0) have landed AND the fetcher has written edge record x
-  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_out + OR * 32);
+  T* s_gh = s_out + OR * 32;    // [2][kTT]: ghost phi below / above each column
+  // b_fw[x % SF] completes when phi slice x+1 (and, for x = 0, phi slice 0)
+  // has landed AND the fetcher has written edge record x
+  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_gh + 2 * kTT);
   // E[x] (b_step[(eq + x) % EB], x = 0..NS): prep(x) is done -- slice x, phi
   // slice x-1 and edge record x are consumed -- and step x-1 is complete
   // (its R is in s_R / s_out).  One arrival per compute warp per step.
   uint64_t* b_step = b_fw + SF;
-  __shared__ int s_tile, s_last, s_linked, s_fetched;
+  __shared__ int s_tile, s_last, s_linked;
   __shared__ double s_red[kThreads / 32];
 
   const int p = threadIdx.x;
   const int warp = p >> 5, lane = p & 31;
   int ti = 0, tj = 0;
-  if (warp < kLoaderWarp) pos_to_tij(p, ti, tj);
+  if (warp < kComputeWarps) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
   const int pW = ti > 0 ? tile_pos(ti - 1, tj) : 0;
   const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
@@ -465,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
   unsigned* const prog = P.state + kProgOff;
 
   if (p == 0) {
-    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 2);  // loader (expect_tx) + fetcher
+    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 2);  // fetcher: phi slice (expect_tx) + record
     for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
     fence_mbar_init();
   }
@@ -478,7 +540,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     if (p == 0) {
       s_tile = atomicAdd(P.state, 1u);
       s_linked = 0;
-      s_fetched = 0;
     }
     __syncthreads();
     const int tk = s_tile;
@@ -496,74 +557,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       P.trace[4 * tid + 3] = blockIdx.x;
     }
 
-    if (warp == kLoaderWarp) {
-      // ------------------------------------------------------------ loader
-      if (lane == 0) {
-        const T* fw_src = P.fw + td.slot * F_NA * kTT;
-        const T* ph_src = P.phi + td.slot * kTT;
-        // step s's transaction: phi slice s+1 (+ phi slice 0 for s = 0); the
-        // forward pack is read by the compute threads with LDG
-        auto fw = [&](int s) {
-          const uint32_t q = sq + s;
-          uint64_t* bar = &b_fw[q % SF];
-          uint32_t tx = 0;
-          if (s + 1 < NS) tx += slice_bytes<T>(s + 1, nz, 1);
-          if (s == 0) tx += slice_bytes<T>(0, nz, 1);
-          mbar_expect_tx(bar, tx);
-          (void)fw_src;
-          if (s + 1 < NS)
-            issue_slice<T>(s_ph + ((q + 1) % SP) * kTT, ph_src + (long long)(s + 1) * kTT, 1, s + 1,
-                           nz, bar, false, 0);
-          if (s == 0) issue_slice<T>(s_ph + (q % SP) * kTT, ph_src, 1, 0, nz, bar, false, 0);
-        };
-        int l2 = 0;
-        auto pf = [&](int upto) {
-          if (kPF == 0) return;
-          for (; l2 < NS && l2 <= upto; ++l2) {
-            int lo, hi;
-            slice_range<T>(l2, nz, lo, hi);
-            if (lo == 0 && hi == kTT) {
-              prefetch_l2(fw_src + (long long)l2 * F_NA * kTT, F_NA * kTT * sizeof(T));
-            } else {
-              for (int a = 0; a < F_NA; ++a)
-                prefetch_l2(fw_src + ((long long)l2 * F_NA + a) * kTT + lo, (hi - lo) * sizeof(T));
-            }
-            prefetch_l2(ph_src + (long long)l2 * kTT + lo, (hi - lo) * sizeof(T));
-          }
-        };
-        unsigned long long* ltr =
-            (P.trace && tid == P.trace_tile) ? P.trace + 8 * P.ntiles : nullptr;
-        Watchdog wd;
-        // edge record s is announced on the same slot barrier as slice s
-        auto announce = [&](int s) {
-          wait_counter(&s_fetched, s + 1, 46);
-          if (ltr) ltr[16 * s + 10] = TRCLK();
-          mbar_arrive(&b_fw[(sq + s) % SF]);
-        };
-        for (int s = 0; s < SF && s < NS; ++s) {
-          if (ltr) ltr[16 * s + 8] = TRCLK();
-          fw(s);
-        }
-        for (int s = 0; s < SF && s < NS; ++s) announce(s);
-        pf(SF + kPF);
-        for (int x = 0; x < NS; ++x) {
-          const uint32_t qe = eq + x;
-          mbar_wait(&b_step[qe % EB], (qe / EB) & 1, 41);  // slice x consumed by prep(x)
-          if (ltr) ltr[16 * x + 11] = TRCLK();
-          const int s = x + SF;
-          if (s < NS) {
-            // compute step s writes out-record slot s % OR: the publisher must be past s - OR
-            wait_counter(&s_linked, s - OR + 1, 42);
-            if (ltr) ltr[16 * s + 8] = TRCLK();
-            fw(s);  // phi slice s+1 reuses the slot of phi slice s+1-SP = x-1, last read by prep(x)
-            if (ltr) ltr[16 * s + 14] = TRCLK();
-            announce(s);
-            if (ltr) ltr[16 * s + 13] = TRCLK();
-          }
-          pf(s + kPF);
-        }
-      }
-    } else if (warp == kPublisherWarp) {
+    if (warp == kPublisherWarp) {
       // --------------------------------------------------------- publisher
       // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
       // written as tagged words: the consumer validates each value by its tag,
@@ -573,6 +567,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
       const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
       unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
+      const T* fw_pf = P.fw + td.slot * F_NA * kTT;
+      if (lane == 0)  // warm the first kPFL + 1 forward-pack slices (one bulk L2 prefetch each)
+        for (int xs = 0; xs <= kPFL && xs < NS; ++xs)
+          prefetch_l2(fw_pf + (long long)xs * F_NA * kTT, F_NA * kTT * sizeof(T));
+      // phi slices: step s's transaction (phi slice s+1, + slice 0 for s = 0)
+      // on b_fw[s % SF], armed once prep(s - SF) is done (phi slice s+1 reuses
+      // the slot of slice s+1-SP, SP = SF + 2)
+      const T* ph_src = P.phi + td.slot * kTT;
+      auto fw = [&](int s) {  // lane 0
+        const uint32_t q = sq + s;
+        uint64_t* bar = &b_fw[q % SF];
+        uint32_t tx = 64 * sizeof(T);  // static part of edge record s
+        if (s + 1 < NS) tx += slice_bytes<T>(s + 1, nz, 1);
+        if (s == 0) tx += slice_bytes<T>(0, nz, 1);
+        mbar_expect_tx(bar, tx);
+        bulk_g2s(s_edge + (q & (ER - 1)) * NE, P.rec_phi + (td.slot + s) * 64, 64 * sizeof(T), bar);
+        if (s + 1 < NS)
+          issue_slice<T>(s_ph + ((q + 1) % SP) * kTT, ph_src + (long long)(s + 1) * kTT, 1, s + 1,
+                         nz, bar, false, 0);
+        if (s == 0) issue_slice<T>(s_ph + (q % SP) * kTT, ph_src, 1, 0, nz, bar, false, 0);
+      };
+      int f = 0;  // next transaction to issue (lane 0)
+      if (lane == 0)
+        for (; f < NS && f < SF; ++f) fw(f);
       int t = 0;
       while (t < NS) {
         {
@@ -585,48 +603,66 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++t_end;
         }
+        if (lane == 0)  // E[t_end] seen: prep(0 .. t_end) done
+          for (; f < NS && f < t_end + 1 + SF; ++f) fw(f);
+        const int t_pub = t;
+        (void)t_pub;
         for (; t < t_end; ++t) {
           const int k = t - outoff;
           if (outok && k >= 0 && k < nz)
             put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(t % OR) * 32 + lane],
                        edge_tag(epoch, k));
+          // keep the forward pack warm in L2 kPFL steps ahead of the compute LDGs
+          const int xs = t + 1 + kPFL;
+          if (xs < NS && lane == 0) prefetch_l2(fw_pf + (long long)xs * F_NA * kTT, F_NA * kTT * sizeof(T));
         }
         __syncwarp();
         if (lane == 0) {
-          if (P.trace && tid == P.trace_tile) P.trace[8 * P.ntiles + 16 * (t - 1) + 12] = TRCLK();
+          if (kStepTrace && P.trace && tid == P.trace_tile)  // step-trace slot 2: tile A published steps < t
+            for (int u = t_pub; u < t; ++u) P.trace[8 * P.ntiles + 16 * u + 2] = gtime();
           st_release_cta_s(&s_linked, t);
         }
       }
     } else if (warp == kFetcherWarp) {
       // ----------------------------------------------------------- fetcher
-      // lanes 0-15 serve the W/E sides (index = tj), lanes 16-31 the S/N sides (index = ti)
+      // lanes 0-15 poll R of the W neighbour's E column (index = tj), lanes
+      // 16-31 R of the S neighbour's N row (index = ti); the static phi part
+      // of each record comes with the step's bulk copy (k_edge_phi)
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool colok = we ? (c < td.wJ) : (c < td.wI);
-      const int nA = we ? td.nW : td.nS;   // upstream neighbour (R + phi)
-      const int nB = we ? td.nE : td.nN;   // downstream neighbour (phi only)
-      const long long slotA = nA >= 0 ? P.tiles[nA].slot : 0;
-      const long long slotB = nB >= 0 ? P.tiles[nB].slot : 0;
+      const int nA = we ? td.nW : td.nS;  // upstream neighbour
+      const bool live = nA >= 0 && colok;  // lanes with a value to poll (others: R = 0)
       const long long edgeA = nA >= 0 ? P.tiles[nA].edge : 0;
-      const int posA = we ? tile_pos(kTI - 1, c) : tile_pos(c, kTJ - 1);
-      const int posB = we ? tile_pos(0, c) : tile_pos(c, 0);
-      const int lag = we ? kTI : kTJ;      // upstream neighbour slice = t + lag - 1
-      const int offB = we ? (td.wI - 1) + c : c + (td.wJ - 1);  // edge cell of side B: k = t - offB
-      const T* gA = P.ghost + ghost_face_offset(bd, we ? G_W : G_S) + (we ? td.j0 : td.i0) + c;
-      const T* gB = P.ghost + ghost_face_offset(bd, we ? G_E : G_N) + (we ? td.j0 : td.i0) + c;
       const unsigned long long* eA = (we ? P.tagA : P.tagB) + (edgeA + c) * kTagWords<T>;
-      const long long gstride = we ? bd.ny : bd.nx;
-      // e: next record to fetch into deep-ring slot e % ER (reusable once
-      // prep(e - ER + 1) is done); the loader announces fetched records on the
-      // slot barrier of their step (s_fetched = records fetched so far)
-      int e = 0, freed = 0;
+      // Step s's slot barrier b_fw[s % SF] completes when (1) phi slice s+1
+      // (+ slice 0 for s = 0) and the static part of record s have landed
+      // (armed and copied by the publisher) and (2) the R part of record s
+      // is announced here, which also waits for the publisher (compute step
+      // s writes out-record s % OR).  e: next record to fetch into deep-ring
+      // slot e % ER (reusable once prep(e - ER + 1) is done).
+      int e = 0, a = 0, freed = 0;
       Watchdog wd;
-      constexpr int kB = 4;  // records polled per round trip
-      while (e < NS) {
+      constexpr int kB = 8;  // records polled per round trip
+      while (a < NS) {
         while (freed < NS) {  // prep(freed) done? (compute cannot pass the records: bounded)
           const uint32_t q = eq + freed;
           if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
           ++freed;
+        }
+        {
+          const int a_end = __shfl_sync(0xffffffffu,
+                                        min(min(e, freed + SF), ld_relaxed_cta_s(&s_linked) + OR), 0);
+          if (a_end > a) {
+            fence_cta();  // acquire the publisher's progress / order the record stores
+            __syncwarp();
+            if (lane == 0)
+              for (int s2 = a; s2 < a_end; ++s2) {
+                if (kStepTrace && P.trace && tid == P.trace_tile + 1) P.trace[8 * P.ntiles + 16 * s2 + 4] = gtime();
+                mbar_arrive(&b_fw[(sq + s2) % SF]);
+              }
+            a = a_end;
+          }
         }
         const int m = min(NS - 1, freed + ER - 2);
         if (e > m) {
@@ -634,34 +670,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           continue;
         }
         // issue the loads of up to kB records at once, then accept the valid prefix
-        T phA[kB], phB[kB], rA[kB];
+        T rA[kB];
         bool ok[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
           const int s2 = e + j;
-          phA[j] = T(0); phB[j] = T(0); rA[j] = T(0); ok[j] = true;
-          if (s2 > m) continue;
           const int kA = s2 - c;  // W side cell (0, c) / S side cell (c, 0)
-          if (colok && kA >= 0 && kA < nz) {
-            if (nA >= 0) {
-              phA[j] = P.phi[(slotA + s2 + lag - 1) * kTT + posA];
-              ok[j] = get_tagged(eA + (long long)kA * 16 * kTagWords<T>, edge_tag(epoch, kA), rA[j]);
-            } else {
-              phA[j] = gA[gstride * kA];
-            }
-          }
-          const int kB2 = s2 - offB;
-          if (colok && kB2 >= 0 && kB2 < nz)
-            phB[j] = nB >= 0 ? P.phi[(slotB + s2 - lag + 1) * kTT + posB] : gB[gstride * kB2];
+          rA[j] = T(0);
+          ok[j] = true;
+          if (live && s2 <= m && kA >= 0 && kA < nz)
+            ok[j] = get_tagged(eA + (long long)kA * 16 * kTagWords<T>, edge_tag(epoch, kA), rA[j]);
         }
         int n = 0;
 #pragma unroll
         for (int j = 0; j < kB; ++j) {
           if (n == j && e + j <= m && __all_sync(0xffffffffu, ok[j])) {
-            T* rec = s_edge + ((sq + e + j) % ER) * NE;
-            rec[(we ? 0 : 32) + c] = phA[j];
-            rec[(we ? 16 : 48) + c] = phB[j];
-            rec[(we ? 64 : 80) + c] = rA[j];
+            s_edge[((sq + e + j) % ER) * NE + (we ? 64 : 80) + c] = rA[j];
             n = j + 1;
           }
         }
@@ -670,32 +694,54 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
           continue;
         }
         wd.progress();
-        __syncwarp();  // record stores ordered before lane 0's release of s_fetched
-        if (lane == 0 && P.trace && tid == P.trace_tile)
-          for (int s2 = e; s2 < e + n; ++s2) P.trace[8 * P.ntiles + 16 * s2 + 9] = TRCLK();
+        if (kStepTrace && P.trace && tid == P.trace_tile + 1 && lane == 0)  // slot 3: tile B fetched records
+          for (int u = e; u < e + n; ++u) P.trace[8 * P.ntiles + 16 * u + 3] = gtime();
         e += n;
-        if (lane == 0) st_release_cta_s(&s_fetched, e);
       }
-    } else if (warp < kLoaderWarp) {
+    } else if (warp < kComputeWarps) {
       // --------------------------------------------------------- compute warps
+      // Iteration t: the shared loads of critical(t) and of the residual of
+      // step t+1 are issued first (branch-free, always-valid addresses), then
+      // both FP chains, so the residual fills the latency of the recurrence;
+      // then one step-done arrival, one wait for the data of step t+2 and one
+      // named barrier.  All ring positions are 32-bit shared addresses.
+      constexpr uint32_t SZ = sizeof(T);
+      constexpr uint32_t SLICE = kTT * SZ;
       const bool col = ti < td.wI && tj < td.wJ;
       const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
-      const int gi = td.i0 + ti, gj = td.j0 + tj;
-      T ghB = T(0), ghT = T(0);
-      if (col) {
-        ghB = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
-        ghT = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
+      const uint32_t aPh = saddr(smem);
+      const uint32_t aR = aPh + SP * SLICE;
+      const uint32_t aEdge = aR + 2 * SLICE;
+      const uint32_t aOut = aEdge + ER * NE * SZ;
+      const uint32_t aGh = aOut + OR * 32 * SZ;
+      const uint32_t aFw = saddr(b_fw), aStep = saddr(b_step);
+      const uint32_t oP = p * SZ;
+      {
+        const int gi = td.i0 + ti, gj = td.j0 + tj;
+        T gb = T(0), gt = T(0);
+        if (col) {
+          gb = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
+          gt = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
+        }
+        sts(aGh + oP, gb);  // own slots: read back by this thread only
+        sts(aGh + SLICE + oP, gt);
       }
-      // Ring positions advance by one per step: keep them as rolling
-      // registers (SF and SP are not powers of two).
-      int fslot = sq % SF;
+      // neighbour operands: in-tile (offset into a phi slot / R buffer) or
+      // from the edge record (phiW, phiE, phiS, phiN, RW, RS; 16 each)
+      const uint32_t offW = (inW ? pW : tj) * SZ, offE = (inE ? pE : 16 + tj) * SZ;
+      const uint32_t offS = (inS ? pS : 32 + ti) * SZ, offN = (inN ? pN : 48 + ti) * SZ;
+      const uint32_t offRW = (inW ? pW : 64 + tj) * SZ, offRS = (inS ? pS : 80 + ti) * SZ;
+      const uint32_t oOutE = (ti == kTI - 1) ? tj * SZ : 0xFFFFFFFFu;
+      const uint32_t oOutN = (tj == kTJ - 1) ? (16 + ti) * SZ : 0xFFFFFFFFu;
+      uint32_t ph0 = aPh + (sq % SP) * SLICE;  // slot of phi slice x while preparing step x
+      uint32_t rec = aEdge + (sq & (ER - 1)) * NE * SZ;  // edge record of step x
+      uint32_t fwb = aFw + (sq % SF) * 8;
       uint32_t fpar = (sq / SF) & 1;
-      int pc = sq % SP;  // phi slot of slice x while preparing step x
-      T RB = T(0);       // own R of the plane below (0 outside the block)
-      T pre = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
-      // this cell's 12 forward-pack values of the next step to prepare, loaded
-      // with coalesced read-only LDG one step ahead (no shared-memory staging)
-      T nf[F_NA];
+      uint32_t eb = aStep + (eq % EB) * 8;
+      uint32_t ob = aOut;  // out-record slot of step t (t % OR)
+      T RB = T(0);         // own R of the plane below (0 outside the block)
+      T r = T(0), lb = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
+      T nf[F_NA];  // forward-pack values of the next step to prepare (LDG one step ahead)
 #pragma unroll
       for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = T(0);
       const T* fw_cell = P.fw + td.slot * F_NA * kTT + p;
@@ -703,105 +749,104 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         const int k2 = xs - d;
         if (xs < NS && col && k2 >= 0 && k2 < nz) {
           const T* src = fw_cell + (long long)xs * F_NA * kTT;
+#ifdef SIPB_EXP_NOLDG
+#pragma unroll
+          for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = T(0.01) * T(a2 + 1) + T(xs) * T(1e-9);
+          (void)src;
+#else
 #pragma unroll
           for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = __ldg(src + a2 * kTT);
+#endif
         }
       };
-      const T* srcRW = s_R;  // where the prepared step reads R_W / R_S after the barrier
-      const T* srcRS = s_R;
-      bool act = false;
-      unsigned long long* trp = nullptr;  // debug trace slots of the step being prepared
-      const T* fw_pf = P.fw + td.slot * F_NA * kTT;
-      const T* ph_pf = P.phi + td.slot * kTT;
-      auto prep = [&](int x) {
-        // one wait covers FW slice x, phi slice x+1 and edge record x (phi
-        // slices x-1 and x arrived with the transactions of steps x-2 and x-1,
-        // which every compute thread has already waited for)
-        mbar_wait(&b_fw[fslot], fpar, 21);
-        if (trp) trp[3] = TRCLK();
-        const int k = x - d;
-        act = col && k >= 0 && k < nz;
-        const int pm = pc == 0 ? SP - 1 : pc - 1;
-        const int pp = pc + 1 == SP ? 0 : pc + 1;
-        {  // keep the forward pack warm in L2 kPFL steps ahead (one 128-byte line per thread)
-          const int xs = x + kPFL;
-          constexpr int kLines = F_NA * kTT * (int)sizeof(T) / 128;
-          if (xs < NS && p < kLines)
-            prefetch_line_l2(reinterpret_cast<const char*>(fw_pf + (long long)xs * F_NA * kTT) + 128 * p);
-        }
-        if (act) {
-          const T* rec = s_edge + ((sq + x) & (ER - 1)) * NE;
-          const T* f = nf;
-          const T* ph0 = s_ph + pc * kTT;
-          const T* phm = s_ph + pm * kTT;
-          const T* php = s_ph + pp * kTT;
-          // branch-free operand selection: pick the shared address, then load
-          const T fP = ph0[p];
-          const T vB = phm[p], vT = php[p];
-          const T fB = k > 0 ? vB : ghB;
-          const T fT = k + 1 < nz ? vT : ghT;
-          const T fW = *(inW ? phm + pW : rec + tj);
-          const T fE = *(inE ? php + pE : rec + 16 + tj);
-          const T fS = *(inS ? phm + pS : rec + 32 + ti);
-          const T fN = *(inN ? php + pN : rec + 48 + ti);
-          // residual, Listing-1 term order, a_nb = -A_nb
-          T r = -(f[F_AE] * fE);
-          r -= f[F_AW] * fW;
-          r -= f[F_AN] * fN;
-          r -= f[F_AS] * fS;
-          r -= f[F_AT] * fT;
-          r -= f[F_AB] * fB;
-          r += f[F_Q];
-          r -= f[F_AP] * fP;
-          nrm += fabs(static_cast<double>(r));
-          pre = r - f[F_LB] * RB;
-          lw = f[F_LW];
-          ls = f[F_LS];
-          lp = f[F_LP];
-          srcRW = rec + 64 + tj;  // replaced by s_R below for in-tile neighbours
-          srcRS = rec + 80 + ti;
-        }
-        ldg_next(x + 1);  // after the values above are consumed
-        if (trp) trp[4] = TRCLK();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
-        if (trp) trp[5] = TRCLK();
-        fslot = fslot + 1 == SF ? 0 : fslot + 1;
-        fpar ^= (fslot == 0);
-        pc = pp;
+      // residual of step x (Listing-1 term order, a_nb = -A_nb)
+      auto residual = [&](T fP, T fB, T fT, T fW, T fE, T fS, T fN) {
+        T rr = -(nf[F_AE] * fE);
+        rr -= nf[F_AW] * fW;
+        rr -= nf[F_AN] * fN;
+        rr -= nf[F_AS] * fS;
+        rr -= nf[F_AT] * fT;
+        rr -= nf[F_AB] * fB;
+        rr += nf[F_Q];
+        rr -= nf[F_AP] * fP;
+        return rr;
       };
-      const bool tracing = P.trace && p == 0 && tid == P.trace_tile;
+      T* gR = P.R + td.slot * kTT + p;
+      // ---- step 0 preparation (only the (0,0) column is active at k = 0)
       ldg_next(0);
-      prep(0);
-      for (int t = 0; t < NS; ++t) {
-        if (tracing) {
-          trp = P.trace + 8 * P.ntiles + 16 * t;
-          trp[0] = TRCLK();
-        }
-        const bool was = act;
-        T Rv = T(0);
+      mbar_wait_a(fwb, fpar, 21);
+      bool act = col && d == 0 && nz > 0;
+      {
+        const uint32_t php = ring_next(ph0, aPh, SLICE, SP * SLICE);
+        const T fP = lds<T>(ph0 + oP);
+        const T fB = lds<T>(aGh + oP);
+        const T fT = lds<T>((nz > 1 ? php : aGh + SLICE) + oP);
+        const T fW = lds<T>(rec + offW), fE = lds<T>((inE ? php : rec) + offE);
+        const T fS = lds<T>(rec + offS), fN = lds<T>((inN ? php : rec) + offN);
+        const T rr = residual(fP, fB, fT, fW, fE, fS, fN);
         if (act) {
-          const T* sRm = s_R + ((t - 1) & 1) * kTT;
-          const T RW = *(inW ? sRm + pW : srcRW);
-          const T RS = *(inS ? sRm + pS : srcRS);
-          Rv = ((pre - lw * RW) - ls * RS) * lp;
+          nrm += fabs(static_cast<double>(rr));
+          r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
+        }
+      }
+      ldg_next(1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(eb);
+      eb = ring_next(eb, aStep, 8, EB * 8);
+      fwb = ring_next(fwb, aFw, 8, SF * 8);
+      fpar ^= (fwb == aFw);
+      ph0 = ring_next(ph0, aPh, SLICE, SP * SLICE);
+      if (1 < NS) mbar_wait_a(fwb, fpar, 22);
+      for (int t = 0; t < NS; ++t) {
+        const int x = t + 1;
+        // ---- shared loads of critical(t)
+        const uint32_t sRm = aR + ((t - 1) & 1) * SLICE;
+        const T RW = lds<T>((inW ? sRm : rec) + offRW);
+        const T RS = lds<T>((inS ? sRm : rec) + offRS);
+        // ---- shared loads of the residual of step x: slices x-1, x, x+1, record x
+        const uint32_t recx = ring_next(rec, aEdge, NE * SZ, ER * NE * SZ);
+        const uint32_t php = ring_next(ph0, aPh, SLICE, SP * SLICE);
+        const uint32_t phm = ph0 == aPh ? ph0 + (SP - 1) * SLICE : ph0 - SLICE;
+        const int k1 = x - d;
+        const T fP = lds<T>(ph0 + oP);
+        const T fB = lds<T>((k1 > 0 ? phm : aGh) + oP);
+        const T fT = lds<T>((k1 + 1 < nz ? php : aGh + SLICE) + oP);
+        const T fW = lds<T>((inW ? phm : recx) + offW);
+        const T fE = lds<T>((inE ? php : recx) + offE);
+        const T fS = lds<T>((inS ? phm : recx) + offS);
+        const T fN = lds<T>((inN ? php : recx) + offN);
+        // ---- critical(t): R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP
+        const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
+        if (act) {
           RB = Rv;
-          s_R[(t & 1) * kTT + p] = Rv;
-          if (ti == kTI - 1) s_out[(t % OR) * 32 + tj] = Rv;
-          if (tj == kTJ - 1) s_out[(t % OR) * 32 + 16 + ti] = Rv;
+          sts(aR + (t & 1) * SLICE + oP, Rv);
+          if (oOutE != 0xFFFFFFFFu) sts(ob + oOutE, Rv);
+          if (oOutN != 0xFFFFFFFFu) sts(ob + oOutN, Rv);
+#ifndef SIPB_EXP_NOSTG
+          gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
+#endif
         }
-        if (trp) trp[1] = TRCLK();
-        if (trp) trp[2] = TRCLK();
-        if (t + 1 < NS) {
-          prep(t + 1);  // arrives E[t+1]: step t complete, step t+1 prepared
-        } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&b_step[(eq + NS) % EB]);
+        // ---- residual of step x
+        const bool act1 = x < NS && col && k1 >= 0 && k1 < nz;
+        const T rr = residual(fP, fB, fT, fW, fE, fS, fN);
+        if (act1) {
+          nrm += fabs(static_cast<double>(rr));
+          r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
         }
-        if (was) P.R[(td.slot + t) * kTT + p] = Rv;  // consumed only by K3 (next launch)
-        if (trp) trp[6] = TRCLK();
+        ldg_next(x + 1);  // nf consumed above
+        act = act1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_a(eb);  // E[x]: step t done, step x prepared
+        eb = ring_next(eb, aStep, 8, EB * 8);
+        fwb = ring_next(fwb, aFw, 8, SF * 8);
+        fpar ^= (fwb == aFw);
+        ph0 = php;
+        rec = recx;
+        ob = ring_next(ob, aOut, 32 * SZ, OR * 32 * SZ);
+        if (x + 1 < NS) mbar_wait_a(fwb, fpar, 21);  // data of step x+1
+        if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
+          P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
         bar_compute();
-        if (trp) trp[7] = TRCLK();
       }
     }
     sq += NS;
@@ -868,12 +913,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
   // b_rg[u % SB] completes when slot u has landed AND edge record u is written
   uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
   uint64_t* b_step = b_rg + SB;  // E[x] as in K2
-  __shared__ int s_tile, s_last, s_linked, s_fetched;
+  __shared__ int s_tile, s_last, s_linked;
 
   const int p = threadIdx.x;
   const int warp = p >> 5, lane = p & 31;
   int ti = 0, tj = 0;
-  if (warp < kLoaderWarp) pos_to_tij(p, ti, tj);
+  if (warp < kComputeWarps) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
   const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
   const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
@@ -892,7 +937,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
     if (p == 0) {
       s_tile = atomicAdd(P.state, 1u);
       s_linked = 0;
-      s_fetched = 0;
     }
     __syncthreads();
     const int tk = s_tile;
@@ -908,15 +952,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       P.trace[4 * tid + 3] = blockIdx.x;
     }
 
-    if (warp == kLoaderWarp) {
-      // K3 needs no loader: compute threads LDG their own cells, the fetcher
-      // announces edge records
-    } else if (warp == kPublisherWarp) {
+    // no loader: compute threads LDG their own cells, the fetcher announces
+    // edge records, the publisher keeps the slices warm in L2
+    if (warp == kPublisherWarp) {
       // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
       unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
+      // keeps the slices kPFL steps ahead of the compute LDGs warm in L2 (the
+      // publisher gates the compute warps through s_linked, so it cannot fall
+      // a full E ring behind)
+      constexpr int kL1 = kTT * (int)sizeof(T) / 128;  // lines per array slice
+      const char* rb = reinterpret_cast<const char*>(P.R + td.slot * kTT);
+      const char* pb = reinterpret_cast<const char*>(P.phi + td.slot * kTT);
+      const char* ub = reinterpret_cast<const char*>(P.bw + td.slot * B_NA * kTT);
+      auto pf = [&](int xs) {
+        if (xs >= NS) return;
+        const int ts = NS - 1 - xs;
+        for (int l = lane; l < 5 * kL1; l += 32) {
+          const char* a = l < kL1       ? rb + (long long)ts * kTT * sizeof(T) + 128 * l
+                          : l < 2 * kL1 ? pb + (long long)ts * kTT * sizeof(T) + 128 * (l - kL1)
+                                        : ub + (long long)ts * B_NA * kTT * sizeof(T) + 128 * (l - 2 * kL1);
+          prefetch_line_l2(a);
+        }
+      };
+      for (int xs = 0; xs <= kPFL; ++xs) pf(xs);
       int u = 0;
       while (u < NS) {
         {
@@ -934,6 +995,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           if (outok && k >= 0 && k < nz)
             put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(u % OR) * 32 + lane],
                        edge_tag(epoch, k));
+          pf(u + 1 + kPFL);
         }
         __syncwarp();
         if (lane == 0) st_release_cta_s(&s_linked, u);
@@ -999,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
         wd.progress();
         e += n;
       }
-    } else if (warp < kLoaderWarp) {
+    } else if (warp < kComputeWarps) {
       const bool col = ti < td.wI && tj < td.wJ;
       const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
       T dT = T(0);
@@ -1013,27 +1075,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       auto ldg_next = [&](int xs) {
         const int ts = NS - 1 - xs, k2 = ts - d;
         if (xs < NS && col && k2 >= 0 && k2 < nz) {
+#ifdef SIPB_EXP_NOLDG
+          nb[0] = T(ts) * T(1e-9); nb[1] = T(0.5); nb[2] = T(0.1); nb[3] = T(0.2); nb[4] = T(0.3);
+#else
           nb[0] = __ldg(r_cell + (long long)ts * kTT);
           nb[1] = __ldg(ph_cell + (long long)ts * kTT);
           const T* u = bw_cell + (long long)ts * B_NA * kTT;
           nb[2] = __ldg(u);
           nb[3] = __ldg(u + kTT);
           nb[4] = __ldg(u + 2 * kTT);
+#endif
         }
       };
       auto prep = [&](int x) {
         const uint32_t q = sq + x;
-        {  // keep the next slices warm in L2 (one 128-byte line per thread, LSU path)
-          const int xs = x + kPFL;
-          constexpr int kL1 = kTT * (int)sizeof(T) / 128;
-          if (xs < NS && p < 5 * kL1) {
-            const int ts = NS - 1 - xs;
-            const char* base = p < kL1 ? reinterpret_cast<const char*>(r_cell - p + (long long)ts * kTT)
-                             : p < 2 * kL1 ? reinterpret_cast<const char*>(ph_cell - p + (long long)ts * kTT) - kL1 * 128
-                                           : reinterpret_cast<const char*>(bw_cell - p + (long long)ts * B_NA * kTT) - 2 * kL1 * 128;
-            prefetch_line_l2(base + 128 * p);
-          }
-        }
         mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);  // edge record x announced
         const int t = NS - 1 - x;
         kk = t - d;
@@ -1074,7 +1129,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
           __syncwarp();
           if (lane == 0) mbar_arrive(&b_step[(eq + NS) % EB]);
         }
+#ifndef SIPB_EXP_NOSTG
         if (was) P.phi[(td.slot + t) * kTT + p] = phn;
+#endif
         bar_compute();
       }
     }
@@ -1092,6 +1149,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
       if (p == 0) *P.epoch = epoch + 1;
     }
+  }
+}
+
+// =============================================================================
+// Static part of the K2 edge records: for every tile and step s, the old phi
+// of the W / E / S / N neighbour cells the step reads (a neighbour tile's
+// packed phi, or the block's ghost faces); [slot + s][64] in the shared
+// record layout.  Runs after each halo exchange, before K2, so the forward
+// sweep's fetcher only polls the R values that are produced during the sweep.
+// =============================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) k_edge_phi(const SweepParams<T> P) {
+  const TileDesc td = P.tiles[blockIdx.x];
+  const BlockDesc bd = P.blocks[td.block];
+  const int NS = td.ns, nz = td.nz;
+  const int q = threadIdx.x & 63;
+  const bool we = q < 32, sideB = (q & 16) != 0;  // W, E, S, N = 16 each
+  const int c = q & 15;
+  const bool colok = we ? (c < td.wJ) : (c < td.wI);
+  const int nbr = sideB ? (we ? td.nE : td.nN) : (we ? td.nW : td.nS);
+  const long long slotN = nbr >= 0 ? P.tiles[nbr].slot : 0;
+  const int lag = we ? kTI : kTJ;
+  // neighbour cell (upstream: its E column / N row; downstream: its W column / S row)
+  const int posN = sideB ? (we ? tile_pos(0, c) : tile_pos(c, 0))
+                         : (we ? tile_pos(kTI - 1, c) : tile_pos(c, kTJ - 1));
+  const int koff = sideB ? (we ? (td.wI - 1) + c : c + (td.wJ - 1)) : c;  // cell k = s - koff
+  const long long sdelta = sideB ? -(lag - 1) : (lag - 1);                // neighbour slice = s + sdelta
+  const T* g = P.ghost + ghost_face_offset(bd, sideB ? (we ? G_E : G_N) : (we ? G_W : G_S)) +
+               (we ? td.j0 : td.i0) + c;
+  const long long gstride = we ? bd.ny : bd.nx;
+  for (int s = threadIdx.x >> 6; s < NS; s += blockDim.x >> 6) {
+    const int k = s - koff;
+    T v = T(0);
+    if (colok && k >= 0 && k < nz)
+      v = nbr >= 0 ? P.phi[(slotN + s + sdelta) * kTT + posN] : g[gstride * k];
+    P.rec_phi[((long long)td.slot + s) * 64 + q] = v;
   }
 }
 
@@ -1364,6 +1457,15 @@ int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
   k_backward<T, SB><<<grid, kThreads, smem, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
+
+template <typename T>
+int launch_edge_phi(const SweepParams<T>& p, void* stream) {
+  if (p.ntiles <= 0) return SIP_OK;
+  k_edge_phi<T><<<p.ntiles, 256, 0, (cudaStream_t)stream>>>(p);
+  return cudaGetLastError() == cudaSuccess ? SIP_OK : SIP_ERR_CUDA;
+}
+template int launch_edge_phi<float>(const SweepParams<float>&, void*);
+template int launch_edge_phi<double>(const SweepParams<double>&, void*);
 
 int max_resident_ctas(int kind, int precision, int* grid) {
   int dev = 0, sms = 0, per = 0;

@@ -31,7 +31,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsip_b200.so")
+LIB_PATH = os.environ.get("SIPB_LIB") or os.path.join(_HERE, "libsip_b200.so")
 
 SIP_OK, SIP_ERR_SINGULAR, SIP_ERR_STALE, SIP_ERR_MISUSE = 0, 1, 2, 3
 SIP_ERR_CONFIG, SIP_ERR_CUDA, SIP_ERR_NCCL, SIP_ERR_NOMEM = 4, 5, 6, 7
