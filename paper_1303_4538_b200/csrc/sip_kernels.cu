@@ -71,6 +71,11 @@ __device__ __noinline__ void watchdog_fire(int where) {
   printf("sip watchdog: block %d thread %d stalled at site %d\n", blockIdx.x, threadIdx.x, where);
   __trap();
 }
+#ifdef SIPB_EXP_SPIN
+#define SIPB_MBAR_WAIT_OP "mbarrier.test_wait.parity.shared::cta.b64"
+#else
+#define SIPB_MBAR_WAIT_OP "mbarrier.try_wait.parity.shared::cta.b64"
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int where = 0) {
   const uint32_t a = saddr(b);
   uint32_t ok;
@@ -78,7 +83,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int wher
   int n = 0;
   do {
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(a), "r"(parity)
         : "memory");
@@ -363,7 +368,7 @@ __device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int whe
   uint32_t ok;
   do {
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(a), "r"(parity)
         : "memory");
@@ -374,7 +379,7 @@ __device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int whe
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity, int where) {
   uint32_t ok;
   asm volatile(
-      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
       : "=r"(ok)
       : "r"(a), "r"(parity)
       : "memory");
@@ -386,6 +391,9 @@ __device__ __forceinline__ uint32_t ring_next(uint32_t a, uint32_t base, uint32_
   return a >= base + size ? a - size : a;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+#ifdef SIPB_EXP_NOPF
+  return;
+#endif
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
@@ -394,11 +402,20 @@ __device__ __forceinline__ void prefetch_line_l2(const void* p) {
 #ifdef SIPB_EXP_NOPF
   return;
 #endif
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 constexpr int kPFL = 6;  // steps of LSU L2 prefetch beyond the slice ring
 __device__ __forceinline__ void st_release_cta_s(int* p, int v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
+}
+// Progress counter of the publisher (slots of the out-record ring it has
+// read): a relaxed shared store.  A release here (MEMBAR.ALL.CTA) would wait
+// for the publisher's just-issued global edge stores; the only hazard it
+// guards is shared (its reads of out-record slots, whose values its issued
+// stores have already consumed, against the compute warps' later rewrite,
+// ordered through the fetcher's mbarrier arrive and the compute's wait).
+__device__ __forceinline__ void st_progress_s(int* p, int v) {
+  asm volatile("st.relaxed.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ int ld_relaxed_cta_s(const int* p) {
   int v;
@@ -471,76 +488,92 @@ __device__ __forceinline__ bool warp_test(uint64_t* b, uint32_t parity) {
   return __all_sync(0xffffffffu, mbar_test(b, parity));
 }
 
-template <typename T, int SF>
-struct FwdCfg {
-  static constexpr int SP = SF + 2;  // phi slice s is read while preparing steps s-1, s, s+1
-  static constexpr int ER = 16;      // edge records (deep ring; readiness rides on the slot barrier)
-  static constexpr int OR = 8;       // outgoing edge records
-  static constexpr int EB = 32;      // step barriers E[x] (> ER + SF, > OR + SF + 1)
-  static constexpr int NE = 96;      // phiW, phiE, phiS, phiN, RW, RS (16 each)
-  // the forward pack is not staged in shared memory: each compute thread
-  // loads its own cell's 12 values with coalesced LDG one step ahead
-  static constexpr size_t bytes = (size_t)(SP + 4) * kTT * sizeof(T) +
-                                  (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SF + EB) * sizeof(uint64_t);
-};
+// =============================================================================
+// K2 / K3: one CTA of 256 threads per 16x16-column tile, persistent, tiles
+// taken in topological ticket order (an upstream tile always holds an
+// earlier ticket, so spinning on it cannot deadlock).  Each thread owns one
+// column and walks the tile's hyperplanes; per step it meets the other 255
+// threads at one barrier, nothing else.
+//   * own data (forward pack, phi, R / backward pack) are LDG'd by each
+//     thread two or more steps ahead into registers (coalesced: the pack is
+//     slice-major, anti-diagonal positions);
+//   * in-tile neighbour values go through small shared rings (phi slices,
+//     the static edge-phi record, R / delta of the previous step);
+//   * cross-tile values: the producing edge threads store tagged words
+//     (value + (epoch, k) tag) straight to global memory; the consuming edge
+//     threads issue the poll load two steps ahead and re-poll only if the tag
+//     does not match yet.  No service warps, no counters, no fences.
+// Iteration t of K2 computes critical(t) and the residual of step t+1: both
+// sets of shared loads are issued first, so the residual fills the latency
+// of the recurrence.
+// =============================================================================
 
-// Step pipeline of one compute thread (K2):
-//   prep(x):  wait for slice x / edge record x, evaluate the residual of step x
-//             and pre = r - LB*R_B (everything that does not depend on the
-//             in-tile neighbours of step x-1), then signal "slice x consumed";
-//   step(t):  after the named barrier, R = ((pre - LW*R_W) - LS*R_S) * LP,
-//             store, signal "step t done", prep(t+1), barrier.
-// The recurrence's critical path per step is thus two shared loads, four
-// dependent flops and one barrier; the operation order per cell is exactly
-// the oracle's (pre is the oracle's first subtraction).
-template <typename T, int SF>
-__global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P) {
-  using C = FwdCfg<T, SF>;
-  constexpr int SP = C::SP, ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
-  static_assert(EB > ER + SF && EB > OR + SF + 1, "barrier rings must cover the run-ahead");
-  extern __shared__ __align__(128) unsigned char smem[];
-  T* s_ph = reinterpret_cast<T*>(smem);
-  T* s_R = s_ph + SP * kTT;
-  T* s_edge = s_R + 2 * kTT;
-  T* s_out = s_edge + ER * NE;  // [OR][32]: R of the E column (tj) and N row (16 + ti)
-  T* s_gh = s_out + OR * 32;    // [2][kTT]: ghost phi below / above each column
-  // b_fw[x % SF] completes when phi slice x+1 (and, for x = 0, phi slice 0)
-  // has landed AND the fetcher has written edge record x
-  uint64_t* b_fw = reinterpret_cast<uint64_t*>(s_gh + 2 * kTT);
-  // E[x] (b_step[(eq + x) % EB], x = 0..NS): prep(x) is done -- slice x, phi
-  // slice x-1 and edge record x are consumed -- and step x-1 is complete
-  // (its R is in s_R / s_out).  One arrival per compute warp per step.
-  uint64_t* b_step = b_fw + SF;
-  __shared__ int s_tile, s_last, s_linked;
-  __shared__ double s_red[kThreads / 32];
+// Poll words of one tagged value: issued early, decoded when consumed.
+template <typename T>
+struct TagPoll;
+template <>
+struct TagPoll<double> {
+  unsigned long long w0 = ~0ull, w1 = ~0ull;
+  __device__ __forceinline__ void issue(const unsigned long long* src) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(src) : "memory");
+  }
+  __device__ __forceinline__ bool ok(uint32_t tag) const {
+    return (uint32_t)(w0 >> 32) == tag && (uint32_t)(w1 >> 32) == tag;
+  }
+  __device__ __forceinline__ double value() const {
+    return __longlong_as_double((long long)((w0 << 32) | (w1 & 0xFFFFFFFFull)));
+  }
+};
+template <>
+struct TagPoll<float> {
+  unsigned long long w0 = ~0ull;
+  __device__ __forceinline__ void issue(const unsigned long long* src) {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w0) : "l"(src) : "memory");
+  }
+  __device__ __forceinline__ bool ok(uint32_t tag) const { return (uint32_t)(w0 >> 32) == tag; }
+  __device__ __forceinline__ float value() const { return __uint_as_float((uint32_t)w0); }
+};
+// Consume a poll: spin (re-issue) until the tag matches.
+template <typename T>
+__device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long* src, uint32_t tag,
+                                       int where) {
+  if (!pl.ok(tag)) {
+    Watchdog wd;
+    do {
+      pl.issue(src);
+      wd.idle(where);
+    } while (!pl.ok(tag));
+  }
+  return pl.value();
+}
+
+constexpr int kRing = 4;  // phi-slice / edge-record ring of K2 (slices t .. t+3 live)
+
+template <typename T>
+__global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
+  __shared__ __align__(16) T s_ph[kRing][kTT];  // own-column phi of slice y in slot y % 4
+  __shared__ __align__(16) T s_rec[kRing][64];  // static edge record of step y (phiW/E/S/N)
+  __shared__ __align__(16) T s_R[2][kTT];       // R of steps t-1 / t
+  __shared__ __align__(16) T s_gh[2][kTT];      // ghost phi below / above each column
+  __shared__ double s_red[kTT / 32];
+  __shared__ int s_tile, s_last;
+  constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
-  const int warp = p >> 5, lane = p & 31;
-  int ti = 0, tj = 0;
-  if (warp < kComputeWarps) pos_to_tij(p, ti, tj);
+  const int lane = p & 31;
+  int ti, tj;
+  pos_to_tij(p, ti, tj);
   const int d = ti + tj;
-  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : 0;
-  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
-  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : 0;
-  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
-  unsigned* const prog = P.state + kProgOff;
-
-  if (p == 0) {
-    for (int b = 0; b < SF; ++b) mbar_init(&b_fw[b], 2);  // fetcher: phi slice (expect_tx) + record
-    for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
-    fence_mbar_init();
-  }
-  uint32_t sq = 0;  // CTA-uniform step sequence base (slot rings advance NS per tile)
-  uint32_t eq = 0;  // E ring base (advances NS + 1 per tile)
+  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : p;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
+  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : p;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
   const unsigned epoch = *P.epoch;  // stable for this launch (bumped by the finaliser)
+  (void)lane;
 
   for (;;) {
     __syncthreads();
-    if (p == 0) {
-      s_tile = atomicAdd(P.state, 1u);
-      s_linked = 0;
-    }
+    if (p == 0) s_tile = atomicAdd(P.state, 1u);
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -548,7 +581,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     const TileDesc td = P.tiles[tid];
     const BlockDesc bd = P.blocks[td.block];
     const int NS = td.ns, nz = td.nz;
-    double nrm = 0.0;
     if (P.trace && p == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -556,302 +588,172 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
       P.trace[4 * tid + 2] = smid;
       P.trace[4 * tid + 3] = blockIdx.x;
     }
-
-    if (warp == kPublisherWarp) {
-      // --------------------------------------------------------- publisher
-      // outgoing edge: lane c < 16 -> E column cell (TI-1, c), lane >= 16 -> N row cell (c, TJ-1)
-      // written as tagged words: the consumer validates each value by its tag,
-      // so no fence or progress counter is needed
-      const bool we = lane < 16;
-      const int c = lane & 15;
-      const bool outok = we ? (td.nE >= 0 && c < td.wJ) : (td.nN >= 0 && c < td.wI);
-      const int outoff = we ? (kTI - 1) + c : c + (kTJ - 1);
-      unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
-      const T* fw_pf = P.fw + td.slot * F_NA * kTT;
-      if (lane == 0)  // warm the first kPFL + 1 forward-pack slices (one bulk L2 prefetch each)
-        for (int xs = 0; xs <= kPFL && xs < NS; ++xs)
-          prefetch_l2(fw_pf + (long long)xs * F_NA * kTT, F_NA * kTT * sizeof(T));
-      // phi slices: step s's transaction (phi slice s+1, + slice 0 for s = 0)
-      // on b_fw[s % SF], armed once prep(s - SF) is done (phi slice s+1 reuses
-      // the slot of slice s+1-SP, SP = SF + 2)
-      const T* ph_src = P.phi + td.slot * kTT;
-      auto fw = [&](int s) {  // lane 0
-        const uint32_t q = sq + s;
-        uint64_t* bar = &b_fw[q % SF];
-        uint32_t tx = 64 * sizeof(T);  // static part of edge record s
-        if (s + 1 < NS) tx += slice_bytes<T>(s + 1, nz, 1);
-        if (s == 0) tx += slice_bytes<T>(0, nz, 1);
-        mbar_expect_tx(bar, tx);
-        bulk_g2s(s_edge + (q & (ER - 1)) * NE, P.rec_phi + (td.slot + s) * 64, 64 * sizeof(T), bar);
-        if (s + 1 < NS)
-          issue_slice<T>(s_ph + ((q + 1) % SP) * kTT, ph_src + (long long)(s + 1) * kTT, 1, s + 1,
-                         nz, bar, false, 0);
-        if (s == 0) issue_slice<T>(s_ph + (q % SP) * kTT, ph_src, 1, 0, nz, bar, false, 0);
-      };
-      int f = 0;  // next transaction to issue (lane 0)
-      if (lane == 0)
-        for (; f < NS && f < SF; ++f) fw(f);
-      int t = 0;
-      while (t < NS) {
-        {
-          const uint32_t q = eq + t + 1;  // E[t+1]: step t complete
-          mbar_wait(&b_step[q % EB], (q / EB) & 1, 43);
-        }
-        int t_end = t + 1;
-        while (t_end < NS) {
-          const uint32_t q = eq + t_end + 1;
-          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
-          ++t_end;
-        }
-        if (lane == 0)  // E[t_end] seen: prep(0 .. t_end) done
-          for (; f < NS && f < t_end + 1 + SF; ++f) fw(f);
-        const int t_pub = t;
-        (void)t_pub;
-        for (; t < t_end; ++t) {
-          const int k = t - outoff;
-          if (outok && k >= 0 && k < nz)
-            put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(t % OR) * 32 + lane],
-                       edge_tag(epoch, k));
-          // keep the forward pack warm in L2 kPFL steps ahead of the compute LDGs
-          const int xs = t + 1 + kPFL;
-          if (xs < NS && lane == 0) prefetch_l2(fw_pf + (long long)xs * F_NA * kTT, F_NA * kTT * sizeof(T));
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (kStepTrace && P.trace && tid == P.trace_tile)  // step-trace slot 2: tile A published steps < t
-            for (int u = t_pub; u < t; ++u) P.trace[8 * P.ntiles + 16 * u + 2] = gtime();
-          st_release_cta_s(&s_linked, t);
-        }
+    const bool col = ti < td.wI && tj < td.wJ;
+    const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
+    // residual operands outside the tile come from the static edge record
+    const int rW = tj, rE = 16 + tj, rS = 32 + ti, rN = 48 + ti;
+    // cross-tile R: poll the W / S neighbour's E column / N row, publish ours
+    const bool pollW = col && ti == 0 && td.nW >= 0, pollS = col && tj == 0 && td.nS >= 0;
+    const bool pubE = col && ti == kTI - 1 && td.nE >= 0, pubN = col && tj == kTJ - 1 && td.nN >= 0;
+    const unsigned long long* srcW = P.tagA + ((pollW ? P.tiles[td.nW].edge : 0) + tj) * TW;
+    const unsigned long long* srcS = P.tagB + ((pollS ? P.tiles[td.nS].edge : 0) + ti) * TW;
+    unsigned long long* dstE = P.tagA + (td.edge + tj) * TW;
+    unsigned long long* dstN = P.tagB + (td.edge + ti) * TW;
+    {
+      const int gi = td.i0 + ti, gj = td.j0 + tj;
+      T gb = T(0), gt = T(0);
+      if (col) {
+        gb = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
+        gt = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
       }
-    } else if (warp == kFetcherWarp) {
-      // ----------------------------------------------------------- fetcher
-      // lanes 0-15 poll R of the W neighbour's E column (index = tj), lanes
-      // 16-31 R of the S neighbour's N row (index = ti); the static phi part
-      // of each record comes with the step's bulk copy (k_edge_phi)
-      const bool we = lane < 16;
-      const int c = lane & 15;
-      const bool colok = we ? (c < td.wJ) : (c < td.wI);
-      const int nA = we ? td.nW : td.nS;  // upstream neighbour
-      const bool live = nA >= 0 && colok;  // lanes with a value to poll (others: R = 0)
-      const long long edgeA = nA >= 0 ? P.tiles[nA].edge : 0;
-      const unsigned long long* eA = (we ? P.tagA : P.tagB) + (edgeA + c) * kTagWords<T>;
-      // Step s's slot barrier b_fw[s % SF] completes when (1) phi slice s+1
-      // (+ slice 0 for s = 0) and the static part of record s have landed
-      // (armed and copied by the publisher) and (2) the R part of record s
-      // is announced here, which also waits for the publisher (compute step
-      // s writes out-record s % OR).  e: next record to fetch into deep-ring
-      // slot e % ER (reusable once prep(e - ER + 1) is done).
-      int e = 0, a = 0, freed = 0;
-      Watchdog wd;
-      constexpr int kB = 8;  // records polled per round trip
-      while (a < NS) {
-        while (freed < NS) {  // prep(freed) done? (compute cannot pass the records: bounded)
-          const uint32_t q = eq + freed;
-          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
-          ++freed;
-        }
-        {
-          const int a_end = __shfl_sync(0xffffffffu,
-                                        min(min(e, freed + SF), ld_relaxed_cta_s(&s_linked) + OR), 0);
-          if (a_end > a) {
-            fence_cta();  // acquire the publisher's progress / order the record stores
-            __syncwarp();
-            if (lane == 0)
-              for (int s2 = a; s2 < a_end; ++s2) {
-                if (kStepTrace && P.trace && tid == P.trace_tile + 1) P.trace[8 * P.ntiles + 16 * s2 + 4] = gtime();
-                mbar_arrive(&b_fw[(sq + s2) % SF]);
-              }
-            a = a_end;
-          }
-        }
-        const int m = min(NS - 1, freed + ER - 2);
-        if (e > m) {
-          wd.idle(45);
-          continue;
-        }
-        // issue the loads of up to kB records at once, then accept the valid prefix
-        T rA[kB];
-        bool ok[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const int s2 = e + j;
-          const int kA = s2 - c;  // W side cell (0, c) / S side cell (c, 0)
-          rA[j] = T(0);
-          ok[j] = true;
-          if (live && s2 <= m && kA >= 0 && kA < nz)
-            ok[j] = get_tagged(eA + (long long)kA * 16 * kTagWords<T>, edge_tag(epoch, kA), rA[j]);
-        }
-        int n = 0;
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          if (n == j && e + j <= m && __all_sync(0xffffffffu, ok[j])) {
-            s_edge[((sq + e + j) % ER) * NE + (we ? 64 : 80) + c] = rA[j];
-            n = j + 1;
-          }
-        }
-        if (n == 0) {
-          wd.idle(44);
-          continue;
-        }
-        wd.progress();
-        if (kStepTrace && P.trace && tid == P.trace_tile + 1 && lane == 0)  // slot 3: tile B fetched records
-          for (int u = e; u < e + n; ++u) P.trace[8 * P.ntiles + 16 * u + 3] = gtime();
-        e += n;
-      }
-    } else if (warp < kComputeWarps) {
-      // --------------------------------------------------------- compute warps
-      // Iteration t: the shared loads of critical(t) and of the residual of
-      // step t+1 are issued first (branch-free, always-valid addresses), then
-      // both FP chains, so the residual fills the latency of the recurrence;
-      // then one step-done arrival, one wait for the data of step t+2 and one
-      // named barrier.  All ring positions are 32-bit shared addresses.
-      constexpr uint32_t SZ = sizeof(T);
-      constexpr uint32_t SLICE = kTT * SZ;
-      const bool col = ti < td.wI && tj < td.wJ;
-      const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
-      const uint32_t aPh = saddr(smem);
-      const uint32_t aR = aPh + SP * SLICE;
-      const uint32_t aEdge = aR + 2 * SLICE;
-      const uint32_t aOut = aEdge + ER * NE * SZ;
-      const uint32_t aGh = aOut + OR * 32 * SZ;
-      const uint32_t aFw = saddr(b_fw), aStep = saddr(b_step);
-      const uint32_t oP = p * SZ;
-      {
-        const int gi = td.i0 + ti, gj = td.j0 + tj;
-        T gb = T(0), gt = T(0);
-        if (col) {
-          gb = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
-          gt = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
-        }
-        sts(aGh + oP, gb);  // own slots: read back by this thread only
-        sts(aGh + SLICE + oP, gt);
-      }
-      // neighbour operands: in-tile (offset into a phi slot / R buffer) or
-      // from the edge record (phiW, phiE, phiS, phiN, RW, RS; 16 each)
-      const uint32_t offW = (inW ? pW : tj) * SZ, offE = (inE ? pE : 16 + tj) * SZ;
-      const uint32_t offS = (inS ? pS : 32 + ti) * SZ, offN = (inN ? pN : 48 + ti) * SZ;
-      const uint32_t offRW = (inW ? pW : 64 + tj) * SZ, offRS = (inS ? pS : 80 + ti) * SZ;
-      const uint32_t oOutE = (ti == kTI - 1) ? tj * SZ : 0xFFFFFFFFu;
-      const uint32_t oOutN = (tj == kTJ - 1) ? (16 + ti) * SZ : 0xFFFFFFFFu;
-      uint32_t ph0 = aPh + (sq % SP) * SLICE;  // slot of phi slice x while preparing step x
-      uint32_t rec = aEdge + (sq & (ER - 1)) * NE * SZ;  // edge record of step x
-      uint32_t fwb = aFw + (sq % SF) * 8;
-      uint32_t fpar = (sq / SF) & 1;
-      uint32_t eb = aStep + (eq % EB) * 8;
-      uint32_t ob = aOut;  // out-record slot of step t (t % OR)
-      T RB = T(0);         // own R of the plane below (0 outside the block)
-      T r = T(0), lb = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
-      T nf[F_NA];  // forward-pack values of the next step to prepare (LDG one step ahead)
-#pragma unroll
-      for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = T(0);
-      const T* fw_cell = P.fw + td.slot * F_NA * kTT + p;
-      auto ldg_next = [&](int xs) {
-        const int k2 = xs - d;
-        if (xs < NS && col && k2 >= 0 && k2 < nz) {
-          const T* src = fw_cell + (long long)xs * F_NA * kTT;
+      s_gh[0][p] = gb;
+      s_gh[1][p] = gt;
+    }
+    const T* fw_cell = P.fw + td.slot * F_NA * kTT + p;
+    const T* ph_cell = P.phi + td.slot * kTT + p;
+    const T* rp_cell = P.rec_phi + td.slot * 64 + (p & 63);
+    T* gR = P.R + td.slot * kTT + p;
+    auto ldg_fw = [&](T* nf, int x) {
+      const int k = x - d;
+      if (x < NS && col && k >= 0 && k < nz) {
+        const T* src = fw_cell + (long long)x * F_NA * kTT;
 #ifdef SIPB_EXP_NOLDG
 #pragma unroll
-          for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = T(0.01) * T(a2 + 1) + T(xs) * T(1e-9);
-          (void)src;
+        for (int a = 0; a < F_NA; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
+        (void)src;
 #else
 #pragma unroll
-          for (int a2 = 0; a2 < F_NA; ++a2) nf[a2] = __ldg(src + a2 * kTT);
+        for (int a = 0; a < F_NA; ++a) nf[a] = __ldg(src + a * kTT);
 #endif
-        }
-      };
-      // residual of step x (Listing-1 term order, a_nb = -A_nb)
-      auto residual = [&](T fP, T fB, T fT, T fW, T fE, T fS, T fN) {
-        T rr = -(nf[F_AE] * fE);
-        rr -= nf[F_AW] * fW;
-        rr -= nf[F_AN] * fN;
-        rr -= nf[F_AS] * fS;
-        rr -= nf[F_AT] * fT;
-        rr -= nf[F_AB] * fB;
-        rr += nf[F_Q];
-        rr -= nf[F_AP] * fP;
-        return rr;
-      };
-      T* gR = P.R + td.slot * kTT + p;
-      // ---- step 0 preparation (only the (0,0) column is active at k = 0)
-      ldg_next(0);
-      mbar_wait_a(fwb, fpar, 21);
-      bool act = col && d == 0 && nz > 0;
-      {
-        const uint32_t php = ring_next(ph0, aPh, SLICE, SP * SLICE);
-        const T fP = lds<T>(ph0 + oP);
-        const T fB = lds<T>(aGh + oP);
-        const T fT = lds<T>((nz > 1 ? php : aGh + SLICE) + oP);
-        const T fW = lds<T>(rec + offW), fE = lds<T>((inE ? php : rec) + offE);
-        const T fS = lds<T>(rec + offS), fN = lds<T>((inN ? php : rec) + offN);
-        const T rr = residual(fP, fB, fT, fW, fE, fS, fN);
-        if (act) {
-          nrm += fabs(static_cast<double>(rr));
-          r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
-        }
       }
-      ldg_next(1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive_a(eb);
-      eb = ring_next(eb, aStep, 8, EB * 8);
-      fwb = ring_next(fwb, aFw, 8, SF * 8);
-      fpar ^= (fwb == aFw);
-      ph0 = ring_next(ph0, aPh, SLICE, SP * SLICE);
-      if (1 < NS) mbar_wait_a(fwb, fpar, 22);
-      for (int t = 0; t < NS; ++t) {
-        const int x = t + 1;
-        // ---- shared loads of critical(t)
-        const uint32_t sRm = aR + ((t - 1) & 1) * SLICE;
-        const T RW = lds<T>((inW ? sRm : rec) + offRW);
-        const T RS = lds<T>((inS ? sRm : rec) + offRS);
-        // ---- shared loads of the residual of step x: slices x-1, x, x+1, record x
-        const uint32_t recx = ring_next(rec, aEdge, NE * SZ, ER * NE * SZ);
-        const uint32_t php = ring_next(ph0, aPh, SLICE, SP * SLICE);
-        const uint32_t phm = ph0 == aPh ? ph0 + (SP - 1) * SLICE : ph0 - SLICE;
-        const int k1 = x - d;
-        const T fP = lds<T>(ph0 + oP);
-        const T fB = lds<T>((k1 > 0 ? phm : aGh) + oP);
-        const T fT = lds<T>((k1 + 1 < nz ? php : aGh + SLICE) + oP);
-        const T fW = lds<T>((inW ? phm : recx) + offW);
-        const T fE = lds<T>((inE ? php : recx) + offE);
-        const T fS = lds<T>((inS ? phm : recx) + offS);
-        const T fN = lds<T>((inN ? php : recx) + offN);
-        // ---- critical(t): R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP
-        const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
-        if (act) {
-          RB = Rv;
-          sts(aR + (t & 1) * SLICE + oP, Rv);
-          if (oOutE != 0xFFFFFFFFu) sts(ob + oOutE, Rv);
-          if (oOutN != 0xFFFFFFFFu) sts(ob + oOutN, Rv);
-#ifndef SIPB_EXP_NOSTG
-          gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
-#endif
-        }
-        // ---- residual of step x
-        const bool act1 = x < NS && col && k1 >= 0 && k1 < nz;
-        const T rr = residual(fP, fB, fT, fW, fE, fS, fN);
-        if (act1) {
-          nrm += fabs(static_cast<double>(rr));
-          r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
-        }
-        ldg_next(x + 1);  // nf consumed above
-        act = act1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive_a(eb);  // E[x]: step t done, step x prepared
-        eb = ring_next(eb, aStep, 8, EB * 8);
-        fwb = ring_next(fwb, aFw, 8, SF * 8);
-        fpar ^= (fwb == aFw);
-        ph0 = php;
-        rec = recx;
-        ob = ring_next(ob, aOut, 32 * SZ, OR * 32 * SZ);
-        if (x + 1 < NS) mbar_wait_a(fwb, fpar, 21);  // data of step x+1
-        if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
-          P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
-        bar_compute();
+    };
+    auto ldg_phi = [&](int y) -> T {
+      const int k = y - d;
+      return (y < NS && col && k >= 0 && k < nz) ? __ldg(ph_cell + (long long)y * kTT) : T(0);
+    };
+    auto ldg_rec = [&](int y) -> T { return (y < NS && p < 64) ? __ldg(rp_cell + (long long)y * 64) : T(0); };
+    auto poll_issue = [&](TagPoll<T>& pw, TagPoll<T>& ps, int s) {
+      const int k = s - d;
+      if (k >= 0 && k < nz && s < NS) {
+        if (pollW) pw.issue(srcW + (long long)k * 16 * TW);
+        if (pollS) ps.issue(srcS + (long long)k * 16 * TW);
+      }
+    };
+    // residual of step x (Listing-1 term order, a_nb = -A_nb)
+    auto residual = [&](const T* nf, T fP, T fB, T fT, T fW, T fE, T fS, T fN) {
+      T rr = -(nf[F_AE] * fE);
+      rr -= nf[F_AW] * fW;
+      rr -= nf[F_AN] * fN;
+      rr -= nf[F_AS] * fS;
+      rr -= nf[F_AT] * fT;
+      rr -= nf[F_AB] * fB;
+      rr += nf[F_Q];
+      rr -= nf[F_AP] * fP;
+      return rr;
+    };
+    // ---- prologue: slices / records 0..2 into the rings, 3 and 4 in flight
+    for (int y = 0; y < 3; ++y) {
+      s_ph[y][p] = ldg_phi(y);
+      if (p < 64) s_rec[y][p] = ldg_rec(y);
+    }
+    T phB[2], rcB[2];  // in-flight own phi / record value of slices of parity 0 / 1
+    phB[1] = ldg_phi(3); rcB[1] = ldg_rec(3);
+    phB[0] = ldg_phi(4); rcB[0] = ldg_rec(4);
+    T nf0[F_NA], nf1[F_NA];  // forward pack of even / odd steps
+#pragma unroll
+    for (int a = 0; a < F_NA; ++a) nf0[a] = nf1[a] = T(0);
+    ldg_fw(nf0, 0);
+    ldg_fw(nf1, 1);
+    TagPoll<T> pw0, ps0, pw1, ps1;  // R polls of even / odd steps
+    poll_issue(pw0, ps0, 0);
+    poll_issue(pw1, ps1, 1);
+    // L2 prefetch front: the forward pack and phi slice of step x, one
+    // 128-byte line per thread (LSU path; lines spread over the 8 warps)
+    constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
+    auto pf_step = [&](int x) {
+      if (x >= NS) return;
+      if (p < kFwLines)
+        prefetch_line_l2(reinterpret_cast<const char*>(P.fw + (td.slot + x) * F_NA * kTT) + 128 * p);
+      else if (p < kFwLines + kPhLines)
+        prefetch_line_l2(reinterpret_cast<const char*>(P.phi + (td.slot + x) * kTT) + 128 * (p - kFwLines));
+    };
+    for (int x = 0; x <= kPFL; ++x) pf_step(x + 5);
+    __syncthreads();
+    double nrm = 0.0;
+    T RB = T(0);  // own R of the plane below (0 outside the block)
+    T r = T(0), lb = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
+    bool act = col && d == 0 && nz > 0;  // step 0: only the (0,0) column, k = 0
+    {
+      const T fP = s_ph[0][p], fB = s_gh[0][p];
+      const T fT = nz > 1 ? s_ph[1][p] : s_gh[1][p];
+      const T fW = s_rec[0][rW], fS = s_rec[0][rS];
+      const T fE = inE ? s_ph[1][pE] : s_rec[0][rE];
+      const T fN = inN ? s_ph[1][pN] : s_rec[0][rN];
+      const T rr = residual(nf0, fP, fB, fT, fW, fE, fS, fN);
+      if (act) {
+        nrm += fabs(static_cast<double>(rr));
+        r = rr; lb = nf0[F_LB]; lw = nf0[F_LW]; ls = nf0[F_LS]; lp = nf0[F_LP];
       }
     }
-    sq += NS;
-    eq += NS + 1;
-    __syncthreads();  // publisher has published NS (all steps retired)
+    ldg_fw(nf0, 2);
+    __syncthreads();
+    // iteration t: critical(t) and the residual of step t+1
+    auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* nf, T& phb, T& rcb) {
+      const int x = t + 1;
+      const int k = t - d;
+      // ---- shared loads of critical(t)
+      const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
+      // ---- shared loads of the residual of step x: slices x-1, x, x+1, record x
+      const int k1 = x - d;
+      const int sm = t & 3, s0 = x & 3, sp = (x + 1) & 3;
+      const T fP = s_ph[s0][p];
+      const T fB = k1 > 0 ? s_ph[sm][p] : s_gh[0][p];
+      const T fT = k1 + 1 < nz ? s_ph[sp][p] : s_gh[1][p];
+      const T fW = inW ? s_ph[sm][pW] : s_rec[s0][rW];
+      const T fE = inE ? s_ph[sp][pE] : s_rec[s0][rE];
+      const T fS = inS ? s_ph[sm][pS] : s_rec[s0][rS];
+      const T fN = inN ? s_ph[sp][pN] : s_rec[s0][rN];
+      // ---- critical(t): R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP
+      if (act) {
+        const uint32_t tag = edge_tag(epoch, k);
+        const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61) : T(0));
+        const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62) : T(0));
+        const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
+        RB = Rv;
+        s_R[t & 1][p] = Rv;
+        if (pubE) put_tagged(dstE + (long long)k * 16 * TW, Rv, tag);
+        if (pubN) put_tagged(dstN + (long long)k * 16 * TW, Rv, tag);
+#ifndef SIPB_EXP_NOSTG
+        gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
+#endif
+      }
+      poll_issue(pw, ps, t + 2);
+      // ---- residual of step x
+      const bool act1 = x < NS && col && k1 >= 0 && k1 < nz;
+      const T rr = residual(nf, fP, fB, fT, fW, fE, fS, fN);
+      if (act1) {
+        nrm += fabs(static_cast<double>(rr));
+        r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
+      }
+      ldg_fw(nf, x + 2);  // nf consumed above
+      act = act1;
+      // ---- refill the rings: slice / record t+3 (slot of slice t-1, last read in iteration t-1)
+      s_ph[(t + 3) & 3][p] = phb;
+      if (p < 64) s_rec[(t + 3) & 3][p] = rcb;
+      phb = ldg_phi(t + 5);
+      rcb = ldg_rec(t + 5);
+      pf_step(t + 6 + kPFL);  // keep forward pack and phi warm in L2 ahead of the LDGs
+      if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
+        P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
+      __syncthreads();
+    };
+    int t = 0;
+    for (; t + 1 < NS; t += 2) {
+      iter(t, pw0, ps0, nf1, phB[1], rcB[1]);
+      iter(t + 1, pw1, ps1, nf0, phB[0], rcB[0]);
+    }
+    if (t < NS) iter(t, pw0, ps0, nf1, phB[1], rcB[1]);
+
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
@@ -863,14 +765,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
     if (s_last) {
       // finaliser: deterministic per-block norms, then reset the backward state
       __threadfence();
-      const int nw = blockDim.x >> 5;
+      const int warp = p >> 5, nw = blockDim.x >> 5;
       for (int b = warp; b < P.nblocks; b += nw) {
         const BlockDesc bb = P.blocks[b];
         double v = 0.0;
-        for (int x = lane; x < bb.ntiles; x += 32) v += __ldcg(P.partial + bb.tile0 + x);
+        for (int x2 = (p & 31); x2 < bb.ntiles; x2 += 32) v += __ldcg(P.partial + bb.tile0 + x2);
 #pragma unroll
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) P.block_norms[b] = v;
+        if ((p & 31) == 0) P.block_norms[b] = v;
       }
       __syncthreads();
       if (p == 0) {
@@ -878,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
         for (int b = 0; b < P.nblocks; ++b) v += P.block_norms[b];
         *P.norm = v;
       }
-      for (int x = p; x < kProgOff + P.ntiles; x += blockDim.x) P.state_other[x] = 0u;
+      for (int x2 = p; x2 < kProgOff + P.ntiles; x2 += blockDim.x) P.state_other[x2] = 0u;
       if (p == 0) *P.epoch = epoch + 1;
     }
   }
@@ -886,58 +788,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const SweepParams<T> P)
 
 // =============================================================================
 // K3: backward substitution + phi update (backward3d); slices in reverse.
-// Ring slot = {R, phi, UN, UE, UT} of one slice; edge record = delta of the
-// E and N neighbour tiles (16 each).  Same warp roles and step pipeline as K2:
-// prep(x) loads the slot into registers and forms UT*dT; the critical step is
-// ((R - UN*dN) - UE*dE) - UT*dT after the barrier.
+// delta = ((R - UN*dN) - UE*dE) - UT*dT with R, phi, UN, UE, UT LDG'd two
+// steps ahead, dN / dE from the previous step's shared delta or polled from
+// the E / N neighbour tiles (their W column / S row, tagged).
 // =============================================================================
-template <typename T, int SB>
-struct BwdCfg {
-  static constexpr int ER = 16, NE = 32, OR = 8, EB = 32;
-  // R, phi, UN, UE, UT are own-cell data: LDG'd by each compute thread one
-  // step ahead; shared memory holds only the delta exchange and edge records
-  static constexpr size_t bytes = (size_t)2 * kTT * sizeof(T) +
-                                  (size_t)(ER * NE + OR * 32) * sizeof(T) +
-                                  (SB + EB) * sizeof(uint64_t);
-};
-
-template <typename T, int SB>
-__global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P) {
-  using C = BwdCfg<T, SB>;
-  constexpr int ER = C::ER, EB = C::EB, NE = C::NE, OR = C::OR;
-  static_assert(EB > ER + SB && EB > OR + SB + 1, "barrier rings must cover the run-ahead");
-  extern __shared__ __align__(128) unsigned char smem[];
-  T* s_D = reinterpret_cast<T*>(smem);
-  T* s_edge = s_D + 2 * kTT;
-  T* s_out = s_edge + ER * NE;  // [OR][32]: delta of the W column (tj) and S row (16 + ti)
-  // b_rg[u % SB] completes when slot u has landed AND edge record u is written
-  uint64_t* b_rg = reinterpret_cast<uint64_t*>(s_out + OR * 32);
-  uint64_t* b_step = b_rg + SB;  // E[x] as in K2
-  __shared__ int s_tile, s_last, s_linked;
+template <typename T>
+__global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
+  __shared__ __align__(16) T s_D[2][kTT];
+  __shared__ int s_tile, s_last;
+  constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
-  const int warp = p >> 5, lane = p & 31;
-  int ti = 0, tj = 0;
-  if (warp < kComputeWarps) pos_to_tij(p, ti, tj);
+  int ti, tj;
+  pos_to_tij(p, ti, tj);
   const int d = ti + tj;
-  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : 0;
-  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : 0;
-  unsigned* const prog = P.state + kProgOff;
-
-  if (p == 0) {
-    for (int b = 0; b < SB; ++b) mbar_init(&b_rg[b], 1);  // loader: edge record announced
-    for (int b = 0; b < EB; ++b) mbar_init(&b_step[b], kCompute / 32);
-    fence_mbar_init();
-  }
-  uint32_t sq = 0, eq = 0;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
   const unsigned epoch = *P.epoch;
 
   for (;;) {
     __syncthreads();
-    if (p == 0) {
-      s_tile = atomicAdd(P.state, 1u);
-      s_linked = 0;
-    }
+    if (p == 0) s_tile = atomicAdd(P.state, 1u);
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -951,193 +822,86 @@ __global__ void __launch_bounds__(kThreads, 2) k_backward(const SweepParams<T> P
       P.trace[4 * tid + 2] = smid;
       P.trace[4 * tid + 3] = blockIdx.x;
     }
-
-    // no loader: compute threads LDG their own cells, the fetcher announces
-    // edge records, the publisher keeps the slices warm in L2
-    if (warp == kPublisherWarp) {
-      // outgoing edge: lane c < 16 -> W column cell (0, c), lane >= 16 -> S row cell (c, 0)
-      const bool we = lane < 16;
-      const int c = lane & 15;
-      const bool outok = we ? (td.nW >= 0 && c < td.wJ) : (td.nS >= 0 && c < td.wI);
-      unsigned long long* outdst = (we ? P.tagA : P.tagB) + (td.edge + c) * kTagWords<T>;
-      // keeps the slices kPFL steps ahead of the compute LDGs warm in L2 (the
-      // publisher gates the compute warps through s_linked, so it cannot fall
-      // a full E ring behind)
-      constexpr int kL1 = kTT * (int)sizeof(T) / 128;  // lines per array slice
-      const char* rb = reinterpret_cast<const char*>(P.R + td.slot * kTT);
-      const char* pb = reinterpret_cast<const char*>(P.phi + td.slot * kTT);
-      const char* ub = reinterpret_cast<const char*>(P.bw + td.slot * B_NA * kTT);
-      auto pf = [&](int xs) {
-        if (xs >= NS) return;
-        const int ts = NS - 1 - xs;
-        for (int l = lane; l < 5 * kL1; l += 32) {
-          const char* a = l < kL1       ? rb + (long long)ts * kTT * sizeof(T) + 128 * l
-                          : l < 2 * kL1 ? pb + (long long)ts * kTT * sizeof(T) + 128 * (l - kL1)
-                                        : ub + (long long)ts * B_NA * kTT * sizeof(T) + 128 * (l - 2 * kL1);
-          prefetch_line_l2(a);
-        }
-      };
-      for (int xs = 0; xs <= kPFL; ++xs) pf(xs);
-      int u = 0;
-      while (u < NS) {
-        {
-          const uint32_t q = eq + u + 1;
-          mbar_wait(&b_step[q % EB], (q / EB) & 1, 53);
-        }
-        int u_end = u + 1;
-        while (u_end < NS) {
-          const uint32_t q = eq + u_end + 1;
-          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
-          ++u_end;
-        }
-        for (; u < u_end; ++u) {
-          const int k = (NS - 1 - u) - c;
-          if (outok && k >= 0 && k < nz)
-            put_tagged(outdst + (long long)k * 16 * kTagWords<T>, s_out[(u % OR) * 32 + lane],
-                       edge_tag(epoch, k));
-          pf(u + 1 + kPFL);
-        }
-        __syncwarp();
-        if (lane == 0) st_release_cta_s(&s_linked, u);
-      }
-    } else if (warp == kFetcherWarp) {
-      const bool we = lane < 16;
-      const int c = lane & 15;
-      const bool colok = we ? (c < td.wJ) : (c < td.wI);
-      const int nB = we ? td.nE : td.nN;
-      const long long edgeB = nB >= 0 ? P.tiles[nB].edge : 0;
-      const unsigned long long* srcB = (we ? P.tagA : P.tagB) + (edgeB + c) * kTagWords<T>;
-      const int offB = we ? (kTI - 1) + c : c + (kTJ - 1);  // edge cell (TI-1, c) / (c, TJ-1)
-      // Poll tagged deltas into the deep ring (record s -> slot s % ER, reusable
-      // once prep(s - ER + 1) is done) and announce record s on b_rg[s % SB]
-      // once its previous phase is over (prep(s - SB) done).
-      int e = 0, a = 0, freed = 0;
-      Watchdog wd;
-      constexpr int kB = 4;
-      while (a < NS) {
-        while (freed < NS) {
-          const uint32_t q = eq + freed;
-          if (!warp_test(&b_step[q % EB], (q / EB) & 1)) break;
-          ++freed;
-        }
-        // compute step s writes out-record slot s % OR: the publisher must be past s - OR
-        const int a_end = min(min(e, freed + SB), ld_relaxed_cta_s(&s_linked) + OR);
-        if (a_end > a) {
-          fence_cta();  // acquire the publisher's progress / order the record stores
-          __syncwarp();
-          if (lane == 0)
-            for (int s2 = a; s2 < a_end; ++s2) mbar_arrive(&b_rg[(sq + s2) % SB]);
-          a = a_end;
-        }
-        const int m = min(NS - 1, freed + ER - 2);
-        if (e > m) {
-          wd.idle(55);
-          continue;
-        }
-        T v[kB];
-        bool ok[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const int s2 = e + j;
-          v[j] = T(0);
-          ok[j] = true;
-          if (s2 > m) continue;
-          const int k = (NS - 1 - s2) - offB;
-          if (nB >= 0 && colok && k >= 0 && k < nz)
-            ok[j] = get_tagged(srcB + (long long)k * 16 * kTagWords<T>, edge_tag(epoch, k), v[j]);
-        }
-        int n = 0;
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          if (n == j && e + j <= m && __all_sync(0xffffffffu, ok[j])) {
-            s_edge[((sq + e + j) % ER) * NE + (we ? 0 : 16) + c] = v[j];
-            n = j + 1;
-          }
-        }
-        if (n == 0) {
-          wd.idle(54);
-          continue;
-        }
-        wd.progress();
-        e += n;
-      }
-    } else if (warp < kComputeWarps) {
-      const bool col = ti < td.wI && tj < td.wJ;
-      const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
-      T dT = T(0);
-      T rr = T(0), ph = T(0), un = T(0), ue = T(0), utdt = T(0), dnx = T(0), dex = T(0);
-      bool act = false;
-      int kk = 0;
-      const T* r_cell = P.R + td.slot * kTT + p;
-      const T* ph_cell = P.phi + td.slot * kTT + p;
-      const T* bw_cell = P.bw + td.slot * B_NA * kTT + p;
-      T nb[5] = {T(0), T(0), T(0), T(0), T(0)};  // R, phi, UN, UE, UT of the next step
-      auto ldg_next = [&](int xs) {
-        const int ts = NS - 1 - xs, k2 = ts - d;
-        if (xs < NS && col && k2 >= 0 && k2 < nz) {
+    const bool col = ti < td.wI && tj < td.wJ;
+    const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
+    // cross-tile delta: poll the E / N neighbour's W column / S row, publish ours
+    const bool pollE = col && ti == kTI - 1 && td.nE >= 0, pollN = col && tj == kTJ - 1 && td.nN >= 0;
+    const bool pubW = col && ti == 0 && td.nW >= 0, pubS = col && tj == 0 && td.nS >= 0;
+    const unsigned long long* srcE = P.tagA + ((pollE ? P.tiles[td.nE].edge : 0) + tj) * TW;
+    const unsigned long long* srcN = P.tagB + ((pollN ? P.tiles[td.nN].edge : 0) + ti) * TW;
+    unsigned long long* dstW = P.tagA + (td.edge + tj) * TW;
+    unsigned long long* dstS = P.tagB + (td.edge + ti) * TW;
+    const T* r_cell = P.R + td.slot * kTT + p;
+    T* ph_cell = P.phi + td.slot * kTT + p;
+    const T* bw_cell = P.bw + td.slot * B_NA * kTT + p;
+    auto ldg_into = [&](T* nb, int u) {
+      const int t = NS - 1 - u, k = t - d;
+      if (u < NS && col && k >= 0 && k < nz) {
 #ifdef SIPB_EXP_NOLDG
-          nb[0] = T(ts) * T(1e-9); nb[1] = T(0.5); nb[2] = T(0.1); nb[3] = T(0.2); nb[4] = T(0.3);
+        nb[0] = T(t) * T(1e-9); nb[1] = T(0.5); nb[2] = T(0.1); nb[3] = T(0.2); nb[4] = T(0.3);
 #else
-          nb[0] = __ldg(r_cell + (long long)ts * kTT);
-          nb[1] = __ldg(ph_cell + (long long)ts * kTT);
-          const T* u = bw_cell + (long long)ts * B_NA * kTT;
-          nb[2] = __ldg(u);
-          nb[3] = __ldg(u + kTT);
-          nb[4] = __ldg(u + 2 * kTT);
+        nb[0] = __ldg(r_cell + (long long)t * kTT);
+        nb[1] = __ldg(ph_cell + (long long)t * kTT);
+        const T* u3 = bw_cell + (long long)t * B_NA * kTT;
+        nb[2] = __ldg(u3);
+        nb[3] = __ldg(u3 + kTT);
+        nb[4] = __ldg(u3 + 2 * kTT);
 #endif
-        }
-      };
-      auto prep = [&](int x) {
-        const uint32_t q = sq + x;
-        mbar_wait(&b_rg[q % SB], (q / SB) & 1, 31);  // edge record x announced
-        const int t = NS - 1 - x;
-        kk = t - d;
-        act = col && kk >= 0 && kk < nz;
-        if (act) {
-          const T* rec = s_edge + (q % ER) * NE;
-          rr = nb[0];
-          ph = nb[1];
-          un = nb[2];
-          ue = nb[3];
-          utdt = nb[4] * dT;
-          dnx = rec[16 + ti];
-          dex = rec[tj];
-        }
-        ldg_next(x + 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&b_step[(eq + x) % EB]);
-      };
-      ldg_next(0);
-      prep(0);
-      for (int u = 0; u < NS; ++u) {
-        const int t = NS - 1 - u;
-        const bool was = act;
-        T phn = T(0);
-        if (act) {
-          const T dN = inN ? s_D[((u - 1) & 1) * kTT + pN] : dnx;
-          const T dE = inE ? s_D[((u - 1) & 1) * kTT + pE] : dex;
-          const T dl = ((rr - un * dN) - ue * dE) - utdt;
-          dT = dl;
-          phn = ph + dl;
-          s_D[(u & 1) * kTT + p] = dl;
-          if (ti == 0) s_out[(u % OR) * 32 + tj] = dl;
-          if (tj == 0) s_out[(u % OR) * 32 + 16 + ti] = dl;
-        }
-        if (u + 1 < NS) {
-          prep(u + 1);  // arrives E[u+1]
-        } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&b_step[(eq + NS) % EB]);
-        }
-#ifndef SIPB_EXP_NOSTG
-        if (was) P.phi[(td.slot + t) * kTT + p] = phn;
-#endif
-        bar_compute();
       }
+    };
+    auto poll_issue = [&](TagPoll<T>& pe, TagPoll<T>& pn, int u) {
+      const int k = (NS - 1 - u) - d;
+      if (u < NS && k >= 0 && k < nz) {
+        if (pollE) pe.issue(srcE + (long long)k * 16 * TW);
+        if (pollN) pn.issue(srcN + (long long)k * 16 * TW);
+      }
+    };
+    auto pf = [&](int u) {  // three bulk L2 prefetches (R, phi, U slices of step u), thread 0
+      if (u >= NS || p != 0) return;
+      const long long ts = td.slot + NS - 1 - u;
+      prefetch_l2(P.R + ts * kTT, kTT * sizeof(T));
+      prefetch_l2(P.phi + ts * kTT, kTT * sizeof(T));
+      prefetch_l2(P.bw + ts * B_NA * kTT, B_NA * kTT * sizeof(T));
+    };
+    T nb0[5], nb1[5];  // R, phi, UN, UE, UT of even / odd steps
+#pragma unroll
+    for (int a = 0; a < 5; ++a) nb0[a] = nb1[a] = T(0);
+    ldg_into(nb0, 0);
+    ldg_into(nb1, 1);
+    TagPoll<T> pe0, pn0, pe1, pn1;
+    poll_issue(pe0, pn0, 0);
+    poll_issue(pe1, pn1, 1);
+    for (int u = 0; u <= kPFL; ++u) pf(u);
+    T dT = T(0);  // own delta of the plane above (0 outside the block)
+    auto iter = [&](const int u, TagPoll<T>& pe, TagPoll<T>& pn, T* nb) {
+      const int t = NS - 1 - u, k = t - d;
+      const T dNi = s_D[(u - 1) & 1][pN], dEi = s_D[(u - 1) & 1][pE];
+      if (col && k >= 0 && k < nz) {
+        const uint32_t tag = edge_tag(epoch, k);
+        const T dN = inN ? dNi : (pollN ? poll_take(pn, srcN + (long long)k * 16 * TW, tag, 63) : T(0));
+        const T dE = inE ? dEi : (pollE ? poll_take(pe, srcE + (long long)k * 16 * TW, tag, 64) : T(0));
+        const T utdt = nb[4] * dT;
+        const T dl = ((nb[0] - nb[2] * dN) - nb[3] * dE) - utdt;
+        dT = dl;
+        s_D[u & 1][p] = dl;
+        if (pubW) put_tagged(dstW + (long long)k * 16 * TW, dl, tag);
+        if (pubS) put_tagged(dstS + (long long)k * 16 * TW, dl, tag);
+#ifndef SIPB_EXP_NOSTG
+        ph_cell[(long long)t * kTT] = nb[1] + dl;
+#endif
+      }
+      poll_issue(pe, pn, u + 2);
+      ldg_into(nb, u + 2);  // nb consumed above
+      pf(u + 1 + kPFL);
+      __syncthreads();
+    };
+    int u = 0;
+    for (; u + 1 < NS; u += 2) {
+      iter(u, pe0, pn0, nb0);
+      iter(u + 1, pe1, pn1, nb1);
     }
-    sq += NS;
-    eq += NS + 1;
-    __syncthreads();
+    if (u < NS) iter(u, pe0, pn0, nb0);
+
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     if (p == 0) {
       __threadfence();
@@ -1420,13 +1184,6 @@ static int grid_for(long long n, int threads = 256) {
 }
 static inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? SIP_OK : SIP_ERR_CUDA; }
 
-constexpr int kSF64 = 6, kSF32 = 6;  // forward slot ring depth (phi slices + edge records)
-constexpr int kSB64 = 8, kSB32 = 8;  // backward record-announce ring depth
-
-template <typename T> struct Rings;
-template <> struct Rings<double> { static constexpr int SF = kSF64, SB = kSB64; };
-template <> struct Rings<float> { static constexpr int SF = kSF32, SB = kSB32; };
-
 int launch_factor(const FactorParams& p, int grid, void* stream) {
   k_factor<<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
@@ -1434,27 +1191,13 @@ int launch_factor(const FactorParams& p, int grid, void* stream) {
 
 template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
-  constexpr int SF = Rings<T>::SF;
-  const size_t smem = FwdCfg<T, SF>::bytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_forward<T, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_forward<T, SF><<<grid, kThreads, smem, (cudaStream_t)stream>>>(p);
+  k_forward<T><<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
 template <typename T>
 int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
-  constexpr int SB = Rings<T>::SB;
-  const size_t smem = BwdCfg<T, SB>::bytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_backward<T, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_backward<T, SB><<<grid, kThreads, smem, (cudaStream_t)stream>>>(p);
+  k_backward<T><<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1475,33 +1218,13 @@ int max_resident_ctas(int kind, int precision, int* grid) {
   if (kind == 0) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_factor, kTT, 0);
   } else if (kind == 1) {
-    if (precision == SIP_PREC_DOUBLE) {
-      constexpr int SF = Rings<double>::SF;
-      cudaFuncSetAttribute(k_forward<double, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)FwdCfg<double, SF>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, SF>, kThreads,
-                                                        FwdCfg<double, SF>::bytes);
-    } else {
-      constexpr int SF = Rings<float>::SF;
-      cudaFuncSetAttribute(k_forward<float, SF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)FwdCfg<float, SF>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, SF>, kThreads,
-                                                        FwdCfg<float, SF>::bytes);
-    }
+    e = precision == SIP_PREC_DOUBLE
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double>, kTT, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float>, kTT, 0);
   } else {
-    if (precision == SIP_PREC_DOUBLE) {
-      constexpr int SB = Rings<double>::SB;
-      cudaFuncSetAttribute(k_backward<double, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)BwdCfg<double, SB>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double, SB>, kThreads,
-                                                        BwdCfg<double, SB>::bytes);
-    } else {
-      constexpr int SB = Rings<float>::SB;
-      cudaFuncSetAttribute(k_backward<float, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)BwdCfg<float, SB>::bytes);
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float, SB>, kThreads,
-                                                        BwdCfg<float, SB>::bytes);
-    }
+    e = precision == SIP_PREC_DOUBLE
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float>, kTT, 0);
   }
   if (e != cudaSuccess || per < 1) return SIP_ERR_CUDA;
   *grid = per * sms;

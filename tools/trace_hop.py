@@ -31,3 +31,9 @@ print("  A published      -> B fetched rec s", med(fet[x] - pub[a]))
 print("  B fetched        -> B announced    ", med(ann[x] - fet[x]))
 print("  B announced      -> B step s done  ", med(B[x] - ann[x]))
 print("  total A step s+15 -> B step s      ", med(B[x] - A[a]))
+print("startup (us): A step 0/15/16:", f"{A[0]:.2f} {A[15]:.2f} {A[16]:.2f}",
+      "| A published 15/16:", f"{pub[15]:.2f} {pub[16]:.2f}",
+      "| B fetched rec 0/1:", f"{fet[0]:.2f} {fet[1]:.2f}", "| B announced 0/1:", f"{ann[0]:.2f} {ann[1]:.2f}",
+      "| B step 0/1/2:", f"{B[0]:.2f} {B[1]:.2f} {B[2]:.2f}")
+for x in (20, 60, 120):
+    print(f"  s={x}: A step s+15 {A[x+15]:.2f} pub {pub[x+15]:.2f} | B fetched {fet[x]:.2f} ann {ann[x]:.2f} step {B[x]:.2f}")
