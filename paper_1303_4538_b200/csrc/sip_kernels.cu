@@ -548,9 +548,24 @@ __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long*
 }
 
 constexpr int kRing = 4;  // phi-slice / edge-record ring of K2 (slices t .. t+3 live)
+// forward-pack LDG distance of K2 (iterations between load and use): 2 needs
+// two register buffers (fp64: 48 registers) and one CTA per SM
+#ifdef SIPB_FW_D1
+constexpr int kFwdMinBlocks = 2;
+#else
+constexpr int kFwdMinBlocks = 1;
+#endif
+template <typename T>
+struct FwDist {
+#ifdef SIPB_FW_D1
+  static constexpr int value = 1;
+#else
+  static constexpr int value = 2;
+#endif
+};
 
 template <typename T>
-__global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(kTT, kFwdMinBlocks) k_forward(const SweepParams<T> P) {
   __shared__ __align__(16) T s_ph[kRing][kTT];  // own-column phi of slice y in slot y % 4
   __shared__ __align__(16) T s_rec[kRing][64];  // static edge record of step y (phiW/E/S/N)
   __shared__ __align__(16) T s_R[2][kTT];       // R of steps t-1 / t
@@ -662,8 +677,10 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
     T nf0[F_NA], nf1[F_NA];  // forward pack of even / odd steps
 #pragma unroll
     for (int a = 0; a < F_NA; ++a) nf0[a] = nf1[a] = T(0);
+    constexpr int FD = FwDist<T>::value;
+    T* const nfOdd = FD == 2 ? nf1 : nf0;  // buffer of odd steps
     ldg_fw(nf0, 0);
-    ldg_fw(nf1, 1);
+    if (FD == 2) ldg_fw(nf1, 1);
     TagPoll<T> pw0, ps0, pw1, ps1;  // R polls of even / odd steps
     poll_issue(pw0, ps0, 0);
     poll_issue(pw1, ps1, 1);
@@ -695,7 +712,7 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
         r = rr; lb = nf0[F_LB]; lw = nf0[F_LW]; ls = nf0[F_LS]; lp = nf0[F_LP];
       }
     }
-    ldg_fw(nf0, 2);
+    ldg_fw(nf0, FD == 2 ? 2 : 1);
     __syncthreads();
     // iteration t: critical(t) and the residual of step t+1
     auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* nf, T& phb, T& rcb) {
@@ -735,7 +752,7 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
         nrm += fabs(static_cast<double>(rr));
         r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
       }
-      ldg_fw(nf, x + 2);  // nf consumed above
+      ldg_fw(nf, x + FD);  // nf consumed above
       act = act1;
       // ---- refill the rings: slice / record t+3 (slot of slice t-1, last read in iteration t-1)
       s_ph[(t + 3) & 3][p] = phb;
@@ -749,10 +766,10 @@ __global__ void __launch_bounds__(kTT, 1) k_forward(const SweepParams<T> P) {
     };
     int t = 0;
     for (; t + 1 < NS; t += 2) {
-      iter(t, pw0, ps0, nf1, phB[1], rcB[1]);
+      iter(t, pw0, ps0, nfOdd, phB[1], rcB[1]);
       iter(t + 1, pw1, ps1, nf0, phB[0], rcB[0]);
     }
-    if (t < NS) iter(t, pw0, ps0, nf1, phB[1], rcB[1]);
+    if (t < NS) iter(t, pw0, ps0, nfOdd, phB[1], rcB[1]);
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
