@@ -565,26 +565,33 @@ struct FwDist {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kTT, kFwdMinBlocks) k_forward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) {
+  // Two threads per column.  Threads 0..255 ("critical"): the recurrence
+  // R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP of step t, cross-tile R
+  // stores / polls.  Threads 256..511 ("residual"): everything that does
+  // not depend on R -- the residual r of step t+1 and its factors (handed
+  // over through s_prep), the phi / edge-record rings, the forward-pack
+  // LDGs and the L2 prefetch front.  One barrier per step.
   __shared__ __align__(16) T s_ph[kRing][kTT];  // own-column phi of slice y in slot y % 4
   __shared__ __align__(16) T s_rec[kRing][64];  // static edge record of step y (phiW/E/S/N)
   __shared__ __align__(16) T s_R[2][kTT];       // R of steps t-1 / t
   __shared__ __align__(16) T s_gh[2][kTT];      // ghost phi below / above each column
-  __shared__ double s_red[kTT / 32];
+  __shared__ __align__(16) T s_prep[2][5][kTT]; // r, LB, LW, LS, LP of the prepared step
+  __shared__ double s_red[2 * kTT / 32];
   __shared__ int s_tile, s_last;
   constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
-  const int lane = p & 31;
+  const bool crit = p < kTT;
+  const int q = p & (kTT - 1);  // column position
   int ti, tj;
-  pos_to_tij(p, ti, tj);
+  pos_to_tij(q, ti, tj);
   const int d = ti + tj;
-  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : p;
-  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
-  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : p;
-  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
+  const int pW = ti > 0 ? tile_pos(ti - 1, tj) : q;
+  const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : q;
+  const int pS = tj > 0 ? tile_pos(ti, tj - 1) : q;
+  const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : q;
   const unsigned epoch = *P.epoch;  // stable for this launch (bumped by the finaliser)
-  (void)lane;
 
   for (;;) {
     __syncthreads();
@@ -605,171 +612,177 @@ __global__ void __launch_bounds__(kTT, kFwdMinBlocks) k_forward(const SweepParam
     }
     const bool col = ti < td.wI && tj < td.wJ;
     const bool inW = ti > 0, inE = ti + 1 < td.wI, inS = tj > 0, inN = tj + 1 < td.wJ;
-    // residual operands outside the tile come from the static edge record
-    const int rW = tj, rE = 16 + tj, rS = 32 + ti, rN = 48 + ti;
-    // cross-tile R: poll the W / S neighbour's E column / N row, publish ours
-    const bool pollW = col && ti == 0 && td.nW >= 0, pollS = col && tj == 0 && td.nS >= 0;
-    const bool pubE = col && ti == kTI - 1 && td.nE >= 0, pubN = col && tj == kTJ - 1 && td.nN >= 0;
-    const unsigned long long* srcW = P.tagA + ((pollW ? P.tiles[td.nW].edge : 0) + tj) * TW;
-    const unsigned long long* srcS = P.tagB + ((pollS ? P.tiles[td.nS].edge : 0) + ti) * TW;
-    unsigned long long* dstE = P.tagA + (td.edge + tj) * TW;
-    unsigned long long* dstN = P.tagB + (td.edge + ti) * TW;
-    {
-      const int gi = td.i0 + ti, gj = td.j0 + tj;
-      T gb = T(0), gt = T(0);
-      if (col) {
-        gb = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
-        gt = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
+    double nrm = 0.0;
+    if (crit) {
+      // ------------------------------------------------------------ critical
+      const bool pollW = col && ti == 0 && td.nW >= 0, pollS = col && tj == 0 && td.nS >= 0;
+      const bool pubE = col && ti == kTI - 1 && td.nE >= 0, pubN = col && tj == kTJ - 1 && td.nN >= 0;
+      const unsigned long long* srcW = P.tagA + ((pollW ? P.tiles[td.nW].edge : 0) + tj) * TW;
+      const unsigned long long* srcS = P.tagB + ((pollS ? P.tiles[td.nS].edge : 0) + ti) * TW;
+      unsigned long long* dstE = P.tagA + (td.edge + tj) * TW;
+      unsigned long long* dstN = P.tagB + (td.edge + ti) * TW;
+      T* gR = P.R + td.slot * kTT + q;
+      auto poll_issue = [&](TagPoll<T>& pw, TagPoll<T>& ps, int s) {
+        const int k = s - d;
+        if (k >= 0 && k < nz && s < NS) {
+          if (pollW) pw.issue(srcW + (long long)k * 16 * TW);
+          if (pollS) ps.issue(srcS + (long long)k * 16 * TW);
+        }
+      };
+      TagPoll<T> pw0, ps0, pw1, ps1;  // R polls of even / odd steps
+      poll_issue(pw0, ps0, 0);
+      poll_issue(pw1, ps1, 1);
+      __syncthreads();  // prologue: rings filled
+      __syncthreads();  // prologue: step 0 prepared
+      T RB = T(0);  // own R of the plane below (0 outside the block)
+      auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps) {
+        const int k = t - d;
+        const T r = s_prep[t & 1][0][q], lb = s_prep[t & 1][1][q], lw = s_prep[t & 1][2][q];
+        const T ls = s_prep[t & 1][3][q], lp = s_prep[t & 1][4][q];
+        const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
+        if (col && k >= 0 && k < nz) {
+          const uint32_t tag = edge_tag(epoch, k);
+          const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61) : T(0));
+          const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62) : T(0));
+          const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
+          RB = Rv;
+          s_R[t & 1][q] = Rv;
+          if (pubE) put_tagged(dstE + (long long)k * 16 * TW, Rv, tag);
+          if (pubN) put_tagged(dstN + (long long)k * 16 * TW, Rv, tag);
+#ifndef SIPB_EXP_NOSTG
+          gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
+#endif
+        }
+        poll_issue(pw, ps, t + 2);
+        if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
+          P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
+        __syncthreads();
+      };
+      int t = 0;
+      for (; t + 1 < NS; t += 2) {
+        iter(t, pw0, ps0);
+        iter(t + 1, pw1, ps1);
       }
-      s_gh[0][p] = gb;
-      s_gh[1][p] = gt;
-    }
-    const T* fw_cell = P.fw + td.slot * F_NA * kTT + p;
-    const T* ph_cell = P.phi + td.slot * kTT + p;
-    const T* rp_cell = P.rec_phi + td.slot * 64 + (p & 63);
-    T* gR = P.R + td.slot * kTT + p;
-    auto ldg_fw = [&](T* nf, int x) {
-      const int k = x - d;
-      if (x < NS && col && k >= 0 && k < nz) {
-        const T* src = fw_cell + (long long)x * F_NA * kTT;
+      if (t < NS) iter(t, pw0, ps0);
+    } else {
+      // ------------------------------------------------------------ residual
+      const int rW = tj, rE = 16 + tj, rS = 32 + ti, rN = 48 + ti;
+      {
+        const int gi = td.i0 + ti, gj = td.j0 + tj;
+        T gb = T(0), gt = T(0);
+        if (col) {
+          gb = P.ghost[ghost_face_offset(bd, G_B) + gi + (long long)bd.nx * gj];
+          gt = P.ghost[ghost_face_offset(bd, G_T) + gi + (long long)bd.nx * gj];
+        }
+        s_gh[0][q] = gb;
+        s_gh[1][q] = gt;
+      }
+      const T* fw_cell = P.fw + td.slot * F_NA * kTT + q;
+      const T* ph_cell = P.phi + td.slot * kTT + q;
+      const T* rp_cell = P.rec_phi + td.slot * 64 + (q & 63);
+      auto ldg_fw = [&](T* nf, int x) {
+        const int k = x - d;
+        if (x < NS && col && k >= 0 && k < nz) {
+          const T* src = fw_cell + (long long)x * F_NA * kTT;
 #ifdef SIPB_EXP_NOLDG
 #pragma unroll
-        for (int a = 0; a < F_NA; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
-        (void)src;
+          for (int a = 0; a < F_NA; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
+          (void)src;
 #else
 #pragma unroll
-        for (int a = 0; a < F_NA; ++a) nf[a] = __ldg(src + a * kTT);
+          for (int a = 0; a < F_NA; ++a) nf[a] = __ldg(src + a * kTT);
 #endif
+        }
+      };
+      auto ldg_phi = [&](int y) -> T {
+        const int k = y - d;
+        return (y < NS && col && k >= 0 && k < nz) ? __ldg(ph_cell + (long long)y * kTT) : T(0);
+      };
+      auto ldg_rec = [&](int y) -> T { return (y < NS && q < 64) ? __ldg(rp_cell + (long long)y * 64) : T(0); };
+      // residual of step x (Listing-1 term order, a_nb = -A_nb)
+      auto residual = [&](const T* nf, T fP, T fB, T fT, T fW, T fE, T fS, T fN) {
+        T rr = -(nf[F_AE] * fE);
+        rr -= nf[F_AW] * fW;
+        rr -= nf[F_AN] * fN;
+        rr -= nf[F_AS] * fS;
+        rr -= nf[F_AT] * fT;
+        rr -= nf[F_AB] * fB;
+        rr += nf[F_Q];
+        rr -= nf[F_AP] * fP;
+        return rr;
+      };
+      auto publish = [&](int x, T rr, const T* nf) {  // hand the prepared step to the critical thread
+        s_prep[x & 1][0][q] = rr;
+        s_prep[x & 1][1][q] = nf[F_LB];
+        s_prep[x & 1][2][q] = nf[F_LW];
+        s_prep[x & 1][3][q] = nf[F_LS];
+        s_prep[x & 1][4][q] = nf[F_LP];
+      };
+      constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
+      auto pf_step = [&](int x) {  // L2 prefetch front: one 128-byte line per thread
+        if (x >= NS) return;
+        if (q < kFwLines)
+          prefetch_line_l2(reinterpret_cast<const char*>(P.fw + (td.slot + x) * F_NA * kTT) + 128 * q);
+        else if (q < kFwLines + kPhLines)
+          prefetch_line_l2(reinterpret_cast<const char*>(P.phi + (td.slot + x) * kTT) + 128 * (q - kFwLines));
+      };
+      // ---- prologue: slices / records 0..2 into the rings, 3 and 4 in flight
+      for (int y = 0; y < 3; ++y) {
+        s_ph[y][q] = ldg_phi(y);
+        if (q < 64) s_rec[y][q] = ldg_rec(y);
       }
-    };
-    auto ldg_phi = [&](int y) -> T {
-      const int k = y - d;
-      return (y < NS && col && k >= 0 && k < nz) ? __ldg(ph_cell + (long long)y * kTT) : T(0);
-    };
-    auto ldg_rec = [&](int y) -> T { return (y < NS && p < 64) ? __ldg(rp_cell + (long long)y * 64) : T(0); };
-    auto poll_issue = [&](TagPoll<T>& pw, TagPoll<T>& ps, int s) {
-      const int k = s - d;
-      if (k >= 0 && k < nz && s < NS) {
-        if (pollW) pw.issue(srcW + (long long)k * 16 * TW);
-        if (pollS) ps.issue(srcS + (long long)k * 16 * TW);
-      }
-    };
-    // residual of step x (Listing-1 term order, a_nb = -A_nb)
-    auto residual = [&](const T* nf, T fP, T fB, T fT, T fW, T fE, T fS, T fN) {
-      T rr = -(nf[F_AE] * fE);
-      rr -= nf[F_AW] * fW;
-      rr -= nf[F_AN] * fN;
-      rr -= nf[F_AS] * fS;
-      rr -= nf[F_AT] * fT;
-      rr -= nf[F_AB] * fB;
-      rr += nf[F_Q];
-      rr -= nf[F_AP] * fP;
-      return rr;
-    };
-    // ---- prologue: slices / records 0..2 into the rings, 3 and 4 in flight
-    for (int y = 0; y < 3; ++y) {
-      s_ph[y][p] = ldg_phi(y);
-      if (p < 64) s_rec[y][p] = ldg_rec(y);
-    }
-    T phB[2], rcB[2];  // in-flight own phi / record value of slices of parity 0 / 1
-    phB[1] = ldg_phi(3); rcB[1] = ldg_rec(3);
-    phB[0] = ldg_phi(4); rcB[0] = ldg_rec(4);
-    T nf0[F_NA], nf1[F_NA];  // forward pack of even / odd steps
+      T phB[2], rcB[2];
+      phB[1] = ldg_phi(3); rcB[1] = ldg_rec(3);
+      phB[0] = ldg_phi(4); rcB[0] = ldg_rec(4);
+      T nf0[F_NA], nf1[F_NA];  // forward pack of even / odd steps (LDG two iterations ahead)
 #pragma unroll
-    for (int a = 0; a < F_NA; ++a) nf0[a] = nf1[a] = T(0);
-    constexpr int FD = FwDist<T>::value;
-    T* const nfOdd = FD == 2 ? nf1 : nf0;  // buffer of odd steps
-    ldg_fw(nf0, 0);
-    if (FD == 2) ldg_fw(nf1, 1);
-    TagPoll<T> pw0, ps0, pw1, ps1;  // R polls of even / odd steps
-    poll_issue(pw0, ps0, 0);
-    poll_issue(pw1, ps1, 1);
-    // L2 prefetch front: the forward pack and phi slice of step x, one
-    // 128-byte line per thread (LSU path; lines spread over the 8 warps)
-    constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
-    auto pf_step = [&](int x) {
-      if (x >= NS) return;
-      if (p < kFwLines)
-        prefetch_line_l2(reinterpret_cast<const char*>(P.fw + (td.slot + x) * F_NA * kTT) + 128 * p);
-      else if (p < kFwLines + kPhLines)
-        prefetch_line_l2(reinterpret_cast<const char*>(P.phi + (td.slot + x) * kTT) + 128 * (p - kFwLines));
-    };
-    for (int x = 0; x <= kPFL; ++x) pf_step(x + 5);
-    __syncthreads();
-    double nrm = 0.0;
-    T RB = T(0);  // own R of the plane below (0 outside the block)
-    T r = T(0), lb = T(0), lw = T(0), ls = T(0), lp = T(0);  // prepared step
-    bool act = col && d == 0 && nz > 0;  // step 0: only the (0,0) column, k = 0
-    {
-      const T fP = s_ph[0][p], fB = s_gh[0][p];
-      const T fT = nz > 1 ? s_ph[1][p] : s_gh[1][p];
-      const T fW = s_rec[0][rW], fS = s_rec[0][rS];
-      const T fE = inE ? s_ph[1][pE] : s_rec[0][rE];
-      const T fN = inN ? s_ph[1][pN] : s_rec[0][rN];
-      const T rr = residual(nf0, fP, fB, fT, fW, fE, fS, fN);
-      if (act) {
-        nrm += fabs(static_cast<double>(rr));
-        r = rr; lb = nf0[F_LB]; lw = nf0[F_LW]; ls = nf0[F_LS]; lp = nf0[F_LP];
+      for (int a = 0; a < F_NA; ++a) nf0[a] = nf1[a] = T(0);
+      ldg_fw(nf0, 0);
+      ldg_fw(nf1, 1);
+      for (int x = 0; x <= kPFL; ++x) pf_step(x + 5);
+      __syncthreads();  // prologue: rings filled
+      {
+        const T fP = s_ph[0][q], fB = s_gh[0][q];
+        const T fT = nz > 1 ? s_ph[1][q] : s_gh[1][q];
+        const T fW = s_rec[0][rW], fS = s_rec[0][rS];
+        const T fE = inE ? s_ph[1][pE] : s_rec[0][rE];
+        const T fN = inN ? s_ph[1][pN] : s_rec[0][rN];
+        const T rr = residual(nf0, fP, fB, fT, fW, fE, fS, fN);
+        if (col && d == 0 && nz > 0) nrm += fabs(static_cast<double>(rr));
+        publish(0, rr, nf0);
       }
+      ldg_fw(nf0, 2);
+      __syncthreads();  // prologue: step 0 prepared
+      auto iter = [&](const int t, T* nf, T& phb, T& rcb) {
+        const int x = t + 1;
+        const int k1 = x - d;
+        const int sm = t & 3, s0 = x & 3, sp = (x + 1) & 3;
+        const T fP = s_ph[s0][q];
+        const T fB = k1 > 0 ? s_ph[sm][q] : s_gh[0][q];
+        const T fT = k1 + 1 < nz ? s_ph[sp][q] : s_gh[1][q];
+        const T fW = inW ? s_ph[sm][pW] : s_rec[s0][rW];
+        const T fE = inE ? s_ph[sp][pE] : s_rec[s0][rE];
+        const T fS = inS ? s_ph[sm][pS] : s_rec[s0][rS];
+        const T fN = inN ? s_ph[sp][pN] : s_rec[s0][rN];
+        const T rr = residual(nf, fP, fB, fT, fW, fE, fS, fN);
+        if (x < NS && col && k1 >= 0 && k1 < nz) nrm += fabs(static_cast<double>(rr));
+        publish(x, rr, nf);
+        ldg_fw(nf, x + 2);  // nf consumed above
+        // refill the rings: slice / record t+3 (slot of slice t-1, last read in iteration t-1)
+        s_ph[(t + 3) & 3][q] = phb;
+        if (q < 64) s_rec[(t + 3) & 3][q] = rcb;
+        phb = ldg_phi(t + 5);
+        rcb = ldg_rec(t + 5);
+        pf_step(t + 6 + kPFL);
+        __syncthreads();
+      };
+      int t = 0;
+      for (; t + 1 < NS; t += 2) {
+        iter(t, nf1, phB[1], rcB[1]);
+        iter(t + 1, nf0, phB[0], rcB[0]);
+      }
+      if (t < NS) iter(t, nf1, phB[1], rcB[1]);
     }
-    ldg_fw(nf0, FD == 2 ? 2 : 1);
-    __syncthreads();
-    // iteration t: critical(t) and the residual of step t+1
-    auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* nf, T& phb, T& rcb) {
-      const int x = t + 1;
-      const int k = t - d;
-      // ---- shared loads of critical(t)
-      const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
-      // ---- shared loads of the residual of step x: slices x-1, x, x+1, record x
-      const int k1 = x - d;
-      const int sm = t & 3, s0 = x & 3, sp = (x + 1) & 3;
-      const T fP = s_ph[s0][p];
-      const T fB = k1 > 0 ? s_ph[sm][p] : s_gh[0][p];
-      const T fT = k1 + 1 < nz ? s_ph[sp][p] : s_gh[1][p];
-      const T fW = inW ? s_ph[sm][pW] : s_rec[s0][rW];
-      const T fE = inE ? s_ph[sp][pE] : s_rec[s0][rE];
-      const T fS = inS ? s_ph[sm][pS] : s_rec[s0][rS];
-      const T fN = inN ? s_ph[sp][pN] : s_rec[s0][rN];
-      // ---- critical(t): R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP
-      if (act) {
-        const uint32_t tag = edge_tag(epoch, k);
-        const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61) : T(0));
-        const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62) : T(0));
-        const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
-        RB = Rv;
-        s_R[t & 1][p] = Rv;
-        if (pubE) put_tagged(dstE + (long long)k * 16 * TW, Rv, tag);
-        if (pubN) put_tagged(dstN + (long long)k * 16 * TW, Rv, tag);
-#ifndef SIPB_EXP_NOSTG
-        gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
-#endif
-      }
-      poll_issue(pw, ps, t + 2);
-      // ---- residual of step x
-      const bool act1 = x < NS && col && k1 >= 0 && k1 < nz;
-      const T rr = residual(nf, fP, fB, fT, fW, fE, fS, fN);
-      if (act1) {
-        nrm += fabs(static_cast<double>(rr));
-        r = rr; lb = nf[F_LB]; lw = nf[F_LW]; ls = nf[F_LS]; lp = nf[F_LP];
-      }
-      ldg_fw(nf, x + FD);  // nf consumed above
-      act = act1;
-      // ---- refill the rings: slice / record t+3 (slot of slice t-1, last read in iteration t-1)
-      s_ph[(t + 3) & 3][p] = phb;
-      if (p < 64) s_rec[(t + 3) & 3][p] = rcb;
-      phb = ldg_phi(t + 5);
-      rcb = ldg_rec(t + 5);
-      pf_step(t + 6 + kPFL);  // keep forward pack and phi warm in L2 ahead of the LDGs
-      if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
-        P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
-      __syncthreads();
-    };
-    int t = 0;
-    for (; t + 1 < NS; t += 2) {
-      iter(t, pw0, ps0, nfOdd, phB[1], rcB[1]);
-      iter(t + 1, pw1, ps1, nf0, phB[0], rcB[0]);
-    }
-    if (t < NS) iter(t, pw0, ps0, nfOdd, phB[1], rcB[1]);
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     const double s = cta_sum(nrm, s_red);
@@ -1208,7 +1221,7 @@ int launch_factor(const FactorParams& p, int grid, void* stream) {
 
 template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
-  k_forward<T><<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
+  k_forward<T><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1236,8 +1249,8 @@ int max_resident_ctas(int kind, int precision, int* grid) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_factor, kTT, 0);
   } else if (kind == 1) {
     e = precision == SIP_PREC_DOUBLE
-            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double>, kTT, 0)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float>, kTT, 0);
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double>, 2 * kTT, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float>, 2 * kTT, 0);
   } else {
     e = precision == SIP_PREC_DOUBLE
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT, 0)
