@@ -318,10 +318,6 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
 // on shared-memory mbarriers, compute, store, and meet at one named barrier.
 // =============================================================================
 constexpr int kCompute = kTT;       // compute threads (8 warps)
-constexpr int kThreads = kTT + 64;  // + publisher, fetcher warps
-constexpr int kComputeWarps = kTT / 32;
-constexpr int kPublisherWarp = kComputeWarps, kFetcherWarp = kComputeWarps + 1;
-constexpr int kPF = 0;              // L2 prefetch distance (slices; 0 = off: the TMA unit is the per-SM bottleneck)
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
@@ -337,6 +333,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 }
 __device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
   asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+}
+// Named barriers of the split forward sweep (id 0 = __syncthreads).
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 // Explicit 32-bit shared-window accesses: keep ring addresses in plain
 // registers (no generic->shared rematerialisation in the step loops).
@@ -548,35 +551,26 @@ __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long*
 }
 
 constexpr int kRing = 4;  // phi-slice / edge-record ring of K2 (slices t .. t+3 live)
-// forward-pack LDG distance of K2 (iterations between load and use): 2 needs
-// two register buffers (fp64: 48 registers) and one CTA per SM
-#ifdef SIPB_FW_D1
-constexpr int kFwdMinBlocks = 2;
-#else
-constexpr int kFwdMinBlocks = 1;
-#endif
-template <typename T>
-struct FwDist {
-#ifdef SIPB_FW_D1
-  static constexpr int value = 1;
-#else
-  static constexpr int value = 2;
-#endif
-};
+constexpr int kPrep = 4;  // prepared-step ring between the residual and critical groups
+constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
+constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kPrep;
 
 template <typename T>
 __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) {
   // Two threads per column.  Threads 0..255 ("critical"): the recurrence
   // R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP of step t, cross-tile R
   // stores / polls.  Threads 256..511 ("residual"): everything that does
-  // not depend on R -- the residual r of step t+1 and its factors (handed
-  // over through s_prep), the phi / edge-record rings, the forward-pack
-  // LDGs and the L2 prefetch front.  One barrier per step.
-  __shared__ __align__(16) T s_ph[kRing][kTT];  // own-column phi of slice y in slot y % 4
-  __shared__ __align__(16) T s_rec[kRing][64];  // static edge record of step y (phiW/E/S/N)
+  // not depend on R -- the residual r of each step and its factors (handed
+  // over through the s_prep ring of kPrep slots), the phi / edge-record
+  // rings, the forward-pack LDGs and the L2 prefetch front.  The two groups
+  // are decoupled by named barriers (producer/consumer FULL / EMPTY per prep
+  // slot), so the residual group runs up to kPrep steps ahead; each group
+  // meets only itself once per step (its own shared-ring exchange).
+  __shared__ __align__(16) T s_ph[kRingR][kTT];  // own-column phi of slice y in slot y % kRingR
+  __shared__ __align__(16) T s_rec[kRingR][64];  // static edge record of step y (phiW/E/S/N)
   __shared__ __align__(16) T s_R[2][kTT];       // R of steps t-1 / t
   __shared__ __align__(16) T s_gh[2][kTT];      // ghost phi below / above each column
-  __shared__ __align__(16) T s_prep[2][5][kTT]; // r, LB, LW, LS, LP of the prepared step
+  __shared__ __align__(16) T s_prep[kPrep][kTT];  // residual r of prepared steps
   __shared__ double s_red[2 * kTT / 32];
   __shared__ int s_tile, s_last;
   constexpr int TW = kTagWords<T>;
@@ -632,13 +626,27 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       TagPoll<T> pw0, ps0, pw1, ps1;  // R polls of even / odd steps
       poll_issue(pw0, ps0, 0);
       poll_issue(pw1, ps1, 1);
-      __syncthreads();  // prologue: rings filled
-      __syncthreads();  // prologue: step 0 prepared
+      // own factor coefficients LB, LW, LS, LP, LDG'd two steps ahead
+      const T* lf_cell = P.fw + td.slot * F_NA * kTT + F_LB * kTT + q;
+      auto ldg_lf = [&](T* lf, int s) {
+        const int k = s - d;
+        if (s < NS && col && k >= 0 && k < nz) {
+          const T* src = lf_cell + (long long)s * F_NA * kTT;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) lf[a] = __ldg(src + a * kTT);
+        }
+      };
+      T lf0[4] = {T(0), T(0), T(0), T(0)}, lf1[4] = {T(0), T(0), T(0), T(0)};
+      ldg_lf(lf0, 0);
+      ldg_lf(lf1, 1);
       T RB = T(0);  // own R of the plane below (0 outside the block)
-      auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps) {
+      auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* lf) {
         const int k = t - d;
-        const T r = s_prep[t & 1][0][q], lb = s_prep[t & 1][1][q], lw = s_prep[t & 1][2][q];
-        const T ls = s_prep[t & 1][3][q], lp = s_prep[t & 1][4][q];
+        const int sl = t & (kPrep - 1);
+        nbar_sync(kBarFull + sl, 2 * kTT);  // step t prepared
+        const T r = s_prep[sl][q];
+        const T lb = lf[0], lw = lf[1], ls = lf[2], lp = lf[3];
+        if (t + kPrep < NS) nbar_arrive(kBarEmpty + sl, 2 * kTT);  // slot free for step t + kPrep
         const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
         if (col && k >= 0 && k < nz) {
           const uint32_t tag = edge_tag(epoch, k);
@@ -654,18 +662,22 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
 #endif
         }
         poll_issue(pw, ps, t + 2);
+        ldg_lf(lf, t + 2);
         if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
           P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
-        __syncthreads();
+        nbar_sync(kBarCrit, kTT);  // R of step t visible to the group
       };
       int t = 0;
       for (; t + 1 < NS; t += 2) {
-        iter(t, pw0, ps0);
-        iter(t + 1, pw1, ps1);
+        iter(t, pw0, ps0, lf0);
+        iter(t + 1, pw1, ps1, lf1);
       }
-      if (t < NS) iter(t, pw0, ps0);
+      if (t < NS) iter(t, pw0, ps0, lf0);
     } else {
       // ------------------------------------------------------------ residual
+      // Two steps per iteration (two independent residual chains interleave,
+      // one group barrier per two steps).  Iteration m prepares steps 2m+1
+      // and 2m+2, refills ring slices 2m+4 and 2m+5 (ring of kRingR slots).
       const int rW = tj, rE = 16 + tj, rS = 32 + ti, rN = 48 + ti;
       {
         const int gi = td.i0 + ti, gj = td.j0 + tj;
@@ -680,17 +692,17 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       const T* fw_cell = P.fw + td.slot * F_NA * kTT + q;
       const T* ph_cell = P.phi + td.slot * kTT + q;
       const T* rp_cell = P.rec_phi + td.slot * 64 + (q & 63);
-      auto ldg_fw = [&](T* nf, int x) {
+      auto ldg_fw = [&](T* nf, int x) {  // the 8 residual coefficients (AP .. AT, Q)
         const int k = x - d;
         if (x < NS && col && k >= 0 && k < nz) {
           const T* src = fw_cell + (long long)x * F_NA * kTT;
 #ifdef SIPB_EXP_NOLDG
 #pragma unroll
-          for (int a = 0; a < F_NA; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
+          for (int a = 0; a < F_LB; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
           (void)src;
 #else
 #pragma unroll
-          for (int a = 0; a < F_NA; ++a) nf[a] = __ldg(src + a * kTT);
+          for (int a = 0; a < F_LB; ++a) nf[a] = __ldg(src + a * kTT);
 #endif
         }
       };
@@ -711,12 +723,11 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         rr -= nf[F_AP] * fP;
         return rr;
       };
-      auto publish = [&](int x, T rr, const T* nf) {  // hand the prepared step to the critical thread
-        s_prep[x & 1][0][q] = rr;
-        s_prep[x & 1][1][q] = nf[F_LB];
-        s_prep[x & 1][2][q] = nf[F_LW];
-        s_prep[x & 1][3][q] = nf[F_LS];
-        s_prep[x & 1][4][q] = nf[F_LP];
+      auto publish = [&](int x, T rr) {  // hand the residual of step x to the critical group
+        const int sl = x & (kPrep - 1);
+        if (x >= kPrep) nbar_sync(kBarEmpty + sl, 2 * kTT);  // step x - kPrep consumed
+        s_prep[sl][q] = rr;
+        nbar_arrive(kBarFull + sl, 2 * kTT);
       };
       constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
       auto pf_step = [&](int x) {  // L2 prefetch front: one 128-byte line per thread
@@ -726,62 +737,79 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         else if (q < kFwLines + kPhLines)
           prefetch_line_l2(reinterpret_cast<const char*>(P.phi + (td.slot + x) * kTT) + 128 * (q - kFwLines));
       };
-      // ---- prologue: slices / records 0..2 into the rings, 3 and 4 in flight
-      for (int y = 0; y < 3; ++y) {
+      // operands of the residual of step x from ring slots of slices x-1, x, x+1
+      struct Ops { T fP, fB, fT, fW, fE, fS, fN; };
+      auto load_ops = [&](int x) {
+        Ops o;
+        const int k1 = x - d;
+        const int sm = (x - 1) & (kRingR - 1), s0 = x & (kRingR - 1), sp = (x + 1) & (kRingR - 1);
+        const int rr = x & (kRingR - 1);
+        o.fP = s_ph[s0][q];
+        o.fB = k1 > 0 ? s_ph[sm][q] : s_gh[0][q];
+        o.fT = k1 + 1 < nz ? s_ph[sp][q] : s_gh[1][q];
+        o.fW = inW ? s_ph[sm][pW] : s_rec[rr][rW];
+        o.fE = inE ? s_ph[sp][pE] : s_rec[rr][rE];
+        o.fS = inS ? s_ph[sm][pS] : s_rec[rr][rS];
+        o.fN = inN ? s_ph[sp][pN] : s_rec[rr][rN];
+        return o;
+      };
+      auto active = [&](int x) { const int k1 = x - d; return x < NS && col && k1 >= 0 && k1 < nz; };
+      // ---- prologue: slices / records 0..3 into the ring, 4..7 in flight
+      for (int y = 0; y < 4; ++y) {
         s_ph[y][q] = ldg_phi(y);
         if (q < 64) s_rec[y][q] = ldg_rec(y);
       }
-      T phB[2], rcB[2];
-      phB[1] = ldg_phi(3); rcB[1] = ldg_rec(3);
-      phB[0] = ldg_phi(4); rcB[0] = ldg_rec(4);
-      T nf0[F_NA], nf1[F_NA];  // forward pack of even / odd steps (LDG two iterations ahead)
+      T phA[2] = {ldg_phi(4), ldg_phi(5)}, phB[2] = {ldg_phi(6), ldg_phi(7)};
+      T rcA[2] = {ldg_rec(4), ldg_rec(5)}, rcB[2] = {ldg_rec(6), ldg_rec(7)};
+      T nfO[F_LB], nfE[F_LB];  // residual coefficients of odd / even steps
 #pragma unroll
-      for (int a = 0; a < F_NA; ++a) nf0[a] = nf1[a] = T(0);
-      ldg_fw(nf0, 0);
-      ldg_fw(nf1, 1);
-      for (int x = 0; x <= kPFL; ++x) pf_step(x + 5);
-      __syncthreads();  // prologue: rings filled
+      for (int a = 0; a < F_LB; ++a) nfO[a] = nfE[a] = T(0);
+      ldg_fw(nfE, 0);
+      ldg_fw(nfO, 1);
+      for (int x = 0; x <= kPFL; ++x) pf_step(x + 8);
+      nbar_sync(kBarRes, kTT);  // prologue: ring filled
       {
-        const T fP = s_ph[0][q], fB = s_gh[0][q];
-        const T fT = nz > 1 ? s_ph[1][q] : s_gh[1][q];
-        const T fW = s_rec[0][rW], fS = s_rec[0][rS];
-        const T fE = inE ? s_ph[1][pE] : s_rec[0][rE];
-        const T fN = inN ? s_ph[1][pN] : s_rec[0][rN];
-        const T rr = residual(nf0, fP, fB, fT, fW, fE, fS, fN);
-        if (col && d == 0 && nz > 0) nrm += fabs(static_cast<double>(rr));
-        publish(0, rr, nf0);
+        const Ops o = load_ops(0);
+        const T rr = residual(nfE, o.fP, o.fB, o.fT, o.fW, o.fE, o.fS, o.fN);
+        if (active(0)) nrm += fabs(static_cast<double>(rr));
+        publish(0, rr);
       }
-      ldg_fw(nf0, 2);
-      __syncthreads();  // prologue: step 0 prepared
-      auto iter = [&](const int t, T* nf, T& phb, T& rcb) {
-        const int x = t + 1;
-        const int k1 = x - d;
-        const int sm = t & 3, s0 = x & 3, sp = (x + 1) & 3;
-        const T fP = s_ph[s0][q];
-        const T fB = k1 > 0 ? s_ph[sm][q] : s_gh[0][q];
-        const T fT = k1 + 1 < nz ? s_ph[sp][q] : s_gh[1][q];
-        const T fW = inW ? s_ph[sm][pW] : s_rec[s0][rW];
-        const T fE = inE ? s_ph[sp][pE] : s_rec[s0][rE];
-        const T fS = inS ? s_ph[sm][pS] : s_rec[s0][rS];
-        const T fN = inN ? s_ph[sp][pN] : s_rec[s0][rN];
-        const T rr = residual(nf, fP, fB, fT, fW, fE, fS, fN);
-        if (x < NS && col && k1 >= 0 && k1 < nz) nrm += fabs(static_cast<double>(rr));
-        publish(x, rr, nf);
-        ldg_fw(nf, x + 2);  // nf consumed above
-        // refill the rings: slice / record t+3 (slot of slice t-1, last read in iteration t-1)
-        s_ph[(t + 3) & 3][q] = phb;
-        if (q < 64) s_rec[(t + 3) & 3][q] = rcb;
-        phb = ldg_phi(t + 5);
-        rcb = ldg_rec(t + 5);
-        pf_step(t + 6 + kPFL);
-        __syncthreads();
+      ldg_fw(nfE, 2);
+      auto iter = [&](const int m, T* phb, T* rcb) {
+        const int x0 = 2 * m + 1, x1 = x0 + 1;
+        const Ops o0 = load_ops(x0);
+        const Ops o1 = load_ops(x1);
+        const T r0 = residual(nfO, o0.fP, o0.fB, o0.fT, o0.fW, o0.fE, o0.fS, o0.fN);
+        const T r1 = residual(nfE, o1.fP, o1.fB, o1.fT, o1.fW, o1.fE, o1.fS, o1.fN);
+        if (active(x0)) nrm += fabs(static_cast<double>(r0));
+        if (active(x1)) nrm += fabs(static_cast<double>(r1));
+        if (x0 < NS) publish(x0, r0);
+        if (x1 < NS) publish(x1, r1);
+        ldg_fw(nfO, x0 + 2);  // consumed above
+        ldg_fw(nfE, x1 + 2);
+        // refill: slices / records 2m+4, 2m+5 (slots of slices 2m-4, 2m-3, last read in iteration m-2)
+        const int y = 2 * m + 4;
+        s_ph[y & (kRingR - 1)][q] = phb[0];
+        s_ph[(y + 1) & (kRingR - 1)][q] = phb[1];
+        if (q < 64) {
+          s_rec[y & (kRingR - 1)][q] = rcb[0];
+          s_rec[(y + 1) & (kRingR - 1)][q] = rcb[1];
+        }
+        phb[0] = ldg_phi(y + 4);
+        phb[1] = ldg_phi(y + 5);
+        rcb[0] = ldg_rec(y + 4);
+        rcb[1] = ldg_rec(y + 5);
+        pf_step(y + 4 + kPFL);
+        pf_step(y + 5 + kPFL);
+        nbar_sync(kBarRes, kTT);  // ring slices 2m+4, 2m+5 visible to the group
       };
-      int t = 0;
-      for (; t + 1 < NS; t += 2) {
-        iter(t, nf1, phB[1], rcB[1]);
-        iter(t + 1, nf0, phB[0], rcB[0]);
+      // iterations m while 2m+1 < NS
+      int m = 0;
+      for (; 2 * m + 3 < NS; m += 2) {
+        iter(m, phA, rcA);
+        iter(m + 1, phB, rcB);
       }
-      if (t < NS) iter(t, nf1, phB[1], rcB[1]);
+      if (2 * m + 1 < NS) iter(m, phA, rcA);
     }
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
