@@ -1,0 +1,29 @@
+"""Backward tile hop A -> A-1 (A = $SIPB_TRACE_TILE, e.g. 255 = last tile at
+256^3) in one backward sweep; needs a -DSIPB_STEP_TRACE build.  B's step u
+consumes A's step u+15."""
+import ctypes, os, sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_1303_4538_b200 as sip
+prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+ns = n + 30
+s = sip.Solver(None, prec, 0, lattice=((n, n, n), (1, 1, 1)))
+s._nglobal = 1
+s.generate(0, 1304); s.factor(0.92); s.load_phi([sip.field(n, n, n)])
+L = sip.lib()
+nt = ctypes.c_longlong()
+L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
+s.iterate(2)
+buf = np.zeros(8 * nt.value + 16 * ns, dtype=np.uint64)
+L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
+tr = buf[:8 * nt.value].reshape(2, nt.value, 4).astype(np.int64)
+t0 = tr[1, :, 0].min()
+st = (buf[8 * nt.value:].reshape(ns, 16).astype(np.int64) - t0) / 1e3
+A, B = st[:, 2], st[:, 3]
+x = np.arange(40, ns - 40)
+dA, dB = np.diff(A[40:-40]), np.diff(B[40:-40])
+print(f"bwd {prec} {n}^3: A pace median {np.median(dA)*1e3:.0f} mean {dA.mean()*1e3:.0f} ns; B pace median {np.median(dB)*1e3:.0f} mean {dB.mean()*1e3:.0f} ns")
+v = B[x] - A[x + 15]
+print(f"  A step u+15 -> B step u: median {np.median(v):.2f} us (p10 {np.percentile(v,10):.2f}, p90 {np.percentile(v,90):.2f})")
+print(f"  A step 0 {A[0]:.2f}, A step 15 {A[15]:.2f}, B step 0 {B[0]:.2f}; A end {A[-1]:.1f}, B end {B[-1]:.1f}")
