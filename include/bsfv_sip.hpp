@@ -97,6 +97,7 @@ template <class Field>
 struct StencilSystemT {
   Field ap, aw, ae, as, an, ab, at, q;
   long long revision = 0;  // bump after editing the coefficients
+  bool symmetric = false;  // ae(i) = aw(i+1), an(j) = as(j+1), at(k) = ab(k+1)
 };
 
 /// SipFactors: a device context holding the factors,
@@ -171,6 +172,38 @@ std::pair<Field, SolveReport> solve(const StencilSystemT<Field>& A, const Field&
   rep.norms.resize(static_cast<size_t>(used));
   rep.iterations = used;
   return {fi, rep};
+}
+
+/// residual_general / residual_symmetric
+/// of fi on the device; returns a Field of the same shape (interior written).
+/// residual_symmetric throws MisuseError unless A.symmetric, ConfigError if
+/// the coefficients contradict the flag.
+template <class Field>
+Field residual(const StencilSystemT<Field>& A, const Field& fi, bool symmetric, int device = 0) {
+  if (symmetric && !A.symmetric)
+    throw MisuseError("residual_symmetric: system not flagged symmetric");
+  sip_ctx* ctx = nullptr;
+  check(::sip_create(device, A.ap.nx(), A.ap.ny(), A.ap.nz(), SIP_PREC_DOUBLE, &ctx), nullptr,
+        "sip_create");
+  SipFactors holder(ctx, A.revision, false);  // owns ctx
+  check(::sip_set_system(ctx, 0, A.ap.data(), A.aw.data(), A.ae.data(), A.as.data(), A.an.data(),
+                         A.ab.data(), A.at.data(), A.q.data()),
+        ctx, "sip_set_system");
+  if (symmetric) check(::sip_set_symmetric(ctx, 0, 1), ctx, "sip_set_symmetric");
+  const double* in[1] = {fi.data()};
+  check(::sip_load_phi(ctx, const_cast<double* const*>(in)), ctx, "sip_load_phi");
+  Field res = fi;
+  double* out[1] = {res.data()};
+  check(::sip_residual(ctx, symmetric ? 1 : 0, out), ctx, "sip_residual");
+  return res;
+}
+template <class Field>
+Field residual_general(const StencilSystemT<Field>& A, const Field& fi, int device = 0) {
+  return residual(A, fi, false, device);
+}
+template <class Field>
+Field residual_symmetric(const StencilSystemT<Field>& A, const Field& fi, int device = 0) {
+  return residual(A, fi, true, device);
 }
 
 /// sip_sweep: one inner iteration in place, returns the L1 norm.

@@ -124,8 +124,17 @@ int sip_iterate(sip_ctx* ctx, int iters);                 /* enqueue, no host sy
 int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* block_norms);
 int sip_synchronize(sip_ctx* ctx);
 
+/* Flag (symmetric = 1) or unflag the system of local block `local` as
+ * symmetric (StencilSystem invariant: ae(i) = aw(i+1),
+ * an(j) = as(j+1), at(k) = ab(k+1), checked exactly on the device;
+ * SIP_ERR_CONFIG if violated).  sip_set_system clears the flag. */
+int sip_set_symmetric(sip_ctx* ctx, int local, int symmetric);
+
 /* residual_general / residual_symmetric of the current
- * device phi into res[local] (Field3 host arrays, interior written). */
+ * device phi into res[local] (Field3 host arrays, interior written).
+ * symmetric = 1 reads only AE/AN/AT (+ shifted), AP, Q (Listing 1) and
+ * requires every local system to be flagged (SIP_ERR_MISUSE otherwise,
+ * SPEC.md:165). */
 int sip_residual(sip_ctx* ctx, int symmetric, double* const* res);
 
 /* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */

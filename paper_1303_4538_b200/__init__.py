@@ -13,7 +13,7 @@ import numpy as np
 from .sip import (  # noqa: F401
     ARRAYS, EXPORTS, LIB_PATH, ConfigError, Error, MisuseError, SingularFactorError, SipConfig,
     SipFactors, Solver, SolveReport, StaleFactorsError, StencilSystem, factorization_count, field,
-    lib, residual_general, sip_factor, sip_sweep, solve, version,
+    lib, residual_general, residual_symmetric, sip_factor, sip_sweep, solve, version,
 )
 
 

@@ -88,6 +88,7 @@ struct sip_ctx {
   void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
   void *edgeW = nullptr, *edgeS = nullptr;
   void* rec_phi = nullptr;  // [total_slices][64] static part of the K2 edge records
+  std::vector<char> symmetric;  // per local block: system flagged symmetric
   unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
   size_t tag_words = 0;                 // words per buffer
   unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
@@ -684,6 +685,37 @@ int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw, 
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ++ctx->revision;
+  if (ctx->symmetric.size() != ctx->local.size()) ctx->symmetric.assign(ctx->local.size(), 0);
+  ctx->symmetric[local] = 0;  // a new system is not flagged until sip_set_symmetric
+  return SIP_OK;
+}
+
+int sip_set_symmetric(sip_ctx* ctx, int local, int symmetric) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (local < 0 || local >= (int)ctx->local.size()) {
+    ctx->err = "sip_set_symmetric: local block index out of range";
+    return SIP_ERR_MISUSE;
+  }
+  if (ctx->symmetric.size() != ctx->local.size()) ctx->symmetric.assign(ctx->local.size(), 0);
+  if (!symmetric) {
+    ctx->symmetric[local] = 0;
+    return SIP_OK;
+  }
+  CKS(set_device(ctx));
+  const BlockDesc& hb = ctx->hblocks[local];
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->staging);
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), ctx->stream));
+  CKS(launch_check_symmetric(ctx->d_blocks, local, hb, ctx->fw64, bad, ctx->stream));
+  ++ctx->launches;
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h) {
+    ctx->err = "sip_set_symmetric: " + std::to_string(h) +
+               " coefficient pairs violate ae(i)=aw(i+1), an(j)=as(j+1), at(k)=ab(k+1)";
+    return SIP_ERR_CONFIG;
+  }
+  ctx->symmetric[local] = 1;
   return SIP_OK;
 }
 
@@ -733,6 +765,7 @@ int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed) {
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ++ctx->revision;
+  ctx->symmetric.assign(ctx->local.size(), 0);  // generated systems are not flagged
   return SIP_OK;
 }
 
@@ -950,10 +983,13 @@ int sip_solve(sip_ctx* ctx, double* const* phi, int max_iters, double target, do
 
 int sip_residual(sip_ctx* ctx, int symmetric, double* const* res) {
   if (!ctx || !res) return SIP_ERR_MISUSE;
-  if (symmetric) {
-    ctx->err = "residual_symmetric is not available on the device path yet";
-    return SIP_ERR_MISUSE;
-  }
+  if (symmetric)
+    for (size_t lb = 0; lb < ctx->local.size(); ++lb)
+      if (lb >= ctx->symmetric.size() || !ctx->symmetric[lb]) {
+        ctx->err = "residual_symmetric: system of local block " + std::to_string(lb) +
+                   " is not flagged symmetric (sip_set_symmetric)";
+        return SIP_ERR_MISUSE;
+      }
   CKS(set_device(ctx));
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockDesc& hb = ctx->hblocks[lb];
@@ -961,12 +997,12 @@ int sip_residual(sip_ctx* ctx, int symmetric, double* const* res) {
     CK(cudaMemsetAsync(ctx->staging, 0, G * sizeof(double), ctx->stream));
     if (ctx->precision == SIP_PREC_SINGLE)
       CKS(launch_residual<float>(ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
-                                 static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost), 0,
-                                 ctx->staging, ctx->stream));
+                                 static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost),
+                                 symmetric, ctx->staging, ctx->stream));
     else
       CKS(launch_residual<double>(ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->fw),
                                   static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
-                                  0, ctx->staging, ctx->stream));
+                                  symmetric, ctx->staging, ctx->stream));
     ++ctx->launches;
     CK(cudaMemcpyAsync(res[lb], ctx->staging, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   }

@@ -184,6 +184,8 @@ template <typename T>
 int launch_backward(const SweepParams<T>& p, int grid, void* stream);
 template <typename T>
 int launch_edge_phi(const SweepParams<T>& p, void* stream);
+int launch_check_symmetric(const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                           const double* fw, unsigned long long* bad, void* stream);
 template <typename T>
 int launch_scatter(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
                    T* pack, int na, int arr, void* stream);

@@ -1139,7 +1139,13 @@ __global__ void k_face_copy(const FaceCopy* copies, const BlockDesc* blocks, con
 }
 
 // residual_general of the device phi, Field3 fp64 output
-template <typename T>
+// residual_general or, with SYM, residual_symmetric
+// (Listing PAPER.md:503-518): the W / S / B couplings are
+// read as the E / N / T coefficients of the W / S / B neighbour cell (5
+// coefficient arrays instead of 8); at the block's first interior cell the
+// neighbour is the ghost cell, whose AE (AN, AT) equals this cell's AW (AS,
+// AB) by the symmetry invariant, so AW (AS, AB) is read there.
+template <typename T, bool SYM>
 __global__ void k_residual(const BlockDesc* blocks, int b, const T* __restrict__ fw,
                            const T* __restrict__ phi, const T* __restrict__ ghost, double* out) {
   const BlockDesc bd = blocks[b];
@@ -1159,16 +1165,45 @@ __global__ void k_residual(const BlockDesc* blocks, int b, const T* __restrict__
       return phi[pack_index(bd, 1, 0, ii, jj, kk)];
     };
     auto A = [&](int arr) -> T { return fw[pack_index(bd, F_NA, arr, i, j, k)]; };
+    T aw, as, ab;
+    if (SYM) {
+      aw = i > 0 ? fw[pack_index(bd, F_NA, F_AE, i - 1, j, k)] : A(F_AW);
+      as = j > 0 ? fw[pack_index(bd, F_NA, F_AN, i, j - 1, k)] : A(F_AS);
+      ab = k > 0 ? fw[pack_index(bd, F_NA, F_AT, i, j, k - 1)] : A(F_AB);
+    } else {
+      aw = A(F_AW);
+      as = A(F_AS);
+      ab = A(F_AB);
+    }
     T v = -(A(F_AE) * ph(i + 1, j, k));
-    v -= A(F_AW) * ph(i - 1, j, k);
+    v -= aw * ph(i - 1, j, k);
     v -= A(F_AN) * ph(i, j + 1, k);
-    v -= A(F_AS) * ph(i, j - 1, k);
+    v -= as * ph(i, j - 1, k);
     v -= A(F_AT) * ph(i, j, k + 1);
-    v -= A(F_AB) * ph(i, j, k - 1);
+    v -= ab * ph(i, j, k - 1);
     v += A(F_Q);
     v -= A(F_AP) * ph(i, j, k);
     out[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(v);
   }
+}
+
+// Symmetry invariant of a StencilSystem on the fp64 pack:
+// AE(i) == AW(i+1), AN(j) == AS(j+1), AT(k) == AB(k+1) exactly; counts violations.
+__global__ void k_check_symmetric(const BlockDesc* blocks, int b, const double* __restrict__ fw,
+                                  unsigned long long* bad) {
+  const BlockDesc bd = blocks[b];
+  const long long n = (long long)bd.nx * bd.ny * bd.nz;
+  unsigned long long cnt = 0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % bd.nx);
+    const long long r = c / bd.nx;
+    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    if (i + 1 < bd.nx && fw[pack_index(bd, F_NA, F_AE, i, j, k)] != fw[pack_index(bd, F_NA, F_AW, i + 1, j, k)]) ++cnt;
+    if (j + 1 < bd.ny && fw[pack_index(bd, F_NA, F_AN, i, j, k)] != fw[pack_index(bd, F_NA, F_AS, i, j + 1, k)]) ++cnt;
+    if (k + 1 < bd.nz && fw[pack_index(bd, F_NA, F_AT, i, j, k)] != fw[pack_index(bd, F_NA, F_AB, i, j, k + 1)]) ++cnt;
+  }
+  if (cnt) atomicAdd(bad, cnt);
 }
 
 __global__ void k_convert(const double* __restrict__ src, float* __restrict__ dst, long long n) {
@@ -1335,9 +1370,17 @@ int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
 template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
                     const T* phi, const T* ghost, int symmetric, double* out, void* stream) {
-  (void)symmetric;
-  k_residual<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
-      d_blocks, block, fw, phi, ghost, out);
+  const int g = grid_for((long long)hb.nx * hb.ny * hb.nz);
+  if (symmetric)
+    k_residual<T, true><<<g, 256, 0, (cudaStream_t)stream>>>(d_blocks, block, fw, phi, ghost, out);
+  else
+    k_residual<T, false><<<g, 256, 0, (cudaStream_t)stream>>>(d_blocks, block, fw, phi, ghost, out);
+  return cuda_status(cudaGetLastError());
+}
+int launch_check_symmetric(const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                           const double* fw, unsigned long long* bad, void* stream) {
+  k_check_symmetric<<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
+      d_blocks, block, fw, bad);
   return cuda_status(cudaGetLastError());
 }
 template <typename T>

@@ -9,6 +9,7 @@ Names, argument meaning and error behaviour follow the specification:
     SolveReport    (SPEC.md:128-131)   -> SolveReport
     sip_factor     (SPEC.md:143-151)   -> sip_factor
     residual_general (SPEC.md:152-160) -> residual_general
+    residual_symmetric (SPEC.md:161-169) -> residual_symmetric
     sip_sweep      (SPEC.md:170-178)   -> sip_sweep
     solve          (SPEC.md:179-187)   -> solve
     errors         (error.hpp:34-50)   -> SingularFactorError, StaleFactorsError, MisuseError
@@ -44,7 +45,8 @@ EXPORTS = (
     "sip_version", "sip_status_string", "sip_last_error", "sip_create", "sip_create_lattice",
     "sip_destroy", "sip_num_local_blocks", "sip_local_block", "sip_set_system", "sip_set_source",
     "sip_generate_system", "sip_factor", "sip_solve", "sip_load_phi", "sip_store_phi",
-    "sip_iterate", "sip_read_norms", "sip_synchronize", "sip_residual", "sip_set_stream",
+    "sip_iterate", "sip_read_norms", "sip_synchronize", "sip_residual", "sip_set_symmetric",
+    "sip_set_stream",
     "sip_get_stream", "sip_set_profiling", "sip_get_profile", "sip_launch_count", "sip_geometry",
     "sip_nccl_unique_id", "sip_generate_host", "sip_plan_block_ranks", "sip_plan_halo",
 )
@@ -240,6 +242,10 @@ class Solver:
         self._c(lib().sip_set_system(self._ctx, local, *[_ptr(a) for a in A.arrays()]),
                 "sip_set_system")
 
+    def set_symmetric(self, local: int, symmetric: bool = True):
+        """Flag the system of a local block symmetric (checked on the device)."""
+        self._c(lib().sip_set_symmetric(self._ctx, local, int(symmetric)), "sip_set_symmetric")
+
     def set_source(self, local: int, q: np.ndarray):
         self._c(lib().sip_set_source(self._ctx, local, _ptr(q)), "sip_set_source")
 
@@ -367,6 +373,19 @@ def residual_general(A: StencilSystem, fi: np.ndarray, device: int = 0) -> np.nd
     s.set_system(0, A)
     s.load_phi([np.ascontiguousarray(fi, dtype=np.float64)])
     return s.residual()[0]
+
+
+def residual_symmetric(A: StencilSystem, fi: np.ndarray, device: int = 0) -> np.ndarray:
+    """SPEC.md:161-169 / Listing 1: the residual reading only ae, an, at
+    (+ shifted), ap and su.  MisuseError unless A is flagged symmetric;
+    ConfigError if the flag contradicts the coefficients."""
+    if not A.symmetric:
+        raise MisuseError("residual_symmetric: system not flagged symmetric")
+    s = Solver(A.dims, "f64", device)
+    s.set_system(0, A)
+    s.set_symmetric(0, True)
+    s.load_phi([np.ascontiguousarray(fi, dtype=np.float64)])
+    return s.residual(symmetric=True)[0]
 
 
 def sip_sweep(A: StencilSystem, F: SipFactors, fi: np.ndarray) -> float:

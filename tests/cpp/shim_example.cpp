@@ -45,6 +45,18 @@ int main(int argc, char** argv) {
     } catch (const bsfv::b200::StaleFactorsError&) {
       std::printf("stale ok\n");
     }
+    // residual_general on the device; residual_symmetric needs A.symmetric
+    Field3 r = bsfv::b200::residual_general(A, fi0);
+    double l1 = 0.0;
+    for (double v : r.d) l1 += v < 0 ? -v : v;
+    std::printf("residual_general l1 %.17g\n", l1);
+    try {
+      bsfv::b200::residual_symmetric(A, fi0);
+      std::printf("ERROR: unflagged system accepted\n");
+      return 1;
+    } catch (const bsfv::b200::MisuseError&) {
+      std::printf("misuse ok\n");
+    }
   } catch (const bsfv::b200::Error& e) {
     std::printf("error: %s\n", e.what());
     return 3;

@@ -36,9 +36,12 @@ def test_shim_solve_matches_oracle(gpu, tmp_path):
     exe = build(tmp_path)
     for prec, flag in (("f64", "d"), ("f32", "s")):
         r = subprocess.run([exe, "12", flag], capture_output=True, text=True, check=True)
-        lines = r.stdout.split()
-        assert lines[-2:] == ["stale", "ok"]
-        norms = np.array([float(x) for x in lines[:-2]])
+        out = r.stdout.splitlines()
+        assert out[-1] == "misuse ok" and out[-3] == "stale ok", out[-3:]
+        norms = np.array([float(x) for x in out[:-3]])
         A = O.generate(0, 1303, (12, 12, 12))
         ref = O.solve(A, O.field(12, 12, 12), 0.92, 5, prec)
         np.testing.assert_allclose(norms, ref, rtol=1e-12)
+        # residual_general (fp64) of phi0 = 0 is su: its L1 is sum |Q|
+        l1 = float(out[-2].split()[-1])
+        np.testing.assert_allclose(l1, np.abs(A["Q"][1:-1, 1:-1, 1:-1]).sum(), rtol=1e-12)

@@ -126,6 +126,51 @@ def test_residual_general_matches_oracle(gpu):
     assert np.array_equal(rg[1:-1, 1:-1, 1:-1], ro[1:-1, 1:-1, 1:-1])
 
 
+def _symmetrize(A):
+    """A_W(i) = A_E(i-1), A_S(j) = A_N(j-1), A_B(k) = A_T(k-1) over the whole
+    Field3 (ghost layers included), so the SPEC.md:117 invariant holds."""
+    S = {n: a.copy() for n, a in A.items()}
+    S["AW"][:, :, 1:] = S["AE"][:, :, :-1]
+    S["AS"][:, 1:, :] = S["AN"][:, :-1, :]
+    S["AB"][1:, :, :] = S["AT"][:-1, :, :]
+    return S
+
+
+@pytest.mark.parametrize("dims", [(19, 17, 13), (40, 33, 20), (1, 5, 4)])
+def test_residual_symmetric_matches_oracle(gpu, dims):
+    """residual_symmetric (Listing 1) on the device, bitwise
+    vs the oracle's Listing-1 restatement and vs residual_general."""
+    A = _symmetrize(O.generate(0, 5, dims))
+    rng = np.random.default_rng(1)
+    fi = rng.uniform(-1, 1, size=(dims[2] + 2, dims[1] + 2, dims[0] + 2))
+    S = sip.StencilSystem.from_dict(A, symmetric=True)
+    rs = sip.residual_symmetric(S, fi)
+    ro = O.residual_symmetric(A, fi)
+    rg = sip.residual_general(S, fi)
+    inner = (slice(1, -1),) * 3
+    assert np.array_equal(rs[inner], ro[inner])
+    assert np.array_equal(rs[inner], rg[inner])
+
+
+def test_residual_symmetric_errors(gpu):
+    dims = (12, 10, 8)
+    A = O.generate(0, 6, dims)
+    fi = O.field(*dims)
+    with pytest.raises(sip.MisuseError):  # not flagged (SPEC.md:165)
+        sip.residual_symmetric(sip.StencilSystem.from_dict(A), fi)
+    with pytest.raises(sip.ConfigError):  # flagged, but the coefficients are not symmetric
+        sip.residual_symmetric(sip.StencilSystem.from_dict(A, symmetric=True), fi)
+    s = sip.Solver(dims, "f64")
+    s.set_system(0, sip.StencilSystem.from_dict(_symmetrize(A)))
+    s.set_symmetric(0, True)
+    s.load_phi([fi])
+    s.residual(symmetric=True)
+    s.set_system(0, sip.StencilSystem.from_dict(_symmetrize(A)))  # new revision clears the flag
+    with pytest.raises(sip.MisuseError):
+        s.residual(symmetric=True)
+    s.close()
+
+
 def test_source_update_reuses_factors(gpu):
     """solve() on the reuse path: new su, same factors."""
     dims = (24, 24, 24)
