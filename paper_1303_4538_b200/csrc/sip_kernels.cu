@@ -539,13 +539,15 @@ struct TagPoll<float> {
 // Consume a poll: spin (re-issue) until the tag matches.
 template <typename T>
 __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long* src, uint32_t tag,
-                                       int where) {
+                                       int where, unsigned long long* stall = nullptr) {
   if (!pl.ok(tag)) {
     Watchdog wd;
+    const unsigned long long t0 = kStepTrace ? gtime() : 0;
     do {
       pl.issue(src);
       wd.idle(where);
     } while (!pl.ok(tag));
+    if (kStepTrace && stall) atomicAdd(stall, (1ull << 40) + (gtime() - t0));  // events, ns
   }
   return pl.value();
 }
@@ -573,6 +575,7 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
   __shared__ __align__(16) T s_prep[kPrep][kTT];  // residual r of prepared steps
   __shared__ double s_red[2 * kTT / 32];
   __shared__ int s_tile, s_last;
+  __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
@@ -589,7 +592,10 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
 
   for (;;) {
     __syncthreads();
-    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    if (p == 0) {
+      s_tile = atomicAdd(P.state, 1u);
+      s_stall = 0;
+    }
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -650,8 +656,8 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
         if (col && k >= 0 && k < nz) {
           const uint32_t tag = edge_tag(epoch, k);
-          const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61) : T(0));
-          const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62) : T(0));
+          const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61, &s_stall) : T(0));
+          const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62, &s_stall) : T(0));
           const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
           RB = Rv;
           s_R[t & 1][q] = Rv;
@@ -813,6 +819,10 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
     }
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
+    if (kStepTrace && P.trace) {
+      __syncthreads();
+      if (p == 0) P.trace[4 * tid + 3] = s_stall;  // (events << 40) + stalled ns
+    }
     const double s = cta_sum(nrm, s_red);
     if (p == 0) {
       P.partial[tid] = s;
@@ -854,6 +864,7 @@ template <typename T>
 __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
   __shared__ __align__(16) T s_D[2][kTT];
   __shared__ int s_tile, s_last;
+  __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
@@ -866,7 +877,10 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
 
   for (;;) {
     __syncthreads();
-    if (p == 0) s_tile = atomicAdd(P.state, 1u);
+    if (p == 0) {
+      s_tile = atomicAdd(P.state, 1u);
+      s_stall = 0;
+    }
     __syncthreads();
     const int tk = s_tile;
     if (tk >= P.ntiles) break;
@@ -936,8 +950,8 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
       const T dNi = s_D[(u - 1) & 1][pN], dEi = s_D[(u - 1) & 1][pE];
       if (col && k >= 0 && k < nz) {
         const uint32_t tag = edge_tag(epoch, k);
-        const T dN = inN ? dNi : (pollN ? poll_take(pn, srcN + (long long)k * 16 * TW, tag, 63) : T(0));
-        const T dE = inE ? dEi : (pollE ? poll_take(pe, srcE + (long long)k * 16 * TW, tag, 64) : T(0));
+        const T dN = inN ? dNi : (pollN ? poll_take(pn, srcN + (long long)k * 16 * TW, tag, 63, &s_stall) : T(0));
+        const T dE = inE ? dEi : (pollE ? poll_take(pe, srcE + (long long)k * 16 * TW, tag, 64, &s_stall) : T(0));
         const T utdt = nb[4] * dT;
         const T dl = ((nb[0] - nb[2] * dN) - nb[3] * dE) - utdt;
         dT = dl;
@@ -963,6 +977,10 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
     if (u < NS) iter(u, pe0, pn0, nb0);
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
+    if (kStepTrace && P.trace) {
+      __syncthreads();
+      if (p == 0) P.trace[4 * tid + 3] = s_stall;  // (events << 40) + stalled ns
+    }
     if (p == 0) {
       __threadfence();
       s_last = (atomicAdd(P.state + 1, 1u) == (unsigned)P.ntiles - 1);
