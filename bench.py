@@ -9,7 +9,8 @@ configuration's grid.  MLUP/s = cells x iterations / time.
 
     python bench.py                      # N=1: config 1 (256^3, fp64 headline + fp32)
     python bench.py --impl reference     # reference arm: CPU SIP (oracle port) on host cores
-    torchrun --nproc-per-node N bench.py --gpus N   # config 3 weak scaling (8 x 128^3 / GPU)
+    torchrun --nproc-per-node N bench.py --gpus N   # weak scaling: one config-1 block per GPU
+    python bench.py --config 3                       # BASELINE config 3 (8 x 128^3 per GPU)
 
 value: device-resident throughput (inputs in HBM, CUDA events on the
 library's launch stream, max over ranks).  e2e: the same metric through the
@@ -50,6 +51,11 @@ CONFIGS = {
             g=None, p=None, kind=0, iters=50, prec=("f64",)),
     4: dict(workload="config4: 1024x512x512 in 128^3 blocks (128 blocks), block-Jacobi SIP",
             g=(1024, 512, 512), p=(8, 4, 4), kind=0, iters=100, prec=("f32",)),
+    # weak scaling of the headline workload: one config-1 block (256^3) per GPU,
+    # GPUs in a block lattice, face halos exchanged every iteration (at N = 1
+    # this is exactly config 1)
+    5: dict(workload="config1xN: one 256^3 block per GPU (GPU lattice), block-Jacobi SIP, face halos",
+            g=None, p=None, kind=0, iters=50, prec=("f64",)),
 }
 GPU_LATTICE = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 
@@ -120,6 +126,9 @@ def cpu_reference(cfg_id: int, seconds: float = 12.0):
     if cfg_id in (3, 4):
         dims = (128, 128, 128)  # one block of the multi-block configs
         sample_desc = "one 128^3 block of the config, fp64 sweeps"
+    elif cfg_id == 5:
+        dims = (256, 256, 256)  # one block (= one GPU's share) of the weak-scaling lattice
+        sample_desc = "one 256^3 block (one GPU's share) of the config"
     else:
         dims = c["g"]
         sample_desc = f"{dims[0]}x{dims[1]}x{dims[2]} block"
@@ -153,6 +162,10 @@ def make_solver(cfg_id, prec, rank, world, device, nccl_id=None):
         lx, ly, lz = GPU_LATTICE.get(world, (world, 1, 1))
         g = (256 * lx, 256 * ly, 256 * lz)
         p = (2 * lx, 2 * ly, 2 * lz)
+    elif cfg_id == 5:
+        lx, ly, lz = GPU_LATTICE.get(world, (world, 1, 1))
+        g = (256 * lx, 256 * ly, 256 * lz)
+        p = (lx, ly, lz)
     else:
         g, p = c["g"], c["p"]
     s = sip.Solver(None, prec, device, lattice=(g, p), rank=rank, nranks=world, nccl_id=nccl_id)
@@ -167,7 +180,7 @@ def run_gpu(args, rank, world, dist):
     import paper_1303_4538_b200 as sip
 
     torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
-    cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+    cfg_id = args.config if args.config is not None else (1 if world == 1 else 5)
     c = CONFIGS[cfg_id]
     # a dedicated (non-default) stream: the library launches on it and the CUDA
     # events below are recorded on it (a NULL handle would mean "library's own
@@ -185,7 +198,7 @@ def run_gpu(args, rank, world, dist):
             nccl_id = obj[0]
         s, g, p = make_solver(cfg_id, prec, rank, world, torch.cuda.current_device(), nccl_id)
         s.set_stream(stream.cuda_stream)
-        seed = 1303 + cfg_id
+        seed = 1303 + (1 if cfg_id == 5 else cfg_id)
         s.generate(c["kind"], seed)
         s.factor(0.92)
         # resident phi0 = 0 for every local block
@@ -352,7 +365,7 @@ def main():
     if args.impl == "reference":
         # reference arm: CPU SIP on host cores, rank 0 only
         if rank == 0:
-            cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+            cfg_id = args.config if args.config is not None else (1 if world == 1 else 5)
             c = CONFIGS[cfg_id]
             vals = []
             base = None
