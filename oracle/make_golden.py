@@ -10,6 +10,11 @@ TEST INFRASTRUCTURE.  Run in the build container (needs /root/reference):
    by oracle/_ref/ref_tables_dump, which is compiled in place from the
    reference sources (oracle/Makefile target `ref`).  These pin the halo plan
    of the B200 library (sip_plan_halo) to the reference's behaviour.
+3. perf_golden.txt -- the reference's own perf module (proj/src/perf.cpp,
+   compiled in place into oracle/_ref/ref_perf_dump) over the scenarios of
+   tests/golden/perf_scenarios.txt (Eq. 1, Eq. 2, threshold points,
+   iso-efficiency, shortest round-trip formatting, error messages); pins
+   include/bsfv_perf.hpp byte for byte.
 2. sip_golden.npz -- oracle SIP outputs (norm histories, phi checksums) of
    small seeded systems.  The reference has no SIP code to run, so these are
    regression pins of the restatement (checked against the SPEC known-answer
@@ -90,8 +95,19 @@ def make_sip():
     np.savez(os.path.join(GOLD, "sip_golden.npz"), **res)
 
 
+def make_perf():
+    exe = os.path.join(HERE, "_ref", "ref_perf_dump")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", HERE, "ref"], check=True)
+    with open(os.path.join(GOLD, "perf_scenarios.txt")) as f:
+        out = subprocess.run([exe], stdin=f, capture_output=True, text=True, check=True).stdout
+    with open(os.path.join(GOLD, "perf_golden.txt"), "w") as f:
+        f.write(out)
+
+
 if __name__ == "__main__":
     os.makedirs(GOLD, exist_ok=True)
     make_tables()
     make_sip()
+    make_perf()
     print("golden fixtures written to", GOLD)
