@@ -23,6 +23,8 @@
 //   SIP_ERR_MISUSE -> MisuseError, SIP_ERR_CONFIG -> ConfigError, else Error.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -39,6 +41,8 @@ using ConfigError = ::bsfv::ConfigError;
 using SingularFactorError = ::bsfv::SingularFactorError;
 using StaleFactorsError = ::bsfv::StaleFactorsError;
 using MisuseError = ::bsfv::MisuseError;
+using FormatError = ::bsfv::FormatError;
+using ProtocolError = ::bsfv::ProtocolError;
 #else
 class Error : public std::runtime_error {
  public:
@@ -60,6 +64,19 @@ class MisuseError : public Error {
  public:
   explicit MisuseError(const std::string& w) : Error(w) {}
 };
+class FormatError : public Error {  // error.hpp:22-31: the message carries the offset
+ public:
+  FormatError(const std::string& w, std::size_t offset)
+      : Error(w + " (at byte offset " + std::to_string(offset) + ")"), offset_(offset) {}
+  std::size_t offset() const { return offset_; }
+
+ private:
+  std::size_t offset_;
+};
+class ProtocolError : public Error {
+ public:
+  explicit ProtocolError(const std::string& w) : Error(w) {}
+};
 #endif
 
 inline void check(int status, const sip_ctx* ctx, const char* what) {
@@ -71,6 +88,7 @@ inline void check(int status, const sip_ctx* ctx, const char* what) {
     case SIP_ERR_STALE: throw StaleFactorsError(msg);
     case SIP_ERR_MISUSE: throw MisuseError(msg);
     case SIP_ERR_CONFIG: throw ConfigError(msg);
+    case SIP_ERR_PROTOCOL: throw ProtocolError(::sip_last_error(ctx));
     default: throw Error(msg);
   }
 }
@@ -204,6 +222,67 @@ Field residual_general(const StencilSystemT<Field>& A, const Field& fi, int devi
 template <class Field>
 Field residual_symmetric(const StencilSystemT<Field>& A, const Field& fi, int device = 0) {
   return residual(A, fi, true, device);
+}
+
+/// FTT1 transfer tables (tables.hpp:57-71): one vector of int[12] rows per rank
+/// (dir, kind, face, peer, owner, neighbor, ilo, ihi, jlo, jhi, klo, khi).
+using TableRows = std::vector<std::vector<std::array<int, 12>>>;
+
+inline TableRows read_tables(const std::vector<unsigned char>& image) {
+  int nranks = 0;
+  long long total = 0, off = -1;
+  auto fail = [&](int st) {
+    if (st == SIP_ERR_FORMAT) {
+      // sip_last_error carries " (at byte offset N)"; rebuild the typed error
+      std::string m = ::sip_last_error(nullptr);
+      const auto cut = m.rfind(" (at byte offset ");
+      throw FormatError(cut == std::string::npos ? m : m.substr(0, cut), (std::size_t)off);
+    }
+    check(st, nullptr, "sip_ftt1_read");
+  };
+  int st = ::sip_ftt1_read(image.data(), image.size(), &nranks, nullptr, nullptr, 0, &total, &off);
+  if (st != SIP_OK) fail(st);
+  std::vector<int> counts((std::size_t)std::max(1, nranks)), rows((std::size_t)std::max(1LL, total) * 12);
+  st = ::sip_ftt1_read(image.data(), image.size(), &nranks, counts.data(), rows.data(), total, &total,
+                       &off);
+  if (st != SIP_OK) fail(st);
+  TableRows t((std::size_t)nranks);
+  std::size_t at = 0;
+  for (int r = 0; r < nranks; ++r)
+    for (int k = 0; k < counts[r]; ++k, ++at) {
+      std::array<int, 12> row;
+      for (int f = 0; f < 12; ++f) row[f] = rows[at * 12 + f];
+      t[r].push_back(row);
+    }
+  return t;
+}
+
+inline void flatten_tables(const TableRows& t, std::vector<int>& counts, std::vector<int>& rows) {
+  counts.clear();
+  rows.clear();
+  for (const auto& r : t) {
+    counts.push_back((int)r.size());
+    for (const auto& e : r) rows.insert(rows.end(), e.begin(), e.end());
+  }
+}
+
+inline std::vector<unsigned char> write_tables(const TableRows& t) {
+  std::vector<int> counts, rows;
+  flatten_tables(t, counts, rows);
+  std::size_t len = 0;
+  check(::sip_ftt1_write((int)t.size(), counts.data(), rows.data(), nullptr, 0, &len), nullptr,
+        "sip_ftt1_write");
+  std::vector<unsigned char> out(len);
+  check(::sip_ftt1_write((int)t.size(), counts.data(), rows.data(), out.data(), len, &len), nullptr,
+        "sip_ftt1_write");
+  return out;
+}
+
+/// tables.cpp:185-235: throws ProtocolError on an unmatched / orphan entry.
+inline void validate_matching(const TableRows& t) {
+  std::vector<int> counts, rows;
+  flatten_tables(t, counts, rows);
+  check(::sip_ftt1_validate((int)t.size(), counts.data(), rows.data()), nullptr, "sip_ftt1_validate");
 }
 
 /// sip_sweep: one inner iteration in place, returns the L1 norm.

@@ -51,6 +51,8 @@ extern "C" {
 #define SIP_ERR_CUDA 5     /* Error (device failure)               */
 #define SIP_ERR_NCCL 6     /* Error (collective failure)           */
 #define SIP_ERR_NOMEM 7    /* Error (device allocation)            */
+#define SIP_ERR_FORMAT 8   /* FormatError          error.hpp:22-31 (byte offset) */
+#define SIP_ERR_PROTOCOL 9 /* ProtocolError        error.hpp:53-57 */
 
 /* bsfv::Precision (field.hpp:10): relaxation precision. */
 #define SIP_PREC_DOUBLE 0
@@ -136,6 +138,32 @@ int sip_set_symmetric(sip_ctx* ctx, int local, int symmetric);
  * requires every local system to be flagged (SIP_ERR_MISUSE otherwise,
  * SPEC.md:165). */
 int sip_residual(sip_ctx* ctx, int symmetric, double* const* res);
+
+/* ---- FTT1 transfer tables (proj/include/bsfv/tables.hpp:62-71)
+ * Entry rows are int[12]: dir (0 local, 1 send, 2 recv), kind (0 face,
+ * 1 edge, 2 corner), face (E W N S T B = 0..5), peer rank, owner block,
+ * neighbor block, ilo, ihi, jlo, jhi, klo, khi; the ranks' tables are
+ * concatenated, counts[r] entries for rank r.
+ * sip_ftt1_read parses an in-memory image (tables.cpp:140-183): pass NULL
+ * counts/entries to query *nranks / *total first.  SIP_ERR_FORMAT with the
+ * reference's message (sip_last_error(NULL)) and *err_offset on a defect.
+ * sip_ftt1_write produces the image (buf NULL: size query into *len).
+ * sip_ftt1_validate checks send/recv matching (tables.cpp:185-235):
+ * SIP_ERR_PROTOCOL with the reference's message. */
+int sip_ftt1_read(const void* buf, size_t len, int* nranks, int* counts, int* entries,
+                  long long cap_entries, long long* total, long long* err_offset);
+int sip_ftt1_write(int nranks, const int* counts, const int* entries, void* buf, size_t cap,
+                   size_t* len);
+int sip_ftt1_validate(int nranks, const int* counts, const int* entries);
+
+/* Replace the context's face-halo plan by the face entries of this rank's
+ * table (arbitrary decompositions and periodic wraps, transfers.cpp:15-25):
+ * local entries become device face copies, send/recv entries the per-peer
+ * NCCL pack/unpack lists in table order.  The tables are validated first
+ * (SIP_ERR_PROTOCOL); face entries must cover whole block faces of this
+ * context's lattice (SIP_ERR_CONFIG otherwise).  Edge / corner entries are
+ * ignored: the 7-point stencil reads face ghosts only. */
+int sip_set_halo_tables(sip_ctx* ctx, int nranks, const int* counts, const int* entries);
 
 /* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */
 int sip_set_stream(sip_ctx* ctx, void* stream);

@@ -11,9 +11,10 @@ import ctypes
 import numpy as np
 
 from .sip import (  # noqa: F401
-    ARRAYS, EXPORTS, LIB_PATH, ConfigError, Error, MisuseError, SingularFactorError, SipConfig,
-    SipFactors, Solver, SolveReport, StaleFactorsError, StencilSystem, factorization_count, field,
-    lib, residual_general, residual_symmetric, sip_factor, sip_sweep, solve, version,
+    ARRAYS, EXPORTS, LIB_PATH, ConfigError, Error, FormatError, MisuseError, ProtocolError,
+    SingularFactorError, SipConfig, SipFactors, Solver, SolveReport, StaleFactorsError,
+    StencilSystem, factorization_count, field, ftt1_read, ftt1_validate, ftt1_write, lib,
+    residual_general, residual_symmetric, sip_factor, sip_sweep, solve, version,
 )
 
 

@@ -22,6 +22,9 @@ using namespace sipb;
 
 namespace {
 thread_local std::string g_create_err;
+}  // namespace
+void sipb::set_thread_error(const std::string& err) { g_create_err = err; }
+namespace {
 
 // NCCL is resolved at run time (dlopen), only when a multi-rank lattice is
 // built: a host process that already loaded an NCCL (e.g. torch's bundled
@@ -89,6 +92,9 @@ struct sip_ctx {
   void *edgeW = nullptr, *edgeS = nullptr;
   void* rec_phi = nullptr;  // [total_slices][64] static part of the K2 edge records
   std::vector<char> symmetric;  // per local block: system flagged symmetric
+  // per local block, kernel face order: >= 0 where the installed halo plan
+  // writes that ghost face (store_phi returns those ghosts)
+  std::vector<std::array<int, 6>> plan_ghosts;
   unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
   size_t tag_words = 0;                 // words per buffer
   unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
@@ -167,6 +173,98 @@ static size_t field3_elems(const BlockDesc& b) {
 }
 
 // -------------------------------------------------------------- construction
+// Exchange structures of a face-halo plan (this rank's entries, plan order):
+// local entries -> device face copies, send / recv entries -> per-peer NCCL
+// pack / unpack lists.  Replaces a previously installed plan.
+static int install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
+  const size_t es = ctx->esize;
+  if (ctx->d_local_copies) cudaFree(ctx->d_local_copies);
+  ctx->d_local_copies = nullptr;
+  ctx->local_copies.clear();
+  ctx->local_max_plane = 0;
+  for (Peer& p : ctx->peers) {
+    if (p.d_pack) cudaFree(p.d_pack);
+    if (p.d_unpack) cudaFree(p.d_unpack);
+    if (p.sbuf) cudaFree(p.sbuf);
+    if (p.rbuf) cudaFree(p.rbuf);
+  }
+  ctx->peers.clear();
+  ctx->plan_ghosts.assign(ctx->local.size(), {-1, -1, -1, -1, -1, -1});
+  // bsfv face id (E,W,N,S,T,B) -> kernel face (W,E,S,N,B,T)
+  auto kface = [](int f) { static const int m[6] = {G_E, G_W, G_N, G_S, G_T, G_B}; return m[f]; };
+  auto plane = [&](int gblock, int kf, int& n0, int& n1) {
+    const BlockInfo& bi = ctx->L.blocks[gblock];
+    if (kf <= G_E) { n0 = bi.n[1]; n1 = bi.n[2]; }
+    else if (kf <= G_N) { n0 = bi.n[0]; n1 = bi.n[2]; }
+    else { n0 = bi.n[0]; n1 = bi.n[1]; }
+  };
+  for (const HaloEntry& e : plan) {
+    FaceCopy fc{};
+    if (e.dir == 0) {  // local: owner = src block, face = src plane; dst ghost = opposite
+      fc.src_block = ctx->local_of[e.owner];
+      fc.src_face = kface(e.face);
+      fc.dst_block = ctx->local_of[e.neighbor];
+      fc.dst_face = kface(e.face ^ 1);
+      ctx->plan_ghosts[fc.dst_block][fc.dst_face] = e.owner;
+      plane(e.owner, fc.src_face, fc.n0, fc.n1);
+      ctx->local_copies.push_back(fc);
+      ctx->local_max_plane = std::max(ctx->local_max_plane, fc.n0 * fc.n1);
+      continue;
+    }
+    auto it = std::find_if(ctx->peers.begin(), ctx->peers.end(),
+                           [&](const Peer& p) { return p.rank == e.peer; });
+    if (it == ctx->peers.end()) {
+      ctx->peers.emplace_back();
+      ctx->peers.back().rank = e.peer;
+      it = ctx->peers.end() - 1;
+    }
+    if (e.dir == 1) {  // send: owner = local src block, plane face
+      fc.src_block = ctx->local_of[e.owner];
+      fc.src_face = kface(e.face);
+      fc.dst_block = -1;
+      plane(e.owner, fc.src_face, fc.n0, fc.n1);
+      fc.buf = 0;
+      for (auto& q : it->pack) fc.buf += (long long)q.n0 * q.n1;
+      it->pack.push_back(fc);
+    } else {  // recv: owner = local dst block, face = ghost face
+      fc.src_block = -1;
+      fc.dst_block = ctx->local_of[e.owner];
+      fc.dst_face = kface(e.face);
+      ctx->plan_ghosts[fc.dst_block][fc.dst_face] = e.neighbor;
+      plane(e.owner, fc.dst_face, fc.n0, fc.n1);
+      fc.buf = 0;
+      for (auto& q : it->unpack) fc.buf += (long long)q.n0 * q.n1;
+      it->unpack.push_back(fc);
+    }
+    it->max_plane = std::max(it->max_plane, fc.n0 * fc.n1);
+  }
+  if (!ctx->local_copies.empty()) {
+    CKS(dalloc(ctx, &ctx->d_local_copies, sizeof(FaceCopy) * ctx->local_copies.size()));
+    CK(cudaMemcpy(ctx->d_local_copies, ctx->local_copies.data(),
+                  sizeof(FaceCopy) * ctx->local_copies.size(), cudaMemcpyHostToDevice));
+  }
+  for (Peer& p : ctx->peers) {
+    long long ns = 0, nr = 0;
+    for (auto& q : p.pack) ns += (long long)q.n0 * q.n1;
+    for (auto& q : p.unpack) nr += (long long)q.n0 * q.n1;
+    if (ns != nr) {
+      ctx->err = "halo plan: send/recv volume mismatch with rank " + std::to_string(p.rank);
+      return SIP_ERR_CONFIG;
+    }
+    p.count = ns;
+    CKS(dalloc(ctx, &p.d_pack, sizeof(FaceCopy) * std::max<size_t>(1, p.pack.size())));
+    CKS(dalloc(ctx, &p.d_unpack, sizeof(FaceCopy) * std::max<size_t>(1, p.unpack.size())));
+    if (!p.pack.empty())
+      CK(cudaMemcpy(p.d_pack, p.pack.data(), sizeof(FaceCopy) * p.pack.size(), cudaMemcpyHostToDevice));
+    if (!p.unpack.empty())
+      CK(cudaMemcpy(p.d_unpack, p.unpack.data(), sizeof(FaceCopy) * p.unpack.size(),
+                    cudaMemcpyHostToDevice));
+    CKS(dalloc(ctx, &p.sbuf, (size_t)std::max(1LL, p.count) * es));
+    CKS(dalloc(ctx, &p.rbuf, (size_t)std::max(1LL, p.count) * es));
+  }
+  return SIP_OK;
+}
+
 static int build(sip_ctx* ctx) {
   // local blocks and their tiles
   const int nb = (int)ctx->L.blocks.size();
@@ -292,76 +390,7 @@ static int build(sip_ctx* ctx) {
   // halo plan: faces only, canonical order (transfers.cpp:148-165)
   std::vector<HaloEntry> plan;
   plan_halo(ctx->L, ctx->rank_of, ctx->rank, plan);
-  // bsfv face id (E,W,N,S,T,B) -> kernel face (W,E,S,N,B,T)
-  auto kface = [](int f) { static const int m[6] = {G_E, G_W, G_N, G_S, G_T, G_B}; return m[f]; };
-  auto plane = [&](int gblock, int kf, int& n0, int& n1) {
-    const BlockInfo& bi = ctx->L.blocks[gblock];
-    if (kf <= G_E) { n0 = bi.n[1]; n1 = bi.n[2]; }
-    else if (kf <= G_N) { n0 = bi.n[0]; n1 = bi.n[2]; }
-    else { n0 = bi.n[0]; n1 = bi.n[1]; }
-  };
-  for (const HaloEntry& e : plan) {
-    FaceCopy fc{};
-    if (e.dir == 0) {  // local: owner = src block, face = src plane; dst ghost = opposite
-      fc.src_block = ctx->local_of[e.owner];
-      fc.src_face = kface(e.face);
-      fc.dst_block = ctx->local_of[e.neighbor];
-      fc.dst_face = kface(e.face ^ 1);
-      plane(e.owner, fc.src_face, fc.n0, fc.n1);
-      ctx->local_copies.push_back(fc);
-      ctx->local_max_plane = std::max(ctx->local_max_plane, fc.n0 * fc.n1);
-      continue;
-    }
-    auto it = std::find_if(ctx->peers.begin(), ctx->peers.end(),
-                           [&](const Peer& p) { return p.rank == e.peer; });
-    if (it == ctx->peers.end()) {
-      ctx->peers.emplace_back();
-      ctx->peers.back().rank = e.peer;
-      it = ctx->peers.end() - 1;
-    }
-    if (e.dir == 1) {  // send: owner = local src block, plane face
-      fc.src_block = ctx->local_of[e.owner];
-      fc.src_face = kface(e.face);
-      fc.dst_block = -1;
-      plane(e.owner, fc.src_face, fc.n0, fc.n1);
-      fc.buf = 0;
-      for (auto& q : it->pack) fc.buf += (long long)q.n0 * q.n1;
-      it->pack.push_back(fc);
-    } else {  // recv: owner = local dst block, face = ghost face
-      fc.src_block = -1;
-      fc.dst_block = ctx->local_of[e.owner];
-      fc.dst_face = kface(e.face);
-      plane(e.owner, fc.dst_face, fc.n0, fc.n1);
-      fc.buf = 0;
-      for (auto& q : it->unpack) fc.buf += (long long)q.n0 * q.n1;
-      it->unpack.push_back(fc);
-    }
-    it->max_plane = std::max(it->max_plane, fc.n0 * fc.n1);
-  }
-  if (!ctx->local_copies.empty()) {
-    CKS(dalloc(ctx, &ctx->d_local_copies, sizeof(FaceCopy) * ctx->local_copies.size()));
-    CK(cudaMemcpy(ctx->d_local_copies, ctx->local_copies.data(),
-                  sizeof(FaceCopy) * ctx->local_copies.size(), cudaMemcpyHostToDevice));
-  }
-  for (Peer& p : ctx->peers) {
-    long long ns = 0, nr = 0;
-    for (auto& q : p.pack) ns += (long long)q.n0 * q.n1;
-    for (auto& q : p.unpack) nr += (long long)q.n0 * q.n1;
-    if (ns != nr) {
-      ctx->err = "halo plan: send/recv volume mismatch with rank " + std::to_string(p.rank);
-      return SIP_ERR_CONFIG;
-    }
-    p.count = ns;
-    CKS(dalloc(ctx, &p.d_pack, sizeof(FaceCopy) * std::max<size_t>(1, p.pack.size())));
-    CKS(dalloc(ctx, &p.d_unpack, sizeof(FaceCopy) * std::max<size_t>(1, p.unpack.size())));
-    if (!p.pack.empty())
-      CK(cudaMemcpy(p.d_pack, p.pack.data(), sizeof(FaceCopy) * p.pack.size(), cudaMemcpyHostToDevice));
-    if (!p.unpack.empty())
-      CK(cudaMemcpy(p.d_unpack, p.unpack.data(), sizeof(FaceCopy) * p.unpack.size(),
-                    cudaMemcpyHostToDevice));
-    CKS(dalloc(ctx, &p.sbuf, (size_t)std::max(1LL, p.count) * es));
-    CKS(dalloc(ctx, &p.rbuf, (size_t)std::max(1LL, p.count) * es));
-  }
+  CKS(install_plan(ctx, plan));
   CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   ctx->stream = ctx->own_stream;
   return SIP_OK;
@@ -589,6 +618,8 @@ const char* sip_status_string(int s) {
     case SIP_ERR_CUDA: return "CUDA error";
     case SIP_ERR_NCCL: return "NCCL error";
     case SIP_ERR_NOMEM: return "device out of memory";
+    case SIP_ERR_FORMAT: return "malformed transfer table";
+    case SIP_ERR_PROTOCOL: return "transfer table protocol violation";
     default: return "unknown status";
   }
 }
@@ -621,7 +652,7 @@ int sip_destroy(sip_ctx* ctx) {
                   ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
                   ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
                   ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace,
-                  ctx->tags, ctx->epochs};
+                  ctx->tags, ctx->epochs, ctx->rec_phi};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->precision == SIP_PREC_SINGLE) {
@@ -856,16 +887,17 @@ int sip_store_phi(sip_ctx* ctx, double* const* phi) {
   CKS(set_device(ctx));
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockDesc& hb = ctx->hblocks[lb];
-    const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
     double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
-    // interior + interface ghosts are overwritten; domain-boundary ghosts,
-    // edges and corners keep the values loaded by sip_load_phi
+    // interior + the ghost faces the halo plan writes (interfaces, periodic
+    // wraps) are overwritten; other ghosts, edges and corners keep the values
+    // loaded by sip_load_phi
+    const int* written = ctx->plan_ghosts[lb].data();
     if (ctx->precision == SIP_PREC_SINGLE)
       CKS(launch_gather<float>(static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost),
-                               ctx->d_blocks, (int)lb, hb, bi.nbr.data(), st, ctx->stream));
+                               ctx->d_blocks, (int)lb, hb, written, st, ctx->stream));
     else
       CKS(launch_gather<double>(static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
-                                ctx->d_blocks, (int)lb, hb, bi.nbr.data(), st, ctx->stream));
+                                ctx->d_blocks, (int)lb, hb, written, st, ctx->stream));
     ++ctx->launches;
     CK(cudaMemcpyAsync(phi[lb], st, field3_elems(hb) * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -978,6 +1010,73 @@ int sip_solve(sip_ctx* ctx, double* const* phi, int max_iters, double target, do
   if (norms_out) CKS(sip_read_norms(ctx, 0, used, norms_out, nullptr));
   CKS(sip_store_phi(ctx, phi));
   if (iters_used) *iters_used = used;
+  return SIP_OK;
+}
+
+int sip_set_halo_tables(sip_ctx* ctx, int nranks, const int* counts, const int* entries) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (nranks != ctx->nranks || (nranks > 0 && (!counts || !entries))) {
+    ctx->err = "sip_set_halo_tables: the table set has " + std::to_string(nranks) +
+               " ranks, the context " + std::to_string(ctx->nranks);
+    return SIP_ERR_CONFIG;
+  }
+  std::vector<std::vector<std::array<int, 12>>> t(nranks);
+  long long at = 0;
+  for (int r = 0; r < nranks; ++r)
+    for (int k = 0; k < counts[r]; ++k, ++at) {
+      std::array<int, 12> row;
+      for (int f = 0; f < 12; ++f) row[f] = entries[at * 12 + f];
+      t[r].push_back(row);
+    }
+  std::string err;
+  if (!ftt1_validate(t, err)) {
+    ctx->err = err;
+    return SIP_ERR_PROTOCOL;
+  }
+  CKS(set_device(ctx));
+  const int nb = (int)ctx->L.blocks.size();
+  std::vector<HaloEntry> plan;
+  for (const auto& row : t[ctx->rank]) {
+    if (row[1] != 0) continue;  // edge / corner patches: not read by the 7-point stencil
+    HaloEntry e{};
+    e.dir = row[0];
+    e.face = row[2];
+    e.peer = row[3];
+    e.owner = row[4];
+    e.neighbor = row[5];
+    for (int a = 0; a < 3; ++a) {
+      e.lo[a] = row[6 + 2 * a];
+      e.hi[a] = row[7 + 2 * a];
+    }
+    auto bad = [&](const std::string& why) {
+      ctx->err = "sip_set_halo_tables: face entry (owner " + std::to_string(e.owner) +
+                 ", neighbor " + std::to_string(e.neighbor) + ", face " + std::to_string(e.face) +
+                 "): " + why;
+      return SIP_ERR_CONFIG;
+    };
+    if (e.owner < 0 || e.owner >= nb || e.neighbor < 0 || e.neighbor >= nb)
+      return bad("block id outside the lattice");
+    if (ctx->rank_of[e.owner] != ctx->rank) return bad("owner block is not on this rank");
+    if (e.dir == 0 && ctx->rank_of[e.neighbor] != ctx->rank)
+      return bad("local entry with a remote neighbor block");
+    if (e.dir != 0 && ctx->rank_of[e.neighbor] != e.peer)
+      return bad("peer rank does not own the neighbor block");
+    // the whole face: the plane of the owner block normal to the face axis
+    const BlockInfo& bi = ctx->L.blocks[e.owner];
+    const int axis = e.face / 2;
+    long long plane = 1;
+    for (int a = 0; a < 3; ++a)
+      if (a != axis) plane *= bi.n[a];
+    long long cells = 1;
+    for (int a = 0; a < 3; ++a) cells *= std::max(0, e.hi[a] - e.lo[a] + 1);
+    if (cells != plane) return bad("partial face patches are not supported");
+    const BlockInfo& bn = ctx->L.blocks[e.neighbor];
+    for (int a = 0; a < 3; ++a)
+      if (a != axis && bn.n[a] != bi.n[a]) return bad("non-conforming neighbor face");
+    plan.push_back(e);
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CKS(install_plan(ctx, plan));
   return SIP_OK;
 }
 

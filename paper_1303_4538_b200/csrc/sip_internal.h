@@ -112,6 +112,10 @@ struct HaloEntry {
   int lo[3], hi[3];
 };
 
+// Thread-local error text returned by sip_last_error(NULL) (free functions).
+void set_thread_error(const std::string& err);
+bool ftt1_validate(const std::vector<std::vector<std::array<int, 12>>>& t, std::string& err);
+
 bool build_lattice(int gnx, int gny, int gnz, int px, int py, int pz, Lattice& L, std::string& err);
 bool plan_block_ranks(int px, int py, int pz, int nranks, std::vector<int>& out);
 void plan_halo(const Lattice& L, const std::vector<int>& rank_of, int rank,

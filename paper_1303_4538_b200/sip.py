@@ -36,6 +36,7 @@ LIB_PATH = os.environ.get("SIPB_LIB") or os.path.join(_HERE, "libsip_b200.so")
 
 SIP_OK, SIP_ERR_SINGULAR, SIP_ERR_STALE, SIP_ERR_MISUSE = 0, 1, 2, 3
 SIP_ERR_CONFIG, SIP_ERR_CUDA, SIP_ERR_NCCL, SIP_ERR_NOMEM = 4, 5, 6, 7
+SIP_ERR_FORMAT, SIP_ERR_PROTOCOL = 8, 9
 PREC = {"f64": 0, "double": 0, "f32": 1, "single": 1}
 
 ARRAYS = ("AP", "AW", "AE", "AS", "AN", "AB", "AT", "Q")
@@ -49,6 +50,7 @@ EXPORTS = (
     "sip_set_stream",
     "sip_get_stream", "sip_set_profiling", "sip_get_profile", "sip_launch_count", "sip_geometry",
     "sip_nccl_unique_id", "sip_generate_host", "sip_plan_block_ranks", "sip_plan_halo",
+    "sip_ftt1_read", "sip_ftt1_write", "sip_ftt1_validate", "sip_set_halo_tables",
 )
 
 
@@ -72,8 +74,21 @@ class MisuseError(Error):
     """bsfv::MisuseError (error.hpp:47-50)."""
 
 
+class FormatError(Error):
+    """bsfv::FormatError (error.hpp:22-31): malformed FTT1 file; `offset` = byte offset."""
+
+    def __init__(self, what: str, offset: int = -1):
+        super().__init__(what)
+        self.offset = offset
+
+
+class ProtocolError(Error):
+    """bsfv::ProtocolError (error.hpp:53-57): unmatched transfer-table entries."""
+
+
 _EXC = {SIP_ERR_SINGULAR: SingularFactorError, SIP_ERR_STALE: StaleFactorsError,
-        SIP_ERR_MISUSE: MisuseError, SIP_ERR_CONFIG: ConfigError}
+        SIP_ERR_MISUSE: MisuseError, SIP_ERR_CONFIG: ConfigError, SIP_ERR_FORMAT: FormatError,
+        SIP_ERR_PROTOCOL: ProtocolError}
 
 _lib = None
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -245,6 +260,13 @@ class Solver:
     def set_symmetric(self, local: int, symmetric: bool = True):
         """Flag the system of a local block symmetric (checked on the device)."""
         self._c(lib().sip_set_symmetric(self._ctx, local, int(symmetric)), "sip_set_symmetric")
+
+    def set_halo_tables(self, tables):
+        """Drive the face-halo exchange by an FTT1 table set (ftt1_read output:
+        one (n, 12) int array per rank), e.g. periodic decompositions."""
+        counts, flat = _tables_flat(tables)
+        self._c(lib().sip_set_halo_tables(self._ctx, len(tables), counts, flat),
+                "sip_set_halo_tables")
 
     def set_source(self, local: int, q: np.ndarray):
         self._c(lib().sip_set_source(self._ctx, local, _ptr(q)), "sip_set_source")
@@ -421,3 +443,55 @@ def solve(A: StencilSystem, fi0: np.ndarray, cfg: SipConfig, F: Optional[SipFact
 
 def version() -> str:
     return lib().sip_version().decode()
+
+
+# ----------------------------------------------------------------- FTT1 tables
+def _tables_flat(tables):
+    counts = (ctypes.c_int * max(1, len(tables)))(*[len(t) for t in tables])
+    rows = [np.asarray(t, dtype=np.int32).reshape(-1, 12) for t in tables]
+    flat = np.ascontiguousarray(np.concatenate(rows) if rows else np.zeros((0, 12), np.int32),
+                                dtype=np.int32)
+    return counts, flat.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+def ftt1_read(data: bytes):
+    """FTT1 image -> per-rank (n, 12) int arrays (tables.cpp:140-183 semantics;
+    FormatError with the reference's message and byte offset)."""
+    buf = ctypes.create_string_buffer(bytes(data), len(data))
+    nranks, total, off = ctypes.c_int(0), ctypes.c_longlong(0), ctypes.c_longlong(-1)
+    st = lib().sip_ftt1_read(buf, ctypes.c_size_t(len(data)), ctypes.byref(nranks), None, None,
+                             ctypes.c_longlong(0), ctypes.byref(total), ctypes.byref(off))
+    if st == SIP_ERR_FORMAT:
+        raise FormatError(lib().sip_last_error(None).decode(), off.value)
+    _check(None, st, "sip_ftt1_read")
+    counts = (ctypes.c_int * max(1, nranks.value))()
+    ent = np.zeros((max(1, total.value), 12), dtype=np.int32)
+    st = lib().sip_ftt1_read(buf, ctypes.c_size_t(len(data)), ctypes.byref(nranks), counts,
+                             ent.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                             ctypes.c_longlong(total.value), ctypes.byref(total), ctypes.byref(off))
+    _check(None, st, "sip_ftt1_read")
+    out, at = [], 0
+    for r in range(nranks.value):
+        out.append(ent[at:at + counts[r]].copy())
+        at += counts[r]
+    return out
+
+
+def ftt1_write(tables) -> bytes:
+    counts, flat = _tables_flat(tables)
+    n = ctypes.c_size_t(0)
+    _check(None, lib().sip_ftt1_write(len(tables), counts, flat, None, ctypes.c_size_t(0),
+                                      ctypes.byref(n)), "sip_ftt1_write")
+    buf = ctypes.create_string_buffer(n.value)
+    _check(None, lib().sip_ftt1_write(len(tables), counts, flat, buf, n, ctypes.byref(n)),
+           "sip_ftt1_write")
+    return buf.raw[: n.value]
+
+
+def ftt1_validate(tables) -> None:
+    """Send/recv matching (tables.cpp:185-235); ProtocolError on a violation."""
+    counts, flat = _tables_flat(tables)
+    st = lib().sip_ftt1_validate(len(tables), counts, flat)
+    if st == SIP_ERR_PROTOCOL:
+        raise ProtocolError(lib().sip_last_error(None).decode())
+    _check(None, st, "sip_ftt1_validate")

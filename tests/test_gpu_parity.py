@@ -282,3 +282,96 @@ def test_config1_full_size_parity(gpu, prec):
     po, no = _run_oracle(A, g, prec, 0.92, 3)
     np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
     assert np.array_equal(pg, po)
+
+
+def _periodic_system(A, d, o, g, mask):
+    """Generator system of one block with the couplings across periodic
+    domain boundaries restored (the generator zeroes every boundary-pointing
+    coefficient) and AP re-balanced: 1.01 * sum |A_nb|."""
+    A = {n: a.copy() for n, a in A.items()}
+    inner = (slice(1, -1),) * 3
+    for axis, (lo_arr, hi_arr) in enumerate((("AW", "AE"), ("AS", "AN"), ("AB", "AT"))):
+        if not (mask >> axis) & 1:
+            continue
+        sl_lo = [slice(1, -1)] * 3
+        sl_hi = [slice(1, -1)] * 3
+        ax = 2 - axis  # Field3 arrays are (k, j, i)
+        sl_lo[ax] = slice(1, 2)
+        sl_hi[ax] = slice(-2, -1)
+        if o[axis] == 0:
+            A[lo_arr][tuple(sl_lo)] = -0.75
+        if o[axis] + d[axis] == g[axis]:
+            A[hi_arr][tuple(sl_hi)] = -0.75
+    s = sum(np.abs(A[n][inner]) for n in ("AW", "AE", "AS", "AN", "AB", "AT"))
+    A["AP"][inner] = 1.01 * s
+    return A
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("name", ["wall_2x2x1_r1", "perx_2x2x1_r1", "perall_1x2x2_r1"])
+def test_table_driven_halo_matches_oracle(gpu, name, prec):
+    """Face halos driven by an FTT1 table written by the reference
+    (tests/golden/ftt1/, periodic wraps included, px = 1 self-wrap in
+    perall_1x2x2): bitwise equal to the block-Jacobi oracle with the same
+    (wrapped) neighbour table."""
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ftt1")
+    f = json.load(open(os.path.join(gold, "cases.json")))["files"][name]
+    g, pd, mask = tuple(f["g"]), tuple(f["p"]), f["periodic_mask"]
+    tables = sip.ftt1_read(open(os.path.join(gold, name + ".ftt1"), "rb").read())
+    origins, dims, nbr = O.lattice(g, pd)
+    px, py, pz = pd
+    wrapped = []
+    for b in range(len(dims)):
+        bx, by, bz = b % px, (b // px) % py, b // (px * py)
+        bid = lambda x, y, z: (x % px) + px * ((y % py) + py * (z % pz))
+        n = list(nbr[b])
+        for axis, (c, p_) in enumerate(((bx, px), (by, py), (bz, pz))):
+            if (mask >> axis) & 1:
+                lo = [bx, by, bz]; hi = [bx, by, bz]
+                lo[axis] -= 1; hi[axis] += 1
+                n[2 * axis], n[2 * axis + 1] = bid(*lo), bid(*hi)
+        wrapped.append(tuple(n))
+    iters = 6
+    s = sip.Solver(None, prec, 0, lattice=(g, pd))
+    As = []
+    for lb, (bid_, d, o) in enumerate(s.blocks):
+        A = _periodic_system(O.generate(0, 1303 + 7 + bid_, d, g, o), d, o, g, mask)
+        As.append(A)
+        s.set_system(lb, sip.StencilSystem.from_dict(A))
+    s.set_halo_tables(tables)
+    s.factor(0.92)
+    phis = [O.field(*d) for (_, d, _) in s.blocks]
+    s.load_phi(phis)
+    s.iterate(iters)
+    s._nglobal = len(dims)
+    ng = s.read_norms(0, iters)
+    s.store_phi(phis)
+    s.close()
+    blocks = [(As[b], O.field(*dims[b])) for b in range(len(dims))]
+    no, _ = O.solve_multi(blocks, wrapped, 0.92, iters, prec)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
+    for b in range(len(dims)):
+        assert np.array_equal(phis[b], blocks[b][1]), f"block {b}"
+
+
+def test_halo_tables_rejects_bad_tables(gpu):
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ftt1")
+    f = json.load(open(os.path.join(gold, "cases.json")))["files"]["wall_2x2x1_r1"]
+    tables = sip.ftt1_read(open(os.path.join(gold, "wall_2x2x1_r1.ftt1"), "rb").read())
+    s = sip.Solver(None, "f64", 0, lattice=(tuple(f["g"]), tuple(f["p"])))
+    bad = [t.copy() for t in tables]
+    bad[0][0, 3] = 1  # a local entry naming another rank
+    with pytest.raises(sip.ProtocolError):
+        s.set_halo_tables(bad)
+    with pytest.raises(sip.ConfigError):  # a 2-rank table set on a 1-rank context
+        s.set_halo_tables(tables + [tables[0][:0]])
+    part = [t.copy() for t in tables]
+    face_rows = np.where(part[0][:, 1] == 0)[0]
+    part[0][face_rows[0], 9] -= 1  # shrink the first face patch
+    with pytest.raises(sip.ConfigError):
+        s.set_halo_tables(part)
+    s.close()
