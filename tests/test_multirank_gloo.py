@@ -32,7 +32,29 @@ def _box(phi, e):
     return (slice(klo, khi + 1), slice(jlo, jhi + 1), slice(ilo, ihi + 1))
 
 
-def _worker(rank, world, port, out):
+def _periodic_system(A, d, o, g, mask):
+    """Restore the couplings across periodic boundaries (as the GPU test)."""
+    A = {n: a.copy() for n, a in A.items()}
+    inner = (slice(1, -1),) * 3
+    for axis, (lo_arr, hi_arr) in enumerate((("AW", "AE"), ("AS", "AN"), ("AB", "AT"))):
+        if not (mask >> axis) & 1:
+            continue
+        sl_lo, sl_hi = [slice(1, -1)] * 3, [slice(1, -1)] * 3
+        sl_lo[2 - axis], sl_hi[2 - axis] = slice(1, 2), slice(-2, -1)
+        if o[axis] == 0:
+            A[lo_arr][tuple(sl_lo)] = -0.75
+        if o[axis] + d[axis] == g[axis]:
+            A[hi_arr][tuple(sl_hi)] = -0.75
+    A["AP"][inner] = 1.01 * sum(np.abs(A[n][inner]) for n in ("AW", "AE", "AS", "AN", "AB", "AT"))
+    return A
+
+
+def _system(O, b, dims, origins, g, mask):
+    A = O.generate(0, 1303 + 3 + b, dims[b], g, origins[b])
+    return _periodic_system(A, dims[b], origins[b], g, mask) if mask else A
+
+
+def _worker(rank, world, port, out, case=None):
     import sys
     sys.path.insert(0, ROOT)
     import paper_1303_4538_b200 as sip
@@ -41,13 +63,23 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    origins, dims, nbr = O.lattice(G, PD)
-    br = sip.plan_block_ranks(PD, world)
+    g, pd, mask = (G, PD, 0) if case is None else (case["g"], case["p"], case["mask"])
+    origins, dims, nbr = O.lattice(g, pd)
+    if case is None:
+        br = sip.plan_block_ranks(pd, world)
+        plan = sip.plan_halo(g, pd, br, rank).tolist()
+    else:  # reference-written FTT1 table: block placement and plan from the file
+        tables = sip.ftt1_read(open(case["file"], "rb").read())
+        br = [0] * len(dims)
+        for r, t in enumerate(tables):
+            for row in t.tolist():
+                if row[0] != 2:
+                    br[row[4]] = r
+        plan = [row for row in tables[rank].tolist() if row[1] == 0]
     mine = [b for b in range(len(dims)) if br[b] == rank]
-    A = {b: O.generate(0, 1303 + 3 + b, dims[b], G, origins[b]) for b in mine}
+    A = {b: _system(O, b, dims, origins, g, mask) for b in mine}
     F = {b: O.factor(A[b], ALPHA) for b in mine}
     phi = {b: O.field(*dims[b]) for b in mine}
-    plan = sip.plan_halo(G, PD, br, rank).tolist()
     peers = sorted({e[3] for e in plan if e[0] != 0})
 
     def exchange():
@@ -99,17 +131,41 @@ def _ghost_box(d, face):
     return (slice(klo, khi + 1), slice(jlo, jhi + 1), slice(ilo, ihi + 1))
 
 
-def test_two_rank_block_jacobi_matches_single_process():
+def _wrap(nbr, pd, mask):
+    px, py, pz = pd
+    out = []
+    for b, n in enumerate(nbr):
+        c = [b % px, (b // px) % py, b // (px * py)]
+        n = list(n)
+        for axis in range(3):
+            if (mask >> axis) & 1:
+                for s, slot in ((-1, 2 * axis), (1, 2 * axis + 1)):
+                    q = list(c)
+                    q[axis] = (q[axis] + s) % pd[axis]
+                    n[slot] = q[0] + px * (q[1] + py * q[2])
+        out.append(tuple(n))
+    return out
+
+
+@pytest.mark.parametrize("source", ["plan_halo", "ftt1_periodic"])
+def test_two_rank_block_jacobi_matches_single_process(source):
     from oracle import oracle as O
     world = 2
+    case = None
+    g, pd, mask = G, PD, 0
+    if source == "ftt1_periodic":  # reference-written table, periodic in x, 2 ranks
+        import json
+        gold = os.path.join(ROOT, "tests", "golden", "ftt1")
+        f = json.load(open(os.path.join(gold, "cases.json")))["files"]["perx_2x2x1_r2"]
+        g, pd, mask = tuple(f["g"]), tuple(f["p"]), f["periodic_mask"]
+        case = {"g": g, "p": pd, "mask": mask, "file": os.path.join(gold, "perx_2x2x1_r2.ftt1")}
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _port(), out), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _port(), out, case), nprocs=world, join=True,
                        start_method="spawn")
-    origins, dims, nbr = O.lattice(G, PD)
-    blocks = [(O.generate(0, 1303 + 3 + b, dims[b], G, origins[b]), O.field(*dims[b]))
-              for b in range(len(dims))]
-    ref_norms, _ = O.solve_multi(blocks, nbr, ALPHA, ITERS, "f64")
+    origins, dims, nbr = O.lattice(g, pd)
+    blocks = [(_system(O, b, dims, origins, g, mask), O.field(*dims[b])) for b in range(len(dims))]
+    ref_norms, _ = O.solve_multi(blocks, _wrap(nbr, pd, mask), ALPHA, ITERS, "f64")
     for r in range(world):
         np.testing.assert_allclose(out[r]["norms"], ref_norms, rtol=1e-14)
         for b, ph in out[r]["phi"].items():
