@@ -536,6 +536,15 @@ struct TagPoll<float> {
   __device__ __forceinline__ bool ok(uint32_t tag) const { return (uint32_t)(w0 >> 32) == tag; }
   __device__ __forceinline__ float value() const { return __uint_as_float((uint32_t)w0); }
 };
+__device__ __forceinline__ void cp_async8(uint32_t dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+__device__ __forceinline__ void async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 // Consume a poll: spin (re-issue) until the tag matches.
 template <typename T>
 __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long* src, uint32_t tag,
@@ -863,6 +872,11 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
 template <typename T>
 __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
   __shared__ __align__(16) T s_D[2][kTT];
+  // fp64: own R, phi, UN, UE, UT of steps u % 4, copied 4 steps ahead with
+  // cp.async (under full load the HBM latency exceeds two tile steps; the
+  // register double buffer of the fp32 path would need 40 more registers)
+  constexpr bool kNbAsync = sizeof(T) == 8;
+  __shared__ __align__(16) T s_nb[kNbAsync ? 4 : 1][5][kTT];
   __shared__ int s_tile, s_last;
   __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
@@ -938,8 +952,29 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
     T nb0[5], nb1[5];  // R, phi, UN, UE, UT of even / odd steps
 #pragma unroll
     for (int a = 0; a < 5; ++a) nb0[a] = nb1[a] = T(0);
-    ldg_into(nb0, 0);
-    ldg_into(nb1, 1);
+    auto acp = [&](int xs) {
+      const int ts = NS - 1 - xs, k2 = ts - d;
+      if (xs < NS && col && k2 >= 0 && k2 < nz) {
+        const T* srcs[5] = {r_cell + (long long)ts * kTT, ph_cell + (long long)ts * kTT,
+                            bw_cell + (long long)ts * B_NA * kTT, bw_cell + (long long)ts * B_NA * kTT + kTT,
+                            bw_cell + (long long)ts * B_NA * kTT + 2 * kTT};
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+          if (sizeof(T) == 8) cp_async8(saddr(&s_nb[xs & 3][a][p]), srcs[a]);
+          else cp_async4(saddr(&s_nb[xs & 3][a][p]), srcs[a]);
+        }
+      }
+      async_commit();
+    };
+    if constexpr (kNbAsync) {
+      acp(0);
+      acp(1);
+      acp(2);
+      acp(3);
+    } else {
+      ldg_into(nb0, 0);
+      ldg_into(nb1, 1);
+    }
     TagPoll<T> pe0, pn0, pe1, pn1;
     poll_issue(pe0, pn0, 0);
     poll_issue(pe1, pn1, 1);
@@ -947,6 +982,11 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
     T dT = T(0);  // own delta of the plane above (0 outside the block)
     auto iter = [&](const int u, TagPoll<T>& pe, TagPoll<T>& pn, T* nb) {
       const int t = NS - 1 - u, k = t - d;
+      if constexpr (kNbAsync) {
+        async_wait<3>();  // this thread's copies of step u (issued 4 iterations ago) landed
+#pragma unroll
+        for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & 3][a][p];
+      }
       const T dNi = s_D[(u - 1) & 1][pN], dEi = s_D[(u - 1) & 1][pE];
       if (col && k >= 0 && k < nz) {
         const uint32_t tag = edge_tag(epoch, k);
@@ -963,7 +1003,10 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
 #endif
       }
       poll_issue(pe, pn, u + 2);
-      ldg_into(nb, u + 2);  // nb consumed above
+      if constexpr (kNbAsync)
+        acp(u + 4);
+      else
+        ldg_into(nb, u + 2);  // nb consumed above
       pf(u + 1 + kPFL);
       if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile - 1))
         P.trace[8 * P.ntiles - 4 * P.ntiles + 16 * u + 2 + (P.trace_tile - tid)] = gtime();  // K3 slots 2, 3
