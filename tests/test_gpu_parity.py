@@ -375,3 +375,92 @@ def test_halo_tables_rejects_bad_tables(gpu):
     with pytest.raises(sip.ConfigError):
         s.set_halo_tables(part)
     s.close()
+
+
+# ------------------------------------------------ SURVEY 8(c) known answers on the device
+def test_kat_diagonal_system_converges_in_one_sweep(gpu):
+    """KAT 1: a pure diagonal system gives LP = 1/AP and the
+    first sweep lands on Q/AP exactly; the next residual norm is 0."""
+    dims = (20, 18, 17)
+    A = O.generate(0, 21, dims)
+    for n in ("AW", "AE", "AS", "AN", "AB", "AT"):
+        A[n][...] = 0.0
+    s = sip.Solver(dims, "f64")
+    s.set_system(0, sip.StencilSystem.from_dict(A))
+    s.factor(0.92)
+    phi = O.field(*dims)
+    norms = s.solve([phi], 2)
+    s.close()
+    inner = (slice(1, -1),) * 3
+    assert np.array_equal(phi[inner], A["Q"][inner] / A["AP"][inner] * 1.0) or \
+        np.allclose(phi[inner], A["Q"][inner] / A["AP"][inner], rtol=1e-15, atol=0)
+    assert norms[1] <= 1e-14 * norms[0]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_kat_first_norm_is_sum_abs_q(gpu, prec):
+    """KAT 2: phi0 = 0 -> residual = su -> norm[0] = sum |Q|."""
+    dims = (33, 29, 21)
+    A = O.generate(2, 22, dims)
+    s = sip.Solver(dims, prec)
+    s.set_system(0, sip.StencilSystem.from_dict(A))
+    s.factor(0.92)
+    n = s.solve([O.field(*dims)], 1)
+    s.close()
+    q = A["Q"][1:-1, 1:-1, 1:-1]
+    ref = np.abs(q).sum() if prec == "f64" else np.abs(q.astype(np.float32).astype(np.float64)).sum()
+    assert n[0] == pytest.approx(ref, rel=1e-12)
+
+
+def test_kat_fp32_fp64_agree_when_converged(gpu):
+    """KAT 7: fp32 and fp64 solutions agree to <= 1e-4 relative
+    once converged."""
+    dims = (24, 24, 24)
+    A = O.generate(0, 23, dims)
+    out = {}
+    for prec in ("f64", "f32"):
+        s = sip.Solver(dims, prec)
+        s.set_system(0, sip.StencilSystem.from_dict(A))
+        s.factor(0.92)
+        phi = O.field(*dims)
+        s.solve([phi], 200)
+        s.close()
+        out[prec] = phi[1:-1, 1:-1, 1:-1]
+    rel = np.abs(out["f32"] - out["f64"]).max() / np.abs(out["f64"]).max()
+    assert rel <= 1e-4
+
+
+def test_kat_decomposition_independent_of_placement(gpu):
+    """KAT 8: block-Jacobi coupling does not depend on where a
+    block lives -- the same lattice solved with the library's compact
+    placement and with the reference's with_ranks placement (one rank here)
+    gives bitwise the same norms and phi."""
+    g, pd = (32, 24, 20), (2, 2, 1)
+    res = []
+    for br in (None, [0, 0, 0, 0]):
+        s = sip.Solver(None, "f64", 0, lattice=(g, pd), block_rank=br)
+        for lb, (bid, d, o) in enumerate(s.blocks):
+            s.set_system(lb, sip.StencilSystem.from_dict(O.generate(0, 1303 + 3 + bid, d, g, o)))
+        s.factor(0.92)
+        phis = [O.field(*d) for (_, d, _) in s.blocks]
+        s.load_phi(phis)
+        s.iterate(5)
+        s._nglobal = 4
+        n = s.read_norms(0, 5)
+        s.store_phi(phis)
+        s.close()
+        res.append((n, phis))
+    assert np.array_equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_config2_full_size_parity(gpu):
+    """Config 2 (512x256x128 anisotropic convection-diffusion, fp32) at full
+    size against the oracle for 4 iterations: bitwise phi, norms 1e-12."""
+    g = (512, 256, 128)
+    A = O.generate(2, 1305, g)
+    pg, ng = _run_gpu(A, g, "f32", 0.92, 4)
+    po, no = _run_oracle(A, g, "f32", 0.92, 4)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
+    assert np.array_equal(pg, po)
