@@ -1,23 +1,25 @@
 // sip_kernels.cu -- sm_100a kernels of the SIP hot path.
 //
 //   K1 k_factor    Stone ILU factor          wavefront, fp64
-//   K2 k_forward   residual + L1 norm + forward substitution   wavefront, bulk-copy ring
-//                  (resforward3d, SPEC.md:155 + SPEC.md:173)
-//   K3 k_backward  backward substitution + phi update          wavefront, bulk-copy ring
+//   K2 k_forward   residual + L1 norm + forward substitution   wavefront, critical /
+//                  (resforward3d, SPEC.md:155 + SPEC.md:173)    residual thread groups
+//   K3 k_backward  backward substitution + phi update          wavefront
 //                  (backward3d)
+//   k_edge_phi     static edge records of K2 (old neighbour phi / ghosts per step)
 //   K4 k_face_copy face-halo copies / pack / unpack (exvec)
 //   K5 k_convert   fp64 -> fp32 (Field3::cast, field.hpp:61-68)
 //   K7 k_scatter / k_gather / k_ghost_in   Field3 <-> tile-slice layout
+//   k_residual     residual_general / residual_symmetric
 //
-// Wavefront scheme: a CTA owns a 16x16-column tile and walks the
-// tile's hyperplanes t = k + ti + tj.  Inside a tile the W/S neighbours of a
-// cell were produced one step earlier by neighbouring threads (double-buffered
-// shared memory, one __syncthreads per step); the B neighbour is the thread's
-// own previous value (register).  Across tiles, values travel through L2 and
-// each tile publishes a monotone progress counter (release/acquire), so there
-// is no grid-wide barrier: upstream tiles run ahead and the hand-off latency
-// becomes pipeline skew.  Tiles are claimed through an atomic ticket in
-// topological order, so the kernel is deadlock-free for any residency.
+// Wavefront scheme: a persistent CTA owns a 16x16-column
+// tile at a time and walks the tile's hyperplanes t = k + ti + tj.  Inside a
+// tile the W/S (forward) or E/N (backward) neighbours of a cell were produced
+// one step earlier by neighbouring threads (shared memory, one barrier per
+// step); the B/T neighbour is the thread's own previous value (register).
+// Across tiles, the edge threads store self-validating tagged words to global
+// memory and the consuming edge threads poll them ahead of use, so there is no
+// grid-wide barrier and no progress counter.  Tiles are claimed through an
+// atomic ticket in topological order: deadlock-free for any residency.
 //
 // Bitwise parity: every cell performs the oracle's operations in the oracle's
 // order (oracle/sip_oracle.c header); this file is compiled with
@@ -35,27 +37,10 @@ namespace sipb {
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          saddr(dst)),
-      "l"(src), "r"(bytes), "r"(saddr(bar))
-      : "memory");
-}
 // Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
 // (__trap -> the launch fails with an error instead of hanging the GPU).
 constexpr unsigned long long kWatchdogNs = 4000000000ULL;
-#define TRCLK() clock64()
+
 // per-step cycle tracing of one tile (tools/trace_steps.py): debug builds only
 #ifdef SIPB_STEP_TRACE
 constexpr bool kStepTrace = true;
@@ -71,29 +56,7 @@ __device__ __noinline__ void watchdog_fire(int where) {
   printf("sip watchdog: block %d thread %d stalled at site %d\n", blockIdx.x, threadIdx.x, where);
   __trap();
 }
-#ifdef SIPB_EXP_SPIN
-#define SIPB_MBAR_WAIT_OP "mbarrier.test_wait.parity.shared::cta.b64"
-#else
-#define SIPB_MBAR_WAIT_OP "mbarrier.try_wait.parity.shared::cta.b64"
-#endif
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int where = 0) {
-  const uint32_t a = saddr(b);
-  uint32_t ok;
-  unsigned long long t0 = 0;
-  int n = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (!ok && ((++n & 255) == 0)) {
-      if (t0 == 0) t0 = gtime();
-      else if (gtime() - t0 > kWatchdogNs) watchdog_fire(where);
-    }
-  } while (!ok);
-}
-// Idle-loop watchdog of the service warps (reset whenever work was done).
+// Idle-loop watchdog of polling loops (reset whenever progress was made).
 struct Watchdog {
   unsigned long long t0 = 0;
   int n = 0;
@@ -112,9 +75,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ double ld_relaxed(const double* p) {
   double v;
@@ -137,39 +97,8 @@ __device__ __forceinline__ void pos_to_tij(int p, int& ti, int& tj) {
 }
 
 // Valid cell range [lo, hi) of slice t in a tile of nz planes, widened to 16 B.
-template <typename T>
-__device__ __forceinline__ void slice_range(int t, int nz, int& lo, int& hi) {
-  constexpr int EPV = 16 / sizeof(T);
-  const int dlo = t - nz + 1 > 0 ? t - nz + 1 : 0;
-  const int dhi = t < kD - 1 ? t : kD - 1;  // inclusive
-  lo = diag_off(dlo) & ~(EPV - 1);
-  hi = (diag_off(dhi + 1) + EPV - 1) & ~(EPV - 1);
-  if (hi > kTT) hi = kTT;
-}
 
 // Copy `na` arrays of one slice (pack stride na*TT) into smem (stride TT).
-template <typename T>
-__device__ __forceinline__ uint32_t issue_slice(T* dst, const T* src, int na, int t, int nz,
-                                                uint64_t* bar, bool arm, uint32_t extra_tx) {
-  int lo, hi;
-  slice_range<T>(t, nz, lo, hi);
-  const uint32_t bytes = static_cast<uint32_t>(na * (hi - lo) * sizeof(T));
-  if (arm) mbar_expect_tx(bar, bytes + extra_tx);
-  if (lo == 0 && hi == kTT) {
-    bulk_g2s(dst, src, bytes, bar);
-  } else {
-    for (int a = 0; a < na; ++a)
-      bulk_g2s(dst + a * kTT + lo, src + a * kTT + lo, static_cast<uint32_t>((hi - lo) * sizeof(T)),
-               bar);
-  }
-  return bytes;
-}
-template <typename T>
-__device__ __forceinline__ uint32_t slice_bytes(int t, int nz, int na) {
-  int lo, hi;
-  slice_range<T>(t, nz, lo, hi);
-  return static_cast<uint32_t>(na * (hi - lo) * sizeof(T));
-}
 
 // Deterministic CTA sum (fixed xor-tree per warp, warps summed in order).
 __device__ __forceinline__ double cta_sum(double v, double* s_red) {
@@ -299,41 +228,6 @@ __global__ void __launch_bounds__(kTT, 1) k_factor(const FactorParams P) {
   }
 }
 
-// =============================================================================
-// K2 / K3 are warp-specialised: 8 compute warps (one thread per tile column)
-// plus two service warps.
-//   loader warp: retires finished steps and refills the slice ring with bulk
-//                copies (cp.async.bulk -> shared, mbarrier complete_tx), and
-//                keeps an L2 prefetch front (cp.async.bulk.prefetch.L2) kPF
-//                slices ahead, so ring refills hit L2 even on the wavefront's
-//                latency-bound critical path.  Shared-memory work only.
-//   linker warp: forwards the tile's outgoing edge values (copied by the
-//                compute warps into a shared out-record) to global memory,
-//                publishes the tile's progress counter (fence.acq_rel.gpu +
-//                relaxed store = release pattern), polls the upstream tiles'
-//                counters and prefetches every cross-tile value a step needs
-//                (neighbour phi / R / delta, ghost phi) into a shared
-//                "edge record".
-// The compute warps never wait on a global-memory latency: per step they wait
-// on shared-memory mbarriers, compute, store, and meet at one named barrier.
-// =============================================================================
-constexpr int kCompute = kTT;       // compute threads (8 warps)
-
-__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-      : "=r"(ok)
-      : "r"(saddr(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void bar_compute() {  // named barrier of the compute warps
-  asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
-}
 // Named barriers of the split forward sweep (id 0 = __syncthreads).
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -341,65 +235,13 @@ __device__ __forceinline__ void nbar_sync(int id, int count) {
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
-// Explicit 32-bit shared-window accesses: keep ring addresses in plain
-// registers (no generic->shared rematerialisation in the step loops).
-template <typename T>
-__device__ __forceinline__ T lds(uint32_t a);
-template <>
-__device__ __forceinline__ double lds<double>(uint32_t a) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
-template <>
-__device__ __forceinline__ float lds<float>(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts(uint32_t a, double v) {
-  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
-}
-__device__ __forceinline__ void sts(uint32_t a, float v) {
-  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
-}
-__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int where) {
-  const unsigned long long t0 = gtime();
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (!ok && gtime() - t0 > kWatchdogNs) watchdog_fire(where);
-  } while (!ok);
-}
-// Fast path: one try_wait; the (rare) retry loop with its watchdog is out of line.
-__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity, int where) {
-  uint32_t ok;
-  asm volatile(
-      "{ .reg .pred p; " SIPB_MBAR_WAIT_OP " p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-      : "=r"(ok)
-      : "r"(a), "r"(parity)
-      : "memory");
-  if (!ok) mbar_wait_slow(a, parity, where);
-}
-// advance a ring address by one slot (wrap-around without division)
-__device__ __forceinline__ uint32_t ring_next(uint32_t a, uint32_t base, uint32_t slot, uint32_t size) {
-  a += slot;
-  return a >= base + size ? a - size : a;
-}
+// L2 prefetch of a contiguous range by the TMA engine (one instruction).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 #ifdef SIPB_EXP_NOPF
   return;
 #endif
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // LSU-side L2 prefetch of one 128-byte line (does not use the TMA engine)
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
 #ifdef SIPB_EXP_NOPF
@@ -407,45 +249,15 @@ __device__ __forceinline__ void prefetch_line_l2(const void* p) {
 #endif
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-constexpr int kPFL = 6;  // steps of LSU L2 prefetch beyond the slice ring
-__device__ __forceinline__ void st_release_cta_s(int* p, int v) {
-  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
-}
+constexpr int kPFL = 6;  // L2 prefetch distance (steps) beyond the loads it covers
 // Progress counter of the publisher (slots of the out-record ring it has
 // read): a relaxed shared store.  A release here (MEMBAR.ALL.CTA) would wait
 // for the publisher's just-issued global edge stores; the only hazard it
 // guards is shared (its reads of out-record slots, whose values its issued
 // stores have already consumed, against the compute warps' later rewrite,
 // ordered through the fetcher's mbarrier arrive and the compute's wait).
-__device__ __forceinline__ void st_progress_s(int* p, int v) {
-  asm volatile("st.relaxed.cta.shared.u32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_relaxed_cta_s(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
 // Spin until *p >= need with cheap relaxed loads, then one CTA fence (the
 // relaxed load that observed the released value + fence = acquire pattern).
-__device__ __forceinline__ void wait_counter(const int* p, int need, int site) {
-  if (ld_relaxed_cta_s(p) < need) {
-    unsigned long long t0 = 0;
-    int n = 0;
-    while (ld_relaxed_cta_s(p) < need) {
-      if ((++n & 255) == 0) {
-        if (t0 == 0) t0 = gtime();
-        else if (gtime() - t0 > kWatchdogNs) watchdog_fire(site);
-      }
-    }
-  }
-  fence_cta();
-}
-__device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr(p)) : "memory");
-  return v;
-}
 
 // ---- tagged edge words: value bits + 32-bit tag, single-copy atomic 64-bit stores
 __device__ __forceinline__ uint32_t edge_tag(unsigned epoch, int k) {
@@ -481,15 +293,8 @@ constexpr int kTagWords = sizeof(T) / 4;  // 64-bit words per tagged value
 // minimum, so all lanes agree on a value each of them has acquired.  Lanes of
 // a warp may execute independently (Volta+ scheduling): decisions taken from
 // memory must be made uniform explicitly.
-__device__ __forceinline__ unsigned poll_progress(const unsigned* p, unsigned cached, unsigned need) {
-  if (cached >= need) return cached;
-  return __reduce_min_sync(0xffffffffu, ld_acquire(p));
-}
 // Warp-collective test of a step-done barrier: complete only if every lane
 // observed completion (each such lane holds its own acquire).
-__device__ __forceinline__ bool warp_test(uint64_t* b, uint32_t parity) {
-  return __all_sync(0xffffffffu, mbar_test(b, parity));
-}
 
 // =============================================================================
 // K2 / K3: one CTA of 256 threads per 16x16-column tile, persistent, tiles
@@ -561,7 +366,6 @@ __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long*
   return pl.value();
 }
 
-constexpr int kRing = 4;  // phi-slice / edge-record ring of K2 (slices t .. t+3 live)
 constexpr int kPrep = 4;  // prepared-step ring between the residual and critical groups
 constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
 constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kPrep;
