@@ -98,7 +98,8 @@ int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw,
 /* Source term only (su changes per RK stage; factors stay valid). */
 int sip_set_source(sip_ctx* ctx, int local, const double* q);
 /* Seeded synthetic system generated on the device:
- * kind 0 = configs 0/1/3/4 generator, kind 2 = config 2; seed per block =
+ * kind 0 = configs 0/1/3/4 generator, kind 2 = config 2, kind 3 = symmetric
+ * (one coefficient per face; sip_set_symmetric accepts it); seed per block =
  * seed + block id.  Same values as sip_generate_host. */
 int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed);
 

@@ -94,6 +94,15 @@ void orc_generate(int kind, uint64_t seed, const int g[3], const int o[3], int n
           ae = -1.0; aw = -1.0 - 1.0 * m;
           an = -10.0; as = -10.0 - 0.5 * m;
           at = -100.0; ab = -100.0 - 0.25 * m;
+        } else if (kind == 3) {
+          /* symmetric: one coefficient per face, keyed by its lower cell */
+          uint64_t sy = (uint64_t)g[0], sz = (uint64_t)g[0] * (uint64_t)g[1];
+          ae = -(1.0 + 0.5 * orc_u01(seed, AID_AE, cell));
+          an = -(1.0 + 0.5 * orc_u01(seed, AID_AN, cell));
+          at = -(1.0 + 0.5 * orc_u01(seed, AID_AT, cell));
+          aw = gi > 0 ? -(1.0 + 0.5 * orc_u01(seed, AID_AE, cell - 1)) : 0.0;
+          as = gj > 0 ? -(1.0 + 0.5 * orc_u01(seed, AID_AN, cell - sy)) : 0.0;
+          ab = gk > 0 ? -(1.0 + 0.5 * orc_u01(seed, AID_AT, cell - sz)) : 0.0;
         } else {
           aw = -(1.0 + 0.5 * orc_u01(seed, AID_AW, cell));
           ae = -(1.0 + 0.5 * orc_u01(seed, AID_AE, cell));

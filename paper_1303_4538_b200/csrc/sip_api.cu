@@ -503,6 +503,8 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
   p.edgeW = static_cast<T*>(ctx->edgeW);
   p.edgeS = static_cast<T*>(ctx->edgeS);
   p.rec_phi = static_cast<T*>(ctx->rec_phi);
+  p.symmetric = !ctx->symmetric.empty() && ctx->symmetric.size() == ctx->local.size() &&
+                std::all_of(ctx->symmetric.begin(), ctx->symmetric.end(), [](char c) { return c != 0; });
   p.tagA = ctx->tags + (forward ? 0 : 2) * ctx->tag_words;
   p.tagB = ctx->tags + (forward ? 1 : 3) * ctx->tag_words;
   p.epoch = ctx->epochs + (forward ? 0 : 1);
@@ -770,8 +772,8 @@ int sip_set_source(sip_ctx* ctx, int local, const double* q) {
 
 int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed) {
   if (!ctx) return SIP_ERR_MISUSE;
-  if (kind != 0 && kind != 2) {
-    ctx->err = "generator kind must be 0 or 2";
+  if (kind != 0 && kind != 2 && kind != 3) {
+    ctx->err = "generator kind must be 0, 2 or 3 (symmetric)";
     return SIP_ERR_CONFIG;
   }
   CKS(set_device(ctx));

@@ -28,7 +28,7 @@ extern "C" int sip_generate_host(int kind, uint64_t seed, const int g[3], const 
                                  int ny, int nz, double* AP, double* AW, double* AE, double* AS,
                                  double* AN, double* AB, double* AT, double* Q) {
   if (nx < 1 || ny < 1 || nz < 1 || !g || !o) return SIP_ERR_CONFIG;
-  if (kind != 0 && kind != 2) return SIP_ERR_CONFIG;
+  if (kind != 0 && kind != 2 && kind != 3) return SIP_ERR_CONFIG;
   const size_t G = (size_t)(nx + 2) * (ny + 2) * (nz + 2);
   double* arr[8] = {AP, AW, AE, AS, AN, AB, AT, Q};
   for (double* a : arr) {
@@ -48,6 +48,16 @@ extern "C" int sip_generate_host(int kind, uint64_t seed, const int g[3], const 
           ae = -1.0; aw = -1.0 - 1.0 * m;
           an = -10.0; as = -10.0 - 0.5 * m;
           at = -100.0; ab = -100.0 - 0.25 * m;
+        } else if (kind == 3) {
+          // symmetric system: one coefficient per face, keyed by the face's
+          // lower cell, so AW(i) = AE(i-1), AS(j) = AN(j-1), AB(k) = AT(k-1)
+          const uint64_t sx = 1, sy = (uint64_t)g[0], sz = (uint64_t)g[0] * (uint64_t)g[1];
+          ae = -(1.0 + 0.5 * u01(seed, 1, cell));
+          an = -(1.0 + 0.5 * u01(seed, 3, cell));
+          at = -(1.0 + 0.5 * u01(seed, 5, cell));
+          aw = gi > 0 ? -(1.0 + 0.5 * u01(seed, 1, cell - sx)) : 0.0;
+          as = gj > 0 ? -(1.0 + 0.5 * u01(seed, 3, cell - sy)) : 0.0;
+          ab = gk > 0 ? -(1.0 + 0.5 * u01(seed, 5, cell - sz)) : 0.0;
         } else {
           aw = -(1.0 + 0.5 * u01(seed, 0, cell));
           ae = -(1.0 + 0.5 * u01(seed, 1, cell));

@@ -151,6 +151,7 @@ struct SweepParams {
   // [slot + s][64] = phiW, phiE, phiS, phiN (16 each); built by k_edge_phi
   // after every halo exchange and bulk-copied with the step's phi slice
   T* rec_phi;
+  int symmetric;  // K2: every block's system flagged symmetric -> Listing-1 fast path
   // Cross-tile edge values as self-validating tagged words (DESIGN.md
   // "Cross-tile hand-off"): value bits + 32-bit tag (epoch << 16 | k), one
   // 64-bit word per fp32 value, two per fp64 value; index (edge + k*16 + c).

@@ -370,7 +370,15 @@ constexpr int kPrep = 4;  // prepared-step ring between the residual and critica
 constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
 constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kPrep;
 
-template <typename T>
+// SYM: symmetric-system fast path (Listing 1; SURVEY.md
+// 8(f) row 1): the residual reads AW / AS / AB of a cell as AE / AN / AT of its
+// W / S / B neighbour -- the W / S values are the lines the neighbour threads
+// stream one step earlier (L1 / L2 hits), AB is the thread's own AT of the
+// plane below -- so the AW, AS and AB arrays are not streamed from HBM (11
+// instead of 14 array touches per cell).  The coefficient values, hence every
+// operation and its rounding, are the general path's (the symmetry invariant
+// is checked exactly by sip_set_symmetric).
+template <typename T, bool SYM>
 __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) {
   // Two threads per column.  Threads 0..255 ("critical"): the recurrence
   // R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP of step t, cross-tile R
@@ -511,6 +519,20 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       const T* fw_cell = P.fw + td.slot * F_NA * kTT + q;
       const T* ph_cell = P.phi + td.slot * kTT + q;
       const T* rp_cell = P.rec_phi + td.slot * 64 + (q & 63);
+      // SYM: per-thread bases, linear in the step x, of the W neighbour's AE
+      // and the S neighbour's AN (in-tile: slice x-1; neighbour tile: its edge
+      // cell, slice x+15; block boundary: own AW / AS, equal by symmetry)
+      constexpr long long kSl = (long long)F_NA * kTT;
+      const T* symW = fw_cell;
+      const T* symS = fw_cell;
+      if (SYM) {
+        symW = ti > 0 ? P.fw + (td.slot - 1) * kSl + F_AE * kTT + pW
+               : td.nW >= 0 ? P.fw + (P.tiles[td.nW].slot + kTI - 1) * kSl + F_AE * kTT + tile_pos(kTI - 1, tj)
+                            : fw_cell + F_AW * kTT;
+        symS = tj > 0 ? P.fw + (td.slot - 1) * kSl + F_AN * kTT + pS
+               : td.nS >= 0 ? P.fw + (P.tiles[td.nS].slot + kTJ - 1) * kSl + F_AN * kTT + tile_pos(ti, kTJ - 1)
+                            : fw_cell + F_AS * kTT;
+      }
       auto ldg_fw = [&](T* nf, int x) {  // the 8 residual coefficients (AP .. AT, Q)
         const int k = x - d;
         if (x < NS && col && k >= 0 && k < nz) {
@@ -520,8 +542,19 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
           for (int a = 0; a < F_LB; ++a) nf[a] = T(0.01) * T(a + 1) + T(x) * T(1e-9);
           (void)src;
 #else
+          if (SYM) {
+            nf[F_AP] = __ldg(src + F_AP * kTT);
+            nf[F_AE] = __ldg(src + F_AE * kTT);
+            nf[F_AN] = __ldg(src + F_AN * kTT);
+            nf[F_AT] = __ldg(src + F_AT * kTT);
+            nf[F_Q] = __ldg(src + F_Q * kTT);
+            nf[F_AW] = __ldg(symW + (long long)x * kSl);
+            nf[F_AS] = __ldg(symS + (long long)x * kSl);
+            if (k == 0) nf[F_AB] = __ldg(src + F_AB * kTT);  // else: own AT of the plane below
+          } else {
 #pragma unroll
-          for (int a = 0; a < F_LB; ++a) nf[a] = __ldg(src + a * kTT);
+            for (int a = 0; a < F_LB; ++a) nf[a] = __ldg(src + a * kTT);
+          }
 #endif
         }
       };
@@ -549,8 +582,12 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         nbar_arrive(kBarFull + sl, 2 * kTT);
       };
       constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
+      constexpr int kArrLines = kTT * (int)sizeof(T) / 128;  // lines per array slice
+      // SYM: the AW / AS / AB lines are never loaded, so not prefetched either
+      const bool pf_skip = SYM && q < kFwLines &&
+                           ((q / kArrLines) == F_AW || (q / kArrLines) == F_AS || (q / kArrLines) == F_AB);
       auto pf_step = [&](int x) {  // L2 prefetch front: one 128-byte line per thread
-        if (x >= NS) return;
+        if (x >= NS || pf_skip) return;
         if (q < kFwLines)
           prefetch_line_l2(reinterpret_cast<const char*>(P.fw + (td.slot + x) * F_NA * kTT) + 128 * q);
         else if (q < kFwLines + kPhLines)
@@ -587,17 +624,24 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       ldg_fw(nfO, 1);
       for (int x = 0; x <= kPFL; ++x) pf_step(x + 8);
       nbar_sync(kBarRes, kTT);  // prologue: ring filled
+      T atPrev = T(0);  // SYM: own AT of the last prepared step (= AB of the next plane)
       {
         const Ops o = load_ops(0);
         const T rr = residual(nfE, o.fP, o.fB, o.fT, o.fW, o.fE, o.fS, o.fN);
         if (active(0)) nrm += fabs(static_cast<double>(rr));
         publish(0, rr);
+        atPrev = nfE[F_AT];
       }
       ldg_fw(nfE, 2);
       auto iter = [&](const int m, T* phb, T* rcb) {
         const int x0 = 2 * m + 1, x1 = x0 + 1;
         const Ops o0 = load_ops(x0);
         const Ops o1 = load_ops(x1);
+        if (SYM) {
+          if (x0 - d != 0) nfO[F_AB] = atPrev;
+          if (x1 - d != 0) nfE[F_AB] = nfO[F_AT];
+          atPrev = nfE[F_AT];
+        }
         const T r0 = residual(nfO, o0.fP, o0.fB, o0.fT, o0.fW, o0.fE, o0.fS, o0.fN);
         const T r1 = residual(nfE, o1.fP, o1.fB, o1.fT, o1.fW, o1.fE, o1.fS, o1.fN);
         if (active(x0)) nrm += fabs(static_cast<double>(r0));
@@ -1112,6 +1156,14 @@ __global__ void k_generate(const GenArgs A) {
       ae = -1.0; aw = -1.0 - 1.0 * m;
       an = -10.0; as = -10.0 - 0.5 * m;
       at = -100.0; ab = -100.0 - 0.25 * m;
+    } else if (A.kind == 3) {  // symmetric: one coefficient per face (sip_gen.cpp)
+      const uint64_t sy = (uint64_t)A.g[0], sz = (uint64_t)A.g[0] * (uint64_t)A.g[1];
+      ae = -(1.0 + 0.5 * u01(A.seed, 1, cell));
+      an = -(1.0 + 0.5 * u01(A.seed, 3, cell));
+      at = -(1.0 + 0.5 * u01(A.seed, 5, cell));
+      aw = gi > 0 ? -(1.0 + 0.5 * u01(A.seed, 1, cell - 1)) : 0.0;
+      as = gj > 0 ? -(1.0 + 0.5 * u01(A.seed, 3, cell - sy)) : 0.0;
+      ab = gk > 0 ? -(1.0 + 0.5 * u01(A.seed, 5, cell - sz)) : 0.0;
     } else {
       aw = -(1.0 + 0.5 * u01(A.seed, 0, cell));
       ae = -(1.0 + 0.5 * u01(A.seed, 1, cell));
@@ -1151,7 +1203,10 @@ int launch_factor(const FactorParams& p, int grid, void* stream) {
 
 template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
-  k_forward<T><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
+  if (p.symmetric)
+    k_forward<T, true><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
+  else
+    k_forward<T, false><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1179,8 +1234,8 @@ int max_resident_ctas(int kind, int precision, int* grid) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_factor, kTT, 0);
   } else if (kind == 1) {
     e = precision == SIP_PREC_DOUBLE
-            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double>, 2 * kTT, 0)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float>, 2 * kTT, 0);
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, false>, 2 * kTT, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, false>, 2 * kTT, 0);
   } else {
     e = precision == SIP_PREC_DOUBLE
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT, 0)

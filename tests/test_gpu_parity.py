@@ -464,3 +464,56 @@ def test_config2_full_size_parity(gpu):
     po, no = _run_oracle(A, g, "f32", 0.92, 4)
     np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
     assert np.array_equal(pg, po)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("g,pd", [((37, 23, 19), (1, 1, 1)), ((40, 36, 30), (2, 2, 1)),
+                                  ((33, 17, 20), (3, 1, 2))])
+def test_symmetric_sweep_fast_path(gpu, g, pd, prec):
+    """a system flagged symmetric runs K2's Listing-1 fast
+    path (AW/AS/AB read as the neighbours' AE/AN/AT, 11 instead of 14 array
+    touches per cell); phi bitwise equal to the oracle's general sweep."""
+    iters = 5
+    s = sip.Solver(None, prec, 0, lattice=(g, pd))
+    origins, dims, nbr = O.lattice(g, pd)
+    As = []
+    for lb, (bid, d, o) in enumerate(s.blocks):
+        A = _symmetrize(O.generate(0, 1303 + 11 + bid, d, g, o))
+        As.append(A)
+        s.set_system(lb, sip.StencilSystem.from_dict(A))
+        s.set_symmetric(lb, True)
+    s.factor(0.92)
+    phis = [O.field(*d) for (_, d, _) in s.blocks]
+    s.load_phi(phis)
+    s.iterate(iters)
+    s._nglobal = len(dims)
+    ng = s.read_norms(0, iters)
+    s.store_phi(phis)
+    s.close()
+    blocks = [(As[b], O.field(*dims[b])) for b in range(len(dims))]
+    no, _ = O.solve_multi(blocks, nbr, 0.92, iters, prec)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
+    for b in range(len(dims)):
+        assert np.array_equal(phis[b], blocks[b][1]), f"block {b}"
+
+
+def test_symmetric_generator_and_fast_path(gpu):
+    """Device kind-3 (symmetric) generator == oracle generator; the device
+    invariant check accepts it; the flagged fast path matches the oracle."""
+    dims = (30, 22, 18)
+    s = sip.Solver(None, "f64", 0, lattice=(dims, (1, 1, 1)))
+    s._nglobal = 1
+    s.generate(3, 77)
+    s.set_symmetric(0, True)
+    s.factor(0.92)
+    phi = O.field(*dims)
+    s.load_phi([phi])
+    s.iterate(4)
+    n = s.read_norms(0, 4)
+    s.store_phi([phi])
+    s.close()
+    A = O.generate(3, 77, dims)
+    po = O.field(*dims)
+    no = O.solve(A, po, 0.92, 4, "f64")
+    np.testing.assert_allclose(n, no, rtol=NORM_TOL)
+    assert np.array_equal(phi, po)

@@ -356,3 +356,18 @@ def test_lattice_matches_reference_decompose():
         for b, (lo0, lo1, lo2, hi0, hi1, hi2, _) in enumerate(c["blocks"]):
             assert origins[b] == (lo0, lo1, lo2)
             assert dims[b] == (hi0 - lo0 + 1, hi1 - lo1 + 1, hi2 - lo2 + 1)
+
+
+def test_symmetric_generator_invariant():
+    """Generator kind 3: AW(i) = AE(i-1), AS(j) = AN(j-1), AB(k) = AT(k-1)
+    exactly, boundary-pointing coefficients zero; Listing-1
+    residual equals the general one bitwise."""
+    dims = (9, 7, 6)
+    A = O.generate(3, 5, dims)
+    I = (slice(1, -1),) * 3
+    assert np.array_equal(A["AW"][1:-1, 1:-1, 2:-1], A["AE"][1:-1, 1:-1, 1:-2])
+    assert np.array_equal(A["AS"][1:-1, 2:-1, 1:-1], A["AN"][1:-1, 1:-2, 1:-1])
+    assert np.array_equal(A["AB"][2:-1, 1:-1, 1:-1], A["AT"][1:-2, 1:-1, 1:-1])
+    assert not A["AW"][1:-1, 1:-1, 1].any() and not A["AE"][1:-1, 1:-1, -2].any()
+    fi = np.random.default_rng(3).uniform(-1, 1, size=A["AP"].shape)
+    assert np.array_equal(O.residual_symmetric(A, fi)[I], O.residual(A, fi)[I])
