@@ -718,8 +718,14 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
 // the E / N neighbour tiles (their W column / S row, tagged).
 // =============================================================================
 template <typename T>
-__global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P) {
+  // threads 0..255: one per tile column, no cross-tile code at all;
+  // warp 8 ("edge warp"): publishes the tile's W column / S row delta one
+  // step after it is computed and polls the E / N neighbours' values three
+  // steps ahead, depositing each step's 32 edge values into s_rec before the
+  // columns need them.  All 288 threads meet at one barrier per step.
   __shared__ __align__(16) T s_D[2][kTT];
+  __shared__ __align__(16) T s_rec[2][32];  // [step & 1]: dE (c < 16), dN (16 + c)
   // fp64: own R, phi, UN, UE, UT of steps u % 4, copied 4 steps ahead with
   // cp.async (under full load the HBM latency exceeds two tile steps; the
   // register double buffer of the fp32 path would need 40 more registers)
@@ -730,8 +736,10 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
   constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
-  int ti, tj;
-  pos_to_tij(p, ti, tj);
+  const bool edge_warp = p >= kTT;
+  const int lane = p & 31;
+  int ti = 0, tj = 0;
+  if (!edge_warp) pos_to_tij(p, ti, tj);
   const int d = ti + tj;
   const int pE = ti < kTI - 1 ? tile_pos(ti + 1, tj) : p;
   const int pN = tj < kTJ - 1 ? tile_pos(ti, tj + 1) : p;
@@ -756,15 +764,67 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
       P.trace[4 * tid + 2] = smid;
       P.trace[4 * tid + 3] = blockIdx.x;
     }
+    if (edge_warp) {
+      // ------------------------------------------------------------ edge warp
+      // lane c < 16: E side (poll the E tile's W column, cell (15, c) here) and
+      // W side (publish cell (0, c)); lane 16 + c: N side / S side (cells (c, 15), (c, 0))
+      const bool we = lane < 16;
+      const int c = lane & 15;
+      const bool colok = we ? (c < td.wJ) : (c < td.wI);
+      const int nPoll = we ? td.nE : td.nN, nPub = we ? td.nW : td.nS;
+      const bool poll = colok && nPoll >= 0, pub = colok && nPub >= 0;
+      // plane k of the polled cell at step u: k = (NS - 1 - u) - dPoll
+      const int dPoll = we ? (kTI - 1) + c : c + (kTJ - 1), dPub = c;  // d of cells (15,c)/(c,15), (0,c)/(c,0)
+      const unsigned long long* src =
+          (we ? P.tagA : P.tagB) + ((poll ? P.tiles[nPoll].edge : 0) + c) * TW;
+      unsigned long long* dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
+      const int pubPos = we ? tile_pos(0, c) : tile_pos(c, 0);
+      auto k_of = [&](int u, int dd) { return (NS - 1 - u) - dd; };
+      TagPoll<T> q0, q1, q2, q3;  // polls of steps u % 4 (issued three steps ahead)
+      auto issue = [&](TagPoll<T>& q, int u) {
+        const int k = k_of(u, dPoll);
+        if (poll && u < NS && k >= 0 && k < nz) q.issue(src + (long long)k * 16 * TW);
+      };
+      auto deposit = [&](TagPoll<T>& q, int u) {  // value of step u into s_rec[u & 1]
+        const int k = k_of(u, dPoll);
+        T v = T(0);
+        if (poll && u < NS && k >= 0 && k < nz)
+          v = poll_take(q, src + (long long)k * 16 * TW, edge_tag(epoch, k), 64, &s_stall);
+        s_rec[u & 1][lane] = v;
+      };
+      auto publish = [&](int u) {  // delta of step u (still in s_D[u & 1])
+        const int k = k_of(u, dPub);
+        if (pub && u >= 0 && k >= 0 && k < nz)
+          put_tagged(dst + (long long)k * 16 * TW, s_D[u & 1][pubPos], edge_tag(epoch, k));
+      };
+      issue(q0, 0);
+      issue(q1, 1);
+      issue(q2, 2);
+      deposit(q0, 0);
+      issue(q3, 3);
+      __syncthreads();  // prologue barrier: record of step 0 in place
+      // step u: publish u-1, deposit u+1 (polled at step u-2), issue u+4
+      auto estep = [&](int u, TagPoll<T>& qn, TagPoll<T>& qi) {
+        publish(u - 1);
+        deposit(qn, u + 1);
+        issue(qi, u + 4);
+        nbar_sync(1, kTT + 32);
+      };
+      int u = 0;
+      for (; u + 3 < NS; u += 4) {
+        estep(u, q1, q0);
+        estep(u + 1, q2, q1);
+        estep(u + 2, q3, q2);
+        estep(u + 3, q0, q3);
+      }
+      if (u < NS) estep(u, q1, q0);
+      if (u + 1 < NS) estep(u + 1, q2, q1);
+      if (u + 2 < NS) estep(u + 2, q3, q2);
+      publish(NS - 1);
+    } else {
+    // -------------------------------------------------------------- columns
     const bool col = ti < td.wI && tj < td.wJ;
     const bool inE = ti + 1 < td.wI, inN = tj + 1 < td.wJ;
-    // cross-tile delta: poll the E / N neighbour's W column / S row, publish ours
-    const bool pollE = col && ti == kTI - 1 && td.nE >= 0, pollN = col && tj == kTJ - 1 && td.nN >= 0;
-    const bool pubW = col && ti == 0 && td.nW >= 0, pubS = col && tj == 0 && td.nS >= 0;
-    const unsigned long long* srcE = P.tagA + ((pollE ? P.tiles[td.nE].edge : 0) + tj) * TW;
-    const unsigned long long* srcN = P.tagB + ((pollN ? P.tiles[td.nN].edge : 0) + ti) * TW;
-    unsigned long long* dstW = P.tagA + (td.edge + tj) * TW;
-    unsigned long long* dstS = P.tagB + (td.edge + ti) * TW;
     const T* r_cell = P.R + td.slot * kTT + p;
     T* ph_cell = P.phi + td.slot * kTT + p;
     const T* bw_cell = P.bw + td.slot * B_NA * kTT + p;
@@ -781,13 +841,6 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
         nb[3] = __ldg(u3 + kTT);
         nb[4] = __ldg(u3 + 2 * kTT);
 #endif
-      }
-    };
-    auto poll_issue = [&](TagPoll<T>& pe, TagPoll<T>& pn, int u) {
-      const int k = (NS - 1 - u) - d;
-      if (u < NS && k >= 0 && k < nz) {
-        if (pollE) pe.issue(srcE + (long long)k * 16 * TW);
-        if (pollN) pn.issue(srcN + (long long)k * 16 * TW);
       }
     };
     auto pf = [&](int u) {  // three bulk L2 prefetches (R, phi, U slices of step u), thread 0
@@ -823,34 +876,28 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
       ldg_into(nb0, 0);
       ldg_into(nb1, 1);
     }
-    TagPoll<T> pe0, pn0, pe1, pn1;
-    poll_issue(pe0, pn0, 0);
-    poll_issue(pe1, pn1, 1);
     for (int u = 0; u <= kPFL; ++u) pf(u);
+    __syncthreads();  // prologue barrier (edge record of step 0)
     T dT = T(0);  // own delta of the plane above (0 outside the block)
-    auto iter = [&](const int u, TagPoll<T>& pe, TagPoll<T>& pn, T* nb) {
+    auto iter = [&](const int u, T* nb) {
       const int t = NS - 1 - u, k = t - d;
       if constexpr (kNbAsync) {
         async_wait<3>();  // this thread's copies of step u (issued 4 iterations ago) landed
 #pragma unroll
         for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & 3][a][p];
       }
-      const T dNi = s_D[(u - 1) & 1][pN], dEi = s_D[(u - 1) & 1][pE];
+      // in-tile neighbours from the previous step, tile-edge ones from the edge record
+      const T dN = inN ? s_D[(u - 1) & 1][pN] : s_rec[u & 1][16 + ti];
+      const T dE = inE ? s_D[(u - 1) & 1][pE] : s_rec[u & 1][tj];
       if (col && k >= 0 && k < nz) {
-        const uint32_t tag = edge_tag(epoch, k);
-        const T dN = inN ? dNi : (pollN ? poll_take(pn, srcN + (long long)k * 16 * TW, tag, 63, &s_stall) : T(0));
-        const T dE = inE ? dEi : (pollE ? poll_take(pe, srcE + (long long)k * 16 * TW, tag, 64, &s_stall) : T(0));
         const T utdt = nb[4] * dT;
         const T dl = ((nb[0] - nb[2] * dN) - nb[3] * dE) - utdt;
         dT = dl;
         s_D[u & 1][p] = dl;
-        if (pubW) put_tagged(dstW + (long long)k * 16 * TW, dl, tag);
-        if (pubS) put_tagged(dstS + (long long)k * 16 * TW, dl, tag);
 #ifndef SIPB_EXP_NOSTG
         ph_cell[(long long)t * kTT] = nb[1] + dl;
 #endif
       }
-      poll_issue(pe, pn, u + 2);
       if constexpr (kNbAsync)
         acp(u + 4);
       else
@@ -858,14 +905,15 @@ __global__ void __launch_bounds__(kTT, 2) k_backward(const SweepParams<T> P) {
       pf(u + 1 + kPFL);
       if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile - 1))
         P.trace[8 * P.ntiles - 4 * P.ntiles + 16 * u + 2 + (P.trace_tile - tid)] = gtime();  // K3 slots 2, 3
-      __syncthreads();
+      nbar_sync(1, kTT + 32);
     };
     int u = 0;
     for (; u + 1 < NS; u += 2) {
-      iter(u, pe0, pn0, nb0);
-      iter(u + 1, pe1, pn1, nb1);
+      iter(u, nb0);
+      iter(u + 1, nb1);
     }
-    if (u < NS) iter(u, pe0, pn0, nb0);
+    if (u < NS) iter(u, nb0);
+    }  // columns
 
     if (P.trace && p == 0) P.trace[4 * tid + 1] = gtime();
     if (kStepTrace && P.trace) {
@@ -1212,7 +1260,7 @@ int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
 
 template <typename T>
 int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
-  k_backward<T><<<grid, kTT, 0, (cudaStream_t)stream>>>(p);
+  k_backward<T><<<grid, kTT + 32, 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1238,8 +1286,8 @@ int max_resident_ctas(int kind, int precision, int* grid) {
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, false>, 2 * kTT, 0);
   } else {
     e = precision == SIP_PREC_DOUBLE
-            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT, 0)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float>, kTT, 0);
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT + 32, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float>, kTT + 32, 0);
     // one tile per SM: a second co-resident tile halves both tiles' pace
     // (the sweep is step-latency bound) -- measured 4-5% faster at 256^3
     per = per > 0 ? 1 : per;
