@@ -366,6 +366,73 @@ __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long*
   return pl.value();
 }
 
+// Edge warp of K2 / K3: the 32 cross-tile cells of a tile, one lane each.
+// Lane c < 16 polls the upstream neighbour in i (cell d = dPoll of row c) and
+// publishes the own downstream cell of row c; lane 16 + c does the same in j.
+// At step u (between the group barriers of steps u-1 and u) it publishes the
+// value of step u-1 (s_val[(u-1) & 1][pub_pos], written by the tile's
+// columns before barrier u-1) and deposits the polled value of step u+1 into
+// s_rec[(u+1) & 1][lane], which the columns read after barrier u.  Polls are
+// issued kPD - 1 steps before their deposit (ring q[v % kPD]): under full
+// load an L2 round trip to a peer tile's words takes up to ~1 us.  Forward
+// sweeps run plane k = u - d at step u, backward sweeps k = NS - 1 - u - d.
+#ifdef SIPB_EXP_PD
+constexpr int kPD = SIPB_EXP_PD;
+#else
+constexpr int kPD = 8;
+#endif
+template <typename T>
+struct EdgeLane {
+  bool fwd, poll, pub;
+  int d_poll, d_pub, pub_pos, NS, nz, lane;
+  const unsigned long long* src;  // polled words of this lane's upstream cell (plane 0)
+  unsigned long long* dst;        // published words of this lane's downstream cell
+  __device__ __forceinline__ int k_of(int u, int dd) const { return fwd ? u - dd : (NS - 1 - u) - dd; }
+};
+template <typename T>
+__device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_val)[kTT], T (*s_rec)[32],
+                                              unsigned epoch, int bar, int bar_count,
+                                              unsigned long long* stall) {
+  constexpr int TW = kTagWords<T>;
+  TagPoll<T> q[kPD];
+  auto issue = [&](TagPoll<T>& qq, int u) {
+    const int k = e.k_of(u, e.d_poll);
+    if (e.poll && u < e.NS && k >= 0 && k < e.nz) qq.issue(e.src + (long long)k * 16 * TW);
+  };
+  auto deposit = [&](TagPoll<T>& qq, int u) {
+    const int k = e.k_of(u, e.d_poll);
+    T v = T(0);
+    if (e.poll && u < e.NS && k >= 0 && k < e.nz)
+      v = poll_take(qq, e.src + (long long)k * 16 * TW, edge_tag(epoch, k), 64, stall);
+    s_rec[u & 1][e.lane] = v;
+  };
+  auto publish = [&](int u) {
+    const int k = e.k_of(u, e.d_pub);
+    if (e.pub && u >= 0 && k >= 0 && k < e.nz)
+      put_tagged(e.dst + (long long)k * 16 * TW, s_val[u & 1][e.pub_pos], edge_tag(epoch, k));
+  };
+#pragma unroll
+  for (int v = 0; v < kPD; ++v) issue(q[v], v);
+  deposit(q[0], 0);
+  issue(q[0], kPD);
+  nbar_sync(bar, bar_count);  // prologue barrier: record of step 0 in place
+  auto estep = [&](int u, TagPoll<T>& qq) {
+    publish(u - 1);
+    deposit(qq, u + 1);
+    issue(qq, u + 1 + kPD);
+    nbar_sync(bar, bar_count);
+  };
+  int u = 0;
+  for (; u + kPD - 1 < e.NS; u += kPD) {
+#pragma unroll
+    for (int j = 0; j < kPD; ++j) estep(u + j, q[(j + 1) % kPD]);
+  }
+#pragma unroll
+  for (int j = 0; j < kPD - 1; ++j)
+    if (u + j < e.NS) estep(u + j, q[(j + 1) % kPD]);
+  publish(e.NS - 1);
+}
+
 constexpr int kPrep = 4;  // prepared-step ring between the residual and critical groups
 constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
 constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kPrep;
@@ -729,8 +796,13 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
   // fp64: own R, phi, UN, UE, UT of steps u % 4, copied 4 steps ahead with
   // cp.async (under full load the HBM latency exceeds two tile steps; the
   // register double buffer of the fp32 path would need 40 more registers)
-  constexpr bool kNbAsync = sizeof(T) == 8;
-  __shared__ __align__(16) T s_nb[kNbAsync ? 4 : 1][5][kTT];
+  constexpr bool kNbAsync = true;
+#ifdef SIPB_EXP_NBD
+  constexpr int kNbD = sizeof(T) == 8 ? 4 : SIPB_EXP_NBD;
+#else
+  constexpr int kNbD = 4;  // cp.async depth (steps)
+#endif
+  __shared__ __align__(16) T s_nb[kNbAsync ? kNbD : 1][5][kTT];
   __shared__ int s_tile, s_last;
   __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
@@ -766,61 +838,25 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
     }
     if (edge_warp) {
       // ------------------------------------------------------------ edge warp
-      // lane c < 16: E side (poll the E tile's W column, cell (15, c) here) and
-      // W side (publish cell (0, c)); lane 16 + c: N side / S side (cells (c, 15), (c, 0))
+      // lane c < 16: poll the E tile's W column (cell (15, c) here), publish
+      // cell (0, c); lane 16 + c: N tile's S row (cell (c, 15)), publish (c, 0)
+      EdgeLane<T> e;
       const bool we = lane < 16;
       const int c = lane & 15;
       const bool colok = we ? (c < td.wJ) : (c < td.wI);
       const int nPoll = we ? td.nE : td.nN, nPub = we ? td.nW : td.nS;
-      const bool poll = colok && nPoll >= 0, pub = colok && nPub >= 0;
-      // plane k of the polled cell at step u: k = (NS - 1 - u) - dPoll
-      const int dPoll = we ? (kTI - 1) + c : c + (kTJ - 1), dPub = c;  // d of cells (15,c)/(c,15), (0,c)/(c,0)
-      const unsigned long long* src =
-          (we ? P.tagA : P.tagB) + ((poll ? P.tiles[nPoll].edge : 0) + c) * TW;
-      unsigned long long* dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
-      const int pubPos = we ? tile_pos(0, c) : tile_pos(c, 0);
-      auto k_of = [&](int u, int dd) { return (NS - 1 - u) - dd; };
-      TagPoll<T> q0, q1, q2, q3;  // polls of steps u % 4 (issued three steps ahead)
-      auto issue = [&](TagPoll<T>& q, int u) {
-        const int k = k_of(u, dPoll);
-        if (poll && u < NS && k >= 0 && k < nz) q.issue(src + (long long)k * 16 * TW);
-      };
-      auto deposit = [&](TagPoll<T>& q, int u) {  // value of step u into s_rec[u & 1]
-        const int k = k_of(u, dPoll);
-        T v = T(0);
-        if (poll && u < NS && k >= 0 && k < nz)
-          v = poll_take(q, src + (long long)k * 16 * TW, edge_tag(epoch, k), 64, &s_stall);
-        s_rec[u & 1][lane] = v;
-      };
-      auto publish = [&](int u) {  // delta of step u (still in s_D[u & 1])
-        const int k = k_of(u, dPub);
-        if (pub && u >= 0 && k >= 0 && k < nz)
-          put_tagged(dst + (long long)k * 16 * TW, s_D[u & 1][pubPos], edge_tag(epoch, k));
-      };
-      issue(q0, 0);
-      issue(q1, 1);
-      issue(q2, 2);
-      deposit(q0, 0);
-      issue(q3, 3);
-      __syncthreads();  // prologue barrier: record of step 0 in place
-      // step u: publish u-1, deposit u+1 (polled at step u-2), issue u+4
-      auto estep = [&](int u, TagPoll<T>& qn, TagPoll<T>& qi) {
-        publish(u - 1);
-        deposit(qn, u + 1);
-        issue(qi, u + 4);
-        nbar_sync(1, kTT + 32);
-      };
-      int u = 0;
-      for (; u + 3 < NS; u += 4) {
-        estep(u, q1, q0);
-        estep(u + 1, q2, q1);
-        estep(u + 2, q3, q2);
-        estep(u + 3, q0, q3);
-      }
-      if (u < NS) estep(u, q1, q0);
-      if (u + 1 < NS) estep(u + 1, q2, q1);
-      if (u + 2 < NS) estep(u + 2, q3, q2);
-      publish(NS - 1);
+      e.fwd = false;
+      e.poll = colok && nPoll >= 0;
+      e.pub = colok && nPub >= 0;
+      e.d_poll = we ? (kTI - 1) + c : c + (kTJ - 1);
+      e.d_pub = c;
+      e.pub_pos = we ? tile_pos(0, c) : tile_pos(c, 0);
+      e.NS = NS;
+      e.nz = nz;
+      e.lane = lane;
+      e.src = (we ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
+      e.dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
+      edge_warp_run<T>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
     } else {
     // -------------------------------------------------------------- columns
     const bool col = ti < td.wI && tj < td.wJ;
@@ -861,8 +897,8 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
                             bw_cell + (long long)ts * B_NA * kTT + 2 * kTT};
 #pragma unroll
         for (int a = 0; a < 5; ++a) {
-          if (sizeof(T) == 8) cp_async8(saddr(&s_nb[xs & 3][a][p]), srcs[a]);
-          else cp_async4(saddr(&s_nb[xs & 3][a][p]), srcs[a]);
+          if (sizeof(T) == 8) cp_async8(saddr(&s_nb[xs & (kNbD - 1)][a][p]), srcs[a]);
+          else cp_async4(saddr(&s_nb[xs & (kNbD - 1)][a][p]), srcs[a]);
         }
       }
       async_commit();
@@ -871,20 +907,20 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
       acp(0);
       acp(1);
       acp(2);
-      acp(3);
+      for (int x = 3; x < kNbD; ++x) acp(x);
     } else {
       ldg_into(nb0, 0);
       ldg_into(nb1, 1);
     }
-    for (int u = 0; u <= kPFL; ++u) pf(u);
-    __syncthreads();  // prologue barrier (edge record of step 0)
+    for (int u = 0; u < kNbD + 3; ++u) pf(u);
+    nbar_sync(1, kTT + 32);  // prologue barrier (edge record of step 0)
     T dT = T(0);  // own delta of the plane above (0 outside the block)
     auto iter = [&](const int u, T* nb) {
       const int t = NS - 1 - u, k = t - d;
       if constexpr (kNbAsync) {
-        async_wait<3>();  // this thread's copies of step u (issued 4 iterations ago) landed
+        async_wait<kNbD - 1>();  // this thread's copies of step u (issued kNbD iterations ago) landed
 #pragma unroll
-        for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & 3][a][p];
+        for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & (kNbD - 1)][a][p];
       }
       // in-tile neighbours from the previous step, tile-edge ones from the edge record
       const T dN = inN ? s_D[(u - 1) & 1][pN] : s_rec[u & 1][16 + ti];
@@ -899,10 +935,10 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
 #endif
       }
       if constexpr (kNbAsync)
-        acp(u + 4);
+        acp(u + kNbD);
       else
         ldg_into(nb, u + 2);  // nb consumed above
-      pf(u + 1 + kPFL);
+      pf(u + kNbD + 3);  // L2 prefetch three steps beyond the copies
       if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile - 1))
         P.trace[8 * P.ntiles - 4 * P.ntiles + 16 * u + 2 + (P.trace_tile - tid)] = gtime();  // K3 slots 2, 3
       nbar_sync(1, kTT + 32);
@@ -1290,7 +1326,9 @@ int max_resident_ctas(int kind, int precision, int* grid) {
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float>, kTT + 32, 0);
     // one tile per SM: a second co-resident tile halves both tiles' pace
     // (the sweep is step-latency bound) -- measured 4-5% faster at 256^3
+#ifndef SIPB_EXP_K3PER2
     per = per > 0 ? 1 : per;
+#endif
   }
   if (e != cudaSuccess || per < 1) return SIP_ERR_CUDA;
   *grid = per * sms;

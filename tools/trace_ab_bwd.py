@@ -27,3 +27,8 @@ print(f"bwd {prec} {n}^3: A pace median {np.median(dA)*1e3:.0f} mean {dA.mean()*
 v = B[x] - A[x + 15]
 print(f"  A step u+15 -> B step u: median {np.median(v):.2f} us (p10 {np.percentile(v,10):.2f}, p90 {np.percentile(v,90):.2f})")
 print(f"  A step 0 {A[0]:.2f}, A step 15 {A[15]:.2f}, B step 0 {B[0]:.2f}; A end {A[-1]:.1f}, B end {B[-1]:.1f}")
+for nm, dd in (("A", dA), ("B", dB)):
+    q = np.percentile(dd, [50, 75, 90, 95, 99]) * 1e3
+    slow = dd[dd > 0.5]
+    print(f"  {nm} step ns p50/75/90/95/99: {' '.join(f'{v:.0f}' for v in q)}; steps>500ns: {len(slow)} "
+          f"taking {slow.sum():.1f} of {dd.sum():.1f} us")
