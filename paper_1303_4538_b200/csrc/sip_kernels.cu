@@ -96,10 +96,6 @@ __device__ __forceinline__ void pos_to_tij(int p, int& ti, int& tj) {
   tj = d - ti;
 }
 
-// Valid cell range [lo, hi) of slice t in a tile of nz planes, widened to 16 B.
-
-// Copy `na` arrays of one slice (pack stride na*TT) into smem (stride TT).
-
 // Deterministic CTA sum (fixed xor-tree per warp, warps summed in order).
 __device__ __forceinline__ double cta_sum(double v, double* s_red) {
 #pragma unroll
@@ -249,7 +245,11 @@ __device__ __forceinline__ void prefetch_line_l2(const void* p) {
 #endif
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-constexpr int kPFL = 6;  // L2 prefetch distance (steps) beyond the loads it covers
+#ifdef SIPB_EXP_PFL
+constexpr int kPFL = SIPB_EXP_PFL;
+#else
+constexpr int kPFL = 2;  // L2 prefetch distance (steps) beyond the loads it covers
+#endif
 // Progress counter of the publisher (slots of the out-record ring it has
 // read): a relaxed shared store.  A release here (MEMBAR.ALL.CTA) would wait
 // for the publisher's just-issued global edge stores; the only hazard it
@@ -376,11 +376,6 @@ __device__ __forceinline__ T poll_take(TagPoll<T>& pl, const unsigned long long*
 // issued kPD - 1 steps before their deposit (ring q[v % kPD]): under full
 // load an L2 round trip to a peer tile's words takes up to ~1 us.  Forward
 // sweeps run plane k = u - d at step u, backward sweeps k = NS - 1 - u - d.
-#ifdef SIPB_EXP_PD
-constexpr int kPD = SIPB_EXP_PD;
-#else
-constexpr int kPD = 8;
-#endif
 template <typename T>
 struct EdgeLane {
   bool fwd, poll, pub;
@@ -389,7 +384,7 @@ struct EdgeLane {
   unsigned long long* dst;        // published words of this lane's downstream cell
   __device__ __forceinline__ int k_of(int u, int dd) const { return fwd ? u - dd : (NS - 1 - u) - dd; }
 };
-template <typename T>
+template <typename T, int kPD>
 __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_val)[kTT], T (*s_rec)[32],
                                               unsigned epoch, int bar, int bar_count,
                                               unsigned long long* stall) {
@@ -433,6 +428,11 @@ __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_
   publish(e.NS - 1);
 }
 
+#ifdef SIPB_EXP_PD
+constexpr int kPollK3 = SIPB_EXP_PD;
+#else
+constexpr int kPollK3 = 8;  // K3 poll ring (tile step ~0.3 us under load)
+#endif
 constexpr int kPrep = 4;  // prepared-step ring between the residual and critical groups
 constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
 constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kPrep;
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
       e.lane = lane;
       e.src = (we ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
       e.dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
-      edge_warp_run<T>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
+      edge_warp_run<T, kPollK3>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
     } else {
     // -------------------------------------------------------------- columns
     const bool col = ti < td.wI && tj < td.wJ;

@@ -28,3 +28,6 @@ print(f"{prec} {n}^3 tiles {tr[0,:,0].size}: A pace median {np.median(dA)*1e3:.0
 v = B[x] - A[x + 15]
 print(f"  A step s+15 -> B step s: median {np.median(v):.2f} us (p10 {np.percentile(v,10):.2f}, p90 {np.percentile(v,90):.2f})")
 print(f"  A step 0 {A[0]:.2f}, A step 15 {A[15]:.2f}, B step 0 {B[0]:.2f}; A end {A[-1]:.1f}, B end {B[-1]:.1f}")
+for nm, dd in (("A", dA), ("B", dB)):
+    q = np.percentile(dd, [10, 50, 75, 90, 99]) * 1e3
+    print(f"  {nm} step ns p10/50/75/90/99: {' '.join(f'{v:.0f}' for v in q)}")
