@@ -21,6 +21,9 @@
  *   Endpoint::all_reduce   proj/include/bsfv/net.hpp:131  (inside; NCCL)
  *   exchange_nonblocking   SPEC.md:263-271       (inside; device copies + NCCL)
  *   Field3<double>         proj/include/bsfv/field.hpp:21-44  host array layout
+ *   assemble_poisson       SPEC.md:134-142       sip_assemble_poisson
+ *   pressure_correct       SPEC.md:341-349       sip_flow_* / sip_pressure_correct
+ *   build_transfers (periodic wraps) transfers.cpp:15-25  sip_plan_halo_periodic
  *
  * Host arrays use the reference's Field3 layout: (nx+2)*(ny+2)*(nz+2) doubles,
  * index i + (nx+2)*(j + (ny+2)*k), interior 1..n, one ghost layer.  The sign
@@ -53,6 +56,8 @@ extern "C" {
 #define SIP_ERR_NOMEM 7    /* Error (device allocation)            */
 #define SIP_ERR_FORMAT 8   /* FormatError          error.hpp:22-31 (byte offset) */
 #define SIP_ERR_PROTOCOL 9 /* ProtocolError        error.hpp:53-57 */
+#define SIP_ERR_NOCONV 10  /* pressure_correct: outer cap reached above the mass threshold
+                              (non-convergence error carrying the defect norm) */
 
 /* bsfv::Precision (field.hpp:10): relaxation precision. */
 #define SIP_PREC_DOUBLE 0
@@ -208,6 +213,64 @@ int sip_plan_block_ranks(int px, int py, int pz, int nranks, int* block_rank);
  * capacity on input (entries may be NULL to query the count). */
 int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz, const int* block_rank,
                   int rank, int* n_entries, int* entries /* [n][12] */);
+
+/* Same with periodic wraps: bit a of periodic_mask makes axis a (x, y, z)
+ * periodic (GridSpec bc, transfers.cpp:15-25); px = 1 wraps a block onto itself. */
+int sip_plan_halo_periodic(int gnx, int gny, int gnz, int px, int py, int pz,
+                           const int* block_rank, int rank, int periodic_mask, int* n_entries,
+                           int* entries /* [n][12] */);
+
+/* ---- the caller: pressure correction with factor reuse ----
+ * Boundary kinds per domain face, order W,E,S,N,B,T (GridSpec bc). */
+#define SIP_BC_WALL 0
+#define SIP_BC_PERIODIC 1
+#define SIP_BC_SYMMETRY 2
+
+/*
+ * assemble_poisson: the 7-point Laplacian of the pressure
+ * correction on the context's lattice, domain lengths len[3] (cell sizes
+ * h = len / global cells), boundary kinds bc[6].  Coefficients a_nb = face
+ * area / distance (uniform cubes of size h: a_nb = h, AP = 6h), zero through a
+ * wall or symmetry face (homogeneous Neumann, AP reduced accordingly),
+ * coupled across periodic faces; Q = 0.  The system is singular (pure
+ * Neumann / periodic), so global cell (0,0,0) is pinned as an identity row
+ * (AP = 1, A_nb = 0, Q = 0).  Periodic axes install the wrapped
+ * face-halo plan (sip_plan_halo_periodic).  Bumps the system revision: call
+ * sip_factor once; sip_pressure_correct then reuses the factors for every
+ * step (factorization counter = 1).  Periodic faces must come in
+ * opposite pairs (SIP_ERR_CONFIG otherwise).
+ */
+int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]);
+
+/* FlowState: u, v, w, p as fp64 Field3 arrays per local
+ * block, resident on the context's device. */
+typedef struct sip_flow sip_flow;
+#define SIP_FLOW_U 0
+#define SIP_FLOW_V 1
+#define SIP_FLOW_W 2
+#define SIP_FLOW_P 3
+int sip_flow_create(sip_ctx* ctx, sip_flow** out);  /* after sip_assemble_poisson */
+int sip_flow_destroy(sip_flow* flow);
+/* Host Field3 arrays (one per local block, interior used) -> device field. */
+int sip_flow_set(sip_flow* flow, int field, double* const* per_block);
+/* Device field -> host Field3 arrays (interior + face ghosts of the last update). */
+int sip_flow_get(sip_flow* flow, int field, double* const* per_block);
+/* Discrete divergence L1 = sum over cells of |div u| * cell volume (all ranks). */
+int sip_flow_divergence(sip_flow* flow, double* l1);
+/*
+ * pressure_correct: outer loop of
+ *   check  d = L1(div u); stop when d <= threshold
+ *   su     Q = -(V * div u) / dt        (pinned cell: 0)
+ *   solve  p' = 0, `sweeps` SIP iterations on the factored system (no refactor)
+ *   update u -= dt * dp'/dx, v -= dt * dp'/dy, w -= dt * dp'/dz, p += p'
+ * with co-located central differences and face ghosts from the
+ * halo plan (walls: u_n ghost = -u_n, p' ghost = p').  *outer_used = solves
+ * run; div_hist[0..outer_used] = L1 before each check (capacity max_outer+1,
+ * may be NULL).  Returns SIP_ERR_NOCONV with the last defect in div_hist when
+ * max_outer solves leave it above threshold.
+ */
+int sip_pressure_correct(sip_flow* flow, double dt, double threshold, int max_outer, int sweeps,
+                         int* outer_used, double* div_hist);
 
 #ifdef __cplusplus
 }

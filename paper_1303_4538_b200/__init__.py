@@ -11,10 +11,11 @@ import ctypes
 import numpy as np
 
 from .sip import (  # noqa: F401
-    ARRAYS, EXPORTS, LIB_PATH, ConfigError, Error, FormatError, MisuseError, ProtocolError,
-    SingularFactorError, SipConfig, SipFactors, Solver, SolveReport, StaleFactorsError,
-    StencilSystem, factorization_count, field, ftt1_read, ftt1_validate, ftt1_write, lib,
-    residual_general, residual_symmetric, sip_factor, sip_sweep, solve, version,
+    ARRAYS, BC, EXPORTS, LIB_PATH, ConfigError, Error, Flow, FormatError, MisuseError,
+    NonConvergenceError, ProtocolError, SingularFactorError, SipConfig, SipFactors, Solver,
+    SolveReport, StaleFactorsError, StencilSystem, assemble_poisson, factorization_count, field,
+    ftt1_read, ftt1_validate, ftt1_write, lib, pressure_correct, residual_general,
+    residual_symmetric, sip_factor, sip_sweep, solve, version,
 )
 
 
@@ -42,16 +43,17 @@ def plan_block_ranks(p, nranks: int):
     return list(out)
 
 
-def plan_halo(g, p, block_rank, rank: int):
+def plan_halo(g, p, block_rank, rank: int, periodic_mask: int = 0):
     """Face-halo entries of one rank: rows of (dir, kind, face, peer, owner,
-    neighbor, ilo, ihi, jlo, jhi, klo, khi) as in the reference's FTT1 entry."""
+    neighbor, ilo, ihi, jlo, jhi, klo, khi) as in the reference's FTT1 entry;
+    bit a of periodic_mask wraps axis a (transfers.cpp:15-25)."""
     n = ctypes.c_int(0)
     br = None if block_rank is None else (ctypes.c_int * len(block_rank))(*block_rank)
-    st = lib().sip_plan_halo(*g, *p, br, rank, ctypes.byref(n), None)
+    st = lib().sip_plan_halo_periodic(*g, *p, br, rank, periodic_mask, ctypes.byref(n), None)
     if st != 0:
         raise ConfigError("sip_plan_halo failed")
     buf = (ctypes.c_int * (12 * max(n.value, 1)))()
-    st = lib().sip_plan_halo(*g, *p, br, rank, ctypes.byref(n), buf)
+    st = lib().sip_plan_halo_periodic(*g, *p, br, rank, periodic_mask, ctypes.byref(n), buf)
     if st != 0:
         raise ConfigError("sip_plan_halo failed")
     return np.array(buf[: 12 * n.value], dtype=np.int64).reshape(n.value, 12)

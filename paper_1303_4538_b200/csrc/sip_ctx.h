@@ -1,0 +1,164 @@
+// sip_ctx.h -- the library context behind the opaque sip_ctx handle and the
+// host helpers shared by the C-ABI translation units (sip_api.cu: system,
+// factor, sweep and halo entry points; sip_flow.cu: the pressure-correction
+// caller).  Host code only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "sip_internal.h"
+
+namespace sipb {
+
+// NCCL is resolved at run time (dlopen), only when a multi-rank lattice is
+// built: a host process that already loaded an NCCL (e.g. torch's bundled
+// libnccl.so.2) shares it, and single-GPU use needs no NCCL at all.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi& nccl();
+
+struct Peer {
+  int rank = -1;
+  std::vector<FaceCopy> pack, unpack;  // plane -> send buffer, recv buffer -> ghost
+  long long count = 0;                 // elements each way
+  FaceCopy* d_pack = nullptr;
+  FaceCopy* d_unpack = nullptr;
+  void* sbuf = nullptr;
+  void* rbuf = nullptr;
+  int max_plane = 0;
+};
+}  // namespace sipb
+
+using namespace sipb;  // internal header: the context is built from sipb types
+
+struct sip_ctx {
+  int device = 0, precision = 0, rank = 0, nranks = 1;
+  size_t esize = 8;
+  Lattice L;
+  std::vector<int> rank_of, local, local_of;
+  std::vector<BlockDesc> hblocks;
+  std::vector<TileDesc> htiles;
+  std::vector<int> order_f, order_b;
+  BlockDesc* d_blocks = nullptr;
+  TileDesc* d_tiles = nullptr;
+  int* d_order_f = nullptr;
+  int* d_order_b = nullptr;
+  void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
+  void *edgeW = nullptr, *edgeS = nullptr;
+  void* rec_phi = nullptr;  // [total_slices][64] static part of the K2 edge records
+  std::vector<char> symmetric;  // per local block: system flagged symmetric
+  // per local block, kernel face order: >= 0 where the installed halo plan
+  // writes that ghost face (store_phi returns those ghosts)
+  std::vector<std::array<int, 6>> plan_ghosts;
+  unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
+  size_t tag_words = 0;                 // words per buffer
+  unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
+  double *fw64 = nullptr, *bw64 = nullptr;  // fp32 mode: fp64 shadow for the factorisation
+  unsigned *st_f = nullptr, *st_b = nullptr, *st_fac = nullptr;
+  double* partial = nullptr;
+  double* d_norms = nullptr;
+  double* d_bnorms = nullptr;
+  int norm_cap = 0, n_done = 0;
+  unsigned long long* d_bad = nullptr;
+  double* staging = nullptr;  // 8 x Gmax doubles (generator needs all 8)
+  size_t gmax = 0;
+  double* phi_stage = nullptr;       // per local block Field3 fp64 mirror of phi (load/store)
+  std::vector<size_t> phi_stage_off;
+  long long total_slices = 0, total_edge = 0, total_ghost = 0;
+  int grid_f = 1, grid_b = 1, grid_fac = 1;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  long long revision = 0, factor_stamp = -1;
+  bool factored = false;
+  double alpha = 0.92;
+  std::vector<FaceCopy> local_copies;
+  FaceCopy* d_local_copies = nullptr;
+  int local_max_plane = 0;
+  std::vector<sipb::Peer> peers;
+  ncclComm_t comm = nullptr;
+  bool prof = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo
+  double t_fwd = 0, t_bwd = 0, t_halo = 0;
+  long long launches = 0, prof_launches = 0;
+  unsigned long long* trace = nullptr;  // debug: per-tile timestamps of the last F/B sweeps
+  int trace_tile = 0;
+  // pressure-correction caller (sip_flow.cu): grid of the assembled Poisson
+  // system, boundary kinds per face (W,E,S,N,B,T) and the pinned cell
+  bool poisson = false;
+  double h[3] = {1.0, 1.0, 1.0};
+  int bc[6] = {0, 0, 0, 0, 0, 0};
+  int pin_local = -1;  // local block holding global cell (0,0,0), or -1
+  std::string err;
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+      return (e_ == cudaErrorMemoryAllocation) ? SIP_ERR_NOMEM : SIP_ERR_CUDA;      \
+    }                                                                               \
+  } while (0)
+#define CKS(call)                        \
+  do {                                   \
+    int s_ = (call);                     \
+    if (s_ != SIP_OK) {                  \
+      if (ctx->err.empty()) ctx->err = #call; \
+      return s_;                         \
+    }                                    \
+  } while (0)
+#define CKN(call)                                                           \
+  do {                                                                      \
+    ncclResult_t r_ = (call);                                               \
+    if (r_ != ncclSuccess) {                                                \
+      ctx->err = std::string(#call) + ": " + nccl().GetErrorString(r_);     \
+      return SIP_ERR_NCCL;                                                  \
+    }                                                                       \
+  } while (0)
+
+
+namespace sipb {
+
+int set_device(sip_ctx* ctx);
+
+template <typename P>
+int dalloc(sip_ctx* ctx, P** p, size_t bytes) {
+  void* v = nullptr;
+  CK(cudaMalloc(&v, bytes ? bytes : 16));
+  CK(cudaMemset(v, 0, bytes ? bytes : 16));
+  *p = static_cast<P*>(v);
+  return SIP_OK;
+}
+
+inline size_t field3_elems(const BlockDesc& b) {
+  return (size_t)(b.nx + 2) * (b.ny + 2) * (b.nz + 2);
+}
+
+// Exchange structures of a face-halo plan (sip_api.cu).
+int install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan);
+// One face-halo exchange of phi (device copies + NCCL), on ctx->stream.
+template <typename T>
+int exchange(sip_ctx* ctx);
+// `iters` SIP iterations (K2, K3, halo) on ctx->stream.
+template <typename T>
+int iterate_t(sip_ctx* ctx, int iters);
+// Factors present and stamped with the current system revision.
+int check_ready(sip_ctx* ctx);
+
+}  // namespace sipb

@@ -1,0 +1,580 @@
+// sip_flow.cu -- the caller of the SIP hot path:
+// assemble_poisson and the pressure-correction outer loop
+// pressure_correct with factor reuse -- the factors of the
+// constant pressure system are computed once (sip_factor) and every step only
+// refreshes the source Q (factorization counter = 1 over 100
+// steps).
+//
+// Flow fields (u, v, w, p) are fp64 Field3 arrays per local block, resident
+// in HBM next to the solver's packs (same per-block offsets as the phi
+// staging mirror).  Every step is a handful of HBM-bound stencil kernels
+// around the SIP iterations: face ghosts of u, v, w (device copies / NCCL,
+// the solver's halo plan incl. periodic wraps), divergence + source scatter,
+// SIP sweeps from p' = 0, p' gather, velocity / pressure update.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "sip_ctx.h"
+
+using namespace sipb;
+
+namespace {
+
+constexpr int kFlowThreads = 256;
+constexpr int kChunk = 8192;  // cells per partial sum of the divergence norm
+
+__device__ __forceinline__ long long f3(int nx, int ny, int i, int j, int k) {
+  return (long long)i + (long long)(nx + 2) * (j + (long long)(ny + 2) * k);
+}
+
+// Field3 index of plane element (a, c) of face `face` of a block, interior
+// layer (ghost = false) or ghost layer (ghost = true); kernel face order.
+__device__ __forceinline__ long long face_index(const BlockDesc& b, int face, bool ghost, int a,
+                                                int c) {
+  const int nx = b.nx, ny = b.ny, nz = b.nz;
+  switch (face) {
+    case G_W: return f3(nx, ny, ghost ? 0 : 1, a + 1, c + 1);
+    case G_E: return f3(nx, ny, ghost ? nx + 1 : nx, a + 1, c + 1);
+    case G_S: return f3(nx, ny, a + 1, ghost ? 0 : 1, c + 1);
+    case G_N: return f3(nx, ny, a + 1, ghost ? ny + 1 : ny, c + 1);
+    case G_B: return f3(nx, ny, a + 1, c + 1, ghost ? 0 : 1);
+    default: return f3(nx, ny, a + 1, c + 1, ghost ? nz + 1 : nz);
+  }
+}
+
+// 7-point Poisson coefficients of one block into Field3 arrays
+// (AP, AW, AE, AS, AN, AB, AT, Q).  cpl[f]: the block face f is coupled to a
+// neighbour (interface or periodic wrap); a domain wall / symmetry face is not.
+__global__ void k_poisson_coeffs(int nx, int ny, int nz, int4 cpl_wesn, int2 cpl_bt, double ax,
+                                 double ay, double az, int pin, double* const* out8) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / ((long long)nx * ny));
+    const long long x = f3(nx, ny, i + 1, j + 1, k + 1);
+    const double w = (i > 0 || cpl_wesn.x) ? ax : 0.0;
+    const double e = (i < nx - 1 || cpl_wesn.y) ? ax : 0.0;
+    const double s = (j > 0 || cpl_wesn.z) ? ay : 0.0;
+    const double nn = (j < ny - 1 || cpl_wesn.w) ? ay : 0.0;
+    const double b = (k > 0 || cpl_bt.x) ? az : 0.0;
+    const double t = (k < nz - 1 || cpl_bt.y) ? az : 0.0;
+    if (pin && c == 0) {  // identity row
+      out8[0][x] = 1.0;
+      for (int a = 1; a < 8; ++a) out8[a][x] = 0.0;
+      continue;
+    }
+    out8[0][x] = ((((w + e) + s) + nn) + b) + t;
+    out8[1][x] = -w;
+    out8[2][x] = -e;
+    out8[3][x] = -s;
+    out8[4][x] = -nn;
+    out8[5][x] = -b;
+    out8[6][x] = -t;
+    out8[7][x] = 0.0;
+  }
+}
+
+struct FieldSet {
+  double* f[3];  // up to three fields with the same block offsets
+  int nf;
+};
+
+// Face copies of a halo plan applied to Field3 fields: interior plane of the
+// source block -> ghost plane of the destination block, or plane -> buffer
+// (pack) / buffer -> ghost plane (unpack).  Buffer layout [field][count].
+__global__ void k_flow_faces(const FaceCopy* copies, const BlockDesc* blocks, const long long* off,
+                             FieldSet fs, const double* buf_in, double* buf_out, long long count) {
+  const FaceCopy fc = copies[blockIdx.y];
+  const int n = fc.n0 * fc.n1;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const int a = x % fc.n0, c = x / fc.n0;
+    for (int q = 0; q < fs.nf; ++q) {
+      double v;
+      if (fc.src_block >= 0)
+        v = fs.f[q][off[fc.src_block] + face_index(blocks[fc.src_block], fc.src_face, false, a, c)];
+      else
+        v = buf_in[q * count + fc.buf + x];
+      if (fc.dst_block >= 0)
+        fs.f[q][off[fc.dst_block] + face_index(blocks[fc.dst_block], fc.dst_face, true, a, c)] = v;
+      else
+        buf_out[q * count + fc.buf + x] = v;
+    }
+  }
+}
+
+// Domain-boundary ghosts of one block: ghost = sign * interior on the faces
+// with wall[f] != 0 (u_n: -1 -> zero normal velocity at the face; p': +1 ->
+// homogeneous Neumann).  sign[q][f] per field.
+__global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double* f2,
+                             int wall_mask, int sign_mask0, int sign_mask1, int sign_mask2) {
+  const int face = blockIdx.y;
+  if (!((wall_mask >> face) & 1)) return;
+  const int n0 = face <= G_E ? b.ny : b.nx;
+  const int n1 = face <= G_N ? b.nz : b.ny;
+  double* fl[3] = {f0, f1, f2};
+  const int sm[3] = {sign_mask0, sign_mask1, sign_mask2};
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n0 * n1; x += gridDim.x * blockDim.x) {
+    const int a = x % n0, c = x / n0;
+    const long long gi = face_index(b, face, true, a, c), ii = face_index(b, face, false, a, c);
+    for (int q = 0; q < nf; ++q) fl[q][gi] = ((sm[q] >> face) & 1) ? -fl[q][ii] : fl[q][ii];
+  }
+}
+
+// Co-located central divergence of one block; Q = -(V * div) / dt into a
+// Field3 staging array (pinned cell: 0) and |div| * V per interior cell.
+__global__ void k_divergence(int nx, int ny, int nz, const double* u, const double* v,
+                             const double* w, double c2x, double c2y, double c2z, double vol,
+                             double dt, int pin, double* q, double* absdiv) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % nx) + 1, j = (int)((c / nx) % ny) + 1,
+              k = (int)(c / ((long long)nx * ny)) + 1;
+    const long long x = f3(nx, ny, i, j, k);
+    const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+    const double dv = ((u[x + sx] - u[x - sx]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
+                      (w[x + sz] - w[x - sz]) / c2z;
+    q[x] = (pin && c == 0) ? 0.0 : -(vol * dv) / dt;
+    absdiv[c] = fabs(dv) * vol;
+  }
+}
+
+// Deterministic partial sums: CTA b sums cells [b*kChunk, (b+1)*kChunk) in a
+// fixed order (strided per thread, then a fixed shuffle / shared tree).
+__global__ void k_chunk_sums(const double* x, long long n, double* partial) {
+  __shared__ double s[kFlowThreads / 32];
+  const long long lo = (long long)blockIdx.x * kChunk;
+  const long long hi = lo + kChunk < n ? lo + kChunk : n;
+  double acc = 0.0;
+  for (long long c = lo + threadIdx.x; c < hi; c += blockDim.x) acc += x[c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kFlowThreads / 32; ++q) t += s[q];
+    partial[blockIdx.x] = t;
+  }
+}
+__global__ void k_sum_in_order(const double* partial, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < n; ++b) t += partial[b];
+    *out = t;
+  }
+}
+
+// u -= dt * dp'/dx (central), v, w likewise; p += p'.
+__global__ void k_correct(int nx, int ny, int nz, double* u, double* v, double* w, double* p,
+                          const double* pp, double c2x, double c2y, double c2z, double dt) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c % nx) + 1, j = (int)((c / nx) % ny) + 1,
+              k = (int)(c / ((long long)nx * ny)) + 1;
+    const long long x = f3(nx, ny, i, j, k);
+    const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+    u[x] = u[x] - dt * ((pp[x + sx] - pp[x - sx]) / c2x);
+    v[x] = v[x] - dt * ((pp[x + sy] - pp[x - sy]) / c2y);
+    w[x] = w[x] - dt * ((pp[x + sz] - pp[x - sz]) / c2z);
+    p[x] = p[x] + pp[x];
+  }
+}
+
+int grid_for(long long n) {
+  const long long g = (n + kFlowThreads - 1) / kFlowThreads;
+  return (int)std::max(1LL, std::min(g, 148LL * 16));
+}
+
+}  // namespace
+
+struct sip_flow {
+  sip_ctx* ctx = nullptr;
+  double* f[4] = {nullptr, nullptr, nullptr, nullptr};  // u, v, w, p
+  long long* d_off = nullptr;    // per local block Field3 offset (= phi_stage_off)
+  double* absdiv = nullptr;      // |div| * V per interior cell of the largest block
+  double* partial = nullptr;     // chunk partials
+  double* d_blocksum = nullptr;  // per local block L1
+  std::vector<int> wall;         // per local block: bit f = domain wall / symmetry face
+  std::vector<std::pair<double*, double*>> pbuf;  // per peer: 3-field send / recv buffers
+  long long max_cells = 0;
+};
+
+namespace {
+
+int flow_err(sip_ctx* ctx, const std::string& e, int code) {
+  ctx->err = e;
+  return code;
+}
+
+// Face ghosts of the fields in `fs` from the context's halo plan (local
+// copies + NCCL send / recv of all fields in one message per peer).
+int flow_exchange(sip_flow* fl, const FieldSet& fs) {
+  sip_ctx* ctx = fl->ctx;
+  const cudaStream_t st = ctx->stream;
+  if (!ctx->local_copies.empty()) {
+    dim3 g((unsigned)std::max(1, std::min(64, (ctx->local_max_plane + kFlowThreads - 1) / kFlowThreads)),
+           (unsigned)ctx->local_copies.size());
+    k_flow_faces<<<g, kFlowThreads, 0, st>>>(ctx->d_local_copies, ctx->d_blocks, fl->d_off, fs,
+                                             nullptr, nullptr, 0);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  }
+  if (!ctx->peers.empty()) {
+    for (size_t pi = 0; pi < ctx->peers.size(); ++pi) {
+      Peer& p = ctx->peers[pi];
+      if (p.pack.empty()) continue;
+      dim3 g((unsigned)std::max(1, std::min(64, (p.max_plane + kFlowThreads - 1) / kFlowThreads)),
+             (unsigned)p.pack.size());
+      k_flow_faces<<<g, kFlowThreads, 0, st>>>(p.d_pack, ctx->d_blocks, fl->d_off, fs, nullptr,
+                                               fl->pbuf[pi].first, p.count);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+    CKN(nccl().GroupStart());
+    for (size_t pi = 0; pi < ctx->peers.size(); ++pi) {
+      Peer& p = ctx->peers[pi];
+      const size_t n = (size_t)p.count * fs.nf;
+      CKN(nccl().Recv(fl->pbuf[pi].second, n, ncclFloat64, p.rank, ctx->comm, st));
+      CKN(nccl().Send(fl->pbuf[pi].first, n, ncclFloat64, p.rank, ctx->comm, st));
+    }
+    CKN(nccl().GroupEnd());
+    for (size_t pi = 0; pi < ctx->peers.size(); ++pi) {
+      Peer& p = ctx->peers[pi];
+      if (p.unpack.empty()) continue;
+      dim3 g((unsigned)std::max(1, std::min(64, (p.max_plane + kFlowThreads - 1) / kFlowThreads)),
+             (unsigned)p.unpack.size());
+      k_flow_faces<<<g, kFlowThreads, 0, st>>>(p.d_unpack, ctx->d_blocks, fl->d_off, fs,
+                                               fl->pbuf[pi].second, nullptr, p.count);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+  }
+  return SIP_OK;
+}
+
+// Domain-wall ghosts of up to three fields of every local block.
+int flow_walls(sip_flow* fl, double* const* fields, int nf, const int* sign_masks) {
+  sip_ctx* ctx = fl->ctx;
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    if (!fl->wall[lb]) continue;
+    const BlockDesc& b = ctx->hblocks[lb];
+    const size_t o = ctx->phi_stage_off[lb];
+    const int plane = std::max(b.nx, b.ny) * std::max(b.ny, b.nz);
+    dim3 g((unsigned)std::max(1, std::min(64, (plane + kFlowThreads - 1) / kFlowThreads)), 6);
+    k_flow_walls<<<g, kFlowThreads, 0, ctx->stream>>>(
+        b, nf, fields[0] + o, nf > 1 ? fields[1] + o : nullptr,
+        nf > 2 ? fields[2] + o : nullptr, fl->wall[lb], sign_masks[0], nf > 1 ? sign_masks[1] : 0,
+        nf > 2 ? sign_masks[2] : 0);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  }
+  return SIP_OK;
+}
+
+// Sum of per-block values over all ranks in global block order (the fixed
+// order makes the result independent of the block placement).
+int allsum_blocks(sip_ctx* ctx, const std::vector<double>& local_vals, double* out) {
+  const int nb = (int)ctx->L.blocks.size();
+  std::vector<double> all(nb, 0.0);
+  if (ctx->nranks == 1) {
+    for (size_t lb = 0; lb < ctx->local.size(); ++lb) all[ctx->local[lb]] = local_vals[lb];
+  } else {
+    std::vector<std::vector<int>> blocks_of(ctx->nranks);
+    for (int b = 0; b < nb; ++b) blocks_of[ctx->rank_of[b]].push_back(b);
+    int maxl = 1;
+    for (auto& v : blocks_of) maxl = std::max<int>(maxl, (int)v.size());
+    double *d_send = nullptr, *d_recv = nullptr;
+    CKS(dalloc(ctx, &d_send, sizeof(double) * maxl));
+    CKS(dalloc(ctx, &d_recv, sizeof(double) * maxl * ctx->nranks));
+    std::vector<double> pad(maxl, 0.0);
+    for (size_t lb = 0; lb < ctx->local.size(); ++lb) pad[lb] = local_vals[lb];
+    CK(cudaMemcpyAsync(d_send, pad.data(), sizeof(double) * maxl, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(nccl().AllGather(d_send, d_recv, (size_t)maxl, ncclFloat64, ctx->comm, ctx->stream));
+    std::vector<double> got((size_t)maxl * ctx->nranks);
+    CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_send);
+    cudaFree(d_recv);
+    for (int r = 0; r < ctx->nranks; ++r)
+      for (size_t lb = 0; lb < blocks_of[r].size(); ++lb) all[blocks_of[r][lb]] = got[(size_t)maxl * r + lb];
+  }
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += all[b];
+  *out = s;
+  return SIP_OK;
+}
+
+// Ghosts of u, v, w, then divergence: Q scattered into the system's source
+// (fp64 pack and, in single mode, the fp32 pack) and the L1 norm.
+int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
+  sip_ctx* ctx = fl->ctx;
+  FieldSet fs{{fl->f[0], fl->f[1], fl->f[2]}, 3};
+  CKS(flow_exchange(fl, fs));
+  const int signs[3] = {(1 << G_W) | (1 << G_E), (1 << G_S) | (1 << G_N), (1 << G_B) | (1 << G_T)};
+  CKS(flow_walls(fl, fl->f, 3, signs));
+  const double hx = ctx->h[0], hy = ctx->h[1], hz = ctx->h[2];
+  const double vol = (hx * hy) * hz;
+  std::vector<double> vals(ctx->local.size(), 0.0);
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& b = ctx->hblocks[lb];
+    const size_t o = ctx->phi_stage_off[lb];
+    const long long n = (long long)b.nx * b.ny * b.nz;
+    double* q = ctx->staging;  // Field3 Q of this block (ghosts unused by the scatter)
+    k_divergence<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
+        b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz,
+        vol, dt, (int)lb == ctx->pin_local, q, fl->absdiv);
+    CK(cudaGetLastError());
+    const int nch = (int)((n + kChunk - 1) / kChunk);
+    k_chunk_sums<<<nch, kFlowThreads, 0, ctx->stream>>>(fl->absdiv, n, fl->partial);
+    k_sum_in_order<<<1, 32, 0, ctx->stream>>>(fl->partial, nch, fl->d_blocksum + lb);
+    CK(cudaGetLastError());
+    ctx->launches += 3;
+    if (write_q) {
+      if (ctx->precision == SIP_PREC_SINGLE)
+        CKS(launch_scatter<float>(q, ctx->d_blocks, (int)lb, b, static_cast<float*>(ctx->fw), F_NA,
+                                  F_Q, ctx->stream));
+      CKS(launch_scatter<double>(q, ctx->d_blocks, (int)lb, b, ctx->fw64, F_NA, F_Q, ctx->stream));
+      ctx->launches += ctx->precision == SIP_PREC_SINGLE ? 2 : 1;
+    }
+  }
+  CK(cudaMemcpyAsync(vals.data(), fl->d_blocksum, sizeof(double) * vals.size(), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return allsum_blocks(ctx, vals, l1);
+}
+
+// p' = 0 (interior and ghosts), `sweeps` SIP iterations, p' -> Field3 mirror
+// (plan ghosts from the last exchange, Neumann ghosts at walls).
+template <typename T>
+int flow_solve(sip_flow* fl, int sweeps) {
+  sip_ctx* ctx = fl->ctx;
+  const size_t S = (size_t)ctx->total_slices * kTT;
+  CK(cudaMemsetAsync(ctx->phi, 0, S * sizeof(T), ctx->stream));
+  CK(cudaMemsetAsync(ctx->ghost, 0, (size_t)ctx->total_ghost * sizeof(T), ctx->stream));
+  ctx->n_done = 0;
+  CKS(iterate_t<T>(ctx, sweeps));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& b = ctx->hblocks[lb];
+    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    CKS(launch_gather<T>(static_cast<T*>(ctx->phi), static_cast<T*>(ctx->ghost), ctx->d_blocks,
+                         (int)lb, b, ctx->plan_ghosts[lb].data(), st, ctx->stream));
+    ++ctx->launches;
+  }
+  double* pp[1] = {ctx->phi_stage};
+  const int none[1] = {0};
+  return flow_walls(fl, pp, 1, none);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (!len || !bc) return flow_err(ctx, "sip_assemble_poisson: null arguments", SIP_ERR_MISUSE);
+  for (int a = 0; a < 3; ++a)
+    if (!(len[a] > 0.0) || !std::isfinite(len[a]))
+      return flow_err(ctx, "assemble_poisson: domain lengths must be positive", SIP_ERR_CONFIG);
+  int mask = 0;
+  for (int f = 0; f < 6; ++f) {
+    if (bc[f] < SIP_BC_WALL || bc[f] > SIP_BC_SYMMETRY)
+      return flow_err(ctx, "assemble_poisson: unknown boundary kind", SIP_ERR_CONFIG);
+    if ((bc[f] == SIP_BC_PERIODIC) != (bc[f ^ 1] == SIP_BC_PERIODIC))
+      return flow_err(ctx, "grid: periodic faces must come in opposing pairs", SIP_ERR_CONFIG);
+    if (bc[f] == SIP_BC_PERIODIC) mask |= 1 << (f / 2);
+  }
+  CKS(set_device(ctx));
+  double h[3];
+  for (int a = 0; a < 3; ++a) h[a] = len[a] / ctx->L.g[a];
+  // halo plan with the periodic wraps of this grid
+  std::vector<HaloEntry> plan;
+  plan_halo(ctx->L, ctx->rank_of, ctx->rank, plan, mask);
+  CK(cudaStreamSynchronize(ctx->stream));
+  CKS(install_plan(ctx, plan));
+  const double ax = (h[1] * h[2]) / h[0], ay = (h[0] * h[2]) / h[1], az = (h[0] * h[1]) / h[2];
+  const int arr[8] = {F_AP, F_AW, F_AE, F_AS, F_AN, F_AB, F_AT, F_Q};
+  ctx->pin_local = ctx->local_of.empty() ? -1 : ctx->local_of[0];  // global cell (0,0,0) is in block 0
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& hb = ctx->hblocks[lb];
+    const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
+    int cpl[6];
+    for (int f = 0; f < 6; ++f) cpl[f] = bi.nbr[f] >= 0 || bc[f] == SIP_BC_PERIODIC;
+    const size_t G = field3_elems(hb);
+    double* out8[8];
+    for (int a = 0; a < 8; ++a) out8[a] = ctx->staging + a * G;
+    CK(cudaMemsetAsync(ctx->staging, 0, 8 * G * sizeof(double), ctx->stream));
+    double** d_out8 = nullptr;
+    CKS(dalloc(ctx, &d_out8, sizeof(out8)));
+    CK(cudaMemcpy(d_out8, out8, sizeof(out8), cudaMemcpyHostToDevice));
+    const long long n = (long long)hb.nx * hb.ny * hb.nz;
+    k_poisson_coeffs<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
+        hb.nx, hb.ny, hb.nz, make_int4(cpl[0], cpl[1], cpl[2], cpl[3]), make_int2(cpl[4], cpl[5]),
+        ax, ay, az, (int)lb == ctx->pin_local, d_out8);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    for (int a = 0; a < 8; ++a) {
+      if (ctx->precision == SIP_PREC_SINGLE)
+        CKS(launch_scatter<float>(out8[a], ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
+                                  F_NA, arr[a], ctx->stream));
+      CKS(launch_scatter<double>(out8[a], ctx->d_blocks, (int)lb, hb, ctx->fw64, F_NA, arr[a],
+                                 ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_out8);
+  }
+  ++ctx->revision;
+  // the identity row of the pinned cell breaks ae(i) = aw(i+1) next to it, so
+  // the system is not flagged symmetric (the general Listing-1 path runs)
+  ctx->symmetric.assign(ctx->local.size(), 0);
+  ctx->poisson = true;
+  for (int a = 0; a < 3; ++a) ctx->h[a] = h[a];
+  for (int f = 0; f < 6; ++f) ctx->bc[f] = bc[f];
+  return SIP_OK;
+}
+
+int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
+  if (!ctx || !out) return SIP_ERR_MISUSE;
+  *out = nullptr;
+  if (!ctx->poisson)
+    return flow_err(ctx, "sip_flow_create: assemble the pressure system first", SIP_ERR_MISUSE);
+  CKS(set_device(ctx));
+  sip_flow* fl = new sip_flow();
+  fl->ctx = ctx;
+  size_t total = 0;
+  for (const BlockDesc& b : ctx->hblocks) {
+    total += field3_elems(b);
+    fl->max_cells = std::max(fl->max_cells, (long long)b.nx * b.ny * b.nz);
+  }
+  auto fail = [&](int s) {
+    sip_flow_destroy(fl);
+    return s;
+  };
+  int s = SIP_OK;
+  for (int q = 0; q < 4 && s == SIP_OK; ++q) s = dalloc(ctx, &fl->f[q], sizeof(double) * std::max<size_t>(1, total));
+  if (s == SIP_OK) s = dalloc(ctx, &fl->absdiv, sizeof(double) * std::max(1LL, fl->max_cells));
+  if (s == SIP_OK)
+    s = dalloc(ctx, &fl->partial, sizeof(double) * std::max(1LL, (fl->max_cells + kChunk - 1) / kChunk));
+  if (s == SIP_OK) s = dalloc(ctx, &fl->d_blocksum, sizeof(double) * std::max<size_t>(1, ctx->local.size()));
+  if (s == SIP_OK) s = dalloc(ctx, &fl->d_off, sizeof(long long) * std::max<size_t>(1, ctx->local.size()));
+  if (s != SIP_OK) return fail(s);
+  std::vector<long long> off(ctx->phi_stage_off.begin(), ctx->phi_stage_off.end());
+  if (!off.empty() && cudaMemcpy(fl->d_off, off.data(), sizeof(long long) * off.size(),
+                                 cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(flow_err(ctx, "sip_flow_create: offset upload failed", SIP_ERR_CUDA));
+  for (const Peer& p : ctx->peers) {
+    double *a = nullptr, *b = nullptr;
+    s = dalloc(ctx, &a, sizeof(double) * 3 * std::max(1LL, p.count));
+    if (s == SIP_OK) s = dalloc(ctx, &b, sizeof(double) * 3 * std::max(1LL, p.count));
+    fl->pbuf.emplace_back(a, b);
+    if (s != SIP_OK) return fail(s);
+  }
+  // domain walls: faces whose ghosts the halo plan does not write
+  fl->wall.assign(ctx->local.size(), 0);
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb)
+    for (int f = 0; f < 6; ++f)
+      if (ctx->plan_ghosts[lb][f] < 0) fl->wall[lb] |= 1 << f;
+  *out = fl;
+  return SIP_OK;
+}
+
+int sip_flow_destroy(sip_flow* fl) {
+  if (!fl) return SIP_OK;
+  if (fl->ctx) cudaSetDevice(fl->ctx->device);
+  for (double* p : fl->f)
+    if (p) cudaFree(p);
+  void* ptrs[] = {fl->d_off, fl->absdiv, fl->partial, fl->d_blocksum};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& pb : fl->pbuf) {
+    if (pb.first) cudaFree(pb.first);
+    if (pb.second) cudaFree(pb.second);
+  }
+  delete fl;
+  return SIP_OK;
+}
+
+int sip_flow_set(sip_flow* fl, int field, double* const* per_block) {
+  if (!fl || !per_block) return SIP_ERR_MISUSE;
+  sip_ctx* ctx = fl->ctx;
+  if (field < SIP_FLOW_U || field > SIP_FLOW_P)
+    return flow_err(ctx, "sip_flow_set: field must be SIP_FLOW_U .. SIP_FLOW_P", SIP_ERR_MISUSE);
+  CKS(set_device(ctx));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    if (!per_block[lb]) return flow_err(ctx, "sip_flow_set: null block array", SIP_ERR_MISUSE);
+    CK(cudaMemcpyAsync(fl->f[field] + ctx->phi_stage_off[lb], per_block[lb],
+                       field3_elems(ctx->hblocks[lb]) * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_flow_get(sip_flow* fl, int field, double* const* per_block) {
+  if (!fl || !per_block) return SIP_ERR_MISUSE;
+  sip_ctx* ctx = fl->ctx;
+  if (field < SIP_FLOW_U || field > SIP_FLOW_P)
+    return flow_err(ctx, "sip_flow_get: field must be SIP_FLOW_U .. SIP_FLOW_P", SIP_ERR_MISUSE);
+  CKS(set_device(ctx));
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    if (!per_block[lb]) return flow_err(ctx, "sip_flow_get: null block array", SIP_ERR_MISUSE);
+    CK(cudaMemcpyAsync(per_block[lb], fl->f[field] + ctx->phi_stage_off[lb],
+                       field3_elems(ctx->hblocks[lb]) * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_flow_divergence(sip_flow* fl, double* l1) {
+  if (!fl || !l1) return SIP_ERR_MISUSE;
+  sip_ctx* ctx = fl->ctx;
+  CKS(set_device(ctx));
+  return flow_divergence(fl, 1.0, false, l1);
+}
+
+int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_outer, int sweeps,
+                         int* outer_used, double* div_hist) {
+  if (!fl) return SIP_ERR_MISUSE;
+  sip_ctx* ctx = fl->ctx;
+  if (!(dt > 0.0) || max_outer < 0 || sweeps < 1 || !(threshold >= 0.0))
+    return flow_err(ctx, "pressure_correct: need dt > 0, threshold >= 0, max_outer >= 0, sweeps >= 1",
+                    SIP_ERR_CONFIG);
+  CKS(check_ready(ctx));  // factors of the assembled system, reused (never refactored here)
+  CKS(set_device(ctx));
+  if (outer_used) *outer_used = 0;
+  double d = 0.0;
+  for (int outer = 0;; ++outer) {
+    CKS(flow_divergence(fl, dt, true, &d));
+    if (div_hist) div_hist[outer] = d;
+    if (outer_used) *outer_used = outer;
+    if (d <= threshold) return SIP_OK;
+    if (outer == max_outer) {
+      char buf[160];
+      snprintf(buf, sizeof(buf),
+               "pressure_correct: %d outer iterations left the divergence L1 at %.6e > %.6e", outer,
+               d, threshold);
+      return flow_err(ctx, buf, SIP_ERR_NOCONV);
+    }
+    CKS(ctx->precision == SIP_PREC_SINGLE ? flow_solve<float>(fl, sweeps) : flow_solve<double>(fl, sweeps));
+    const double hx = ctx->h[0], hy = ctx->h[1], hz = ctx->h[2];
+    for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+      const BlockDesc& b = ctx->hblocks[lb];
+      const size_t o = ctx->phi_stage_off[lb];
+      const long long n = (long long)b.nx * b.ny * b.nz;
+      k_correct<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
+          b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, fl->f[3] + o,
+          ctx->phi_stage + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+  }
+}
+
+}  // extern "C"

@@ -118,8 +118,9 @@ bool ftt1_validate(const std::vector<std::vector<std::array<int, 12>>>& t, std::
 
 bool build_lattice(int gnx, int gny, int gnz, int px, int py, int pz, Lattice& L, std::string& err);
 bool plan_block_ranks(int px, int py, int pz, int nranks, std::vector<int>& out);
+// face transfers of this rank; bit a of periodic_mask: axis a wraps
 void plan_halo(const Lattice& L, const std::vector<int>& rank_of, int rank,
-               std::vector<HaloEntry>& out);
+               std::vector<HaloEntry>& out, int periodic_mask = 0);
 
 // ---------------------------------------------------------------- kernels
 // One face copy: interior plane of src block -> ghost face of dst block, or

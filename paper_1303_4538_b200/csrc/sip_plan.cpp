@@ -109,7 +109,7 @@ bool plan_block_ranks(int px, int py, int pz, int nranks, std::vector<int>& out)
 // order (transfers.cpp:153-165 key restricted to PatchKind::Face), then the
 // per-rank entries in table order (tables.cpp:25-40).
 void plan_halo(const Lattice& L, const std::vector<int>& rank_of, int rank,
-               std::vector<HaloEntry>& out) {
+               std::vector<HaloEntry>& out, int periodic_mask) {
   struct T {
     int src, dst, face_dst, off[3];
     int src_lo[3], src_hi[3], dst_lo[3], dst_hi[3];
@@ -121,7 +121,12 @@ void plan_halo(const Lattice& L, const std::vector<int>& rank_of, int rank,
     for (int a = 0; a < 3; ++a)
       for (int sign : {+1, -1}) {
         // our nbr order is W,E,S,N,B,T = (a, -1), (a, +1)
-        const int src = X.nbr[2 * a + (sign > 0 ? 1 : 0)];
+        int src = X.nbr[2 * a + (sign > 0 ? 1 : 0)];
+        if (src < 0 && ((periodic_mask >> a) & 1)) {  // wrap (transfers.cpp:15-25)
+          std::array<int, 3> c = X.coord;
+          c[a] = (c[a] + sign + L.p[a]) % L.p[a];
+          src = c[0] + L.p[0] * (c[1] + L.p[1] * c[2]);
+        }
         if (src < 0) continue;
         const BlockInfo& N = L.blocks[src];
         T t{};
@@ -184,8 +189,9 @@ extern "C" int sip_plan_block_ranks(int px, int py, int pz, int nranks, int* blo
   return SIP_OK;
 }
 
-extern "C" int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz,
-                             const int* block_rank, int rank, int* n_entries, int* entries) {
+extern "C" int sip_plan_halo_periodic(int gnx, int gny, int gnz, int px, int py, int pz,
+                                      const int* block_rank, int rank, int periodic_mask,
+                                      int* n_entries, int* entries) {
   sipb::Lattice L;
   std::string err;
   if (!n_entries || !sipb::build_lattice(gnx, gny, gnz, px, py, pz, L, err)) return SIP_ERR_CONFIG;
@@ -197,7 +203,7 @@ extern "C" int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz,
     for (int b = 0; b < nb; ++b) rank_of[b] = b;  // decompose(): one block per rank
   }
   std::vector<sipb::HaloEntry> v;
-  sipb::plan_halo(L, rank_of, rank, v);
+  sipb::plan_halo(L, rank_of, rank, v, periodic_mask);
   if (entries) {
     if (*n_entries < static_cast<int>(v.size())) return SIP_ERR_CONFIG;
     for (size_t n = 0; n < v.size(); ++n) {
@@ -210,4 +216,9 @@ extern "C" int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz,
   }
   *n_entries = static_cast<int>(v.size());
   return SIP_OK;
+}
+
+extern "C" int sip_plan_halo(int gnx, int gny, int gnz, int px, int py, int pz,
+                             const int* block_rank, int rank, int* n_entries, int* entries) {
+  return sip_plan_halo_periodic(gnx, gny, gnz, px, py, pz, block_rank, rank, 0, n_entries, entries);
 }

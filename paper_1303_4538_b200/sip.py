@@ -13,6 +13,9 @@ Names, argument meaning and error behaviour follow the specification:
     sip_sweep      (SPEC.md:170-178)   -> sip_sweep
     solve          (SPEC.md:179-187)   -> solve
     errors         (error.hpp:34-50)   -> SingularFactorError, StaleFactorsError, MisuseError
+    assemble_poisson (SPEC.md:134-142) -> assemble_poisson / Solver.assemble_poisson
+    FlowState   -> Flow (device-resident u, v, w, p)
+    pressure_correct (SPEC.md:341-349) -> pressure_correct / Flow.pressure_correct
 
 Arrays are numpy float64 Field3 arrays (proj/include/bsfv/field.hpp:25-44):
 shape (nz+2, ny+2, nx+2), i fastest, interior 1..n.  Coefficients use the
@@ -36,7 +39,9 @@ LIB_PATH = os.environ.get("SIPB_LIB") or os.path.join(_HERE, "libsip_b200.so")
 
 SIP_OK, SIP_ERR_SINGULAR, SIP_ERR_STALE, SIP_ERR_MISUSE = 0, 1, 2, 3
 SIP_ERR_CONFIG, SIP_ERR_CUDA, SIP_ERR_NCCL, SIP_ERR_NOMEM = 4, 5, 6, 7
-SIP_ERR_FORMAT, SIP_ERR_PROTOCOL = 8, 9
+SIP_ERR_FORMAT, SIP_ERR_PROTOCOL, SIP_ERR_NOCONV = 8, 9, 10
+BC = {"wall": 0, "periodic": 1, "symmetry": 2}
+FLOW_FIELDS = {"u": 0, "v": 1, "w": 2, "p": 3}
 PREC = {"f64": 0, "double": 0, "f32": 1, "single": 1}
 
 ARRAYS = ("AP", "AW", "AE", "AS", "AN", "AB", "AT", "Q")
@@ -51,6 +56,8 @@ EXPORTS = (
     "sip_get_stream", "sip_set_profiling", "sip_get_profile", "sip_launch_count", "sip_geometry",
     "sip_nccl_unique_id", "sip_generate_host", "sip_plan_block_ranks", "sip_plan_halo",
     "sip_ftt1_read", "sip_ftt1_write", "sip_ftt1_validate", "sip_set_halo_tables",
+    "sip_plan_halo_periodic", "sip_assemble_poisson", "sip_flow_create", "sip_flow_destroy",
+    "sip_flow_set", "sip_flow_get", "sip_flow_divergence", "sip_pressure_correct",
 )
 
 
@@ -84,6 +91,15 @@ class FormatError(Error):
 
 class ProtocolError(Error):
     """bsfv::ProtocolError (error.hpp:53-57): unmatched transfer-table entries."""
+
+
+class NonConvergenceError(Error):
+    """bsfv::NonConvergenceError (error.hpp:72-80): the pressure-correction outer
+    loop hit its cap with the divergence above the threshold; `defect` = last L1."""
+
+    def __init__(self, what: str, defect: float = float("nan")):
+        super().__init__(what)
+        self.defect = defect
 
 
 _EXC = {SIP_ERR_SINGULAR: SingularFactorError, SIP_ERR_STALE: StaleFactorsError,
@@ -275,7 +291,19 @@ class Solver:
         self._c(lib().sip_generate_system(self._ctx, kind, ctypes.c_uint64(seed)),
                 "sip_generate_system")
 
+    def assemble_poisson(self, lengths, bc=("wall",) * 6):
+        """assemble_poisson: 7-point pressure Laplacian of the
+        lattice over a domain of `lengths` (lx, ly, lz); bc per face W,E,S,N,B,T
+        ("wall" | "periodic" | "symmetry").  Global cell (0,0,0) is pinned."""
+        codes = [BC[b] if isinstance(b, str) else int(b) for b in bc]
+        if len(codes) != 6:
+            raise ConfigError("assemble_poisson: bc needs 6 faces (W,E,S,N,B,T)")
+        self._c(lib().sip_assemble_poisson(self._ctx, (ctypes.c_double * 3)(*lengths),
+                                           (ctypes.c_int * 6)(*codes)), "sip_assemble_poisson")
+
     def factor(self, alpha: float):
+        global _factor_count
+        _factor_count += 1
         bb, bc = ctypes.c_longlong(-1), ctypes.c_longlong(-1)
         st = lib().sip_factor(self._ctx, ctypes.c_double(alpha), ctypes.byref(bb), ctypes.byref(bc))
         if st == SIP_ERR_SINGULAR:
@@ -350,6 +378,78 @@ class Solver:
 
 
 # ----------------------------------------------------------------- SPEC operations
+class Flow:
+    """FlowState of a Solver whose system was assembled by
+    assemble_poisson: u, v, w, p as fp64 Field3 arrays per local block, kept in
+    device memory; set / get copy host arrays in and out."""
+
+    def __init__(self, solver: "Solver"):
+        self.solver = solver
+        self._h = ctypes.c_void_p()
+        _check(solver.handle, lib().sip_flow_create(solver.handle, ctypes.byref(self._h)),
+               "sip_flow_create")
+
+    def close(self):
+        if self._h:
+            lib().sip_flow_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, st, what):
+        if st == SIP_ERR_NOCONV:
+            raise NonConvergenceError(
+                f"{what}: {lib().sip_last_error(self.solver.handle).decode(errors='replace')}")
+        _check(self.solver.handle, st, what)
+
+    def set(self, name: str, arrays: Sequence[np.ndarray]):
+        self._c(lib().sip_flow_set(self._h, FLOW_FIELDS[name], self.solver._phis(arrays)),
+                "sip_flow_set")
+
+    def get(self, name: str, arrays: Sequence[np.ndarray]):
+        self._c(lib().sip_flow_get(self._h, FLOW_FIELDS[name], self.solver._phis(arrays)),
+                "sip_flow_get")
+
+    def divergence(self) -> float:
+        """L1 of the co-located central divergence, sum |div u| * cell volume."""
+        d = ctypes.c_double()
+        self._c(lib().sip_flow_divergence(self._h, ctypes.byref(d)), "sip_flow_divergence")
+        return d.value
+
+    def pressure_correct(self, dt: float, threshold: float, max_outer: int = 20,
+                         sweeps: int = 5):
+        """pressure_correct with the factors of the assembled
+        system reused.  Returns (outer iterations, divergence L1 history);
+        raises NonConvergenceError (with .defect) at the outer cap."""
+        hist = np.zeros(max_outer + 1)
+        used = ctypes.c_int(0)
+        st = lib().sip_pressure_correct(self._h, ctypes.c_double(dt), ctypes.c_double(threshold),
+                                        max_outer, sweeps, ctypes.byref(used),
+                                        hist.ctypes.data_as(_dp))
+        if st == SIP_ERR_NOCONV:
+            raise NonConvergenceError(
+                lib().sip_last_error(self.solver.handle).decode(errors="replace"),
+                float(hist[used.value]))
+        self._c(st, "sip_pressure_correct")
+        return used.value, hist[:used.value + 1]
+
+
+def assemble_poisson(solver: "Solver", lengths, bc=("wall",) * 6, dt: Optional[float] = None):
+    """SPEC.md:134-142 (dt does not enter the coefficients; kept for the signature)."""
+    solver.assemble_poisson(lengths, bc)
+    return solver
+
+
+def pressure_correct(flow: Flow, dt: float, threshold: float, max_outer: int = 20,
+                     sweeps: int = 5):
+    """see Flow.pressure_correct."""
+    return flow.pressure_correct(dt, threshold, max_outer, sweeps)
+
+
 class SipFactors:
     """Factors of one StencilSystem, resident on the device and stamped with
     the system revision they were computed from."""
