@@ -20,7 +20,12 @@
 //
 // Error mapping (proj/include/bsfv/error.hpp:34-50):
 //   SIP_ERR_SINGULAR -> SingularFactorError, SIP_ERR_STALE -> StaleFactorsError,
-//   SIP_ERR_MISUSE -> MisuseError, SIP_ERR_CONFIG -> ConfigError, else Error.
+//   SIP_ERR_MISUSE -> MisuseError, SIP_ERR_CONFIG -> ConfigError,
+//   SIP_ERR_NOCONV -> NonConvergenceError (PressureSolver), else Error.
+//
+// The caller of the SIP: PressureSolver assembles
+// the pressure-correction Laplacian on a block lattice, factors it once and
+// runs pressure_correct steps on a device-resident flow state.
 #pragma once
 
 #include <algorithm>
@@ -43,6 +48,7 @@ using StaleFactorsError = ::bsfv::StaleFactorsError;
 using MisuseError = ::bsfv::MisuseError;
 using FormatError = ::bsfv::FormatError;
 using ProtocolError = ::bsfv::ProtocolError;
+using NonConvergenceError = ::bsfv::NonConvergenceError;
 #else
 class Error : public std::runtime_error {
  public:
@@ -76,6 +82,14 @@ class FormatError : public Error {  // error.hpp:22-31: the message carries the 
 class ProtocolError : public Error {
  public:
   explicit ProtocolError(const std::string& w) : Error(w) {}
+};
+class NonConvergenceError : public Error {  // error.hpp:72-80: carries the defect
+ public:
+  NonConvergenceError(const std::string& w, double defect) : Error(w), defect_(defect) {}
+  double defect() const { return defect_; }
+
+ private:
+  double defect_;
 };
 #endif
 
@@ -296,6 +310,97 @@ double sip_sweep(const StencilSystemT<Field>& A, SipFactors& F, Field& fi) {
   check(::sip_solve(F.ctx(), phis, 1, 0.0, &norm, &used), F.ctx(), "sip_solve");
   return norm;
 }
+
+/// Boundary kind per domain face (GridSpec bc), order W,E,S,N,B,T.
+enum class Bc { Wall = SIP_BC_WALL, Periodic = SIP_BC_PERIODIC, Symmetry = SIP_BC_SYMMETRY };
+
+/// Result of one pressure_correct call: outer iterations run and the
+/// divergence L1 before each mass check.
+struct CorrectionReport {
+  int outer = 0;
+  std::vector<double> divergence;
+};
+
+/// assemble_poisson + sip_factor + pressure_correct with factor reuse
+/// (SPEC.md:134-142, 341-349): one device context over a block lattice of one
+/// rank, the pressure system assembled and factored once at construction,
+/// FlowState (u, v, w, p) resident on the device.  factorizations() is the
+/// work-avoidance counter: it stays 1 for the object's life.
+class PressureSolver {
+ public:
+  PressureSolver(std::array<int, 3> cells, std::array<int, 3> blocks, std::array<double, 3> lengths,
+                 std::array<Bc, 6> bc, const SipConfig& cfg = SipConfig(), int device = 0) {
+    check(::sip_create_lattice(device, cells[0], cells[1], cells[2], blocks[0], blocks[1], blocks[2],
+                               nullptr, 0, 1, nullptr,
+                               cfg.single_precision ? SIP_PREC_SINGLE : SIP_PREC_DOUBLE, &ctx_),
+          nullptr, "sip_create_lattice");
+    try {
+      int b[6];
+      for (int f = 0; f < 6; ++f) b[f] = static_cast<int>(bc[f]);
+      check(::sip_assemble_poisson(ctx_, lengths.data(), b), ctx_, "assemble_poisson");
+      long long bb = -1, bcell = -1;
+      check(::sip_factor(ctx_, cfg.alpha, &bb, &bcell), ctx_, "sip_factor");
+      ++factorizations_;
+      check(::sip_flow_create(ctx_, &flow_), ctx_, "sip_flow_create");
+      int n = 0;
+      ::sip_num_local_blocks(ctx_, &n);
+      for (int lb = 0; lb < n; ++lb) {
+        std::array<int, 3> d{}, o{};
+        int id = 0;
+        ::sip_local_block(ctx_, lb, &id, d.data(), o.data());
+        dims_.push_back(d);
+      }
+    } catch (...) {
+      release();
+      throw;
+    }
+  }
+  PressureSolver(const PressureSolver&) = delete;
+  PressureSolver& operator=(const PressureSolver&) = delete;
+  ~PressureSolver() { release(); }
+
+  int num_blocks() const { return static_cast<int>(dims_.size()); }
+  std::array<int, 3> block_dims(int b) const { return dims_.at(static_cast<std::size_t>(b)); }
+  long long factorizations() const { return factorizations_; }
+
+  /// field: SIP_FLOW_U .. SIP_FLOW_P; one Field3 array per local block.
+  void set(int field, const std::vector<const double*>& per_block) {
+    std::vector<double*> p(per_block.size());
+    for (std::size_t b = 0; b < p.size(); ++b) p[b] = const_cast<double*>(per_block[b]);
+    check(::sip_flow_set(flow_, field, p.data()), ctx_, "sip_flow_set");
+  }
+  void get(int field, const std::vector<double*>& per_block) {
+    check(::sip_flow_get(flow_, field, per_block.data()), ctx_, "sip_flow_get");
+  }
+  double divergence() {
+    double d = 0.0;
+    check(::sip_flow_divergence(flow_, &d), ctx_, "sip_flow_divergence");
+    return d;
+  }
+  /// pressure_correct; NonConvergenceError carries the defect.
+  CorrectionReport pressure_correct(double dt, double threshold, int max_outer, int sweeps = 5) {
+    CorrectionReport r;
+    r.divergence.assign(static_cast<std::size_t>(max_outer) + 1, 0.0);
+    const int st = ::sip_pressure_correct(flow_, dt, threshold, max_outer, sweeps, &r.outer,
+                                          r.divergence.data());
+    r.divergence.resize(static_cast<std::size_t>(r.outer) + 1);
+    if (st == SIP_ERR_NOCONV) throw NonConvergenceError(::sip_last_error(ctx_), r.divergence.back());
+    check(st, ctx_, "pressure_correct");
+    return r;
+  }
+
+ private:
+  void release() {
+    if (flow_) ::sip_flow_destroy(flow_);
+    if (ctx_) ::sip_destroy(ctx_);
+    flow_ = nullptr;
+    ctx_ = nullptr;
+  }
+  sip_ctx* ctx_ = nullptr;
+  sip_flow* flow_ = nullptr;
+  long long factorizations_ = 0;
+  std::vector<std::array<int, 3>> dims_;
+};
 
 }  // namespace b200
 }  // namespace bsfv

@@ -45,3 +45,38 @@ def test_shim_solve_matches_oracle(gpu, tmp_path):
         # residual_general (fp64) of phi0 = 0 is su: its L1 is sum |Q|
         l1 = float(out[-2].split()[-1])
         np.testing.assert_allclose(l1, np.abs(A["Q"][1:-1, 1:-1, 1:-1]).sum(), rtol=1e-12)
+
+
+def build_flow(tmp_path):
+    exe = str(tmp_path / "flow_example")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "flow_example.cpp"), "-L", LIBDIR,
+                    "-lsip_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    return exe
+
+
+def test_flow_shim_compiles_and_reports_missing_device(tmp_path):
+    exe = build_flow(tmp_path)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present (covered by the gpu test)")
+    except Exception:
+        pass
+    r = subprocess.run([exe, "8"], capture_output=True, text=True)
+    assert r.returncode == 3 and "CUDA error" in r.stdout
+
+
+@pytest.mark.gpu
+def test_flow_shim_reuses_one_factorization(gpu, tmp_path):
+    """PressureSolver (C++ shim): 100 pressure_correct steps on one
+    factorisation, NonConvergenceError carries the defect."""
+    exe = build_flow(tmp_path)
+    r = subprocess.run([exe, "16"], capture_output=True, text=True, check=True)
+    out = r.stdout.splitlines()
+    assert out[-1] == "factorizations 1" and out[-2] == "noconv ok", out[-2:]
+    steps = [ln.split() for ln in out if ln.startswith("step")]
+    assert len(steps) == 4
+    for s in steps:
+        d0, d1 = float(s[5]), float(s[7])
+        assert int(s[3]) >= 1 and d1 <= 0.1 * d0
