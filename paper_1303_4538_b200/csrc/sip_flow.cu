@@ -25,7 +25,7 @@ using namespace sipb;
 namespace {
 
 constexpr int kFlowThreads = 256;
-constexpr int kChunk = 8192;  // cells per partial sum of the divergence norm
+constexpr int kChunk = 4096;  // cells per partial sum of the divergence norm
 
 __device__ __forceinline__ long long f3(int nx, int ny, int i, int j, int k) {
   return (long long)i + (long long)(nx + 2) * (j + (long long)(ny + 2) * k);
@@ -125,46 +125,55 @@ __global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double
 }
 
 // Co-located central divergence of one block; Q = -(V * div) / dt into a
-// Field3 staging array (pinned cell: 0) and |div| * V per interior cell.
-__global__ void k_divergence(int nx, int ny, int nz, const double* u, const double* v,
-                             const double* w, double c2x, double c2y, double c2z, double vol,
-                             double dt, int pin, double* q, double* absdiv) {
+// Field3 staging array (pinned cell: 0) and the block's L1 partials: CTA b
+// owns cells [b*kChunk, (b+1)*kChunk) and sums |div| * V over them in a fixed
+// order (strided per thread, fixed shuffle tree, warps in order), so the norm
+// is deterministic.
+__global__ void __launch_bounds__(kFlowThreads) k_divergence(int nx, int ny, int nz, const double* u,
+                                                             const double* v, const double* w,
+                                                             double c2x, double c2y, double c2z,
+                                                             double vol, double dt, int pin,
+                                                             double* q, double* partial) {
+  __shared__ double s[kFlowThreads / 32];
   const long long n = (long long)nx * ny * nz;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-       c += (long long)gridDim.x * blockDim.x) {
+  const long long lo = (long long)blockIdx.x * kChunk;
+  const long long hi = lo + kChunk < n ? lo + kChunk : n;
+  const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+  double acc = 0.0;
+  for (long long c = lo + threadIdx.x; c < hi; c += kFlowThreads) {
     const int i = (int)(c % nx) + 1, j = (int)((c / nx) % ny) + 1,
               k = (int)(c / ((long long)nx * ny)) + 1;
     const long long x = f3(nx, ny, i, j, k);
-    const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
     const double dv = ((u[x + sx] - u[x - sx]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
                       (w[x + sz] - w[x - sz]) / c2z;
     q[x] = (pin && c == 0) ? 0.0 : -(vol * dv) / dt;
-    absdiv[c] = fabs(dv) * vol;
+    acc += fabs(dv) * vol;
   }
-}
-
-// Deterministic partial sums: CTA b sums cells [b*kChunk, (b+1)*kChunk) in a
-// fixed order (strided per thread, then a fixed shuffle / shared tree).
-__global__ void k_chunk_sums(const double* x, long long n, double* partial) {
-  __shared__ double s[kFlowThreads / 32];
-  const long long lo = (long long)blockIdx.x * kChunk;
-  const long long hi = lo + kChunk < n ? lo + kChunk : n;
-  double acc = 0.0;
-  for (long long c = lo + threadIdx.x; c < hi; c += blockDim.x) acc += x[c];
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int q = 0; q < kFlowThreads / 32; ++q) t += s[q];
+    for (int r = 0; r < kFlowThreads / 32; ++r) t += s[r];
     partial[blockIdx.x] = t;
   }
 }
-__global__ void k_sum_in_order(const double* partial, int n, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
+
+// Sum of n partials in a fixed order by one CTA: thread t sums t, t+256, ...,
+// then the fixed shuffle tree and the warps in order.
+__global__ void __launch_bounds__(kFlowThreads) k_sum_partials(const double* partial, int n,
+                                                               double* out) {
+  __shared__ double s[kFlowThreads / 32];
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < n; b += kFlowThreads) acc += partial[b];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int b = 0; b < n; ++b) t += partial[b];
+    for (int r = 0; r < kFlowThreads / 32; ++r) t += s[r];
     *out = t;
   }
 }
@@ -197,7 +206,6 @@ struct sip_flow {
   sip_ctx* ctx = nullptr;
   double* f[4] = {nullptr, nullptr, nullptr, nullptr};  // u, v, w, p
   long long* d_off = nullptr;    // per local block Field3 offset (= phi_stage_off)
-  double* absdiv = nullptr;      // |div| * V per interior cell of the largest block
   double* partial = nullptr;     // chunk partials
   double* d_blocksum = nullptr;  // per local block L1
   std::vector<int> wall;         // per local block: bit f = domain wall / symmetry face
@@ -327,15 +335,13 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
     const size_t o = ctx->phi_stage_off[lb];
     const long long n = (long long)b.nx * b.ny * b.nz;
     double* q = ctx->staging;  // Field3 Q of this block (ghosts unused by the scatter)
-    k_divergence<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
-        b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz,
-        vol, dt, (int)lb == ctx->pin_local, q, fl->absdiv);
-    CK(cudaGetLastError());
     const int nch = (int)((n + kChunk - 1) / kChunk);
-    k_chunk_sums<<<nch, kFlowThreads, 0, ctx->stream>>>(fl->absdiv, n, fl->partial);
-    k_sum_in_order<<<1, 32, 0, ctx->stream>>>(fl->partial, nch, fl->d_blocksum + lb);
+    k_divergence<<<nch, kFlowThreads, 0, ctx->stream>>>(
+        b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz,
+        vol, dt, (int)lb == ctx->pin_local, q, fl->partial);
+    k_sum_partials<<<1, kFlowThreads, 0, ctx->stream>>>(fl->partial, nch, fl->d_blocksum + lb);
     CK(cudaGetLastError());
-    ctx->launches += 3;
+    ctx->launches += 2;
     if (write_q) {
       if (ctx->precision == SIP_PREC_SINGLE)
         CKS(launch_scatter<float>(q, ctx->d_blocks, (int)lb, b, static_cast<float*>(ctx->fw), F_NA,
@@ -458,7 +464,6 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   };
   int s = SIP_OK;
   for (int q = 0; q < 4 && s == SIP_OK; ++q) s = dalloc(ctx, &fl->f[q], sizeof(double) * std::max<size_t>(1, total));
-  if (s == SIP_OK) s = dalloc(ctx, &fl->absdiv, sizeof(double) * std::max(1LL, fl->max_cells));
   if (s == SIP_OK)
     s = dalloc(ctx, &fl->partial, sizeof(double) * std::max(1LL, (fl->max_cells + kChunk - 1) / kChunk));
   if (s == SIP_OK) s = dalloc(ctx, &fl->d_blocksum, sizeof(double) * std::max<size_t>(1, ctx->local.size()));
@@ -489,7 +494,7 @@ int sip_flow_destroy(sip_flow* fl) {
   if (fl->ctx) cudaSetDevice(fl->ctx->device);
   for (double* p : fl->f)
     if (p) cudaFree(p);
-  void* ptrs[] = {fl->d_off, fl->absdiv, fl->partial, fl->d_blocksum};
+  void* ptrs[] = {fl->d_off, fl->partial, fl->d_blocksum};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& pb : fl->pbuf) {
