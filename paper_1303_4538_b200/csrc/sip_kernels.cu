@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
 // sweep's fetcher only polls the R values that are produced during the sweep.
 // =============================================================================
 template <typename T>
-__global__ void __launch_bounds__(256) k_edge_phi(const SweepParams<T> P) {
+__global__ void __launch_bounds__(1024) k_edge_phi(const SweepParams<T> P) {
   const TileDesc td = P.tiles[blockIdx.x];
   const BlockDesc bd = P.blocks[td.block];
   const int NS = td.ns, nz = td.nz;
@@ -996,6 +996,7 @@ __global__ void __launch_bounds__(256) k_edge_phi(const SweepParams<T> P) {
   const T* g = P.ghost + ghost_face_offset(bd, sideB ? (we ? G_E : G_N) : (we ? G_W : G_S)) +
                (we ? td.j0 : td.i0) + c;
   const long long gstride = we ? bd.ny : bd.nx;
+#pragma unroll 4
   for (int s = threadIdx.x >> 6; s < NS; s += blockDim.x >> 6) {
     const int k = s - koff;
     T v = T(0);
@@ -1303,7 +1304,7 @@ int launch_backward(const SweepParams<T>& p, int grid, void* stream) {
 template <typename T>
 int launch_edge_phi(const SweepParams<T>& p, void* stream) {
   if (p.ntiles <= 0) return SIP_OK;
-  k_edge_phi<T><<<p.ntiles, 256, 0, (cudaStream_t)stream>>>(p);
+  k_edge_phi<T><<<p.ntiles, 1024, 0, (cudaStream_t)stream>>>(p);
   return cudaGetLastError() == cudaSuccess ? SIP_OK : SIP_ERR_CUDA;
 }
 template int launch_edge_phi<float>(const SweepParams<float>&, void*);
