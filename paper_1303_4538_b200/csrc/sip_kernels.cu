@@ -445,11 +445,22 @@ constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kP
 // instead of 14 array touches per cell).  The coefficient values, hence every
 // operation and its rounding, are the general path's (the symmetry invariant
 // is checked exactly by sip_set_symmetric).
+// fp32 general path: the critical group's cross-tile polls / publishes run in
+// an edge warp (threads 512..543, edge_warp_run) -- 6 % faster at 256^3.  fp64
+// and the symmetric path keep them in the critical threads: a 17th warp caps
+// the kernel at 96 registers (fp64: the residual group spills; fp32 SYM:
+// measured 6 % slower).
 template <typename T, bool SYM>
-__global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) {
+__host__ __device__ constexpr bool k2_edge_warp() { return sizeof(T) == 4 && !SYM; }
+constexpr int kPollK2 = 3;  // K2 edge-warp poll ring (tile step ~0.5-0.9 us under load)
+
+template <typename T, bool SYM>
+__global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1)
+    k_forward(const SweepParams<T> P) {
   // Two threads per column.  Threads 0..255 ("critical"): the recurrence
   // R = (((r - LB*R_B) - LW*R_W) - LS*R_S) * LP of step t, cross-tile R
-  // stores / polls.  Threads 256..511 ("residual"): everything that does
+  // stores / polls (fp32: done by the edge warp, see k2_edge_warp).
+  // Threads 256..511 ("residual"): everything that does
   // not depend on R -- the residual r of each step and its factors (handed
   // over through the s_prep ring of kPrep slots), the phi / edge-record
   // rings, the forward-pack LDGs and the L2 prefetch front.  The two groups
@@ -459,15 +470,18 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
   __shared__ __align__(16) T s_ph[kRingR][kTT];  // own-column phi of slice y in slot y % kRingR
   __shared__ __align__(16) T s_rec[kRingR][64];  // static edge record of step y (phiW/E/S/N)
   __shared__ __align__(16) T s_R[2][kTT];       // R of steps t-1 / t
+  __shared__ __align__(16) T s_eR[2][32];       // edge warp: polled R of the W column / S row
   __shared__ __align__(16) T s_gh[2][kTT];      // ghost phi below / above each column
   __shared__ __align__(16) T s_prep[kPrep][kTT];  // residual r of prepared steps
-  __shared__ double s_red[2 * kTT / 32];
+  __shared__ double s_red[2 * kTT / 32 + 1];
+  constexpr bool kEdge = k2_edge_warp<T, SYM>();
+  constexpr int kCritBar = kTT + (kEdge ? 32 : 0);  // critical-group barrier (+ edge warp)
   __shared__ int s_tile, s_last;
   __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
 
   const int p = threadIdx.x;
-  const bool crit = p < kTT;
+  const bool crit = p < kTT, edgew = p >= 2 * kTT;
   const int q = p & (kTT - 1);  // column position
   int ti, tj;
   pos_to_tij(q, ti, tj);
@@ -512,7 +526,7 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       T* gR = P.R + td.slot * kTT + q;
       auto poll_issue = [&](TagPoll<T>& pw, TagPoll<T>& ps, int s) {
         const int k = s - d;
-        if (k >= 0 && k < nz && s < NS) {
+        if (!kEdge && k >= 0 && k < nz && s < NS) {
           if (pollW) pw.issue(srcW + (long long)k * 16 * TW);
           if (pollS) ps.issue(srcS + (long long)k * 16 * TW);
         }
@@ -533,6 +547,7 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
       T lf0[4] = {T(0), T(0), T(0), T(0)}, lf1[4] = {T(0), T(0), T(0), T(0)};
       ldg_lf(lf0, 0);
       ldg_lf(lf1, 1);
+      if (kEdge) nbar_sync(kBarCrit, kCritBar);  // prologue: edge record of step 0 in place
       T RB = T(0);  // own R of the plane below (0 outside the block)
       auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* lf) {
         const int k = t - d;
@@ -544,13 +559,19 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
         if (col && k >= 0 && k < nz) {
           const uint32_t tag = edge_tag(epoch, k);
-          const T RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61, &s_stall) : T(0));
-          const T RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62, &s_stall) : T(0));
+          T RW, RS;
+          if constexpr (kEdge) {
+            RW = inW ? RWi : s_eR[t & 1][tj];  // 0 at a block face
+            RS = inS ? RSi : s_eR[t & 1][16 + ti];
+          } else {
+            RW = inW ? RWi : (pollW ? poll_take(pw, srcW + (long long)k * 16 * TW, tag, 61, &s_stall) : T(0));
+            RS = inS ? RSi : (pollS ? poll_take(ps, srcS + (long long)k * 16 * TW, tag, 62, &s_stall) : T(0));
+          }
           const T Rv = (((r - lb * RB) - lw * RW) - ls * RS) * lp;
           RB = Rv;
           s_R[t & 1][q] = Rv;
-          if (pubE) put_tagged(dstE + (long long)k * 16 * TW, Rv, tag);
-          if (pubN) put_tagged(dstN + (long long)k * 16 * TW, Rv, tag);
+          if (!kEdge && pubE) put_tagged(dstE + (long long)k * 16 * TW, Rv, tag);
+          if (!kEdge && pubN) put_tagged(dstN + (long long)k * 16 * TW, Rv, tag);
 #ifndef SIPB_EXP_NOSTG
           gR[(long long)t * kTT] = Rv;  // consumed only by K3 (next launch)
 #endif
@@ -559,7 +580,7 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         ldg_lf(lf, t + 2);
         if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
           P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
-        nbar_sync(kBarCrit, kTT);  // R of step t visible to the group
+        nbar_sync(kBarCrit, kCritBar);  // R of step t visible to the group (and the edge warp)
       };
       int t = 0;
       for (; t + 1 < NS; t += 2) {
@@ -567,6 +588,30 @@ __global__ void __launch_bounds__(2 * kTT, 1) k_forward(const SweepParams<T> P) 
         iter(t + 1, pw1, ps1, lf1);
       }
       if (t < NS) iter(t, pw0, ps0, lf0);
+    } else if (edgew) {
+      if constexpr (kEdge) {
+        // ---------------------------------------------------------- edge warp
+        // lane c < 16: poll the W tile's E column (cell (0, c) here), publish
+        // cell (15, c); lane 16 + c: S tile's N row (cell (c, 0)), publish (c, 15)
+        const int lane = p & 31, c = lane & 15;
+        const bool wi = lane < 16;
+        EdgeLane<T> e;
+        const int nPoll = wi ? td.nW : td.nS, nPub = wi ? td.nE : td.nN;
+        const bool colok = wi ? (c < td.wJ) : (c < td.wI);
+        const bool full = wi ? (td.wI == kTI) : (td.wJ == kTJ);  // the published cell exists
+        e.fwd = true;
+        e.poll = colok && nPoll >= 0;
+        e.pub = colok && full && nPub >= 0;
+        e.d_poll = c;
+        e.d_pub = c + (wi ? kTI - 1 : kTJ - 1);
+        e.pub_pos = wi ? tile_pos(kTI - 1, c) : tile_pos(c, kTJ - 1);
+        e.NS = NS;
+        e.nz = nz;
+        e.lane = lane;
+        e.src = (wi ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
+        e.dst = (wi ? P.tagA : P.tagB) + (td.edge + c) * TW;
+        edge_warp_run<T, kPollK2>(e, s_R, s_eR, epoch, kBarCrit, kCritBar, &s_stall);
+      }
     } else {
       // ------------------------------------------------------------ residual
       // Two steps per iteration (two independent residual chains interleave,
@@ -1288,10 +1333,18 @@ int launch_factor(const FactorParams& p, int grid, void* stream) {
 
 template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream) {
-  if (p.symmetric)
-    k_forward<T, true><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
-  else
-    k_forward<T, false><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
+  // The symmetric fast path (identical values, identical rounding) saves HBM
+  // reads; it pays in fp64 (1.4 % at 256^3) but not in fp32, whose forward
+  // sweep is latency- rather than bandwidth-bound (the neighbour-line reads
+  // lengthen the residual chain: 6.9 % slower), so fp32 always runs the
+  // general kernel.
+  if constexpr (sizeof(T) == 8) {
+    if (p.symmetric) {
+      k_forward<T, true><<<grid, 2 * kTT, 0, (cudaStream_t)stream>>>(p);
+      return cuda_status(cudaGetLastError());
+    }
+  }
+  k_forward<T, false><<<grid, 2 * kTT + (k2_edge_warp<T, false>() ? 32 : 0), 0, (cudaStream_t)stream>>>(p);
   return cuda_status(cudaGetLastError());
 }
 
@@ -1320,7 +1373,7 @@ int max_resident_ctas(int kind, int precision, int* grid) {
   } else if (kind == 1) {
     e = precision == SIP_PREC_DOUBLE
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<double, false>, 2 * kTT, 0)
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, false>, 2 * kTT, 0);
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_forward<float, false>, 2 * kTT + 32, 0);
   } else {
     e = precision == SIP_PREC_DOUBLE
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT + 32, 0)
