@@ -429,9 +429,11 @@ __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_
 }
 
 #ifdef SIPB_EXP_PD
-constexpr int kPollK3 = SIPB_EXP_PD;
+constexpr int kPollK3 = 8, kPollK3f = SIPB_EXP_PD;
 #else
-constexpr int kPollK3 = 8;  // K3 poll ring (tile step ~0.3 us under load)
+// K3 poll rings: issued kPoll - 1 steps ahead (tile step ~0.3 us fp64,
+// ~0.2 us fp32 under load; an L2 round trip to a peer tile ~1 us)
+constexpr int kPollK3 = 8, kPollK3f = 12;
 #endif
 constexpr int kPrep = 4;  // prepared-step ring between the residual and critical groups
 constexpr int kRingR = 8; // phi-slice / record ring of the split K2 (two slices per iteration)
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
       e.lane = lane;
       e.src = (we ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
       e.dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
-      edge_warp_run<T, kPollK3>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
+      edge_warp_run<T, sizeof(T) == 8 ? kPollK3 : kPollK3f>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
     } else {
     // -------------------------------------------------------------- columns
     const bool col = ti < td.wI && tj < td.wJ;
