@@ -80,6 +80,48 @@ int sipb::install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
   };
   for (const HaloEntry& e : plan) {
     FaceCopy fc{};
+    if (e.dir == 0 && ctx->nccl_self) {
+      // debugging / hardware test of the multi-rank path on one GPU: a local
+      // transfer becomes a send + recv pair with this rank itself, so the
+      // pack kernels, NCCL send / recv and unpack kernels all run
+      HaloEntry snd = e, rcv = e;
+      snd.dir = 1;
+      snd.peer = ctx->rank;
+      rcv.dir = 2;
+      rcv.peer = ctx->rank;
+      rcv.owner = e.neighbor;
+      rcv.neighbor = e.owner;
+      rcv.face = e.face ^ 1;
+      std::vector<HaloEntry> pair = {snd, rcv};
+      for (const HaloEntry& x : pair) {
+        auto it = std::find_if(ctx->peers.begin(), ctx->peers.end(),
+                               [&](const Peer& pp) { return pp.rank == x.peer; });
+        if (it == ctx->peers.end()) {
+          ctx->peers.emplace_back();
+          ctx->peers.back().rank = x.peer;
+          it = ctx->peers.end() - 1;
+        }
+        FaceCopy f{};
+        if (x.dir == 1) {
+          f.src_block = ctx->local_of[x.owner];
+          f.src_face = kface(x.face);
+          f.dst_block = -1;
+          plane(x.owner, f.src_face, f.n0, f.n1);
+          for (auto& q : it->pack) f.buf += (long long)q.n0 * q.n1;
+          it->pack.push_back(f);
+        } else {
+          f.src_block = -1;
+          f.dst_block = ctx->local_of[x.owner];
+          f.dst_face = kface(x.face);
+          ctx->plan_ghosts[f.dst_block][f.dst_face] = x.neighbor;
+          plane(x.owner, f.dst_face, f.n0, f.n1);
+          for (auto& q : it->unpack) f.buf += (long long)q.n0 * q.n1;
+          it->unpack.push_back(f);
+        }
+        it->max_plane = std::max(it->max_plane, f.n0 * f.n1);
+      }
+      continue;
+    }
     if (e.dir == 0) {  // local: owner = src block, face = src plane; dst ghost = opposite
       fc.src_block = ctx->local_of[e.owner];
       fc.src_face = kface(e.face);
@@ -316,8 +358,20 @@ static int create_common(int device, int gnx, int gny, int gnz, int px, int py, 
     delete ctx;
     return SIP_ERR_CONFIG;
   }
+  if (nranks == 1 && getenv("SIPB_NCCL_SELF")) ctx->nccl_self = atoi(getenv("SIPB_NCCL_SELF")) != 0;
   int s = set_device(ctx);
   if (s == SIP_OK) s = build(ctx);
+  if (s == SIP_OK && ctx->nccl_self) {  // 1-rank communicator for the self-exchange test mode
+    ncclUniqueId id;
+    if (!nccl().ok) {
+      ctx->err = nccl().err;
+      s = SIP_ERR_NCCL;
+    } else if (nccl().GetUniqueId(&id) != ncclSuccess ||
+               nccl().CommInitRank(&ctx->comm, 1, id, 0) != ncclSuccess) {
+      ctx->err = "ncclCommInitRank (self mode) failed";
+      s = SIP_ERR_NCCL;
+    }
+  }
   if (s == SIP_OK && nranks > 1) {
     if (!nccl_id) {
       ctx->err = "nccl_id required when nranks > 1";

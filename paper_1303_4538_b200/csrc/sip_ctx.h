@@ -104,6 +104,9 @@ struct sip_ctx {
   double h[3] = {1.0, 1.0, 1.0};
   int bc[6] = {0, 0, 0, 0, 0, 0};
   int pin_local = -1;  // local block holding global cell (0,0,0), or -1
+  // test mode (env SIPB_NCCL_SELF=1, single rank): local face transfers go
+  // through the NCCL pack / send / recv / unpack path to this rank itself
+  bool nccl_self = false;
   std::string err;
 };
 
