@@ -25,7 +25,6 @@ using namespace sipb;
 namespace {
 
 constexpr int kFlowThreads = 256;
-constexpr int kChunk = 4096;  // cells per partial sum of the divergence norm
 
 __device__ __forceinline__ long long f3(int nx, int ny, int i, int j, int k) {
   return (long long)i + (long long)(nx + 2) * (j + (long long)(ny + 2) * k);
@@ -124,30 +123,38 @@ __global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double
   }
 }
 
-// Co-located central divergence of one block; Q = -(V * div) / dt into a
-// Field3 staging array (pinned cell: 0) and the block's L1 partials: CTA b
-// owns cells [b*kChunk, (b+1)*kChunk) and sums |div| * V over them in a fixed
-// order (strided per thread, fixed shuffle tree, warps in order), so the norm
-// is deterministic.
-__global__ void __launch_bounds__(kFlowThreads) k_divergence(int nx, int ny, int nz, const double* u,
-                                                             const double* v, const double* w,
-                                                             double c2x, double c2y, double c2z,
-                                                             double vol, double dt, int pin,
-                                                             double* q, double* partial) {
+// Co-located central divergence of one block; Q = -(V * div) / dt straight
+// into the source array of the system's tile-slice pack (fp64, and the fp32
+// copy in single mode; pinned cell: 0) and the block's L1 partials: one per
+// CTA, summed over its 256 cells by a fixed shuffle tree and the warps in
+// order, so the norm is deterministic.
+__global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* blocks, int blk,
+                                                             const double* u, const double* v,
+                                                             const double* w, double c2x, double c2y,
+                                                             double c2z, double vol, double dt, int pin,
+                                                             double* fw64, float* fw32,
+                                                             double* partial) {
+  // CTA (x, k) owns cells [256x, 256x + 256) of plane k (i fastest): a fixed
+  // cell -> CTA map, so the partial sums are deterministic.
   __shared__ double s[kFlowThreads / 32];
-  const long long n = (long long)nx * ny * nz;
-  const long long lo = (long long)blockIdx.x * kChunk;
-  const long long hi = lo + kChunk < n ? lo + kChunk : n;
-  const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+  const BlockDesc bd = blocks[blk];
+  const int nx = bd.nx, ny = bd.ny;
+  const int k = blockIdx.y;
+  const int ij = blockIdx.x * kFlowThreads + threadIdx.x;
   double acc = 0.0;
-  for (long long c = lo + threadIdx.x; c < hi; c += kFlowThreads) {
-    const int i = (int)(c % nx) + 1, j = (int)((c / nx) % ny) + 1,
-              k = (int)(c / ((long long)nx * ny)) + 1;
-    const long long x = f3(nx, ny, i, j, k);
-    const double dv = ((u[x + sx] - u[x - sx]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
+  if (ij < nx * ny) {
+    const int i = ij % nx, j = ij / nx;
+    const long long x = f3(nx, ny, i + 1, j + 1, k + 1);
+    const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+    const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
                       (w[x + sz] - w[x - sz]) / c2z;
-    q[x] = (pin && c == 0) ? 0.0 : -(vol * dv) / dt;
-    acc += fabs(dv) * vol;
+    if (fw64) {
+      const double q = (pin && ij == 0 && k == 0) ? 0.0 : -(vol * dv) / dt;
+      const long long pi = pack_index(bd, F_NA, F_Q, i, j, k);
+      fw64[pi] = q;
+      if (fw32) fw32[pi] = static_cast<float>(q);
+    }
+    acc = fabs(dv) * vol;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_divergence(int nx, int ny, int
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int r = 0; r < kFlowThreads / 32; ++r) t += s[r];
-    partial[blockIdx.x] = t;
+    partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
 }
 
@@ -178,21 +185,21 @@ __global__ void __launch_bounds__(kFlowThreads) k_sum_partials(const double* par
   }
 }
 
-// u -= dt * dp'/dx (central), v, w likewise; p += p'.
-__global__ void k_correct(int nx, int ny, int nz, double* u, double* v, double* w, double* p,
-                          const double* pp, double c2x, double c2y, double c2z, double dt) {
-  const long long n = (long long)nx * ny * nz;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-       c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % nx) + 1, j = (int)((c / nx) % ny) + 1,
-              k = (int)(c / ((long long)nx * ny)) + 1;
-    const long long x = f3(nx, ny, i, j, k);
-    const long long sx = 1, sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
-    u[x] = u[x] - dt * ((pp[x + sx] - pp[x - sx]) / c2x);
-    v[x] = v[x] - dt * ((pp[x + sy] - pp[x - sy]) / c2y);
-    w[x] = w[x] - dt * ((pp[x + sz] - pp[x - sz]) / c2z);
-    p[x] = p[x] + pp[x];
-  }
+// u -= dt * dp'/dx (central), v, w likewise; p += p'.  CTA (x, k): cells
+// [256x, 256x + 256) of plane k.
+__global__ void __launch_bounds__(kFlowThreads) k_correct(int nx, int ny, double* u, double* v,
+                                                          double* w, double* p, const double* pp,
+                                                          double c2x, double c2y, double c2z,
+                                                          double dt) {
+  const int ij = blockIdx.x * kFlowThreads + threadIdx.x;
+  if (ij >= nx * ny) return;
+  const int i = ij % nx + 1, j = ij / nx + 1, k = blockIdx.y + 1;
+  const long long x = f3(nx, ny, i, j, k);
+  const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+  u[x] = u[x] - dt * ((pp[x + 1] - pp[x - 1]) / c2x);
+  v[x] = v[x] - dt * ((pp[x + sy] - pp[x - sy]) / c2y);
+  w[x] = w[x] - dt * ((pp[x + sz] - pp[x - sz]) / c2z);
+  p[x] = p[x] + pp[x];
 }
 
 int grid_for(long long n) {
@@ -211,6 +218,7 @@ struct sip_flow {
   std::vector<int> wall;         // per local block: bit f = domain wall / symmetry face
   std::vector<std::pair<double*, double*>> pbuf;  // per peer: 3-field send / recv buffers
   long long max_cells = 0;
+  long long max_parts = 0;  // divergence partial sums of the largest block
 };
 
 namespace {
@@ -334,21 +342,17 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
     const BlockDesc& b = ctx->hblocks[lb];
     const size_t o = ctx->phi_stage_off[lb];
     const long long n = (long long)b.nx * b.ny * b.nz;
-    double* q = ctx->staging;  // Field3 Q of this block (ghosts unused by the scatter)
-    const int nch = (int)((n + kChunk - 1) / kChunk);
-    k_divergence<<<nch, kFlowThreads, 0, ctx->stream>>>(
-        b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz,
-        vol, dt, (int)lb == ctx->pin_local, q, fl->partial);
+    const dim3 grid((unsigned)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads), (unsigned)b.nz);
+    const int nch = (int)(grid.x * grid.y);
+    double* q64 = write_q ? ctx->fw64 : nullptr;
+    float* q32 = write_q && ctx->precision == SIP_PREC_SINGLE ? static_cast<float*>(ctx->fw) : nullptr;
+    (void)n;
+    k_divergence<<<grid, kFlowThreads, 0, ctx->stream>>>(
+        ctx->d_blocks, (int)lb, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy,
+        2.0 * hz, vol, dt, (int)lb == ctx->pin_local, q64, q32, fl->partial);
     k_sum_partials<<<1, kFlowThreads, 0, ctx->stream>>>(fl->partial, nch, fl->d_blocksum + lb);
     CK(cudaGetLastError());
     ctx->launches += 2;
-    if (write_q) {
-      if (ctx->precision == SIP_PREC_SINGLE)
-        CKS(launch_scatter<float>(q, ctx->d_blocks, (int)lb, b, static_cast<float*>(ctx->fw), F_NA,
-                                  F_Q, ctx->stream));
-      CKS(launch_scatter<double>(q, ctx->d_blocks, (int)lb, b, ctx->fw64, F_NA, F_Q, ctx->stream));
-      ctx->launches += ctx->precision == SIP_PREC_SINGLE ? 2 : 1;
-    }
   }
   CK(cudaMemcpyAsync(vals.data(), fl->d_blocksum, sizeof(double) * vals.size(), cudaMemcpyDeviceToHost,
                      ctx->stream));
@@ -457,6 +461,8 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   for (const BlockDesc& b : ctx->hblocks) {
     total += field3_elems(b);
     fl->max_cells = std::max(fl->max_cells, (long long)b.nx * b.ny * b.nz);
+    fl->max_parts = std::max(fl->max_parts,
+                             (long long)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads) * b.nz);
   }
   auto fail = [&](int s) {
     sip_flow_destroy(fl);
@@ -465,7 +471,7 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   int s = SIP_OK;
   for (int q = 0; q < 4 && s == SIP_OK; ++q) s = dalloc(ctx, &fl->f[q], sizeof(double) * std::max<size_t>(1, total));
   if (s == SIP_OK)
-    s = dalloc(ctx, &fl->partial, sizeof(double) * std::max(1LL, (fl->max_cells + kChunk - 1) / kChunk));
+    s = dalloc(ctx, &fl->partial, sizeof(double) * std::max(1LL, fl->max_parts));
   if (s == SIP_OK) s = dalloc(ctx, &fl->d_blocksum, sizeof(double) * std::max<size_t>(1, ctx->local.size()));
   if (s == SIP_OK) s = dalloc(ctx, &fl->d_off, sizeof(long long) * std::max<size_t>(1, ctx->local.size()));
   if (s != SIP_OK) return fail(s);
@@ -572,10 +578,10 @@ int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_oute
     for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
       const BlockDesc& b = ctx->hblocks[lb];
       const size_t o = ctx->phi_stage_off[lb];
-      const long long n = (long long)b.nx * b.ny * b.nz;
-      k_correct<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
-          b.nx, b.ny, b.nz, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, fl->f[3] + o,
-          ctx->phi_stage + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
+      const dim3 grid((unsigned)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads), (unsigned)b.nz);
+      k_correct<<<grid, kFlowThreads, 0, ctx->stream>>>(
+          b.nx, b.ny, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, ctx->phi_stage + o,
+          2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
       CK(cudaGetLastError());
       ++ctx->launches;
     }
