@@ -1067,9 +1067,8 @@ __global__ void k_scatter(const double* __restrict__ src, const BlockDesc* block
   const long long n = (long long)bd.nx * bd.ny * bd.nz;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % bd.nx);
-    const long long r = c / bd.nx;
-    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    const unsigned cu = (unsigned)c, r = cu / (unsigned)bd.nx;  // blocks < 2^32 cells
+    const int i = (int)(cu - r * (unsigned)bd.nx), j = (int)(r % (unsigned)bd.ny), k = (int)(r / (unsigned)bd.ny);
     pack[pack_index(bd, na, arr, i, j, k)] = static_cast<T>(src[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)]);
   }
 }
@@ -1115,9 +1114,8 @@ __global__ void k_gather(const T* __restrict__ pack, const T* __restrict__ ghost
   const long long n = (long long)bd.nx * bd.ny * bd.nz;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % bd.nx);
-    const long long r = c / bd.nx;
-    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    const unsigned cu = (unsigned)c, r = cu / (unsigned)bd.nx;  // blocks < 2^32 cells
+    const int i = (int)(cu - r * (unsigned)bd.nx), j = (int)(r % (unsigned)bd.ny), k = (int)(r / (unsigned)bd.ny);
     dst[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(pack[pack_index(bd, 1, 0, i, j, k)]);
   }
   // interface ghosts (faces with a neighbour block): values of the last exchange
@@ -1143,9 +1141,8 @@ __global__ void k_gather_any(const T* __restrict__ pack, int na, int arr, const 
   const long long n = (long long)bd.nx * bd.ny * bd.nz;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % bd.nx);
-    const long long r = c / bd.nx;
-    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    const unsigned cu = (unsigned)c, r = cu / (unsigned)bd.nx;  // blocks < 2^32 cells
+    const int i = (int)(cu - r * (unsigned)bd.nx), j = (int)(r % (unsigned)bd.ny), k = (int)(r / (unsigned)bd.ny);
     dst[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(pack[pack_index(bd, na, arr, i, j, k)]);
   }
 }
@@ -1193,9 +1190,8 @@ __global__ void k_residual(const BlockDesc* blocks, int b, const T* __restrict__
   const long long n = (long long)bd.nx * bd.ny * bd.nz;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % bd.nx);
-    const long long r = c / bd.nx;
-    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    const unsigned cu = (unsigned)c, r = cu / (unsigned)bd.nx;  // blocks < 2^32 cells
+    const int i = (int)(cu - r * (unsigned)bd.nx), j = (int)(r % (unsigned)bd.ny), k = (int)(r / (unsigned)bd.ny);
     auto ph = [&](int ii, int jj, int kk) -> T {
       if (ii < 0) return ghost[ghost_face_offset(bd, G_W) + jj + (long long)bd.ny * kk];
       if (ii >= bd.nx) return ghost[ghost_face_offset(bd, G_E) + jj + (long long)bd.ny * kk];
@@ -1237,9 +1233,8 @@ __global__ void k_check_symmetric(const BlockDesc* blocks, int b, const double* 
   unsigned long long cnt = 0;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(c % bd.nx);
-    const long long r = c / bd.nx;
-    const int j = (int)(r % bd.ny), k = (int)(r / bd.ny);
+    const unsigned cu = (unsigned)c, r = cu / (unsigned)bd.nx;  // blocks < 2^32 cells
+    const int i = (int)(cu - r * (unsigned)bd.nx), j = (int)(r % (unsigned)bd.ny), k = (int)(r / (unsigned)bd.ny);
     if (i + 1 < bd.nx && fw[pack_index(bd, F_NA, F_AE, i, j, k)] != fw[pack_index(bd, F_NA, F_AW, i + 1, j, k)]) ++cnt;
     if (j + 1 < bd.ny && fw[pack_index(bd, F_NA, F_AN, i, j, k)] != fw[pack_index(bd, F_NA, F_AS, i, j + 1, k)]) ++cnt;
     if (k + 1 < bd.nz && fw[pack_index(bd, F_NA, F_AT, i, j, k)] != fw[pack_index(bd, F_NA, F_AB, i, j, k + 1)]) ++cnt;

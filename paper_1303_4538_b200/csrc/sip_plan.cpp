@@ -59,6 +59,12 @@ bool build_lattice(int gnx, int gny, int gnz, int px, int py, int pz, Lattice& L
           c[a] += s;
           bi.nbr[f] = (c[a] < 0 || c[a] >= p[a]) ? -1 : c[0] + px * (c[1] + py * c[2]);
         }
+        // device kernels index a block's cells with 32-bit arithmetic
+        if ((long long)bi.n[0] * bi.n[1] >= (1LL << 31) ||
+            (long long)bi.n[0] * bi.n[1] * bi.n[2] >= (1LL << 32)) {
+          err = "decompose: a block must have fewer than 2^32 cells (2^31 per k-plane)";
+          return false;
+        }
         L.blocks[bx + px * (by + py * bz)] = bi;
       }
   return true;
