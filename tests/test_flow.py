@@ -138,13 +138,18 @@ def test_assemble_matches_oracle(gpu, bc):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("case", ["walls_2x2x1", "perx_2x1x2", "perall_1x2x1"])
+@pytest.mark.parametrize("case", ["walls_2x2x1", "perx_2x1x2", "perall_1x2x1", "ragged_sym_2x1x1",
+                                  "thin_1x1x3"])
 def test_pressure_correct_matches_oracle(gpu, prec, case):
     """Fields after a capped outer loop and the divergence history: bitwise /
-    1e-12 relative against the oracle (GPU SIP parity is bitwise already)."""
+    1e-12 relative against the oracle (GPU SIP parity is bitwise already).
+    Ragged tiles (extents not multiples of 16), symmetry faces, 1-cell-thin
+    blocks included."""
     g, p, bc = {"walls_2x2x1": ((16, 12, 8), (2, 2, 1), (W,) * 6),
                 "perx_2x1x2": ((16, 8, 12), (2, 1, 2), (P, P, W, W, W, W)),
-                "perall_1x2x1": ((12, 16, 8), (1, 2, 1), (P,) * 6)}[case]
+                "perall_1x2x1": ((12, 16, 8), (1, 2, 1), (P,) * 6),
+                "ragged_sym_2x1x1": ((37, 21, 9), (2, 1, 1), (S, W, P, P, S, S)),
+                "thin_1x1x3": ((5, 3, 3), (1, 1, 3), (P, P, W, W, P, P))}[case]
     lengths = (1.0, 0.75, 0.5)
     dt, outer_cap, sweeps = 0.05, 3, 4
     s = _gpu_setup(g, p, bc, prec, lengths)
