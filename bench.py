@@ -340,6 +340,56 @@ def load_traffic(cfg_id, prec):
         return None
 
 
+def run_caller(cfg_id):
+    """The SIP's caller on the config grid (one block, one GPU): assemble_poisson
+    (periodic x / y, walls z), one factorisation, then pressure_correct outer
+    iterations of 5 SIP sweeps each.
+    Timed end to end per call (the call syncs once per outer iteration for the
+    mass check); the SIP share from the library's CUDA-event profile."""
+    import torch
+
+    import paper_1303_4538_b200 as sip
+
+    c = CONFIGS[cfg_id]
+    g = tuple(c["g"])
+    outer, sweeps = 4, 5
+    s = sip.Solver(None, "f64", 0, lattice=(g, (1, 1, 1)))
+    s.assemble_poisson((1.0, 1.0, 1.0), ("periodic", "periodic", "periodic", "periodic", "wall", "wall"))
+    s.factor(0.92)
+    fl = sip.Flow(s)
+    (_, d, o) = s.blocks[0]
+    x = (np.arange(d[0]) + 0.5) / g[0]
+    z = (np.arange(d[2]) + 0.5) / g[2]
+    for name, amp in zip("uvwp", (1.0, 0.0, 0.5, 0.0)):
+        f = sip.field(*d)
+        f[1:-1, 1:-1, 1:-1] = amp * np.sin(2 * np.pi * x)[None, None, :] * np.cos(np.pi * z)[:, None, None]
+        fl.set(name, [f])
+    ms = []
+    for rep in range(3):  # rep 0 warms up
+        s.set_profiling(True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        try:
+            fl.pressure_correct(0.01, 0.0, outer, sweeps)
+        except sip.NonConvergenceError:
+            pass  # threshold 0: the cap is the point
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        pr = s.profile()
+        s.set_profiling(False)
+        if rep:
+            ms.append((wall * 1e3, pr["fwd_ms"] + pr["bwd_ms"] + pr["halo_ms"]))
+    fl.close()
+    s.close()
+    wall_ms = statistics.median(m[0] for m in ms) / outer
+    sip_ms = statistics.median(m[1] for m in ms) / outer
+    cells = g[0] * g[1] * g[2]
+    return {"workload": f"pressure_correct {g[0]}x{g[1]}x{g[2]} fp64, periodic x/y, walls z",
+            "sweeps_per_outer": sweeps, "ms_per_outer": wall_ms, "sip_ms_per_outer": sip_ms,
+            "caller_ms_per_outer": wall_ms - sip_ms,
+            "sip_mlups": cells * sweeps / (sip_ms * 1e-3) / 1e6, "factorizations": 1}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -350,6 +400,7 @@ def main():
     ap.add_argument("--precision", default="auto", choices=["auto", "f64", "f32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-caller", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -401,6 +452,9 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu:
             cpu = cpu_reference(cfg_id, seconds=12.0)
+        caller = None
+        if world == 1 and not args.no_caller and cfg_id == 1:
+            caller = run_caller(cfg_id)
         line = {
             "metric": "SIP inner-iteration MLUP/s", "value": r["value"], "unit": "MLUP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -417,6 +471,7 @@ def main():
             "kernel_ms_per_iter": r["kernel_ms_per_iter"],
             "timed_ms_per_iter": r["ms"] / c["iters"],
             "first_norms": r["first_norms"],
+            "caller": caller,
         }
         for prec, rr in res.items():
             if prec == head:
