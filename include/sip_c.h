@@ -250,6 +250,8 @@ typedef struct sip_flow sip_flow;
 #define SIP_FLOW_W 2
 #define SIP_FLOW_P 3
 int sip_flow_create(sip_ctx* ctx, sip_flow** out);  /* after sip_assemble_poisson */
+/* Destroy every flow of a context before sip_destroy(ctx); a later
+ * sip_assemble_poisson (new halo plan) also requires a new flow. */
 int sip_flow_destroy(sip_flow* flow);
 /* Host Field3 arrays (one per local block, interior used) -> device field. */
 int sip_flow_set(sip_flow* flow, int field, double* const* per_block);

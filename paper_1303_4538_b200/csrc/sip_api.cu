@@ -58,6 +58,7 @@ int sipb::set_device(sip_ctx* ctx) {
 // pack / unpack lists.  Replaces a previously installed plan.
 int sipb::install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
   const size_t es = ctx->esize;
+  ++ctx->plan_gen;
   if (ctx->d_local_copies) cudaFree(ctx->d_local_copies);
   ctx->d_local_copies = nullptr;
   ctx->local_copies.clear();

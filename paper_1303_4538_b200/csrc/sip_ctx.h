@@ -107,6 +107,7 @@ struct sip_ctx {
   // test mode (env SIPB_NCCL_SELF=1, single rank): local face transfers go
   // through the NCCL pack / send / recv / unpack path to this rank itself
   bool nccl_self = false;
+  long long plan_gen = 0;  // bumped by install_plan (flows are bound to one plan)
   std::string err;
 };
 

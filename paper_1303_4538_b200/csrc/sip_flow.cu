@@ -219,6 +219,7 @@ struct sip_flow {
   std::vector<std::pair<double*, double*>> pbuf;  // per peer: 3-field send / recv buffers
   long long max_cells = 0;
   long long max_parts = 0;  // divergence partial sums of the largest block
+  long long plan_gen = 0;   // the context's halo plan this flow's buffers were sized for
 };
 
 namespace {
@@ -457,6 +458,7 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   CKS(set_device(ctx));
   sip_flow* fl = new sip_flow();
   fl->ctx = ctx;
+  fl->plan_gen = ctx->plan_gen;
   size_t total = 0;
   for (const BlockDesc& b : ctx->hblocks) {
     total += field3_elems(b);
@@ -546,6 +548,8 @@ int sip_flow_get(sip_flow* fl, int field, double* const* per_block) {
 int sip_flow_divergence(sip_flow* fl, double* l1) {
   if (!fl || !l1) return SIP_ERR_MISUSE;
   sip_ctx* ctx = fl->ctx;
+  if (fl->plan_gen != ctx->plan_gen)
+    return flow_err(ctx, "flow created before the current halo plan: create a new flow", SIP_ERR_MISUSE);
   CKS(set_device(ctx));
   return flow_divergence(fl, 1.0, false, l1);
 }
@@ -557,6 +561,8 @@ int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_oute
   if (!(dt > 0.0) || max_outer < 0 || sweeps < 1 || !(threshold >= 0.0))
     return flow_err(ctx, "pressure_correct: need dt > 0, threshold >= 0, max_outer >= 0, sweeps >= 1",
                     SIP_ERR_CONFIG);
+  if (fl->plan_gen != ctx->plan_gen)
+    return flow_err(ctx, "flow created before the current halo plan: create a new flow", SIP_ERR_MISUSE);
   CKS(check_ready(ctx));  // factors of the assembled system, reused (never refactored here)
   CKS(set_device(ctx));
   if (outer_used) *outer_used = 0;

@@ -255,6 +255,8 @@ class Solver:
         return self._ctx
 
     def close(self):
+        for fl in list(getattr(self, "_flows", ())):  # flows live on this context: free them first
+            fl.close()
         if self._ctx:
             lib().sip_destroy(self._ctx)
             self._ctx = ctypes.c_void_p()
@@ -384,10 +386,14 @@ class Flow:
     device memory; set / get copy host arrays in and out."""
 
     def __init__(self, solver: "Solver"):
+        import weakref
         self.solver = solver
         self._h = ctypes.c_void_p()
         _check(solver.handle, lib().sip_flow_create(solver.handle, ctypes.byref(self._h)),
                "sip_flow_create")
+        if not hasattr(solver, "_flows"):
+            solver._flows = weakref.WeakSet()
+        solver._flows.add(self)
 
     def close(self):
         if self._h:

@@ -283,5 +283,11 @@ def test_bad_config_and_misuse(gpu):
     fl = sip.Flow(s)
     with pytest.raises(sip.MisuseError):  # not factored yet
         fl.pressure_correct(0.1, 0.0, 1, 1)
-    fl.close()
-    s.close()
+    s.assemble_poisson((1.0, 1.0, 1.0), ("periodic",) * 6)  # new halo plan
+    s.factor(0.92)
+    with pytest.raises(sip.MisuseError):  # the flow was built for the old plan
+        fl.divergence()
+    fl2 = sip.Flow(s)
+    assert fl2.divergence() == 0.0
+    s.close()  # closes its flows first
+    assert not fl._h and not fl2._h
