@@ -547,7 +547,7 @@ template int sipb::iterate_t<double>(sip_ctx*, int);
 extern "C" {
 
 const char* sip_version(void) {
-  return "b200-sip 0.1 (sm_100a, tiles 16x16, bulk-copy wavefront K1/K2/K3, NCCL halo)";
+  return "b200-sip 0.2 (sm_100a, 16x16-column tile wavefront K1/K2/K3 with tagged cross-tile hand-off, NCCL face halos, pressure-correction caller)";
 }
 
 const char* sip_status_string(int s) {
