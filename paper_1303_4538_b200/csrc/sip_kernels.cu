@@ -840,16 +840,11 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
   // columns need them.  All 288 threads meet at one barrier per step.
   __shared__ __align__(16) T s_D[2][kTT];
   __shared__ __align__(16) T s_rec[2][32];  // [step & 1]: dE (c < 16), dN (16 + c)
-  // fp64: own R, phi, UN, UE, UT of steps u % 4, copied 4 steps ahead with
-  // cp.async (under full load the HBM latency exceeds two tile steps; the
-  // register double buffer of the fp32 path would need 40 more registers)
-  constexpr bool kNbAsync = true;
-#ifdef SIPB_EXP_NBD
-  constexpr int kNbD = sizeof(T) == 8 ? 4 : SIPB_EXP_NBD;
-#else
+  // own R, phi, UN, UE, UT of steps u % 4, copied 4 steps ahead with
+  // cp.async (under full load the HBM latency exceeds two tile steps; a
+  // register double buffer measured slower, 8 steps no faster)
   constexpr int kNbD = 4;  // cp.async depth (steps)
-#endif
-  __shared__ __align__(16) T s_nb[kNbAsync ? kNbD : 1][5][kTT];
+  __shared__ __align__(16) T s_nb[kNbD][5][kTT];
   __shared__ int s_tile, s_last;
   __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
@@ -911,21 +906,6 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
     const T* r_cell = P.R + td.slot * kTT + p;
     T* ph_cell = P.phi + td.slot * kTT + p;
     const T* bw_cell = P.bw + td.slot * B_NA * kTT + p;
-    auto ldg_into = [&](T* nb, int u) {
-      const int t = NS - 1 - u, k = t - d;
-      if (u < NS && col && k >= 0 && k < nz) {
-#ifdef SIPB_EXP_NOLDG
-        nb[0] = T(t) * T(1e-9); nb[1] = T(0.5); nb[2] = T(0.1); nb[3] = T(0.2); nb[4] = T(0.3);
-#else
-        nb[0] = __ldg(r_cell + (long long)t * kTT);
-        nb[1] = __ldg(ph_cell + (long long)t * kTT);
-        const T* u3 = bw_cell + (long long)t * B_NA * kTT;
-        nb[2] = __ldg(u3);
-        nb[3] = __ldg(u3 + kTT);
-        nb[4] = __ldg(u3 + 2 * kTT);
-#endif
-      }
-    };
     auto pf = [&](int u) {  // three bulk L2 prefetches (R, phi, U slices of step u), thread 0
       if (u >= NS || p != 0) return;
       const long long ts = td.slot + NS - 1 - u;
@@ -950,25 +930,15 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
       }
       async_commit();
     };
-    if constexpr (kNbAsync) {
-      acp(0);
-      acp(1);
-      acp(2);
-      for (int x = 3; x < kNbD; ++x) acp(x);
-    } else {
-      ldg_into(nb0, 0);
-      ldg_into(nb1, 1);
-    }
+    for (int x = 0; x < kNbD; ++x) acp(x);
     for (int u = 0; u < kNbD + 3; ++u) pf(u);
     nbar_sync(1, kTT + 32);  // prologue barrier (edge record of step 0)
     T dT = T(0);  // own delta of the plane above (0 outside the block)
     auto iter = [&](const int u, T* nb) {
       const int t = NS - 1 - u, k = t - d;
-      if constexpr (kNbAsync) {
-        async_wait<kNbD - 1>();  // this thread's copies of step u (issued kNbD iterations ago) landed
+      async_wait<kNbD - 1>();  // this thread's copies of step u (issued kNbD iterations ago) landed
 #pragma unroll
-        for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & (kNbD - 1)][a][p];
-      }
+      for (int a = 0; a < 5; ++a) nb[a] = s_nb[u & (kNbD - 1)][a][p];
       // in-tile neighbours from the previous step, tile-edge ones from the edge record
       const T dN = inN ? s_D[(u - 1) & 1][pN] : s_rec[u & 1][16 + ti];
       const T dE = inE ? s_D[(u - 1) & 1][pE] : s_rec[u & 1][tj];
@@ -981,10 +951,7 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
         ph_cell[(long long)t * kTT] = nb[1] + dl;
 #endif
       }
-      if constexpr (kNbAsync)
-        acp(u + kNbD);
-      else
-        ldg_into(nb, u + 2);  // nb consumed above
+      acp(u + kNbD);  // into the slot just consumed
       pf(u + kNbD + 3);  // L2 prefetch three steps beyond the copies
       if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile - 1))
         P.trace[8 * P.ntiles - 4 * P.ntiles + 16 * u + 2 + (P.trace_tile - tid)] = gtime();  // K3 slots 2, 3
@@ -1376,10 +1343,8 @@ int max_resident_ctas(int kind, int precision, int* grid) {
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<double>, kTT + 32, 0)
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_backward<float>, kTT + 32, 0);
     // one tile per SM: a second co-resident tile halves both tiles' pace
-    // (the sweep is step-latency bound) -- measured 4-5% faster at 256^3
-#ifndef SIPB_EXP_K3PER2
+    // (the sweep is step-latency bound) -- measured 4-8 % faster at 256^3
     per = per > 0 ? 1 : per;
-#endif
   }
   if (e != cudaSuccess || per < 1) return SIP_ERR_CUDA;
   *grid = per * sms;
