@@ -562,6 +562,7 @@ const char* sip_status_string(int s) {
     case SIP_ERR_NOMEM: return "device out of memory";
     case SIP_ERR_FORMAT: return "malformed transfer table";
     case SIP_ERR_PROTOCOL: return "transfer table protocol violation";
+    case SIP_ERR_NOCONV: return "pressure correction did not converge";
     default: return "unknown status";
   }
 }

@@ -37,6 +37,7 @@ def test_version_and_status_strings():
     for st in range(0, 8):
         assert L.sip_status_string(st)
     assert L.sip_status_string(1) == b"singular factorization"
+    assert L.sip_status_string(10) == b"pressure correction did not converge"
 
 
 def test_create_without_device_fails_cleanly():
