@@ -384,10 +384,10 @@ struct EdgeLane {
   unsigned long long* dst;        // published words of this lane's downstream cell
   __device__ __forceinline__ int k_of(int u, int dd) const { return fwd ? u - dd : (NS - 1 - u) - dd; }
 };
-template <typename T, int kPD>
+// sync(u): the group barrier that ends step u (u = -1: the prologue barrier).
+template <typename T, int kPD, typename Sync>
 __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_val)[kTT], T (*s_rec)[32],
-                                              unsigned epoch, int bar, int bar_count,
-                                              unsigned long long* stall) {
+                                              unsigned epoch, Sync sync, unsigned long long* stall) {
   constexpr int TW = kTagWords<T>;
   TagPoll<T> q[kPD];
   auto issue = [&](TagPoll<T>& qq, int u) {
@@ -410,12 +410,12 @@ __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_
   for (int v = 0; v < kPD; ++v) issue(q[v], v);
   deposit(q[0], 0);
   issue(q[0], kPD);
-  nbar_sync(bar, bar_count);  // prologue barrier: record of step 0 in place
+  sync(-1);  // prologue barrier: record of step 0 in place
   auto estep = [&](int u, TagPoll<T>& qq) {
     publish(u - 1);
     deposit(qq, u + 1);
     issue(qq, u + 1 + kPD);
-    nbar_sync(bar, bar_count);
+    sync(u);
   };
   int u = 0;
   for (; u + kPD - 1 < e.NS; u += kPD) {
@@ -478,6 +478,10 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
   __shared__ double s_red[2 * kTT / 32 + 1];
   constexpr bool kEdge = k2_edge_warp<T, SYM>();
   constexpr int kCritBar = kTT + (kEdge ? 32 : 0);  // critical-group barrier (+ edge warp)
+  // FULL(slot of step t): residual threads arrive when r(t) is in s_prep; the
+  // critical threads (and the edge warp) sync on it at the end of step t-1,
+  // so one barrier both publishes R(t-1) to the group and admits step t
+  constexpr int kFullBar = 2 * kTT + (kEdge ? 32 : 0);
   __shared__ int s_tile, s_last;
   __shared__ unsigned long long s_stall;  // debug (SIPB_STEP_TRACE): poll stalls of the tile
   constexpr int TW = kTagWords<T>;
@@ -549,13 +553,12 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
       T lf0[4] = {T(0), T(0), T(0), T(0)}, lf1[4] = {T(0), T(0), T(0), T(0)};
       ldg_lf(lf0, 0);
       ldg_lf(lf1, 1);
-      if (kEdge) nbar_sync(kBarCrit, kCritBar);  // prologue: edge record of step 0 in place
+      nbar_sync(kBarFull, kFullBar);  // prologue: step 0 prepared (and its edge record in place)
       T RB = T(0);  // own R of the plane below (0 outside the block)
       auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* lf) {
         const int k = t - d;
         const int sl = t & (kPrep - 1);
-        nbar_sync(kBarFull + sl, 2 * kTT);  // step t prepared
-        const T r = s_prep[sl][q];
+        const T r = s_prep[sl][q];  // step t prepared (FULL barrier that ended step t-1)
         const T lb = lf[0], lw = lf[1], ls = lf[2], lp = lf[3];
         if (t + kPrep < NS) nbar_arrive(kBarEmpty + sl, 2 * kTT);  // slot free for step t + kPrep
         const T RWi = s_R[(t - 1) & 1][pW], RSi = s_R[(t - 1) & 1][pS];
@@ -582,7 +585,11 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
         ldg_lf(lf, t + 2);
         if (kStepTrace && P.trace && p == 0 && (tid == P.trace_tile || tid == P.trace_tile + 1))
           P.trace[8 * P.ntiles + 16 * t + (tid - P.trace_tile)] = gtime();  // slots 0, 1: tiles A, B
-        nbar_sync(kBarCrit, kCritBar);  // R of step t visible to the group (and the edge warp)
+        // R of step t visible to the group (and the edge warp); step t+1 prepared
+        if (t + 1 < NS)
+          nbar_sync(kBarFull + ((t + 1) & (kPrep - 1)), kFullBar);
+        else
+          nbar_sync(kBarCrit, kCritBar);
       };
       int t = 0;
       for (; t + 1 < NS; t += 2) {
@@ -612,7 +619,15 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
         e.lane = lane;
         e.src = (wi ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
         e.dst = (wi ? P.tagA : P.tagB) + (td.edge + c) * TW;
-        edge_warp_run<T, kPollK2>(e, s_R, s_eR, epoch, kBarCrit, kCritBar, &s_stall);
+        edge_warp_run<T, kPollK2>(
+            e, s_R, s_eR, epoch,
+            [&](int u) {
+              if (u + 1 < NS)
+                nbar_sync(kBarFull + ((u + 1) & (kPrep - 1)), kFullBar);
+              else
+                nbar_sync(kBarCrit, kCritBar);
+            },
+            &s_stall);
       }
     } else {
       // ------------------------------------------------------------ residual
@@ -693,7 +708,7 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
         const int sl = x & (kPrep - 1);
         if (x >= kPrep) nbar_sync(kBarEmpty + sl, 2 * kTT);  // step x - kPrep consumed
         s_prep[sl][q] = rr;
-        nbar_arrive(kBarFull + sl, 2 * kTT);
+        nbar_arrive(kBarFull + sl, kFullBar);
       };
       constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;
       constexpr int kArrLines = kTT * (int)sizeof(T) / 128;  // lines per array slice
@@ -898,7 +913,8 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_backward(const SweepParams<T> P
       e.lane = lane;
       e.src = (we ? P.tagA : P.tagB) + ((e.poll ? P.tiles[nPoll].edge : 0) + c) * TW;
       e.dst = (we ? P.tagA : P.tagB) + (td.edge + c) * TW;
-      edge_warp_run<T, sizeof(T) == 8 ? kPollK3 : kPollK3f>(e, s_D, s_rec, epoch, 1, kTT + 32, &s_stall);
+      edge_warp_run<T, sizeof(T) == 8 ? kPollK3 : kPollK3f>(
+          e, s_D, s_rec, epoch, [](int) { nbar_sync(1, kTT + 32); }, &s_stall);
     } else {
     // -------------------------------------------------------------- columns
     const bool col = ti < td.wI && tj < td.wJ;
