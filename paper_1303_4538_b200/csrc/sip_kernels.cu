@@ -558,6 +558,8 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
       auto iter = [&](const int t, TagPoll<T>& pw, TagPoll<T>& ps, T* lf) {
         const int k = t - d;
         const int sl = t & (kPrep - 1);
+        if (kStepTrace && P.trace && p == 0 && tid == P.trace_tile)
+          P.trace[8 * P.ntiles + 16 * t + 7] = gtime();  // slot 7: step t starts (tile A, thread 0)
         const T r = s_prep[sl][q];  // step t prepared (FULL barrier that ended step t-1)
         const T lb = lf[0], lw = lf[1], ls = lf[2], lp = lf[3];
         if (t + kPrep < NS) nbar_arrive(kBarEmpty + sl, 2 * kTT);  // slot free for step t + kPrep
@@ -708,6 +710,8 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
         const int sl = x & (kPrep - 1);
         if (x >= kPrep) nbar_sync(kBarEmpty + sl, 2 * kTT);  // step x - kPrep consumed
         s_prep[sl][q] = rr;
+        if (kStepTrace && P.trace && q == 0 && tid == P.trace_tile)
+          P.trace[8 * P.ntiles + 16 * x + 6] = gtime();  // slot 6: residual of step x published (tile A)
         nbar_arrive(kBarFull + sl, kFullBar);
       };
       constexpr int kFwLines = F_NA * kTT * (int)sizeof(T) / 128, kPhLines = kTT * (int)sizeof(T) / 128;

@@ -31,3 +31,16 @@ print(f"  A step 0 {A[0]:.2f}, A step 15 {A[15]:.2f}, B step 0 {B[0]:.2f}; A end
 for nm, dd in (("A", dA), ("B", dB)):
     q = np.percentile(dd, [10, 50, 75, 90, 99]) * 1e3
     print(f"  {nm} step ns p10/50/75/90/99: {' '.join(f'{v:.0f}' for v in q)}")
+# who waits: crit thread 0 reaches the end of step t-1 (slot 0 at t-1) vs the residual
+# group publishing r(t) (slot 6 at t); positive = the critical group waits for the residual
+R6 = st[:, 6]
+if R6.max() > 0:
+    w = R6[41:-40] - A[40:-41]
+    print(f"  residual r(t) after crit end of t-1: median {np.median(w)*1e3:.0f} ns, "
+          f"p90 {np.percentile(w,90)*1e3:.0f} ns, share of steps where crit waits {np.mean(w>0)*100:.0f}%")
+S7 = st[:, 7]
+if S7.max() > 0:
+    inner = A[40:-40] - S7[40:-40]          # thread 0 inside step t (incl. its own W/S polls)
+    wait = S7[41:-40] - A[40:-41]           # barrier wait after step t-1 (slowest thread / warp)
+    print(f"  thread 0 in-step: median {np.median(inner)*1e3:.0f} ns p90 {np.percentile(inner,90)*1e3:.0f}; "
+          f"barrier wait: median {np.median(wait)*1e3:.0f} ns p90 {np.percentile(wait,90)*1e3:.0f}")
