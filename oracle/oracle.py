@@ -47,6 +47,8 @@ def lib():
         L.orc_factor.restype = ctypes.c_int
         L.orc_sweep_d.restype = ctypes.c_double
         L.orc_sweep_f.restype = ctypes.c_double
+        L.orc_sweep_pipe_d.restype = ctypes.c_double
+        L.orc_sweep_pipe_f.restype = ctypes.c_double
         L.orc_solve.restype = ctypes.c_int
         L.orc_solve_multi.restype = ctypes.c_int
         _lib = L
@@ -115,6 +117,17 @@ def sweep(A: dict, F: dict, phi: np.ndarray) -> float:
         fn = lib().orc_sweep_f
     return fn(nx, ny, nz, *[_p(A[n]) for n in ARRAYS], *[_p(F[n]) for n in FACTORS], _p(phi),
               _p(work))
+
+
+def sweep_pipe(A: dict, F: dict, phi: np.ndarray, nthreads: int, work=None) -> float:
+    """sweep() on `nthreads` host threads (j-slab pipeline, bitwise-equal phi);
+    `work` (zero ghost layer, phi's dtype) may be reused across calls."""
+    nz, ny, nx = (s - 2 for s in A["AP"].shape)
+    if work is None:
+        work = field(nx, ny, nz, phi.dtype)
+    fn = lib().orc_sweep_pipe_d if phi.dtype == np.float64 else lib().orc_sweep_pipe_f
+    return fn(nx, ny, nz, *[_p(A[n]) for n in ARRAYS], *[_p(F[n]) for n in FACTORS], _p(phi),
+              _p(work), int(nthreads))
 
 
 def forward(A: dict, F: dict, phi: np.ndarray) -> np.ndarray:

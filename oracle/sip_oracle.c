@@ -45,6 +45,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdatomic.h>
+#include <omp.h>
 
 #define IDX(i, j, k) ((size_t)(i) + (size_t)(nx + 2) * ((size_t)(j) + (size_t)(ny + 2) * (size_t)(k)))
 
@@ -315,6 +317,83 @@ double orc_sweep_f(int nx, int ny, int nz, const float* AP, const float* AW, con
       }
   return norm;
 }
+
+/* ------------------------------------------------------------------------ */
+/* The same iteration on `nthreads` host threads (the CPU reference arm of   */
+/* bench.py: "the reference's algorithm with all the host threads it can     */
+/* use").  Pipelined over j-slabs: thread t owns rows [j0_t, j1_t); in the   */
+/* forward pass it processes plane k after thread t-1 finished plane k (the  */
+/* S neighbour row), in the backward pass after thread t+1 finished it.      */
+/* Every cell does the serial sweep's operations on the same operands, so    */
+/* phi is bitwise equal to orc_sweep_d/_f; the norm is summed per thread and */
+/* the partials in thread order (a different summation order).  work must    */
+/* be zero on its ghost layer (it is never written there).                   */
+/* ------------------------------------------------------------------------ */
+#define SWEEP_PIPE(NAME, T)                                                                       \
+  double NAME(int nx, int ny, int nz, const T* AP, const T* AW, const T* AE, const T* AS,          \
+              const T* AN, const T* AB, const T* AT, const T* Q, const T* LB, const T* LW,         \
+              const T* LS, const T* LP, const T* UN, const T* UE, const T* UT, T* phi, T* work,    \
+              int nthreads) {                                                                     \
+    const size_t sj = nx + 2, sk = (size_t)(nx + 2) * (ny + 2);                                   \
+    int nt = nthreads < 1 ? 1 : nthreads;                                                         \
+    if (nt > ny) nt = ny;                                                                         \
+    /* per-thread progress, one cache line each: planes done (forward, backward) */               \
+    _Atomic int* prog = (_Atomic int*)calloc((size_t)nt * 32, sizeof(int));                       \
+    double* part = (double*)calloc((size_t)nt, sizeof(double));                                   \
+    _Pragma("omp parallel num_threads(nt)")                                                       \
+    {                                                                                             \
+      const int t = omp_get_thread_num();                                                         \
+      const int j0 = 1 + (int)((long long)ny * t / nt), j1 = 1 + (int)((long long)ny * (t + 1) / nt); \
+      _Atomic int* fwd = prog + 32 * t;                                                           \
+      _Atomic int* bwd = prog + 32 * t + 16;                                                      \
+      double norm = 0.0;                                                                          \
+      for (int k = 1; k <= nz; ++k) {                                                             \
+        if (t > 0)                                                                                \
+          while (atomic_load_explicit(prog + 32 * (t - 1), memory_order_acquire) < k) {           \
+          }                                                                                       \
+        for (int j = j0; j < j1; ++j)                                                             \
+          for (int i = 1; i <= nx; ++i) {                                                         \
+            size_t c = IDX(i, j, k);                                                              \
+            T r = -(AE[c] * phi[c + 1]);                                                          \
+            r -= AW[c] * phi[c - 1];                                                              \
+            r -= AN[c] * phi[c + sj];                                                             \
+            r -= AS[c] * phi[c - sj];                                                             \
+            r -= AT[c] * phi[c + sk];                                                             \
+            r -= AB[c] * phi[c - sk];                                                             \
+            r += Q[c];                                                                            \
+            r -= AP[c] * phi[c];                                                                  \
+            norm += fabs((double)r);                                                              \
+            work[c] = (((r - LB[c] * work[c - sk]) - LW[c] * work[c - 1]) - LS[c] * work[c - sj]) * LP[c]; \
+          }                                                                                       \
+        atomic_store_explicit(fwd, k, memory_order_release);                                      \
+      }                                                                                           \
+      /* all residuals are read from the old phi: no thread may update phi  */                    \
+      /* before every thread finished its forward pass                       */                   \
+      _Pragma("omp barrier")                                                                      \
+      for (int k = nz; k >= 1; --k) {                                                             \
+        if (t < nt - 1)                                                                           \
+          while (atomic_load_explicit(prog + 32 * (t + 1) + 16, memory_order_acquire) <           \
+                 nz - k + 1) {                                                                    \
+          }                                                                                       \
+        for (int j = j1 - 1; j >= j0; --j)                                                        \
+          for (int i = nx; i >= 1; --i) {                                                         \
+            size_t c = IDX(i, j, k);                                                              \
+            T d = ((work[c] - UN[c] * work[c + sj]) - UE[c] * work[c + 1]) - UT[c] * work[c + sk]; \
+            work[c] = d;                                                                          \
+            phi[c] += d;                                                                          \
+          }                                                                                       \
+        atomic_store_explicit(bwd, nz - k + 1, memory_order_release);                             \
+      }                                                                                           \
+      part[t] = norm;                                                                             \
+    }                                                                                             \
+    double norm = 0.0;                                                                            \
+    for (int t = 0; t < nt; ++t) norm += part[t];                                                 \
+    free(prog);                                                                                   \
+    free(part);                                                                                   \
+    return norm;                                                                                  \
+  }
+SWEEP_PIPE(orc_sweep_pipe_d, double)
+SWEEP_PIPE(orc_sweep_pipe_f, float)
 
 /* ------------------------------------------------------------------------ */
 /* Single-block solve with a fixed iteration count.        */

@@ -371,3 +371,24 @@ def test_symmetric_generator_invariant():
     assert not A["AW"][1:-1, 1:-1, 1].any() and not A["AE"][1:-1, 1:-1, -2].any()
     fi = np.random.default_rng(3).uniform(-1, 1, size=A["AP"].shape)
     assert np.array_equal(O.residual_symmetric(A, fi)[I], O.residual(A, fi)[I])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("nthreads", [1, 2, 3, 7, 64])
+def test_pipelined_sweep_matches_serial(prec, nthreads):
+    """The multi-threaded oracle sweep (the CPU reference arm of bench.py) is
+    bitwise equal to the serial sweep in phi; norms to 1e-12."""
+    dims = (13, 11, 9)
+    A = O.generate(0, 1303, dims)
+    F = O.factor(A, 0.92)
+    dt = np.float64 if prec == "f64" else np.float32
+    A = {n: v.astype(dt) for n, v in A.items()}
+    F = {n: v.astype(dt) for n, v in F.items()}
+    p1 = O.field(*dims, dtype=dt)
+    p2 = O.field(*dims, dtype=dt)
+    work = O.field(*dims, dtype=dt)
+    for _ in range(3):
+        n1 = O.sweep(A, F, p1)
+        n2 = O.sweep_pipe(A, F, p2, nthreads, work)
+        assert np.array_equal(p1, p2)
+        assert n2 == pytest.approx(n1, rel=1e-12)
