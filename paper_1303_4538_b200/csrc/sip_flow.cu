@@ -125,36 +125,42 @@ __global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double
 
 // Co-located central divergence of one block; Q = -(V * div) / dt straight
 // into the source array of the system's tile-slice pack (fp64, and the fp32
-// copy in single mode; pinned cell: 0) and the block's L1 partials: one per
-// CTA, summed over its 256 cells by a fixed shuffle tree and the warps in
-// order, so the norm is deterministic.
+// copy in single mode; pinned cell: 0) and the block's L1 partials.  CTA
+// (tile, c) owns the tile's 16 x 16 columns over planes [kDivKC*c, +kDivKC):
+// it reads u, v, w row-wise (coalesced 128-byte rows), keeps Q of the chunk in
+// shared memory in the pack's position order and writes it slice by slice --
+// the chunk's cells of slice t = k + ti + tj are one contiguous position
+// range, so the pack writes are coalesced too.  The partial of a CTA sums its
+// cells in a fixed order (per column over k, fixed shuffle tree, warps in
+// order): deterministic.
+constexpr int kDivKC = 16;
 __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* blocks, int blk,
                                                              const double* u, const double* v,
                                                              const double* w, double c2x, double c2y,
                                                              double c2z, double vol, double dt, int pin,
                                                              double* fw64, float* fw32,
                                                              double* partial) {
-  // CTA (x, k) owns cells [256x, 256x + 256) of plane k (i fastest): a fixed
-  // cell -> CTA map, so the partial sums are deterministic.
+  __shared__ double sq[kDivKC][kTT];
   __shared__ double s[kFlowThreads / 32];
   const BlockDesc bd = blocks[blk];
-  const int nx = bd.nx, ny = bd.ny;
-  const int k = blockIdx.y;
-  const int ij = blockIdx.x * kFlowThreads + threadIdx.x;
+  const int nx = bd.nx, ny = bd.ny, nz = bd.nz;
+  const int ta = blockIdx.x % bd.TX, tb = blockIdx.x / bd.TX;
+  const int i0 = ta * kTI, j0 = tb * kTJ, k0 = blockIdx.y * kDivKC;
+  const int wI = min(kTI, nx - i0), wJ = min(kTJ, ny - j0), wK = min(kDivKC, nz - k0);
+  const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
+  // phase 1: thread (ti, tj) row-major; one column of the chunk per thread
+  const int ti = threadIdx.x % kTI, tj = threadIdx.x / kTI;
+  const int pos = tile_pos(ti, tj);
   double acc = 0.0;
-  if (ij < nx * ny) {
-    const int i = ij % nx, j = ij / nx;
-    const long long x = f3(nx, ny, i + 1, j + 1, k + 1);
-    const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
-    const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
-                      (w[x + sz] - w[x - sz]) / c2z;
-    if (fw64) {
-      const double q = (pin && ij == 0 && k == 0) ? 0.0 : -(vol * dv) / dt;
-      const long long pi = pack_index(bd, F_NA, F_Q, i, j, k);
-      fw64[pi] = q;
-      if (fw32) fw32[pi] = static_cast<float>(q);
+  if (ti < wI && tj < wJ) {
+    for (int kk = 0; kk < wK; ++kk) {
+      const long long x = f3(nx, ny, i0 + ti + 1, j0 + tj + 1, k0 + kk + 1);
+      const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
+                        (w[x + sz] - w[x - sz]) / c2z;
+      const bool pinned = pin && blockIdx.x == 0 && k0 + kk == 0 && ti == 0 && tj == 0;
+      sq[kk][pos] = pinned ? 0.0 : -(vol * dv) / dt;
+      acc += fabs(dv) * vol;
     }
-    acc = fabs(dv) * vol;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -164,6 +170,29 @@ __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* bl
     double t = 0.0;
     for (int r = 0; r < kFlowThreads / 32; ++r) t += s[r];
     partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+  if (!fw64) return;
+  // phase 2: thread = pack position; slice t holds plane t - d of this position
+  int pi = 0, pj = 0;
+  {
+    const int q = threadIdx.x;
+    int dd = 0;
+    while (diag_off(dd + 1) <= q) ++dd;
+    const int lo = dd - (kTJ - 1) > 0 ? dd - (kTJ - 1) : 0;
+    pi = lo + (q - diag_off(dd));
+    pj = dd - pi;
+  }
+  const int d = pi + pj;
+  const bool colok = pi < wI && pj < wJ;
+  const long long slot = bd.slot0 + (long long)(ta + bd.TX * tb) * bd.ns;
+  for (int t = k0; t < k0 + wK + kTI + kTJ - 2; ++t) {
+    const int kk = t - d - k0;
+    if (colok && kk >= 0 && kk < wK) {
+      const double q = sq[kk][threadIdx.x];
+      const long long at = ((slot + t) * F_NA + F_Q) * kTT + threadIdx.x;
+      fw64[at] = q;
+      if (fw32) fw32[at] = static_cast<float>(q);
+    }
   }
 }
 
@@ -343,7 +372,7 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
     const BlockDesc& b = ctx->hblocks[lb];
     const size_t o = ctx->phi_stage_off[lb];
     const long long n = (long long)b.nx * b.ny * b.nz;
-    const dim3 grid((unsigned)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads), (unsigned)b.nz);
+    const dim3 grid((unsigned)(b.TX * b.TY), (unsigned)((b.nz + kDivKC - 1) / kDivKC));
     const int nch = (int)(grid.x * grid.y);
     double* q64 = write_q ? ctx->fw64 : nullptr;
     float* q32 = write_q && ctx->precision == SIP_PREC_SINGLE ? static_cast<float*>(ctx->fw) : nullptr;
@@ -463,8 +492,7 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   for (const BlockDesc& b : ctx->hblocks) {
     total += field3_elems(b);
     fl->max_cells = std::max(fl->max_cells, (long long)b.nx * b.ny * b.nz);
-    fl->max_parts = std::max(fl->max_parts,
-                             (long long)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads) * b.nz);
+    fl->max_parts = std::max(fl->max_parts, (long long)b.TX * b.TY * ((b.nz + kDivKC - 1) / kDivKC));
   }
   auto fail = [&](int s) {
     sip_flow_destroy(fl);
