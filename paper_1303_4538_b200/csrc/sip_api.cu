@@ -661,6 +661,7 @@ int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw, 
   ++ctx->revision;
   if (ctx->symmetric.size() != ctx->local.size()) ctx->symmetric.assign(ctx->local.size(), 0);
   ctx->symmetric[local] = 0;  // a new system is not flagged until sip_set_symmetric
+  ctx->poisson = false;       // no longer the assembled pressure system
   return SIP_OK;
 }
 
@@ -740,6 +741,7 @@ int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed) {
   CK(cudaStreamSynchronize(ctx->stream));
   ++ctx->revision;
   ctx->symmetric.assign(ctx->local.size(), 0);  // generated systems are not flagged
+  ctx->poisson = false;
   return SIP_OK;
 }
 

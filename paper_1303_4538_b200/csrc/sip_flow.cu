@@ -591,6 +591,10 @@ int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_oute
                     SIP_ERR_CONFIG);
   if (fl->plan_gen != ctx->plan_gen)
     return flow_err(ctx, "flow created before the current halo plan: create a new flow", SIP_ERR_MISUSE);
+  if (!ctx->poisson)
+    return flow_err(ctx, "pressure_correct: the context's system is no longer the assembled pressure "
+                         "system (sip_set_system / sip_generate_system since sip_assemble_poisson)",
+                    SIP_ERR_MISUSE);
   CKS(check_ready(ctx));  // factors of the assembled system, reused (never refactored here)
   CKS(set_device(ctx));
   if (outer_used) *outer_used = 0;

@@ -289,5 +289,9 @@ def test_bad_config_and_misuse(gpu):
         fl.divergence()
     fl2 = sip.Flow(s)
     assert fl2.divergence() == 0.0
+    s.generate(0, 7)  # the pressure system is replaced: the caller refuses to run on it
+    s.factor(0.92)
+    with pytest.raises(sip.MisuseError):
+        fl2.pressure_correct(0.1, 0.0, 1, 1)
     s.close()  # closes its flows first
     assert not fl._h and not fl2._h
