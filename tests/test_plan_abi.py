@@ -60,6 +60,10 @@ def test_create_rejects_bad_config():
     assert L.sip_create_lattice(0, 4, 4, 4, 5, 1, 1, None, 0, 1, None, 0,
                                 ctypes.byref(ctx)) == sip.sip.SIP_ERR_CONFIG
     assert b"more blocks" in L.sip_last_error(None)
+    # device kernels index a block's cells with 32-bit arithmetic
+    assert L.sip_create_lattice(0, 4096, 4096, 512, 1, 1, 1, None, 0, 1, None, 0,
+                                ctypes.byref(ctx)) == sip.sip.SIP_ERR_CONFIG
+    assert b"2^32" in L.sip_last_error(None)
 
 
 def load_cases():
