@@ -249,6 +249,7 @@ struct sip_flow {
   long long max_cells = 0;
   long long max_parts = 0;  // divergence partial sums of the largest block
   long long plan_gen = 0;   // the context's halo plan this flow's buffers were sized for
+  double* d_gather = nullptr;  // multi-rank L1: per-block values, send + all-gather receive
 };
 
 namespace {
@@ -325,7 +326,8 @@ int flow_walls(sip_flow* fl, double* const* fields, int nf, const int* sign_mask
 
 // Sum of per-block values over all ranks in global block order (the fixed
 // order makes the result independent of the block placement).
-int allsum_blocks(sip_ctx* ctx, const std::vector<double>& local_vals, double* out) {
+int allsum_blocks(sip_flow* fl, const std::vector<double>& local_vals, double* out) {
+  sip_ctx* ctx = fl->ctx;
   const int nb = (int)ctx->L.blocks.size();
   std::vector<double> all(nb, 0.0);
   if (ctx->nranks == 1) {
@@ -335,9 +337,8 @@ int allsum_blocks(sip_ctx* ctx, const std::vector<double>& local_vals, double* o
     for (int b = 0; b < nb; ++b) blocks_of[ctx->rank_of[b]].push_back(b);
     int maxl = 1;
     for (auto& v : blocks_of) maxl = std::max<int>(maxl, (int)v.size());
-    double *d_send = nullptr, *d_recv = nullptr;
-    CKS(dalloc(ctx, &d_send, sizeof(double) * maxl));
-    CKS(dalloc(ctx, &d_recv, sizeof(double) * maxl * ctx->nranks));
+    double* d_send = fl->d_gather;  // [maxl] send, then [nranks * maxl] receive
+    double* d_recv = fl->d_gather + maxl;
     std::vector<double> pad(maxl, 0.0);
     for (size_t lb = 0; lb < ctx->local.size(); ++lb) pad[lb] = local_vals[lb];
     CK(cudaMemcpyAsync(d_send, pad.data(), sizeof(double) * maxl, cudaMemcpyHostToDevice, ctx->stream));
@@ -346,8 +347,6 @@ int allsum_blocks(sip_ctx* ctx, const std::vector<double>& local_vals, double* o
     CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_send);
-    cudaFree(d_recv);
     for (int r = 0; r < ctx->nranks; ++r)
       for (size_t lb = 0; lb < blocks_of[r].size(); ++lb) all[blocks_of[r][lb]] = got[(size_t)maxl * r + lb];
   }
@@ -387,7 +386,7 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
   CK(cudaMemcpyAsync(vals.data(), fl->d_blocksum, sizeof(double) * vals.size(), cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  return allsum_blocks(ctx, vals, l1);
+  return allsum_blocks(fl, vals, l1);
 }
 
 // p' = 0 (interior and ghosts), `sweeps` SIP iterations, p' -> Field3 mirror
@@ -441,6 +440,12 @@ int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]) {
   const double ax = (h[1] * h[2]) / h[0], ay = (h[0] * h[2]) / h[1], az = (h[0] * h[1]) / h[2];
   const int arr[8] = {F_AP, F_AW, F_AE, F_AS, F_AN, F_AB, F_AT, F_Q};
   ctx->pin_local = ctx->local_of.empty() ? -1 : ctx->local_of[0];  // global cell (0,0,0) is in block 0
+  double** d_out8 = nullptr;  // device copy of the 8 staging array pointers
+  CKS(dalloc(ctx, &d_out8, 8 * sizeof(double*)));
+  struct Free {
+    void* p;
+    ~Free() { cudaFree(p); }
+  } free_out8{d_out8};
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockDesc& hb = ctx->hblocks[lb];
     const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
@@ -450,9 +455,7 @@ int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]) {
     double* out8[8];
     for (int a = 0; a < 8; ++a) out8[a] = ctx->staging + a * G;
     CK(cudaMemsetAsync(ctx->staging, 0, 8 * G * sizeof(double), ctx->stream));
-    double** d_out8 = nullptr;
-    CKS(dalloc(ctx, &d_out8, sizeof(out8)));
-    CK(cudaMemcpy(d_out8, out8, sizeof(out8), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(d_out8, out8, sizeof(out8), cudaMemcpyHostToDevice, ctx->stream));
     const long long n = (long long)hb.nx * hb.ny * hb.nz;
     k_poisson_coeffs<<<grid_for(n), kFlowThreads, 0, ctx->stream>>>(
         hb.nx, hb.ny, hb.nz, make_int4(cpl[0], cpl[1], cpl[2], cpl[3]), make_int2(cpl[4], cpl[5]),
@@ -466,8 +469,7 @@ int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]) {
       CKS(launch_scatter<double>(out8[a], ctx->d_blocks, (int)lb, hb, ctx->fw64, F_NA, arr[a],
                                  ctx->stream));
     }
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_out8);
+    CK(cudaStreamSynchronize(ctx->stream));  // out8 (host array) and staging reused next block
   }
   ++ctx->revision;
   // the identity row of the pinned cell breaks ae(i) = aw(i+1) next to it, so
@@ -504,6 +506,12 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
     s = dalloc(ctx, &fl->partial, sizeof(double) * std::max(1LL, fl->max_parts));
   if (s == SIP_OK) s = dalloc(ctx, &fl->d_blocksum, sizeof(double) * std::max<size_t>(1, ctx->local.size()));
   if (s == SIP_OK) s = dalloc(ctx, &fl->d_off, sizeof(long long) * std::max<size_t>(1, ctx->local.size()));
+  if (s == SIP_OK) {
+    std::vector<int> per_rank(std::max(1, ctx->nranks), 0);
+    for (int r : ctx->rank_of) ++per_rank[r];
+    const int maxl = std::max(1, *std::max_element(per_rank.begin(), per_rank.end()));
+    s = dalloc(ctx, &fl->d_gather, sizeof(double) * (size_t)maxl * (1 + std::max(1, ctx->nranks)));
+  }
   if (s != SIP_OK) return fail(s);
   std::vector<long long> off(ctx->phi_stage_off.begin(), ctx->phi_stage_off.end());
   if (!off.empty() && cudaMemcpy(fl->d_off, off.data(), sizeof(long long) * off.size(),
@@ -530,7 +538,7 @@ int sip_flow_destroy(sip_flow* fl) {
   if (fl->ctx) cudaSetDevice(fl->ctx->device);
   for (double* p : fl->f)
     if (p) cudaFree(p);
-  void* ptrs[] = {fl->d_off, fl->partial, fl->d_blocksum};
+  void* ptrs[] = {fl->d_off, fl->partial, fl->d_blocksum, fl->d_gather};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& pb : fl->pbuf) {
