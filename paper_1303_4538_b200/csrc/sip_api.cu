@@ -595,7 +595,7 @@ int sip_destroy(sip_ctx* ctx) {
                   ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
                   ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
                   ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace,
-                  ctx->tags, ctx->epochs, ctx->rec_phi};
+                  ctx->tags, ctx->epochs, ctx->rec_phi, ctx->d_gather};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->precision == SIP_PREC_SINGLE) {
@@ -890,9 +890,18 @@ int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* bl
     for (int b = 0; b < nb; ++b) blocks_of[ctx->rank_of[b]].push_back(b);
     for (auto& v : blocks_of) maxl = std::max<int>(maxl, (int)v.size());
     const size_t per = (size_t)count * maxl;
-    double *d_send = nullptr, *d_recv = nullptr;
-    CKS(dalloc(ctx, &d_send, sizeof(double) * std::max<size_t>(1, per)));
-    CKS(dalloc(ctx, &d_recv, sizeof(double) * std::max<size_t>(1, per * ctx->nranks)));
+    // persistent gather buffers (sip_solve with a target reads one norm per
+    // iteration: no allocation on that path)
+    const size_t need = std::max<size_t>(1, per) * (1 + ctx->nranks);
+    if (need > ctx->gather_cap) {
+      if (ctx->d_gather) cudaFree(ctx->d_gather);
+      ctx->d_gather = nullptr;
+      ctx->gather_cap = 0;
+      CKS(dalloc(ctx, &ctx->d_gather, sizeof(double) * need));
+      ctx->gather_cap = need;
+    }
+    double* d_send = ctx->d_gather;
+    double* d_recv = ctx->d_gather + std::max<size_t>(1, per);
     std::vector<double> pad(per, 0.0);
     for (int it = 0; it < count; ++it)
       for (int lb = 0; lb < (int)ctx->local.size(); ++lb) pad[(size_t)it * maxl + lb] = bn[(size_t)it * nl + lb];
@@ -902,8 +911,6 @@ int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* bl
     CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_send);
-    cudaFree(d_recv);
     for (int r = 0; r < ctx->nranks; ++r)
       for (int it = 0; it < count; ++it)
         for (size_t lb = 0; lb < blocks_of[r].size(); ++lb)

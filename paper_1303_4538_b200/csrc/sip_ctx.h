@@ -108,6 +108,8 @@ struct sip_ctx {
   // through the NCCL pack / send / recv / unpack path to this rank itself
   bool nccl_self = false;
   long long plan_gen = 0;  // bumped by install_plan (flows are bound to one plan)
+  double* d_gather = nullptr;  // multi-rank norm all-gather buffers (sip_read_norms)
+  size_t gather_cap = 0;       // doubles
   std::string err;
 };
 
