@@ -275,6 +275,11 @@ static int build(sip_ctx* ctx) {
   // tag 0xFFFFFFFF never matches a live (epoch, k) tag (k < 65535)
   CK(cudaMemset(ctx->tags, 0xff, 4 * ctx->tag_words * sizeof(unsigned long long)));
   CKS(dalloc(ctx, &ctx->epochs, 2 * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->d_norm_it, sizeof(unsigned)));
+  // CUDA-graph replay of sip_iterate: measured 1.5 % slower at config 1 (the
+  // 3 launches per 1.1 ms iteration are already enqueued back to back), so it
+  // is opt-in (SIPB_GRAPH=1)
+  if (const char* gr = getenv("SIPB_GRAPH")) ctx->use_graphs = atoi(gr) != 0;
   if (ctx->precision == SIP_PREC_SINGLE) {
     CKS(dalloc(ctx, &ctx->fw64, S * F_NA * sizeof(double)));
     CKS(dalloc(ctx, &ctx->bw64, S * B_NA * sizeof(double)));
@@ -446,8 +451,10 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
   p.state = forward ? ctx->st_f : ctx->st_b;
   p.state_other = forward ? ctx->st_b : ctx->st_f;
   p.partial = ctx->partial;
-  p.block_norms = ctx->d_bnorms + (size_t)it * std::max<size_t>(1, ctx->local.size());
-  p.norm = ctx->d_norms + it;
+  (void)it;  // the iteration's norm slot comes from the device counter d_norm_it
+  p.norms_base = ctx->d_norms;
+  p.bnorms_base = ctx->d_bnorms;
+  p.norm_it = ctx->d_norm_it;
   p.trace = ctx->trace ? ctx->trace + (forward ? 0 : 4 * ctx->htiles.size()) : nullptr;
   p.trace_tile = ctx->trace_tile;
   return p;
@@ -505,8 +512,7 @@ int sipb::exchange(sip_ctx* ctx) {
 }
 
 template <typename T>
-int sipb::iterate_t(sip_ctx* ctx, int iters) {
-  CKS(ensure_norm_cap(ctx, ctx->n_done + iters));
+static int launch_iterations(sip_ctx* ctx, int iters) {
   for (int n = 0; n < iters; ++n) {
     const int it = ctx->n_done + n;
     cudaEvent_t e;
@@ -520,6 +526,57 @@ int sipb::iterate_t(sip_ctx* ctx, int iters) {
     ++ctx->launches;
     ev_end(ctx);
     CKS(exchange<T>(ctx));
+  }
+  return SIP_OK;
+}
+
+static void drop_graph(sip_ctx* ctx) {
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  ctx->graph_exec = nullptr;
+  ctx->graph_iters = -1;
+}
+
+// `iters` iterations.  Single-rank contexts without profiling / tracing replay
+// a CUDA graph of the whole call (edge records, K2, K3 and the local halo
+// copies of every iteration): captured on the first call with this iteration
+// count, re-captured when the halo plan, the norm buffers, the stream or the
+// kernel variant change.  Norm slots come from the device counter, so the
+// replay needs no new parameters.
+template <typename T>
+int sipb::iterate_t(sip_ctx* ctx, int iters) {
+  CKS(ensure_norm_cap(ctx, ctx->n_done + iters));
+  const int sym = sweep_params<T>(ctx, true, 0).symmetric ? 1 : 0;
+  const bool graph = ctx->use_graphs && iters > 0 && !ctx->prof && !ctx->trace && ctx->peers.empty();
+  if (!graph) {
+    CKS(launch_iterations<T>(ctx, iters));
+  } else {
+    if (!(ctx->graph_exec && ctx->graph_iters == iters && ctx->graph_plan == ctx->plan_gen &&
+          ctx->graph_norms == ctx->d_norms && ctx->graph_stream == ctx->stream &&
+          ctx->graph_sym == sym)) {
+      drop_graph(ctx);
+      const long long l0 = ctx->launches;
+      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const int st = launch_iterations<T>(ctx, iters);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+      if (st != SIP_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      CK(ec);
+      const cudaError_t ei = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ei);
+      ctx->graph_launches = ctx->launches - l0;
+      ctx->launches = l0;
+      ctx->graph_iters = iters;
+      ctx->graph_plan = ctx->plan_gen;
+      ctx->graph_norms = ctx->d_norms;
+      ctx->graph_stream = ctx->stream;
+      ctx->graph_sym = sym;
+    }
+    CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+    ctx->launches += ctx->graph_launches;
   }
   ctx->n_done += iters;
   return SIP_OK;
@@ -595,7 +652,8 @@ int sip_destroy(sip_ctx* ctx) {
                   ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
                   ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
                   ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace,
-                  ctx->tags, ctx->epochs, ctx->rec_phi, ctx->d_gather};
+                  ctx->tags, ctx->epochs, ctx->rec_phi, ctx->d_gather, ctx->d_norm_it};
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->precision == SIP_PREC_SINGLE) {
@@ -824,6 +882,7 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi) {
   // interface ghosts <- neighbours' phi0 (the exchange that precedes sweep 1)
   int s = ctx->precision == SIP_PREC_SINGLE ? exchange<float>(ctx) : exchange<double>(ctx);
   ctx->n_done = 0;
+  CK(cudaMemsetAsync(ctx->d_norm_it, 0, sizeof(unsigned), ctx->stream));
   return s;
 }
 
@@ -1133,6 +1192,9 @@ int sip_debug_forward(sip_ctx* ctx) {
   }
   CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
   CK(cudaMemsetAsync(ctx->st_b, 0, st, ctx->stream));
+  // the debug sweep does not count as an iteration: put the norm slot back
+  const unsigned it = (unsigned)ctx->n_done;
+  CK(cudaMemcpyAsync(ctx->d_norm_it, &it, sizeof(it), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
 }

@@ -108,6 +108,16 @@ struct sip_ctx {
   // through the NCCL pack / send / recv / unpack path to this rank itself
   bool nccl_self = false;
   long long plan_gen = 0;  // bumped by install_plan (flows are bound to one plan)
+  unsigned* d_norm_it = nullptr;  // device iteration counter (== n_done between calls)
+  // CUDA graph of one sip_iterate(iters) call (single rank, no profiling,
+  // opt-in): kernels of `iters` iterations captured once and replayed
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_iters = -1;
+  long long graph_plan = -1, graph_launches = 0;
+  const void* graph_norms = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int graph_sym = -1;
+  bool use_graphs = false;  // opt-in: env SIPB_GRAPH=1 at context creation
   double* d_gather = nullptr;  // multi-rank norm all-gather buffers (sip_read_norms)
   size_t gather_cap = 0;       // doubles
   std::string err;

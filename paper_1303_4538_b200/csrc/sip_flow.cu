@@ -398,6 +398,7 @@ int flow_solve(sip_flow* fl, int sweeps) {
   CK(cudaMemsetAsync(ctx->phi, 0, S * sizeof(T), ctx->stream));
   CK(cudaMemsetAsync(ctx->ghost, 0, (size_t)ctx->total_ghost * sizeof(T), ctx->stream));
   ctx->n_done = 0;
+  CK(cudaMemsetAsync(ctx->d_norm_it, 0, sizeof(unsigned), ctx->stream));
   CKS(iterate_t<T>(ctx, sweeps));
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockDesc& b = ctx->hblocks[lb];

@@ -164,8 +164,12 @@ struct SweepParams {
   unsigned* state;        // this sweep: [0] ticket, [1] done, prog at state + 32
   unsigned* state_other;  // the other sweep's state, reset by our finaliser
   double* partial;        // [ntiles] tile norm partials
-  double* block_norms;    // [nblocks] row of this iteration (forward only)
-  double* norm;           // scalar slot of this iteration (forward only)
+  // forward only: norms of iteration it = *norm_it go to norms_base[it] and
+  // bnorms_base[it * nblocks + b]; the finaliser then bumps *norm_it, so a
+  // captured CUDA graph of several iterations replays without new parameters
+  double* norms_base;
+  double* bnorms_base;
+  unsigned* norm_it;
   unsigned long long* trace;  // optional [ntiles][4]: start ns, end ns, smid, cta (debug)
   int trace_tile;             // debug: tile whose per-step times are recorded after the table
 };

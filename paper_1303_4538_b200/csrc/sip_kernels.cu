@@ -823,6 +823,8 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
     if (s_last) {
       // finaliser: deterministic per-block norms, then reset the backward state
       __threadfence();
+      const unsigned it = *P.norm_it;  // iteration index (written by the previous launch)
+      double* bnorms = P.bnorms_base + (size_t)it * P.nblocks;
       const int warp = p >> 5, nw = blockDim.x >> 5;
       for (int b = warp; b < P.nblocks; b += nw) {
         const BlockDesc bb = P.blocks[b];
@@ -830,13 +832,14 @@ __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1
         for (int x2 = (p & 31); x2 < bb.ntiles; x2 += 32) v += __ldcg(P.partial + bb.tile0 + x2);
 #pragma unroll
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if ((p & 31) == 0) P.block_norms[b] = v;
+        if ((p & 31) == 0) bnorms[b] = v;
       }
       __syncthreads();
       if (p == 0) {
         double v = 0.0;
-        for (int b = 0; b < P.nblocks; ++b) v += P.block_norms[b];
-        *P.norm = v;
+        for (int b = 0; b < P.nblocks; ++b) v += bnorms[b];
+        P.norms_base[it] = v;
+        *P.norm_it = it + 1;
       }
       for (int x2 = p; x2 < kProgOff + P.ntiles; x2 += blockDim.x) P.state_other[x2] = 0u;
       if (p == 0) *P.epoch = epoch + 1;

@@ -556,3 +556,41 @@ def test_config4_full_size_first_iteration_parity(gpu):
             O.solve(A, phi, 0.92, 1, "f32")
             assert np.array_equal(f[1:-1, 1:-1, 1:-1], phi[1:-1, 1:-1, 1:-1]), bid
     assert n[0] == pytest.approx(qsum, rel=1e-6)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_cuda_graph_replay_matches_oracle(gpu, prec):
+    """sip_iterate through a captured CUDA graph (SIPB_GRAPH=1; replayed for
+    every call with the same iteration count, norm slots from the device
+    counter) gives the oracle's phi bitwise and its norms."""
+    import os
+    old = os.environ.get("SIPB_GRAPH")
+    os.environ["SIPB_GRAPH"] = "1"
+    try:
+        g, pd = (40, 24, 20), (2, 1, 1)
+        s = sip.Solver(None, prec, 0, lattice=(g, pd))
+        s._nglobal = 2
+        origins, dims, nbr = O.lattice(g, pd)
+        As = []
+        for lb, (bid, d, o) in enumerate(s.blocks):
+            A = O.generate(0, 1303 + 21 + bid, d, g, o)
+            As.append(A)
+            s.set_system(lb, sip.StencilSystem.from_dict(A))
+        s.factor(0.92)
+        phis = [O.field(*d) for (_, d, _) in s.blocks]
+        s.load_phi(phis)
+        for _ in range(3):
+            s.iterate(2)  # capture once, replay twice
+        ng = s.read_norms(0, 6)
+        s.store_phi(phis)
+        s.close()
+    finally:
+        if old is None:
+            del os.environ["SIPB_GRAPH"]
+        else:
+            os.environ["SIPB_GRAPH"] = old
+    blocks = [(As[b], O.field(*dims[b])) for b in range(2)]
+    no, _ = O.solve_multi(blocks, nbr, 0.92, 6, prec)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
+    for b in range(2):
+        assert np.array_equal(phis[b], blocks[b][1])
