@@ -454,7 +454,11 @@ constexpr int kBarCrit = 1, kBarRes = 2, kBarFull = 3, kBarEmpty = kBarFull + kP
 // measured 6 % slower).
 template <typename T, bool SYM>
 __host__ __device__ constexpr bool k2_edge_warp() { return sizeof(T) == 4 && !SYM; }
-constexpr int kPollK2 = 3;  // K2 edge-warp poll ring (tile step ~0.5-0.9 us under load)
+#ifdef SIPB_EXP_PD2
+constexpr int kPollK2 = SIPB_EXP_PD2;
+#else
+constexpr int kPollK2 = 2;  // K2 edge-warp poll ring (tile step ~0.5-0.9 us; 2: -1 % vs 3)
+#endif
 
 template <typename T, bool SYM>
 __global__ void __launch_bounds__(2 * kTT + (k2_edge_warp<T, SYM>() ? 32 : 0), 1)
