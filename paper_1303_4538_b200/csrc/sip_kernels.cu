@@ -428,7 +428,9 @@ __device__ __forceinline__ void edge_warp_run(const EdgeLane<T>& e, const T (*s_
   publish(e.NS - 1);
 }
 
-#ifdef SIPB_EXP_PD
+#if defined(SIPB_EXP_PD64)
+constexpr int kPollK3 = SIPB_EXP_PD64, kPollK3f = 12;
+#elif defined(SIPB_EXP_PD)
 constexpr int kPollK3 = 8, kPollK3f = SIPB_EXP_PD;
 #else
 // K3 poll rings: issued kPoll - 1 steps ahead (tile step ~0.3 us fp64,
