@@ -173,7 +173,6 @@ def make_solver(cfg_id, prec, rank, world, device, nccl_id=None):
     else:
         g, p = c["g"], c["p"]
     s = sip.Solver(None, prec, device, lattice=(g, p), rank=rank, nranks=world, nccl_id=nccl_id)
-    s._nglobal = p[0] * p[1] * p[2]
     s._g = g
     return s, g, p
 

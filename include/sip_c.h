@@ -183,8 +183,13 @@ int sip_get_profile(sip_ctx* ctx, double* fwd_ms, double* bwd_ms, double* halo_m
                     long long* launches);
 /* Total kernel launches enqueued by this context so far. */
 long long sip_launch_count(const sip_ctx* ctx);
-/* Tile geometry of the wavefront kernels (TI, TJ, tiles, slices). */
+/* Brick geometry of the wavefront kernels: brick extents along i and j
+ * (kW, kL), number of bricks, slices of the forward / backward packs. */
 int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long long* slices);
+/* Factorisation counter: K1 launches of this context so far. */
+long long sip_factor_count(const sip_ctx* ctx);
+/* Blocks of the whole lattice (all ranks): sizes sip_read_norms' block_norms. */
+int sip_num_global_blocks(const sip_ctx* ctx, int* n);
 
 /* ---- debugging / test helpers (not part of the reference interface) ---- */
 /* One forward sweep (K2) on the current device phi (writes R). */

@@ -189,7 +189,7 @@ int sipb::install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
 }
 
 static int build(sip_ctx* ctx) {
-  // local blocks and their tiles
+  // local blocks and their bricks (sip_internal.h layout)
   const int nb = (int)ctx->L.blocks.size();
   ctx->local_of.assign(nb, -1);
   for (int b = 0; b < nb; ++b)
@@ -197,97 +197,115 @@ static int build(sip_ctx* ctx) {
       ctx->local_of[b] = (int)ctx->local.size();
       ctx->local.push_back(b);
     }
-  long long slot = 0, edge = 0, ghost = 0;
+  long long slot = 0, pslot = 0, medge = 0, mrow = 0;
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockInfo& bi = ctx->L.blocks[ctx->local[lb]];
     BlockDesc bd{};
     bd.id = ctx->local[lb];
     bd.nx = bi.n[0]; bd.ny = bi.n[1]; bd.nz = bi.n[2];
-    bd.TX = (bd.nx + kTI - 1) / kTI;
-    bd.TY = (bd.ny + kTJ - 1) / kTJ;
-    bd.ns = bd.nz + kD - 1;
+    bd.BX = (bd.nx + kW - 1) / kW;
+    bd.BY = (bd.ny + kL - 1) / kL;
+    bd.ns = bd.nz * kW + kL;
+    bd.brick0 = (int)ctx->hbricks.size();
+    bd.nbricks = bd.BX * bd.BY;
+    bd.gE = bd.nx % kW == 0;
+    bd.gN = bd.ny % kL == 0;
     bd.slot0 = slot;
-    bd.ghost = ghost;
-    bd.tile0 = (int)ctx->htiles.size();
-    bd.ntiles = bd.TX * bd.TY;
-    for (int c = 0; c < bd.TY; ++c)
-      for (int a = 0; a < bd.TX; ++a) {
-        TileDesc td{};
-        td.slot = slot;
-        td.edge = edge;
-        td.block = (int)lb;
-        td.i0 = a * kTI; td.j0 = c * kTJ;
-        td.wI = std::min(kTI, bd.nx - td.i0);
-        td.wJ = std::min(kTJ, bd.ny - td.j0);
-        auto idx = [&](int aa, int cc) { return bd.tile0 + aa + bd.TX * cc; };
-        td.nW = a > 0 ? idx(a - 1, c) : -1;
-        td.nE = a + 1 < bd.TX ? idx(a + 1, c) : -1;
-        td.nS = c > 0 ? idx(a, c - 1) : -1;
-        td.nN = c + 1 < bd.TY ? idx(a, c + 1) : -1;
-        td.ns = bd.ns;
-        td.nz = bd.nz;
-        ctx->htiles.push_back(td);
-        slot += bd.ns;
-        edge += (long long)bd.nz * std::max(kTI, kTJ);
+    bd.pbase = pslot;
+    bd.medge0 = medge;
+    bd.mrow0 = mrow;
+    const long long me = (long long)kL * bd.nz, mr = (long long)kW * bd.nz;
+    for (int bj = 0; bj < bd.BY; ++bj)
+      for (int bi = 0; bi < bd.BX; ++bi) {
+        const int r = bi + bd.BX * bj;
+        BrickDesc k{};
+        k.slot = slot + (long long)r * bd.ns;
+        k.pslot = phi_slot(bd, r);
+        k.pW = bi > 0 ? phi_slot(bd, r - 1) : phi_slot(bd, bd.nbricks + bj);
+        k.pE = bi + 1 < bd.BX ? phi_slot(bd, r + 1) : bd.gE ? phi_slot(bd, bd.nbricks + bd.BY + bj) : k.pslot;
+        k.pS = bj > 0 ? phi_slot(bd, r - bd.BX) : phi_slot(bd, bd.nbricks + bd.BY * (1 + bd.gE) + bi);
+        k.pN = bj + 1 < bd.BY ? phi_slot(bd, r + bd.BX)
+               : bd.gN ? phi_slot(bd, bd.nbricks + bd.BY * (1 + bd.gE) + bd.BX + bi) : k.pslot;
+        k.medge = medge + r * me;
+        k.mrow = mrow + r * mr;
+        k.mWe = bi > 0 ? medge + (r - 1) * me : -1;
+        k.mEe = bi + 1 < bd.BX ? medge + (r + 1) * me : -1;
+        k.mSr = bj > 0 ? mrow + (r - bd.BX) * mr : -1;
+        k.mNr = bj + 1 < bd.BY ? mrow + (r + bd.BX) * mr : -1;
+        k.block = (int)lb;
+        k.bi = bi; k.bj = bj;
+        k.i0 = bi * kW; k.j0 = bj * kL;
+        k.wI = std::min(kW, bd.nx - k.i0);
+        k.wJ = std::min(kL, bd.ny - k.j0);
+        k.nz = bd.nz;
+        k.ns = bd.ns;
+        ctx->hbricks.push_back(k);
       }
-    ghost += ghost_count(bd.nx, bd.ny, bd.nz);
+    slot += (long long)bd.nbricks * bd.ns;
+    pslot += (long long)phi_bricks(bd) * phi_stride(bd);
+    medge += (long long)bd.nbricks * me;
+    mrow += (long long)bd.nbricks * mr;
     ctx->hblocks.push_back(bd);
     ctx->gmax = std::max(ctx->gmax, field3_elems(bd));
   }
   ctx->total_slices = slot;
-  ctx->total_edge = edge;
-  ctx->total_ghost = ghost;
-  const int nt = (int)ctx->htiles.size();
-  // topological ticket order: anti-diagonal of the tile lattice, then block
+  ctx->total_phi_slices = pslot;
+  ctx->total_edge = medge;
+  ctx->total_row = mrow;
+  const int nt = (int)ctx->hbricks.size();
+  // topological ticket order: a brick lags its W neighbour by about one
+  // stage plus the hand-off latency and its S neighbour by about kL steps,
+  // so order by bi + 2 bj (ties: block, then bi)
   std::vector<std::tuple<int, int, int, int>> keys;
   for (int t = 0; t < nt; ++t) {
-    const TileDesc& td = ctx->htiles[t];
-    keys.emplace_back(td.i0 / kTI + td.j0 / kTJ, td.block, td.i0, t);
+    const BrickDesc& k = ctx->hbricks[t];
+    keys.emplace_back(k.bi + 2 * k.bj, k.block, k.bi, t);
   }
   std::sort(keys.begin(), keys.end());
   for (auto& k : keys) ctx->order_f.push_back(std::get<3>(k));
   ctx->order_b.assign(ctx->order_f.rbegin(), ctx->order_f.rend());
 
   const size_t es = ctx->esize;
-  const size_t TT = kTT;
   CKS(dalloc(ctx, &ctx->d_blocks, sizeof(BlockDesc) * std::max<size_t>(1, ctx->hblocks.size())));
-  CKS(dalloc(ctx, &ctx->d_tiles, sizeof(TileDesc) * std::max(1, nt)));
+  CKS(dalloc(ctx, &ctx->d_bricks, sizeof(BrickDesc) * std::max(1, nt)));
   CKS(dalloc(ctx, &ctx->d_order_f, sizeof(int) * std::max(1, nt)));
   CKS(dalloc(ctx, &ctx->d_order_b, sizeof(int) * std::max(1, nt)));
   if (nt) {
     CK(cudaMemcpy(ctx->d_blocks, ctx->hblocks.data(), sizeof(BlockDesc) * ctx->hblocks.size(),
                   cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->d_tiles, ctx->htiles.data(), sizeof(TileDesc) * nt, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bricks, ctx->hbricks.data(), sizeof(BrickDesc) * nt, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_order_f, ctx->order_f.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_order_b, ctx->order_b.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
   }
-  const size_t S = (size_t)ctx->total_slices * TT;
+  const size_t S = (size_t)ctx->total_slices * kL;
   CKS(dalloc(ctx, &ctx->fw, S * F_NA * es));
   CKS(dalloc(ctx, &ctx->bw, S * B_NA * es));
-  CKS(dalloc(ctx, &ctx->phi, S * es));
   CKS(dalloc(ctx, &ctx->R, S * es));
-  CKS(dalloc(ctx, &ctx->ghost, (size_t)ctx->total_ghost * es));
-  CKS(dalloc(ctx, &ctx->edgeW, (size_t)ctx->total_edge * es));
-  CKS(dalloc(ctx, &ctx->edgeS, (size_t)ctx->total_edge * es));
-  CKS(dalloc(ctx, &ctx->rec_phi, (size_t)ctx->total_slices * 64 * es));
-  ctx->tag_words = (size_t)std::max(1LL, ctx->total_edge) * (es / 4);
-  CKS(dalloc(ctx, &ctx->tags, 4 * ctx->tag_words * sizeof(unsigned long long)));
-  // tag 0xFFFFFFFF never matches a live (epoch, k) tag (k < 65535)
-  CK(cudaMemset(ctx->tags, 0xff, 4 * ctx->tag_words * sizeof(unsigned long long)));
-  CKS(dalloc(ctx, &ctx->epochs, 2 * sizeof(unsigned)));
-  CKS(dalloc(ctx, &ctx->d_norm_it, sizeof(unsigned)));
-  // CUDA-graph replay of sip_iterate: measured 1.5 % slower at config 1 (the
-  // 3 launches per 1.1 ms iteration are already enqueued back to back), so it
-  // is opt-in (SIPB_GRAPH=1)
-  if (const char* gr = getenv("SIPB_GRAPH")) ctx->use_graphs = atoi(gr) != 0;
+  CKS(dalloc(ctx, &ctx->phi, (size_t)ctx->total_phi_slices * kL * es));
   if (ctx->precision == SIP_PREC_SINGLE) {
-    CKS(dalloc(ctx, &ctx->fw64, S * F_NA * sizeof(double)));
-    CKS(dalloc(ctx, &ctx->bw64, S * B_NA * sizeof(double)));
+    CKS(dalloc(ctx, &ctx->coef64, S * C_NA * sizeof(double)));
+    ctx->coef_na = C_NA;
   } else {
-    ctx->fw64 = static_cast<double*>(ctx->fw);
-    ctx->bw64 = static_cast<double*>(ctx->bw);
+    ctx->coef64 = static_cast<double*>(ctx->fw);
+    ctx->coef_na = F_NA;
   }
-  const size_t st = 32 + (size_t)std::max(1, nt);
+  // mailboxes: edge entries (kL * nz per brick) and row entries (kW * nz per
+  // brick); words per entry: es / 4 (K2, K3), 6 (K1: three fp64 values)
+  const size_t ew = es / 4;
+  const size_t words[6] = {ew * ctx->total_edge, ew * ctx->total_row, ew * ctx->total_edge,
+                           ew * ctx->total_row, 6 * (size_t)ctx->total_edge, 6 * (size_t)ctx->total_row};
+  for (int m = 0; m < 6; ++m) {
+    ctx->mbox_bytes[m] = std::max<size_t>(1, words[m]) * sizeof(unsigned long long);
+    CKS(dalloc(ctx, &ctx->mbox[m], ctx->mbox_bytes[m]));
+    // tag 0xFFFFFFFF never matches a live epoch
+    CK(cudaMemset(ctx->mbox[m], 0xff, ctx->mbox_bytes[m]));
+  }
+  CKS(dalloc(ctx, &ctx->epochs, 4 * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->d_norm_it, sizeof(unsigned)));
+  // CUDA-graph replay of sip_iterate is opt-in (SIPB_GRAPH=1): the two
+  // launches per iteration are already enqueued back to back
+  if (const char* gr = getenv("SIPB_GRAPH")) ctx->use_graphs = atoi(gr) != 0;
+  const size_t st = 32;
   CKS(dalloc(ctx, &ctx->st_f, st * sizeof(unsigned)));
   CKS(dalloc(ctx, &ctx->st_b, st * sizeof(unsigned)));
   CKS(dalloc(ctx, &ctx->st_fac, st * sizeof(unsigned)));
@@ -428,35 +446,29 @@ static int ensure_norm_cap(sip_ctx* ctx, int need) {
 }
 
 template <typename T>
-static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward, int it) {
+static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward) {
   SweepParams<T> p{};
-  p.tiles = ctx->d_tiles;
+  p.bricks = ctx->d_bricks;
   p.blocks = ctx->d_blocks;
   p.order = forward ? ctx->d_order_f : ctx->d_order_b;
-  p.ntiles = (int)ctx->htiles.size();
+  p.nbricks = (int)ctx->hbricks.size();
   p.nblocks = (int)ctx->hblocks.size();
   p.fw = static_cast<T*>(ctx->fw);
   p.bw = static_cast<T*>(ctx->bw);
   p.phi = static_cast<T*>(ctx->phi);
   p.R = static_cast<T*>(ctx->R);
-  p.ghost = static_cast<T*>(ctx->ghost);
-  p.edgeW = static_cast<T*>(ctx->edgeW);
-  p.edgeS = static_cast<T*>(ctx->edgeS);
-  p.rec_phi = static_cast<T*>(ctx->rec_phi);
-  p.symmetric = !ctx->symmetric.empty() && ctx->symmetric.size() == ctx->local.size() &&
-                std::all_of(ctx->symmetric.begin(), ctx->symmetric.end(), [](char c) { return c != 0; });
-  p.tagA = ctx->tags + (forward ? 0 : 2) * ctx->tag_words;
-  p.tagB = ctx->tags + (forward ? 1 : 3) * ctx->tag_words;
+  p.mA = ctx->mbox[forward ? 0 : 2];
+  p.mB = ctx->mbox[forward ? 1 : 3];
   p.epoch = ctx->epochs + (forward ? 0 : 1);
   p.state = forward ? ctx->st_f : ctx->st_b;
   p.state_other = forward ? ctx->st_b : ctx->st_f;
   p.partial = ctx->partial;
-  (void)it;  // the iteration's norm slot comes from the device counter d_norm_it
+  // the iteration's norm slot comes from the device counter d_norm_it
   p.norms_base = ctx->d_norms;
   p.bnorms_base = ctx->d_bnorms;
   p.norm_it = ctx->d_norm_it;
-  p.trace = ctx->trace ? ctx->trace + (forward ? 0 : 4 * ctx->htiles.size()) : nullptr;
-  p.trace_tile = ctx->trace_tile;
+  p.trace = ctx->trace ? ctx->trace + (forward ? 0 : 4 * ctx->hbricks.size()) : nullptr;
+  p.trace_brick = ctx->trace_brick;
   return p;
 }
 
@@ -479,17 +491,16 @@ int sipb::exchange(sip_ctx* ctx) {
   cudaEvent_t e;
   ev_begin(ctx, 2, &e);
   T* phi = static_cast<T*>(ctx->phi);
-  T* ghost = static_cast<T*>(ctx->ghost);
   if (!ctx->local_copies.empty()) {
     CKS(launch_face_copies<T>(ctx->d_local_copies, (int)ctx->local_copies.size(),
-                              ctx->local_max_plane, ctx->d_blocks, phi, ghost, nullptr, nullptr,
+                              ctx->local_max_plane, ctx->d_blocks, phi, nullptr, nullptr,
                               ctx->stream));
     ++ctx->launches;
   }
   if (!ctx->peers.empty()) {
     for (Peer& p : ctx->peers) {
       CKS(launch_face_copies<T>(p.d_pack, (int)p.pack.size(), p.max_plane, ctx->d_blocks, phi,
-                                ghost, nullptr, static_cast<T*>(p.sbuf), ctx->stream));
+                                nullptr, static_cast<T*>(p.sbuf), ctx->stream));
       ++ctx->launches;
     }
     const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
@@ -503,7 +514,7 @@ int sipb::exchange(sip_ctx* ctx) {
     CKN(nccl().GroupEnd());
     for (Peer& p : ctx->peers) {
       CKS(launch_face_copies<T>(p.d_unpack, (int)p.unpack.size(), p.max_plane, ctx->d_blocks, phi,
-                                ghost, static_cast<T*>(p.rbuf), nullptr, ctx->stream));
+                                static_cast<T*>(p.rbuf), nullptr, ctx->stream));
       ++ctx->launches;
     }
   }
@@ -514,15 +525,14 @@ int sipb::exchange(sip_ctx* ctx) {
 template <typename T>
 static int launch_iterations(sip_ctx* ctx, int iters) {
   for (int n = 0; n < iters; ++n) {
-    const int it = ctx->n_done + n;
+    (void)n;
     cudaEvent_t e;
     ev_begin(ctx, 0, &e);
-    CKS(launch_edge_phi<T>(sweep_params<T>(ctx, true, it), ctx->stream));
-    CKS(launch_forward<T>(sweep_params<T>(ctx, true, it), ctx->grid_f, ctx->stream));
-    ctx->launches += 2;
+    CKS(launch_forward<T>(sweep_params<T>(ctx, true), ctx->grid_f, ctx->stream));
+    ++ctx->launches;
     ev_end(ctx);
     ev_begin(ctx, 1, &e);
-    CKS(launch_backward<T>(sweep_params<T>(ctx, false, it), ctx->grid_b, ctx->stream));
+    CKS(launch_backward<T>(sweep_params<T>(ctx, false), ctx->grid_b, ctx->stream));
     ++ctx->launches;
     ev_end(ctx);
     CKS(exchange<T>(ctx));
@@ -545,7 +555,7 @@ static void drop_graph(sip_ctx* ctx) {
 template <typename T>
 int sipb::iterate_t(sip_ctx* ctx, int iters) {
   CKS(ensure_norm_cap(ctx, ctx->n_done + iters));
-  const int sym = sweep_params<T>(ctx, true, 0).symmetric ? 1 : 0;
+  const int sym = 0;  // one forward kernel for general and symmetric systems
   const bool graph = ctx->use_graphs && iters > 0 && !ctx->prof && !ctx->trace && ctx->peers.empty();
   if (!graph) {
     CKS(launch_iterations<T>(ctx, iters));
@@ -593,6 +603,42 @@ int sipb::check_ready(sip_ctx* ctx) {
     return SIP_ERR_STALE;
   }
   return SIP_OK;
+}
+
+// One Field3 array (device staging) of a local block into the packs: the
+// forward pack in the context precision and, in single mode, the fp64
+// coefficient pack the factorisation reads (AP..AT; Q is not needed there).
+int sipb::scatter_array(sip_ctx* ctx, int local, const double* src, int arr) {
+  const BlockDesc& hb = ctx->hblocks[local];
+  if (ctx->precision == SIP_PREC_SINGLE) {
+    CKS(launch_scatter<float>(src, ctx->d_blocks, local, hb, static_cast<float*>(ctx->fw), F_NA, arr,
+                              ctx->stream));
+    if (arr < C_NA) CKS(launch_scatter<double>(src, ctx->d_blocks, local, hb, ctx->coef64, C_NA, arr, ctx->stream));
+  } else {
+    CKS(launch_scatter<double>(src, ctx->d_blocks, local, hb, static_cast<double*>(ctx->fw), F_NA, arr,
+                               ctx->stream));
+  }
+  return SIP_OK;
+}
+
+template <typename T>
+static FactorParams<T> factor_params(sip_ctx* ctx, double alpha) {
+  FactorParams<T> fp{};
+  fp.bricks = ctx->d_bricks;
+  fp.blocks = ctx->d_blocks;
+  fp.order = ctx->d_order_f;
+  fp.nbricks = (int)ctx->hbricks.size();
+  fp.alpha = alpha;
+  fp.coef = ctx->coef64;
+  fp.coef_na = ctx->coef_na;
+  fp.fw = static_cast<T*>(ctx->fw);
+  fp.bw = static_cast<T*>(ctx->bw);
+  fp.mA = ctx->mbox[4];
+  fp.mB = ctx->mbox[5];
+  fp.epoch = ctx->epochs + 2;
+  fp.state = ctx->st_fac;
+  fp.bad = ctx->d_bad;
+  return fp;
 }
 
 template int sipb::exchange<float>(sip_ctx*);
@@ -648,18 +694,17 @@ int sip_destroy(sip_ctx* ctx) {
     cudaEventDestroy(std::get<1>(e));
     cudaEventDestroy(std::get<2>(e));
   }
-  void* ptrs[] = {ctx->d_blocks, ctx->d_tiles, ctx->d_order_f, ctx->d_order_b, ctx->fw, ctx->bw,
-                  ctx->phi, ctx->R, ctx->ghost, ctx->edgeW, ctx->edgeS, ctx->st_f, ctx->st_b,
-                  ctx->st_fac, ctx->partial, ctx->d_norms, ctx->d_bnorms, ctx->d_bad,
-                  ctx->staging, ctx->d_local_copies, ctx->phi_stage, ctx->trace,
-                  ctx->tags, ctx->epochs, ctx->rec_phi, ctx->d_gather, ctx->d_norm_it};
+  void* ptrs[] = {ctx->d_blocks, ctx->d_bricks, ctx->d_order_f, ctx->d_order_b, ctx->fw, ctx->bw,
+                  ctx->phi, ctx->R, ctx->st_f, ctx->st_b, ctx->st_fac, ctx->partial, ctx->d_norms,
+                  ctx->d_bnorms, ctx->d_bad, ctx->staging, ctx->d_local_copies, ctx->phi_stage,
+                  ctx->trace, ctx->epochs, ctx->d_gather, ctx->d_norm_it, ctx->d_pad};
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (ctx->precision == SIP_PREC_SINGLE) {
-    if (ctx->fw64) cudaFree(ctx->fw64);
-    if (ctx->bw64) cudaFree(ctx->bw64);
-  }
+  for (auto* m : ctx->mbox)
+    if (m) cudaFree(m);
+  if (ctx->precision == SIP_PREC_SINGLE && ctx->coef64) cudaFree(ctx->coef64);
+  if (ctx->h_pad) cudaFreeHost(ctx->h_pad);
   for (Peer& p : ctx->peers) {
     if (p.d_pack) cudaFree(p.d_pack);
     if (p.d_unpack) cudaFree(p.d_unpack);
@@ -708,12 +753,7 @@ int sip_set_system(sip_ctx* ctx, int local, const double* ap, const double* aw, 
   const size_t G = field3_elems(hb);
   for (int a = 0; a < 8; ++a) {
     CK(cudaMemcpyAsync(ctx->staging, src[a], G * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    if (ctx->precision == SIP_PREC_SINGLE) {
-      CKS(launch_scatter<float>(ctx->staging, ctx->d_blocks, local, hb, static_cast<float*>(ctx->fw),
-                                F_NA, arr[a], ctx->stream));
-    }
-    CKS(launch_scatter<double>(ctx->staging, ctx->d_blocks, local, hb, ctx->fw64, F_NA, arr[a],
-                               ctx->stream));
+    CKS(scatter_array(ctx, local, ctx->staging, arr[a]));
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ++ctx->revision;
@@ -738,7 +778,7 @@ int sip_set_symmetric(sip_ctx* ctx, int local, int symmetric) {
   const BlockDesc& hb = ctx->hblocks[local];
   unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->staging);
   CK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), ctx->stream));
-  CKS(launch_check_symmetric(ctx->d_blocks, local, hb, ctx->fw64, bad, ctx->stream));
+  CKS(launch_check_symmetric(ctx->d_blocks, local, hb, ctx->coef64, ctx->coef_na, bad, ctx->stream));
   ++ctx->launches;
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -762,11 +802,7 @@ int sip_set_source(sip_ctx* ctx, int local, const double* q) {
   const BlockDesc& hb = ctx->hblocks[local];
   CK(cudaMemcpyAsync(ctx->staging, q, field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
                      ctx->stream));
-  if (ctx->precision == SIP_PREC_SINGLE)
-    CKS(launch_scatter<float>(ctx->staging, ctx->d_blocks, local, hb, static_cast<float*>(ctx->fw),
-                              F_NA, F_Q, ctx->stream));
-  CKS(launch_scatter<double>(ctx->staging, ctx->d_blocks, local, hb, ctx->fw64, F_NA, F_Q,
-                             ctx->stream));
+  CKS(scatter_array(ctx, local, ctx->staging, F_Q));
   return SIP_OK;
 }
 
@@ -788,13 +824,7 @@ int sip_generate_system(sip_ctx* ctx, int kind, uint64_t seed) {
     const int g[3] = {ctx->L.g[0], ctx->L.g[1], ctx->L.g[2]};
     CKS(launch_generate(kind, seed + (uint64_t)ctx->local[lb], g, bi.lo.data(), hb.nx, hb.ny, hb.nz, out8,
                         ctx->stream));
-    for (int a = 0; a < 8; ++a) {
-      if (ctx->precision == SIP_PREC_SINGLE)
-        CKS(launch_scatter<float>(out8[a], ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
-                                  F_NA, arr[a], ctx->stream));
-      CKS(launch_scatter<double>(out8[a], ctx->d_blocks, (int)lb, hb, ctx->fw64, F_NA, arr[a],
-                                 ctx->stream));
-    }
+    for (int a = 0; a < 8; ++a) CKS(scatter_array(ctx, (int)lb, out8[a], arr[a]));
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ++ctx->revision;
@@ -810,28 +840,16 @@ int sip_factor(sip_ctx* ctx, double alpha, long long* bad_block, long long* bad_
     return SIP_ERR_CONFIG;
   }
   CKS(set_device(ctx));
-  const int nt = (int)ctx->htiles.size();
-  CK(cudaMemsetAsync(ctx->st_fac, 0, (32 + (size_t)std::max(1, nt)) * sizeof(unsigned), ctx->stream));
+  const int nt = (int)ctx->hbricks.size();
+  CK(cudaMemsetAsync(ctx->st_fac, 0, 32 * sizeof(unsigned), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_bad, 0xff, sizeof(unsigned long long), ctx->stream));
-  FactorParams fp{};
-  fp.tiles = ctx->d_tiles;
-  fp.blocks = ctx->d_blocks;
-  fp.order = ctx->d_order_f;
-  fp.ntiles = nt;
-  fp.alpha = alpha;
-  fp.fw = ctx->fw64;
-  fp.bw = ctx->bw64;
-  fp.state = ctx->st_fac;
-  fp.bad = ctx->d_bad;
   if (nt) {
-    CKS(launch_factor(fp, ctx->grid_fac, ctx->stream));
+    if (ctx->precision == SIP_PREC_SINGLE)
+      CKS(launch_factor<float>(factor_params<float>(ctx, alpha), ctx->grid_fac, ctx->stream));
+    else
+      CKS(launch_factor<double>(factor_params<double>(ctx, alpha), ctx->grid_fac, ctx->stream));
     ++ctx->launches;
-  }
-  if (ctx->precision == SIP_PREC_SINGLE) {
-    const long long S = ctx->total_slices * kTT;
-    CKS(launch_convert(ctx->fw64, static_cast<float*>(ctx->fw), S * F_NA, ctx->stream));
-    CKS(launch_convert(ctx->bw64, static_cast<float*>(ctx->bw), S * B_NA, ctx->stream));
-    ctx->launches += 2;
+    ++ctx->factor_count;
   }
   unsigned long long bad = ~0ULL;
   CK(cudaMemcpyAsync(&bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
@@ -866,18 +884,11 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi) {
     // Field3 -> device mirror (keeps the caller's ghost layer for the store)
     CK(cudaMemcpyAsync(st, phi[lb], field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
                        ctx->stream));
-    if (ctx->precision == SIP_PREC_SINGLE) {
-      CKS(launch_scatter<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->phi), 1, 0,
-                                ctx->stream));
-      CKS(launch_ghost_in<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->ghost),
-                                 ctx->stream));
-    } else {
-      CKS(launch_scatter<double>(st, ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->phi), 1,
-                                 0, ctx->stream));
-      CKS(launch_ghost_in<double>(st, ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->ghost),
-                                  ctx->stream));
-    }
-    ctx->launches += 2;
+    if (ctx->precision == SIP_PREC_SINGLE)
+      CKS(launch_phi_in<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->phi), ctx->stream));
+    else
+      CKS(launch_phi_in<double>(st, ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->phi), ctx->stream));
+    ++ctx->launches;
   }
   // interface ghosts <- neighbours' phi0 (the exchange that precedes sweep 1)
   int s = ctx->precision == SIP_PREC_SINGLE ? exchange<float>(ctx) : exchange<double>(ctx);
@@ -897,11 +908,11 @@ int sip_store_phi(sip_ctx* ctx, double* const* phi) {
     // loaded by sip_load_phi
     const int* written = ctx->plan_ghosts[lb].data();
     if (ctx->precision == SIP_PREC_SINGLE)
-      CKS(launch_gather<float>(static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost),
-                               ctx->d_blocks, (int)lb, hb, written, st, ctx->stream));
+      CKS(launch_gather<float>(static_cast<float*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
+                               ctx->stream));
     else
-      CKS(launch_gather<double>(static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
-                                ctx->d_blocks, (int)lb, hb, written, st, ctx->stream));
+      CKS(launch_gather<double>(static_cast<double*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
+                                ctx->stream));
     ++ctx->launches;
     CK(cudaMemcpyAsync(phi[lb], st, field3_elems(hb) * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -961,10 +972,19 @@ int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* bl
     }
     double* d_send = ctx->d_gather;
     double* d_recv = ctx->d_gather + std::max<size_t>(1, per);
-    std::vector<double> pad(per, 0.0);
+    if (per > ctx->h_pad_cap) {
+      if (ctx->h_pad) cudaFreeHost(ctx->h_pad);
+      ctx->h_pad = nullptr;
+      ctx->h_pad_cap = 0;
+      CK(cudaMallocHost(&ctx->h_pad, per * sizeof(double)));
+      ctx->h_pad_cap = per;
+    }
+    double* pad = ctx->h_pad;
+    std::fill(pad, pad + per, 0.0);
     for (int it = 0; it < count; ++it)
       for (int lb = 0; lb < (int)ctx->local.size(); ++lb) pad[(size_t)it * maxl + lb] = bn[(size_t)it * nl + lb];
-    CK(cudaMemcpy(d_send, pad.data(), per * sizeof(double), cudaMemcpyHostToDevice));
+    // stream-ordered with the all-gather (the context stream is non-blocking)
+    CK(cudaMemcpyAsync(d_send, pad, per * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CKN(nccl().AllGather(d_send, d_recv, per, ncclFloat64, ctx->comm, ctx->stream));
     std::vector<double> got(per * ctx->nranks);
     CK(cudaMemcpyAsync(got.data(), d_recv, got.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1107,12 +1127,10 @@ int sip_residual(sip_ctx* ctx, int symmetric, double* const* res) {
     CK(cudaMemsetAsync(ctx->staging, 0, G * sizeof(double), ctx->stream));
     if (ctx->precision == SIP_PREC_SINGLE)
       CKS(launch_residual<float>(ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
-                                 static_cast<float*>(ctx->phi), static_cast<float*>(ctx->ghost),
-                                 symmetric, ctx->staging, ctx->stream));
+                                 static_cast<float*>(ctx->phi), symmetric, ctx->staging, ctx->stream));
     else
       CKS(launch_residual<double>(ctx->d_blocks, (int)lb, hb, static_cast<double*>(ctx->fw),
-                                  static_cast<double*>(ctx->phi), static_cast<double*>(ctx->ghost),
-                                  symmetric, ctx->staging, ctx->stream));
+                                  static_cast<double*>(ctx->phi), symmetric, ctx->staging, ctx->stream));
     ++ctx->launches;
     CK(cudaMemcpyAsync(res[lb], ctx->staging, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   }
@@ -1167,10 +1185,18 @@ long long sip_launch_count(const sip_ctx* ctx) { return ctx ? ctx->launches : 0;
 
 int sip_geometry(const sip_ctx* ctx, int* ti, int* tj, long long* tiles, long long* slices) {
   if (!ctx) return SIP_ERR_MISUSE;
-  if (ti) *ti = kTI;
-  if (tj) *tj = kTJ;
-  if (tiles) *tiles = (long long)ctx->htiles.size();
+  if (ti) *ti = kW;
+  if (tj) *tj = kL;
+  if (tiles) *tiles = (long long)ctx->hbricks.size();
   if (slices) *slices = ctx->total_slices;
+  return SIP_OK;
+}
+
+long long sip_factor_count(const sip_ctx* ctx) { return ctx ? ctx->factor_count : 0; }
+
+int sip_num_global_blocks(const sip_ctx* ctx, int* n) {
+  if (!ctx || !n) return SIP_ERR_MISUSE;
+  *n = (int)ctx->L.blocks.size();
   return SIP_OK;
 }
 
@@ -1181,15 +1207,12 @@ int sip_debug_forward(sip_ctx* ctx) {
   CKS(check_ready(ctx));
   CKS(set_device(ctx));
   CKS(ensure_norm_cap(ctx, ctx->n_done + 1));
-  const size_t st = (32 + std::max<size_t>(1, ctx->htiles.size())) * sizeof(unsigned);
+  const size_t st = 32 * sizeof(unsigned);
   CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
-  if (ctx->precision == SIP_PREC_SINGLE) {
-    CKS(launch_edge_phi<float>(sweep_params<float>(ctx, true, ctx->n_done), ctx->stream));
-    CKS(launch_forward<float>(sweep_params<float>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
-  } else {
-    CKS(launch_edge_phi<double>(sweep_params<double>(ctx, true, ctx->n_done), ctx->stream));
-    CKS(launch_forward<double>(sweep_params<double>(ctx, true, ctx->n_done), ctx->grid_f, ctx->stream));
-  }
+  if (ctx->precision == SIP_PREC_SINGLE)
+    CKS(launch_forward<float>(sweep_params<float>(ctx, true), ctx->grid_f, ctx->stream));
+  else
+    CKS(launch_forward<double>(sweep_params<double>(ctx, true), ctx->grid_f, ctx->stream));
   CK(cudaMemsetAsync(ctx->st_f, 0, st, ctx->stream));
   CK(cudaMemsetAsync(ctx->st_b, 0, st, ctx->stream));
   // the debug sweep does not count as an iteration: put the norm slot back
@@ -1202,74 +1225,47 @@ int sip_debug_forward(sip_ctx* ctx) {
 // Gathers a device pack (0 = phi, 1 = R, 2..13 = forward pack arrays
 // AP..LP, 14..16 = UN/UE/UT) of one local block into a Field3 array.
 int sip_debug_field(sip_ctx* ctx, int local, int which, double* out) {
-  if (!ctx || !out || local < 0 || local >= (int)ctx->local.size()) return SIP_ERR_MISUSE;
+  if (!ctx || !out || local < 0 || local >= (int)ctx->local.size() || which < 0 || which > 16)
+    return SIP_ERR_MISUSE;
   CKS(set_device(ctx));
   const BlockDesc& hb = ctx->hblocks[local];
   const size_t G = field3_elems(hb);
-  const int none[6] = {-1, -1, -1, -1, -1, -1};
   CK(cudaMemsetAsync(ctx->staging, 0, G * sizeof(double), ctx->stream));
-  // gather reads pack index (na = 1, arr = 0); offset the base pointer for other packs
-  auto run = [&](auto* base, int na, int arr) -> int {
-    using T = std::remove_pointer_t<decltype(base)>;
-    return launch_gather_any<T>(base, na, arr, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
+  auto run = [&](auto* phi, auto* R, auto* fw, auto* bw) -> int {
+    using T = std::remove_pointer_t<decltype(phi)>;
+    if (which == 0) return launch_gather_any<T>(phi, 0, 0, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
+    if (which == 1) return launch_gather_any<T>(R, 1, 0, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
+    if (which < 14)
+      return launch_gather_any<T>(fw, F_NA, which - 2, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
+    return launch_gather_any<T>(bw, B_NA, which - 14, ctx->d_blocks, local, hb, ctx->staging, ctx->stream);
   };
-  int rc;
-  if (ctx->precision == SIP_PREC_SINGLE) {
-    float* phi = static_cast<float*>(ctx->phi);
-    float* R = static_cast<float*>(ctx->R);
-    float* fw = static_cast<float*>(ctx->fw);
-    float* bw = static_cast<float*>(ctx->bw);
-    rc = which == 0 ? run(phi, 1, 0) : which == 1 ? run(R, 1, 0)
-         : which < 14 ? run(fw, F_NA, which - 2) : run(bw, B_NA, which - 14);
-  } else {
-    double* phi = static_cast<double*>(ctx->phi);
-    double* R = static_cast<double*>(ctx->R);
-    double* fw = static_cast<double*>(ctx->fw);
-    double* bw = static_cast<double*>(ctx->bw);
-    rc = which == 0 ? run(phi, 1, 0) : which == 1 ? run(R, 1, 0)
-         : which < 14 ? run(fw, F_NA, which - 2) : run(bw, B_NA, which - 14);
-  }
-  (void)none;
+  const int rc = ctx->precision == SIP_PREC_SINGLE
+                     ? run(static_cast<float*>(ctx->phi), static_cast<float*>(ctx->R),
+                           static_cast<float*>(ctx->fw), static_cast<float*>(ctx->bw))
+                     : run(static_cast<double*>(ctx->phi), static_cast<double*>(ctx->R),
+                           static_cast<double*>(ctx->fw), static_cast<double*>(ctx->bw));
   CKS(rc);
   CK(cudaMemcpyAsync(out, ctx->staging, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
 }
 
-// Raw copy of the cross-tile edge buffers (which = 0: edgeW, 1: edgeS) as doubles.
-int sip_debug_edges(sip_ctx* ctx, int which, double* out, long long* count) {
-  if (!ctx || !count) return SIP_ERR_MISUSE;
-  CKS(set_device(ctx));
-  const long long n = ctx->total_edge;
-  if (out) {
-    std::vector<char> tmp((size_t)n * ctx->esize);
-    CK(cudaMemcpy(tmp.data(), which ? ctx->edgeS : ctx->edgeW, tmp.size(), cudaMemcpyDeviceToHost));
-    for (long long x = 0; x < n; ++x)
-      out[x] = ctx->esize == 8 ? reinterpret_cast<double*>(tmp.data())[x]
-                               : (double)reinterpret_cast<float*>(tmp.data())[x];
-  }
-  *count = n;
-  return SIP_OK;
-}
-
-// Per-tile timestamps (ns) of the most recent forward and backward sweep:
-// out[2][ntiles][4] = {start, end, smid, cta}.  Enabled by the first call.
+// Per-brick timestamps (ns) of the most recent forward and backward sweep:
+// out[2][nbricks][4] = {start, end, smid, 0}.  Enabled by the first call.
 int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
   if (!ctx || !ntiles) return SIP_ERR_MISUSE;
   CKS(set_device(ctx));
-  const size_t nt = ctx->htiles.size();
+  const size_t nt = ctx->hbricks.size();
   *ntiles = (long long)nt;
   if (!ctx->trace) {
-    // table [2][nt][4] + per-step record of one tile (forward: 4 x slices)
-    const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
-    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 16 * ns)));
-    if (const char* tt = getenv("SIPB_TRACE_TILE")) ctx->trace_tile = atoi(tt);
+    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 2 * kTraceStages * kTraceMarks)));
+    if (const char* tb = getenv("SIPB_TRACE_BRICK")) ctx->trace_brick = atoi(tb);
     return SIP_OK;
   }
   if (out) {
-    const size_t ns = ctx->hblocks.empty() ? 1 : (size_t)ctx->hblocks[0].ns;
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 16 * ns), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 2 * kTraceStages * kTraceMarks),
+                  cudaMemcpyDeviceToHost));
   }
   return SIP_OK;
 }

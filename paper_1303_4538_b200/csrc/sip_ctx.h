@@ -54,23 +54,29 @@ struct sip_ctx {
   Lattice L;
   std::vector<int> rank_of, local, local_of;
   std::vector<BlockDesc> hblocks;
-  std::vector<TileDesc> htiles;
+  std::vector<BrickDesc> hbricks;
   std::vector<int> order_f, order_b;
   BlockDesc* d_blocks = nullptr;
-  TileDesc* d_tiles = nullptr;
+  BrickDesc* d_bricks = nullptr;
   int* d_order_f = nullptr;
   int* d_order_b = nullptr;
-  void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr, *ghost = nullptr;
-  void *edgeW = nullptr, *edgeS = nullptr;
-  void* rec_phi = nullptr;  // [total_slices][64] static part of the K2 edge records
+  // packs (brick-slice layout, sip_internal.h): forward (F_NA arrays), backward
+  // (B_NA), R; phi with its ghost cells (porches + ghost bricks)
+  void *fw = nullptr, *bw = nullptr, *phi = nullptr, *R = nullptr;
+  // fp64 AP..AT for the factorisation: the forward pack itself in double
+  // mode (coef_na = F_NA), a C_NA-array pack in single mode (no fp64 factors
+  // are kept: K1 stores the fp32 factors directly)
+  double* coef64 = nullptr;
+  int coef_na = F_NA;
   std::vector<char> symmetric;  // per local block: system flagged symmetric
   // per local block, kernel face order: >= 0 where the installed halo plan
   // writes that ghost face (store_phi returns those ghosts)
   std::vector<std::array<int, 6>> plan_ghosts;
-  unsigned long long* tags = nullptr;  // 4 tagged edge buffers: K2 E/N, K3 W/S
-  size_t tag_words = 0;                 // words per buffer
-  unsigned* epochs = nullptr;           // [0] K2, [1] K3 launch counters
-  double *fw64 = nullptr, *bw64 = nullptr;  // fp32 mode: fp64 shadow for the factorisation
+  // cross-brick mailboxes (tagged words): [0] K2 E col, [1] K2 N row, [2] K3 W col,
+  // [3] K3 S row, [4] K1 E col, [5] K1 N row
+  unsigned long long* mbox[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t mbox_bytes[6] = {0, 0, 0, 0, 0, 0};
+  unsigned* epochs = nullptr;           // [0] K2, [1] K3, [2] K1 launch counters
   unsigned *st_f = nullptr, *st_b = nullptr, *st_fac = nullptr;
   double* partial = nullptr;
   double* d_norms = nullptr;
@@ -81,7 +87,7 @@ struct sip_ctx {
   size_t gmax = 0;
   double* phi_stage = nullptr;       // per local block Field3 fp64 mirror of phi (load/store)
   std::vector<size_t> phi_stage_off;
-  long long total_slices = 0, total_edge = 0, total_ghost = 0;
+  long long total_slices = 0, total_phi_slices = 0, total_edge = 0, total_row = 0;
   int grid_f = 1, grid_b = 1, grid_fac = 1;
   cudaStream_t own_stream = nullptr, stream = nullptr;
   long long revision = 0, factor_stamp = -1;
@@ -96,8 +102,9 @@ struct sip_ctx {
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo
   double t_fwd = 0, t_bwd = 0, t_halo = 0;
   long long launches = 0, prof_launches = 0;
-  unsigned long long* trace = nullptr;  // debug: per-tile timestamps of the last F/B sweeps
-  int trace_tile = 0;
+  long long factor_count = 0;  // K1 launches (SPEC.md:185 factorisation counter)
+  unsigned long long* trace = nullptr;  // debug: per-brick timestamps of the last F/B sweeps
+  int trace_brick = -1;                 // debug: brick with per-stage marks (env SIPB_TRACE_BRICK)
   // pressure-correction caller (sip_flow.cu): grid of the assembled Poisson
   // system, boundary kinds per face (W,E,S,N,B,T) and the pinned cell
   bool poisson = false;
@@ -120,6 +127,9 @@ struct sip_ctx {
   bool use_graphs = false;  // opt-in: env SIPB_GRAPH=1 at context creation
   double* d_gather = nullptr;  // multi-rank norm all-gather buffers (sip_read_norms)
   size_t gather_cap = 0;       // doubles
+  double* h_pad = nullptr;     // pinned host staging of the all-gather send buffer
+  size_t h_pad_cap = 0;
+  double* d_pad = nullptr;     // (reserved)
   std::string err;
 };
 
@@ -174,6 +184,9 @@ int exchange(sip_ctx* ctx);
 // `iters` SIP iterations (K2, K3, halo) on ctx->stream.
 template <typename T>
 int iterate_t(sip_ctx* ctx, int iters);
+// One Field3 array (device) of a local block into the packs (forward pack,
+// and the fp64 coefficient pack in single mode).
+int scatter_array(sip_ctx* ctx, int local, const double* src, int arr);
 // Factors present and stamped with the current system revision.
 int check_ready(sip_ctx* ctx);
 

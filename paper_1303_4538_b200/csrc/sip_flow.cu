@@ -124,41 +124,38 @@ __global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double
 }
 
 // Co-located central divergence of one block; Q = -(V * div) / dt straight
-// into the source array of the system's tile-slice pack (fp64, and the fp32
-// copy in single mode; pinned cell: 0) and the block's L1 partials.  CTA
-// (tile, c) owns the tile's 16 x 16 columns over planes [kDivKC*c, +kDivKC):
-// it reads u, v, w row-wise (coalesced 128-byte rows), keeps Q of the chunk in
-// shared memory in the pack's position order and writes it slice by slice --
-// the chunk's cells of slice t = k + ti + tj are one contiguous position
-// range, so the pack writes are coalesced too.  The partial of a CTA sums its
-// cells in a fixed order (per column over k, fixed shuffle tree, warps in
-// order): deterministic.
-constexpr int kDivKC = 16;
+// into the source array of the system's brick-slice pack (pinned cell: 0) and
+// the block's L1 partials.  CTA (brick, c) owns the brick's kW x kL columns
+// over planes [kDivKC*c, +kDivKC): phase 1 reads u, v, w (thread = (il, jl))
+// and keeps Q of the chunk in shared memory; phase 2 writes it slice by slice
+// -- a warp writes the kL lanes of one slice, so the pack writes are coalesced.
+// The partial of a CTA sums its cells in a fixed order (per column over k,
+// fixed shuffle tree, warps in order): deterministic.
+constexpr int kDivKC = 8;
+template <typename T>
 __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* blocks, int blk,
                                                              const double* u, const double* v,
                                                              const double* w, double c2x, double c2y,
                                                              double c2z, double vol, double dt, int pin,
-                                                             double* fw64, float* fw32,
-                                                             double* partial) {
-  __shared__ double sq[kDivKC][kTT];
+                                                             T* fw, double* partial) {
+  static_assert(kW * kL == kFlowThreads, "one thread per brick column");
+  __shared__ double sq[kDivKC][kL][kW];
   __shared__ double s[kFlowThreads / 32];
   const BlockDesc bd = blocks[blk];
   const int nx = bd.nx, ny = bd.ny, nz = bd.nz;
-  const int ta = blockIdx.x % bd.TX, tb = blockIdx.x / bd.TX;
-  const int i0 = ta * kTI, j0 = tb * kTJ, k0 = blockIdx.y * kDivKC;
-  const int wI = min(kTI, nx - i0), wJ = min(kTJ, ny - j0), wK = min(kDivKC, nz - k0);
+  const int r = blockIdx.x, bi = r % bd.BX, bj = r / bd.BX;
+  const int i0 = bi * kW, j0 = bj * kL, k0 = blockIdx.y * kDivKC;
+  const int wI = min(kW, nx - i0), wJ = min(kL, ny - j0), wK = min(kDivKC, nz - k0);
   const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
-  // phase 1: thread (ti, tj) row-major; one column of the chunk per thread
-  const int ti = threadIdx.x % kTI, tj = threadIdx.x / kTI;
-  const int pos = tile_pos(ti, tj);
+  const int il = threadIdx.x % kW, jl = threadIdx.x / kW;
   double acc = 0.0;
-  if (ti < wI && tj < wJ) {
+  if (il < wI && jl < wJ) {
     for (int kk = 0; kk < wK; ++kk) {
-      const long long x = f3(nx, ny, i0 + ti + 1, j0 + tj + 1, k0 + kk + 1);
+      const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
       const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
                         (w[x + sz] - w[x - sz]) / c2z;
-      const bool pinned = pin && blockIdx.x == 0 && k0 + kk == 0 && ti == 0 && tj == 0;
-      sq[kk][pos] = pinned ? 0.0 : -(vol * dv) / dt;
+      const bool pinned = pin && r == 0 && k0 + kk == 0 && il == 0 && jl == 0;
+      sq[kk][jl][il] = pinned ? 0.0 : -(vol * dv) / dt;
       acc += fabs(dv) * vol;
     }
   }
@@ -168,31 +165,17 @@ __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* bl
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int r = 0; r < kFlowThreads / 32; ++r) t += s[r];
+    for (int x = 0; x < kFlowThreads / 32; ++x) t += s[x];
     partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
-  if (!fw64) return;
-  // phase 2: thread = pack position; slice t holds plane t - d of this position
-  int pi = 0, pj = 0;
-  {
-    const int q = threadIdx.x;
-    int dd = 0;
-    while (diag_off(dd + 1) <= q) ++dd;
-    const int lo = dd - (kTJ - 1) > 0 ? dd - (kTJ - 1) : 0;
-    pi = lo + (q - diag_off(dd));
-    pj = dd - pi;
-  }
-  const int d = pi + pj;
-  const bool colok = pi < wI && pj < wJ;
-  const long long slot = bd.slot0 + (long long)(ta + bd.TX * tb) * bd.ns;
-  for (int t = k0; t < k0 + wK + kTI + kTJ - 2; ++t) {
-    const int kk = t - d - k0;
-    if (colok && kk >= 0 && kk < wK) {
-      const double q = sq[kk][threadIdx.x];
-      const long long at = ((slot + t) * F_NA + F_Q) * kTT + threadIdx.x;
-      fw64[at] = q;
-      if (fw32) fw32[at] = static_cast<float>(q);
-    }
+  if (!fw) return;
+  // phase 2: warp q writes slices tau = 8 k0 + q, + 8, ...; lane = jl
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const long long slot = bd.slot0 + (long long)r * bd.ns;
+  for (int tau = kW * k0 + q; tau < kW * (k0 + wK) + kL - 1; tau += kFlowThreads / 32) {
+    const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
+    if (lane < wJ && c >= 0 && k >= k0 && k < k0 + wK && ci < wI)
+      fw[((slot + tau) * F_NA + F_Q) * kL + lane] = static_cast<T>(sq[k - k0][lane][ci]);
   }
 }
 
@@ -371,14 +354,19 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
     const BlockDesc& b = ctx->hblocks[lb];
     const size_t o = ctx->phi_stage_off[lb];
     const long long n = (long long)b.nx * b.ny * b.nz;
-    const dim3 grid((unsigned)(b.TX * b.TY), (unsigned)((b.nz + kDivKC - 1) / kDivKC));
+    const dim3 grid((unsigned)b.nbricks, (unsigned)((b.nz + kDivKC - 1) / kDivKC));
     const int nch = (int)(grid.x * grid.y);
-    double* q64 = write_q ? ctx->fw64 : nullptr;
-    float* q32 = write_q && ctx->precision == SIP_PREC_SINGLE ? static_cast<float*>(ctx->fw) : nullptr;
     (void)n;
-    k_divergence<<<grid, kFlowThreads, 0, ctx->stream>>>(
-        ctx->d_blocks, (int)lb, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy,
-        2.0 * hz, vol, dt, (int)lb == ctx->pin_local, q64, q32, fl->partial);
+    if (ctx->precision == SIP_PREC_SINGLE)
+      k_divergence<float><<<grid, kFlowThreads, 0, ctx->stream>>>(
+          ctx->d_blocks, (int)lb, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy,
+          2.0 * hz, vol, dt, (int)lb == ctx->pin_local, write_q ? static_cast<float*>(ctx->fw) : nullptr,
+          fl->partial);
+    else
+      k_divergence<double><<<grid, kFlowThreads, 0, ctx->stream>>>(
+          ctx->d_blocks, (int)lb, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, 2.0 * hx, 2.0 * hy,
+          2.0 * hz, vol, dt, (int)lb == ctx->pin_local, write_q ? static_cast<double*>(ctx->fw) : nullptr,
+          fl->partial);
     k_sum_partials<<<1, kFlowThreads, 0, ctx->stream>>>(fl->partial, nch, fl->d_blocksum + lb);
     CK(cudaGetLastError());
     ctx->launches += 2;
@@ -394,17 +382,16 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
 template <typename T>
 int flow_solve(sip_flow* fl, int sweeps) {
   sip_ctx* ctx = fl->ctx;
-  const size_t S = (size_t)ctx->total_slices * kTT;
-  CK(cudaMemsetAsync(ctx->phi, 0, S * sizeof(T), ctx->stream));
-  CK(cudaMemsetAsync(ctx->ghost, 0, (size_t)ctx->total_ghost * sizeof(T), ctx->stream));
+  // p' = 0: interior and every ghost cell (one contiguous phi allocation)
+  CK(cudaMemsetAsync(ctx->phi, 0, (size_t)ctx->total_phi_slices * kL * sizeof(T), ctx->stream));
   ctx->n_done = 0;
   CK(cudaMemsetAsync(ctx->d_norm_it, 0, sizeof(unsigned), ctx->stream));
   CKS(iterate_t<T>(ctx, sweeps));
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
     const BlockDesc& b = ctx->hblocks[lb];
     double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
-    CKS(launch_gather<T>(static_cast<T*>(ctx->phi), static_cast<T*>(ctx->ghost), ctx->d_blocks,
-                         (int)lb, b, ctx->plan_ghosts[lb].data(), st, ctx->stream));
+    CKS(launch_gather<T>(static_cast<T*>(ctx->phi), ctx->d_blocks, (int)lb, b,
+                         ctx->plan_ghosts[lb].data(), st, ctx->stream));
     ++ctx->launches;
   }
   double* pp[1] = {ctx->phi_stage};
@@ -463,13 +450,7 @@ int sip_assemble_poisson(sip_ctx* ctx, const double len[3], const int bc[6]) {
         ax, ay, az, (int)lb == ctx->pin_local, d_out8);
     CK(cudaGetLastError());
     ++ctx->launches;
-    for (int a = 0; a < 8; ++a) {
-      if (ctx->precision == SIP_PREC_SINGLE)
-        CKS(launch_scatter<float>(out8[a], ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->fw),
-                                  F_NA, arr[a], ctx->stream));
-      CKS(launch_scatter<double>(out8[a], ctx->d_blocks, (int)lb, hb, ctx->fw64, F_NA, arr[a],
-                                 ctx->stream));
-    }
+    for (int a = 0; a < 8; ++a) CKS(scatter_array(ctx, (int)lb, out8[a], arr[a]));
     CK(cudaStreamSynchronize(ctx->stream));  // out8 (host array) and staging reused next block
   }
   ++ctx->revision;
@@ -495,7 +476,7 @@ int sip_flow_create(sip_ctx* ctx, sip_flow** out) {
   for (const BlockDesc& b : ctx->hblocks) {
     total += field3_elems(b);
     fl->max_cells = std::max(fl->max_cells, (long long)b.nx * b.ny * b.nz);
-    fl->max_parts = std::max(fl->max_parts, (long long)b.TX * b.TY * ((b.nz + kDivKC - 1) / kDivKC));
+    fl->max_parts = std::max(fl->max_parts, (long long)b.nbricks * ((b.nz + kDivKC - 1) / kDivKC));
   }
   auto fail = [&](int s) {
     sip_flow_destroy(fl);

@@ -1,15 +1,26 @@
 // sip_internal.h -- shared declarations of the B200 SIP library (host + device).
 //
 // Device data layout: every block is cut into
-// (TI x TJ)-column tiles of the (i, j) plane; a tile streams along k.  Cell
-// (ti, tj, k) of a tile is processed at wavefront step t = k + ti + tj (the
-// hyperplane index inside the tile), so each step of a tile touches one
-// "slice" of TI*TJ cells.  Packs store slices contiguously:
-//     pack[((slot + t) * NA + array) * TT + pos(ti, tj)]
-// where slot is the tile's first slice, NA the arrays in the pack and pos()
-// numbers the tile's cells by anti-diagonal (d = ti + tj ascending, then ti),
-// so a slice's valid cells are always one contiguous range -- fill/drain
-// slices are fetched with range-limited bulk copies (no padding traffic).
+// bricks of kW (i) x kL (j) columns that run through all nz planes.  One warp
+// owns a brick: lane jl holds row j0 + jl and walks its cells
+// c = k * kW + il (il = i - i0) in order, one cell per step, skewed by jl
+// steps behind lane 0, so at step ("slice") tau = c + jl every lane sits on
+// its own cell and
+//   * the W neighbour (il - 1) is the lane's own previous step,
+//   * the S neighbour (jl - 1) is lane jl - 1's previous step (one shfl),
+//   * the B neighbour (k - 1) is the lane's own step tau - kW.
+// A slice is one contiguous row of kL values per array, so the packs are
+//   pack[((slot + tau) * NA + array) * kL + jl]
+// (slice-major, array, lane), and a run of slices is one contiguous range --
+// the sweep kernels stream it with TMA bulk copies.  A brick has
+// ns = nz * kW + kL slices (kL - 1 of skew, rounded up to whole stages).
+//
+// phi carries its ghost cells in the same layout: the B / T ghost planes are
+// the skew padding of the brick's own slices (cells c < 0 and c >= nz * kW,
+// inside a porch of kPorch slices on either side), the W / E / S / N ghost
+// faces live in ghost bricks (or in the padding column / lane of a ragged last
+// brick), so every phi value the 7-point residual touches has one address
+// (phi_index) and the halo exchange writes straight into it.
 #pragma once
 
 #include <array>
@@ -26,74 +37,92 @@
 
 namespace sipb {
 
-constexpr int kTI = 16;  // tile extent along i (columns)
-constexpr int kTJ = 16;  // tile extent along j
-constexpr int kTT = kTI * kTJ;
-constexpr int kD = kTI + kTJ - 1;  // diagonals per tile = skew + 1
+constexpr int kW = 8;       // brick extent along i (cells per lane per plane)
+constexpr int kL = 32;      // brick extent along j (one warp lane per row)
+constexpr int kStage = kW;  // slices per pipeline stage (one plane of a lane's cells)
+constexpr int kPorch = 32;  // phi slices kept before tau = 0 and after ns
 
 // forward pack: coefficients, source and lower factors (12 arrays)
 enum FwArray { F_AP = 0, F_AW, F_AE, F_AS, F_AN, F_AB, F_AT, F_Q, F_LB, F_LW, F_LS, F_LP, F_NA };
 // backward pack: upper factors
 enum BwArray { B_UN = 0, B_UE, B_UT, B_NA };
+// fp64 coefficient pack of single-precision contexts (factor input): AP..AT
+constexpr int C_NA = 7;
 
-// Ghost-face order inside a block's ghost record (kernel order).
+// Ghost-face order (kernel order).
 enum GhostFace { G_W = 0, G_E, G_S, G_N, G_B, G_T };
 
-struct TileDesc {
-  long long slot;  // first slice of this tile in the packs
-  long long edge;  // element offset of this tile's delta edge records
-  int block;       // local block index
-  int i0, j0;      // first column, 0-based within the block
-  int wI, wJ;      // valid extents (ragged last tiles)
-  int nW, nE, nS, nN;  // neighbour tile (index into the tile array) or -1
-  int ns;          // slices = nz + kD - 1
-  int nz;
-};
-
 struct BlockDesc {
-  int id;            // global block id
+  int id;              // global block id
   int nx, ny, nz;
-  int TX, TY;        // tiles per axis
-  int ns;            // slices per tile
-  long long slot0;   // first slice of the block's first tile
-  long long ghost;   // element offset of the block's 6 ghost faces
-  int tile0, ntiles; // range in the tile array (block-major, row-major tiles)
+  int BX, BY;          // bricks along i / j
+  int ns;              // slices per brick = nz * kW + kL
+  int brick0, nbricks; // range in the brick array (brick r = bi + BX * bj)
+  int gE, gN;          // ghost brick columns on E (nx % kW == 0) / rows on N (ny % kL == 0)
+  long long slot0;     // fw / bw / R: slice tau = 0 of brick 0 (brick r at slot0 + r * ns)
+  long long pbase;     // phi: first slice of the block's phi region
+  long long medge0;    // mailbox: first edge entry of brick 0 (kL * nz per brick)
+  long long mrow0;     // mailbox: first row entry of brick 0 (kW * nz per brick)
 };
 
-__host__ __device__ inline long long ghost_face_offset(const BlockDesc& b, int face) {
-  const long long yz = (long long)b.ny * b.nz, xz = (long long)b.nx * b.nz;
-  switch (face) {
-    case G_W: return b.ghost;
-    case G_E: return b.ghost + yz;
-    case G_S: return b.ghost + 2 * yz;
-    case G_N: return b.ghost + 2 * yz + xz;
-    case G_B: return b.ghost + 2 * yz + 2 * xz;
-    default: return b.ghost + 2 * yz + 2 * xz + (long long)b.nx * b.ny;
-  }
+// phi bricks of a block: real bricks, then ghost W (BY), E (BY if gE), S (BX), N (BX if gN)
+__host__ __device__ inline long long phi_stride(const BlockDesc& b) { return (long long)b.ns + 2 * kPorch; }
+__host__ __device__ inline int phi_bricks(const BlockDesc& b) {
+  return b.nbricks + b.BY * (1 + b.gE) + b.BX * (1 + b.gN);
 }
-__host__ __device__ inline long long ghost_count(int nx, int ny, int nz) {
-  return 2LL * ny * nz + 2LL * nx * nz + 2LL * nx * ny;
+// slice tau = 0 of phi brick pb (0-based within the block)
+__host__ __device__ inline long long phi_slot(const BlockDesc& b, int pb) {
+  return b.pbase + (long long)pb * phi_stride(b) + kPorch;
 }
 
-// first cell index of diagonal d (0 <= d <= kD) in a square S x S tile:
-// d(d+1)/2 below the main anti-diagonal, S^2 - (2S-1-d)(2S-d)/2 above it.
-static_assert(kTI == kTJ, "closed-form diagonal offsets assume square tiles");
-__host__ __device__ constexpr int diag_off(int d) {
-  return d <= kTI ? d * (d + 1) / 2 : kTT - (2 * kTI - 1 - d) * (2 * kTI - d) / 2;
-}
-__host__ __device__ inline int tile_pos(int ti, int tj) {
-  const int d = ti + tj;
-  const int lo = d - (kTJ - 1) > 0 ? d - (kTJ - 1) : 0;
-  return diag_off(d) + (ti - lo);
-}
+struct BrickDesc {
+  long long slot;            // fw / bw / R slice tau = 0
+  long long pslot;           // phi slice tau = 0
+  long long pW, pE, pS, pN;  // phi slice tau = 0 of the W / E / S / N neighbour (real or ghost)
+  long long medge, mrow;     // own mailbox entries (published: K2 E col / N row, K3 W col / S row)
+  long long mWe, mEe;        // W / E neighbour's edge mailbox (-1: block boundary, value 0)
+  long long mSr, mNr;        // S / N neighbour's row mailbox (-1: block boundary)
+  int block, bi, bj;
+  int i0, j0, wI, wJ;
+  int nz, ns;
+};
 
-// Pack element index of interior cell (i, j, k), 0-based within the block.
+// Slice of interior cell (i, j, k) in its brick (0-based, within the block).
+__host__ __device__ inline long long pack_slice(const BlockDesc& b, int i, int j, int k) {
+  const int bi = i / kW, il = i - bi * kW, bj = j / kL, jl = j - bj * kL;
+  return b.slot0 + (long long)(bi + b.BX * bj) * b.ns + (long long)k * kW + il + jl;
+}
+// Pack element index of interior cell (i, j, k).
 __host__ __device__ inline long long pack_index(const BlockDesc& b, int na, int arr, int i, int j,
                                                 int k) {
-  const int a = i / kTI, ti = i - a * kTI;
-  const int c = j / kTJ, tj = j - c * kTJ;
-  const long long slot = b.slot0 + (long long)(a + b.TX * c) * b.ns + (k + ti + tj);
-  return (slot * na + arr) * kTT + tile_pos(ti, tj);
+  return (pack_slice(b, i, j, k) * na + arr) * kL + (j % kL);
+}
+// phi element index of cell (i, j, k) with i in [-1, nx], j in [-1, ny],
+// k in [-1, nz] (interior or face ghost; edges / corners are not stored).
+__host__ __device__ inline long long phi_index(const BlockDesc& b, int i, int j, int k) {
+  int pb, il, jl;
+  if (i < 0) {
+    pb = b.nbricks + j / kL;
+    il = kW - 1;
+    jl = j % kL;
+  } else if (j < 0) {
+    pb = b.nbricks + b.BY * (1 + b.gE) + i / kW;
+    il = i % kW;
+    jl = kL - 1;
+  } else if (i == b.nx && b.gE) {
+    pb = b.nbricks + b.BY + j / kL;
+    il = 0;
+    jl = j % kL;
+  } else if (j == b.ny && b.gN) {
+    pb = b.nbricks + b.BY * (1 + b.gE) + b.BX + i / kW;
+    il = i % kW;
+    jl = 0;
+  } else {  // interior, B / T ghosts (porch) and ragged E / N ghosts (padding)
+    pb = i / kW + b.BX * (j / kL);
+    il = i % kW;
+    jl = j % kL;
+  }
+  return (phi_slot(b, pb) + (long long)k * kW + il + jl) * kL + jl;
 }
 
 // ---------------------------------------------------------------- planning
@@ -134,90 +163,92 @@ struct FaceCopy {
   int n0, n1;      // plane extents (fast, slow)
 };
 
+// Cross-brick edge values travel as self-validating tagged words: value bits
+// + the 32-bit launch epoch of the producing sweep, one 64-bit word per fp32
+// value, two per fp64 value (each carrying 32 value bits).  A mailbox entry is
+// written exactly once per launch, so a matching epoch means "this launch's
+// value": no flag, fence or counter.
 template <typename T>
 struct SweepParams {
-  const TileDesc* tiles;
+  const BrickDesc* bricks;
   const BlockDesc* blocks;
-  const int* order;  // ticket -> tile (topological order of this sweep)
-  int ntiles;
+  const int* order;  // ticket -> brick (topological order of this sweep)
+  int nbricks;
   int nblocks;
-  T* fw;
-  T* bw;
+  const T* fw;
+  const T* bw;
   T* phi;
   T* R;
-  T* ghost;
-  T* edgeW;  // (factor kernel only) unused by K2/K3
-  T* edgeS;
-  // K2: the static (old-phi / ghost) part of each step's edge record,
-  // [slot + s][64] = phiW, phiE, phiS, phiN (16 each); built by k_edge_phi
-  // after every halo exchange and bulk-copied with the step's phi slice
-  T* rec_phi;
-  int symmetric;  // K2: every block's system flagged symmetric -> Listing-1 fast path
-  // Cross-tile edge values as self-validating tagged words (DESIGN.md
-  // "Cross-tile hand-off"): value bits + 32-bit tag (epoch << 16 | k), one
-  // 64-bit word per fp32 value, two per fp64 value; index (edge + k*16 + c).
-  //   K2: tagA = R of each tile's E column, tagB = R of its N row
-  //   K3: tagA = delta of each tile's W column, tagB = delta of its S row
-  unsigned long long* tagA;
-  unsigned long long* tagB;
+  //   K2: mA = R of each brick's E column (edge entries), mB = R of its N row (row entries)
+  //   K3: mA = delta of each brick's W column,            mB = delta of its S row
+  unsigned long long* mA;
+  unsigned long long* mB;
   unsigned* epoch;        // launch counter of this sweep kind (bumped by the finaliser)
-  unsigned* state;        // this sweep: [0] ticket, [1] done, prog at state + 32
+  unsigned* state;        // this sweep: [0] ticket, [1] done
   unsigned* state_other;  // the other sweep's state, reset by our finaliser
-  double* partial;        // [ntiles] tile norm partials
+  double* partial;        // [nbricks] brick norm partials
   // forward only: norms of iteration it = *norm_it go to norms_base[it] and
   // bnorms_base[it * nblocks + b]; the finaliser then bumps *norm_it, so a
   // captured CUDA graph of several iterations replays without new parameters
   double* norms_base;
   double* bnorms_base;
   unsigned* norm_it;
-  unsigned long long* trace;  // optional [ntiles][4]: start ns, end ns, smid, cta (debug)
-  int trace_tile;             // debug: tile whose per-step times are recorded after the table
+  unsigned long long* trace;  // optional [nbricks][4]: start ns, end ns, smid, stalls (debug)
+  // debug: per-stage clock64 marks of brick trace_brick (first kTraceStages stages,
+  // kTraceMarks each) after the per-brick table
+  int trace_brick;
 };
+constexpr int kTraceStages = 64, kTraceMarks = 6;
 
+template <typename T>
 struct FactorParams {
-  const TileDesc* tiles;
+  const BrickDesc* bricks;
   const BlockDesc* blocks;
   const int* order;
-  int ntiles;
+  int nbricks;
   double alpha;
-  double* fw;
-  double* bw;
+  const double* coef;  // fp64 AP..AT: the fp64 forward pack (coef_na = F_NA) or the
+  int coef_na;         // fp64 coefficient pack of single-precision contexts (C_NA)
+  T* fw;               // out: LB LW LS LP (forward pack)
+  T* bw;               // out: UN UE UT
+  unsigned long long* mA;  // (UN, UE, UT) of each brick's E column, fp64 tagged
+  unsigned long long* mB;  // (UN, UE, UT) of each brick's N row
+  unsigned* epoch;
   unsigned* state;
   unsigned long long* bad;  // (block << 40) | Field3 index of the first singular cell
 };
 
 // launchers (sip_kernels.cu); all asynchronous on `stream`
-int launch_factor(const FactorParams& p, int grid, void* stream);
+template <typename T>
+int launch_factor(const FactorParams<T>& p, int grid, void* stream);
 template <typename T>
 int launch_forward(const SweepParams<T>& p, int grid, void* stream);
 template <typename T>
 int launch_backward(const SweepParams<T>& p, int grid, void* stream);
-template <typename T>
-int launch_edge_phi(const SweepParams<T>& p, void* stream);
 int launch_check_symmetric(const BlockDesc* d_blocks, int block, const BlockDesc& hb,
-                           const double* fw, unsigned long long* bad, void* stream);
+                           const double* coef, int coef_na, unsigned long long* bad, void* stream);
 template <typename T>
 int launch_scatter(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
                    T* pack, int na, int arr, void* stream);
 template <typename T>
-int launch_ghost_in(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
-                    T* ghost, void* stream);
+int launch_phi_in(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                  T* phi, void* stream);
 template <typename T>
-int launch_gather(const T* pack, const T* ghost, const BlockDesc* d_blocks, int block,
-                  const BlockDesc& hb, const int* nbr6, double* dst, void* stream);
+int launch_gather(const T* phi, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
+                  const int* nbr6, double* dst, void* stream);
 template <typename T>
 int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
-                       const BlockDesc* d_blocks, const T* phi, T* ghost, T* buf_in, T* buf_out,
+                       const BlockDesc* d_blocks, T* phi, const T* buf_in, T* buf_out,
                        void* stream);
 template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
-                    const T* phi, const T* ghost, int symmetric, double* out, void* stream);
+                    const T* phi, int symmetric, double* out, void* stream);
 template <typename T>
 int launch_gather_any(const T* pack, int na, int arr, const BlockDesc* d_blocks, int block,
                       const BlockDesc& hb, double* dst, void* stream);
-int launch_convert(const double* src, float* dst, long long n, void* stream);
 int launch_generate(int kind, uint64_t seed, const int g[3], const int o[3], int nx, int ny, int nz,
                     double* const* out8, void* stream);
+// persistent grid of a sweep kind (0 factor, 1 forward, 2 backward)
 int max_resident_ctas(int kind, int precision, int* grid);
 
 }  // namespace sipb

@@ -58,6 +58,7 @@ EXPORTS = (
     "sip_ftt1_read", "sip_ftt1_write", "sip_ftt1_validate", "sip_set_halo_tables",
     "sip_plan_halo_periodic", "sip_assemble_poisson", "sip_flow_create", "sip_flow_destroy",
     "sip_flow_set", "sip_flow_get", "sip_flow_divergence", "sip_pressure_correct",
+    "sip_factor_count", "sip_num_global_blocks",
 )
 
 
@@ -127,6 +128,8 @@ def lib():
         L.sip_get_stream.argtypes = [ctypes.c_void_p]
         L.sip_launch_count.restype = ctypes.c_longlong
         L.sip_launch_count.argtypes = [ctypes.c_void_p]
+        L.sip_factor_count.restype = ctypes.c_longlong
+        L.sip_factor_count.argtypes = [ctypes.c_void_p]
         for name in ("sip_destroy", "sip_synchronize"):
             getattr(L, name).argtypes = [ctypes.c_void_p]
         _lib = L
@@ -343,8 +346,15 @@ class Solver:
                 "sip_read_norms")
         return (n[:count], bn[:count]) if per_block else n[:count]
 
-    def num_global_blocks(self):
-        return self._nglobal if hasattr(self, "_nglobal") else len(self.blocks)
+    def num_global_blocks(self) -> int:
+        """Blocks of the whole lattice (all ranks): the width of read_norms' per-block rows."""
+        n = ctypes.c_int()
+        self._c(lib().sip_num_global_blocks(self._ctx, ctypes.byref(n)), "sip_num_global_blocks")
+        return n.value
+
+    def factor_count(self) -> int:
+        """Library-side factorisation counter: K1 launches of this context."""
+        return int(lib().sip_factor_count(self._ctx))
 
     def synchronize(self):
         self._c(lib().sip_synchronize(self._ctx), "sip_synchronize")
@@ -376,7 +386,7 @@ class Solver:
         nt, ns = ctypes.c_longlong(), ctypes.c_longlong()
         lib().sip_geometry(self._ctx, ctypes.byref(ti), ctypes.byref(tj), ctypes.byref(nt),
                            ctypes.byref(ns))
-        return {"ti": ti.value, "tj": tj.value, "tiles": nt.value, "slices": ns.value}
+        return {"brick_i": ti.value, "brick_j": tj.value, "bricks": nt.value, "slices": ns.value}
 
 
 # ----------------------------------------------------------------- SPEC operations

@@ -113,7 +113,6 @@ def _smooth_fields(g, p, seed=3):
 # ---------------------------------------------------------------- GPU parity
 def _gpu_setup(g, p, bc, prec, lengths=(1.0, 1.0, 1.0), alpha=0.92):
     s = sip.Solver(None, prec, 0, lattice=(g, p))
-    s._nglobal = len(O.lattice(g, p)[1])
     s.assemble_poisson(lengths, [("wall", "periodic", "symmetry")[b] for b in bc])
     s.factor(alpha)
     return s

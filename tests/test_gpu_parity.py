@@ -222,7 +222,6 @@ def test_multiblock_matches_oracle(gpu, g, pd, prec):
     phis = [O.field(*d) for (_, d, _) in s.blocks]
     s.load_phi(phis)
     s.iterate(iters)
-    s._nglobal = len(dims)
     ng, bng = s.read_norms(0, iters, per_block=True)
     s.store_phi(phis)
     s.close()
@@ -242,7 +241,6 @@ def test_device_generator_matches_host(gpu):
     phis = [O.field(*d) for (_, d, _) in s.blocks]
     s.load_phi(phis)
     s.iterate(3)
-    s._nglobal = len(s.blocks)
     ng = s.read_norms(0, 3)
     s.close()
     origins, dims, nbr = O.lattice(g, pd)
@@ -257,7 +255,6 @@ def test_config1_full_size_properties(gpu):
     with the last+1 norm (checksum of checksums)."""
     g = (256, 256, 256)
     s = sip.Solver(None, "f64", 0, lattice=(g, (1, 1, 1)))
-    s._nglobal = 1
     s.generate(0, 1304)
     s.factor(0.92)
     s.load_phi([sip.field(*g)])
@@ -345,7 +342,6 @@ def test_table_driven_halo_matches_oracle(gpu, name, prec):
     phis = [O.field(*d) for (_, d, _) in s.blocks]
     s.load_phi(phis)
     s.iterate(iters)
-    s._nglobal = len(dims)
     ng = s.read_norms(0, iters)
     s.store_phi(phis)
     s.close()
@@ -445,7 +441,6 @@ def test_kat_decomposition_independent_of_placement(gpu):
         phis = [O.field(*d) for (_, d, _) in s.blocks]
         s.load_phi(phis)
         s.iterate(5)
-        s._nglobal = 4
         n = s.read_norms(0, 5)
         s.store_phi(phis)
         s.close()
@@ -486,7 +481,6 @@ def test_symmetric_sweep_fast_path(gpu, g, pd, prec):
     phis = [O.field(*d) for (_, d, _) in s.blocks]
     s.load_phi(phis)
     s.iterate(iters)
-    s._nglobal = len(dims)
     ng = s.read_norms(0, iters)
     s.store_phi(phis)
     s.close()
@@ -502,7 +496,6 @@ def test_symmetric_generator_and_fast_path(gpu):
     invariant check accepts it; the flagged fast path matches the oracle."""
     dims = (30, 22, 18)
     s = sip.Solver(None, "f64", 0, lattice=(dims, (1, 1, 1)))
-    s._nglobal = 1
     s.generate(3, 77)
     s.set_symmetric(0, True)
     s.factor(0.92)
@@ -528,7 +521,6 @@ def test_config4_full_size_first_iteration_parity(gpu):
     import ctypes
     g, pd = (1024, 512, 512), (8, 4, 4)
     s = sip.Solver(None, "f32", 0, lattice=(g, pd))
-    s._nglobal = 128
     s.generate(0, 1307)
     s.factor(0.92)
     s.load_phi([sip.field(*d) for (_, d, _) in s.blocks])
@@ -569,7 +561,6 @@ def test_cuda_graph_replay_matches_oracle(gpu, prec):
     try:
         g, pd = (40, 24, 20), (2, 1, 1)
         s = sip.Solver(None, prec, 0, lattice=(g, pd))
-        s._nglobal = 2
         origins, dims, nbr = O.lattice(g, pd)
         As = []
         for lb, (bid, d, o) in enumerate(s.blocks):

@@ -35,7 +35,6 @@ def test_sip_through_nccl_matches_oracle(gpu, nccl_self, prec):
     g, pd = (40, 36, 24), (2, 2, 2)
     iters = 5
     s = sip.Solver(None, prec, 0, lattice=(g, pd))
-    s._nglobal = 8
     origins, dims, nbr = O.lattice(g, pd)
     As = []
     for lb, (bid, d, o) in enumerate(s.blocks):
@@ -75,7 +74,6 @@ def test_pressure_correct_through_nccl_matches_oracle(gpu, nccl_self):
     g, pd, bc = (16, 12, 8), (2, 2, 1), (OF.PERIODIC, OF.PERIODIC, OF.WALL, OF.WALL, OF.WALL, OF.WALL)
     lengths, dt, cap, sweeps = (1.0, 0.75, 0.5), 0.05, 2, 3
     s = sip.Solver(None, "f64", 0, lattice=(g, pd))
-    s._nglobal = 4
     s.assemble_poisson(lengths, ("periodic", "periodic", "wall", "wall", "wall", "wall"))
     s.factor(0.92)
     us, vs, ws, ps = _smooth_fields(g, pd)
