@@ -51,6 +51,7 @@ def lib():
         L.orc_sweep_pipe_f.restype = ctypes.c_double
         L.orc_solve.restype = ctypes.c_int
         L.orc_solve_multi.restype = ctypes.c_int
+        L.orc_solve_multi_gen.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -179,6 +180,55 @@ def solve_multi(blocks, nbr, alpha: float, iters: int, precision: str = "f64", n
     rc = lib().orc_solve_multi(nb, dims, nb_, 0 if precision == "f64" else 1,
                                ctypes.c_double(alpha), iters, arr, phis, _p(norms), _p(bnorms),
                                nthreads, ctypes.byref(bad))
+    if rc == 1:
+        raise ValueError(f"singular factorization at Field3 index {bad.value}")
+    return norms[:iters], bnorms[:iters]
+
+
+def solve_pipe(A: dict, phi: np.ndarray, alpha: float, iters: int, precision: str = "f64",
+               nthreads: int = 0):
+    """solve() with the sweeps pipelined over host threads (orc_sweep_pipe_*,
+    bitwise equal to the serial sweep): factor in fp64, fp32 mode converts the
+    system, factors and phi once at entry and the interior back at exit
+    (exactly orc_solve).  For the full-size BASELINE configs."""
+    nthreads = nthreads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+    F = factor(A, alpha)
+    norms = np.zeros(iters)
+    if precision == "f64":
+        work = np.zeros_like(phi)
+        for it in range(iters):
+            norms[it] = sweep_pipe(A, F, phi, nthreads, work)
+        return norms
+    A32 = {n: np.ascontiguousarray(v, dtype=np.float32) for n, v in A.items()}
+    F32 = {n: np.ascontiguousarray(v, dtype=np.float32) for n, v in F.items()}
+    ph = phi.astype(np.float32)
+    work = np.zeros_like(ph)
+    for it in range(iters):
+        norms[it] = sweep_pipe(A32, F32, ph, nthreads, work)
+    phi[1:-1, 1:-1, 1:-1] = ph[1:-1, 1:-1, 1:-1].astype(np.float64)
+    return norms
+
+
+def solve_multi_gen(kind: int, seed0: int, gdims, pdims, phis, alpha: float, iters: int,
+                    precision: str = "f64", nthreads: int = 0):
+    """Block-Jacobi SIP over the generated lattice (block b: seed0 + b), each
+    block's system regenerated / refactored on the fly (orc_solve_multi_gen:
+    memory-lean).  phis: one Field3 fp64 array per block (in / out).  Returns
+    (norms[iters], block_norms[iters, nb])."""
+    nthreads = nthreads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+    origins, dims, nbr = lattice(gdims, pdims)
+    nb = len(dims)
+    org_ = (ctypes.c_int * (3 * nb))(*[x for o in origins for x in o])
+    dims_ = (ctypes.c_int * (3 * nb))(*[x for d in dims for x in d])
+    nbr_ = (ctypes.c_int * (6 * nb))(*[x for n in nbr for x in n])
+    ph = (_dp * nb)(*[_p(p) for p in phis])
+    g = (ctypes.c_int * 3)(*gdims)
+    norms = np.zeros(max(iters, 1))
+    bnorms = np.zeros((max(iters, 1), nb))
+    bad = ctypes.c_longlong(-1)
+    rc = lib().orc_solve_multi_gen(kind, ctypes.c_uint64(seed0), g, nb, org_, dims_, nbr_,
+                                   0 if precision == "f64" else 1, ctypes.c_double(alpha), iters, ph,
+                                   _p(norms), _p(bnorms), int(nthreads), ctypes.byref(bad))
     if rc == 1:
         raise ValueError(f"singular factorization at Field3 index {bad.value}")
     return norms[:iters], bnorms[:iters]

@@ -603,3 +603,91 @@ done:
   free(F);
   return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Block-Jacobi SIP over a generated lattice, memory-lean (test driver for   */
+/* the full-size BASELINE configs): same algorithm and results as           */
+/* orc_solve_multi on orc_generate's systems, but each block's system is     */
+/* regenerated and refactored on the fly every iteration (the work arrays    */
+/* of a block live only while a thread relaxes it), so a 128-block lattice   */
+/* needs ~1 phi per block instead of 16 arrays per block.  Block b's system  */
+/* is orc_generate(kind, seed0 + b, g, org[3b..], dims[3b..]).  phi[b]:      */
+/* Field3 fp64, interior written back at the end (fp32: converted once at    */
+/* entry / exit, interface ghosts = neighbours' converted interior).         */
+/* ------------------------------------------------------------------------ */
+int orc_solve_multi_gen(int kind, uint64_t seed0, const int g[3], int nb, const int* org,
+                        const int* dims, const int* nbr, int precision, double alpha, int iters,
+                        double* const* phi, double* norms, double* block_norms, int nthreads,
+                        long long* bad) {
+  int rc = 0;
+  double* bn = (double*)xalloc((size_t)nb * 8);
+  float** ph = NULL;
+  if (precision != 0) {
+    ph = (float**)calloc(nb, sizeof(float*));
+    for (int b = 0; b < nb; ++b) {
+      size_t G = (size_t)(dims[3 * b] + 2) * (dims[3 * b + 1] + 2) * (dims[3 * b + 2] + 2);
+      ph[b] = (float*)xalloc(G * 4);
+      for (size_t n = 0; n < G; ++n) ph[b][n] = (float)phi[b][n];
+    }
+    exchange_faces_f(nb, dims, nbr, ph);
+  } else {
+    exchange_faces(nb, dims, nbr, phi);
+  }
+  for (int it = 0; it < iters && !rc; ++it) {
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1) if (nthreads > 1)
+    for (int b = 0; b < nb; ++b) {
+      int nx = dims[3 * b], ny = dims[3 * b + 1], nz = dims[3 * b + 2];
+      size_t G = (size_t)(nx + 2) * (ny + 2) * (nz + 2);
+      double* A = (double*)xalloc(16 * G * 8); /* 8 arrays + 7 factors + work */
+      double* F = A + 8 * G;
+      orc_generate(kind, seed0 + (uint64_t)b, g, org + 3 * b, nx, ny, nz, A, A + G, A + 2 * G,
+                   A + 3 * G, A + 4 * G, A + 5 * G, A + 6 * G, A + 7 * G);
+      long long bb = -1;
+      int r = orc_factor(nx, ny, nz, alpha, A, A + G, A + 2 * G, A + 3 * G, A + 4 * G, A + 5 * G,
+                         A + 6 * G, F, F + G, F + 2 * G, F + 3 * G, F + 4 * G, F + 5 * G, F + 6 * G,
+                         &bb);
+      if (r) {
+#pragma omp critical
+        {
+          rc = 1;
+          if (bad) *bad = bb;
+        }
+      } else if (precision == 0) {
+        bn[b] = orc_sweep_d(nx, ny, nz, A, A + G, A + 2 * G, A + 3 * G, A + 4 * G, A + 5 * G,
+                            A + 6 * G, A + 7 * G, F, F + G, F + 2 * G, F + 3 * G, F + 4 * G,
+                            F + 5 * G, F + 6 * G, phi[b], F + 7 * G);
+      } else {
+        float* S = (float*)xalloc(16 * G * 4);
+        for (int a = 0; a < 15; ++a)
+          for (size_t n = 0; n < G; ++n) S[a * G + n] = (float)A[a * G + n];
+        bn[b] = orc_sweep_f(nx, ny, nz, S, S + G, S + 2 * G, S + 3 * G, S + 4 * G, S + 5 * G,
+                            S + 6 * G, S + 7 * G, S + 8 * G, S + 9 * G, S + 10 * G, S + 11 * G,
+                            S + 12 * G, S + 13 * G, S + 14 * G, ph[b], S + 15 * G);
+        free(S);
+      }
+      free(A);
+    }
+    if (rc) break;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      s += bn[b];
+      if (block_norms) block_norms[(size_t)it * nb + b] = bn[b];
+    }
+    norms[it] = s;
+    if (precision != 0) exchange_faces_f(nb, dims, nbr, ph);
+    else exchange_faces(nb, dims, nbr, phi);
+  }
+  if (precision != 0) {
+    for (int b = 0; b < nb; ++b) {
+      int nx = dims[3 * b], ny = dims[3 * b + 1], nz = dims[3 * b + 2];
+      for (int k = 1; k <= nz; ++k)
+        for (int j = 1; j <= ny; ++j)
+          for (int i = 1; i <= nx; ++i) phi[b][IDX(i, j, k)] = (double)ph[b][IDX(i, j, k)];
+      free(ph[b]);
+    }
+    free(ph);
+    exchange_faces(nb, dims, nbr, phi);
+  }
+  free(bn);
+  return rc;
+}

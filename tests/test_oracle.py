@@ -392,3 +392,34 @@ def test_pipelined_sweep_matches_serial(prec, nthreads):
         n2 = O.sweep_pipe(A, F, p2, nthreads, work)
         assert np.array_equal(p1, p2)
         assert n2 == pytest.approx(n1, rel=1e-12)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_solve_pipe_equals_solve(prec):
+    """solve_pipe (factor + threaded sweeps, the full-size parity driver) is
+    bitwise the serial orc_solve; the norms are summed per thread (1e-12)."""
+    dims = (21, 35, 9)
+    A = O.generate(0, 77, dims)
+    p1, p2 = O.field(*dims), O.field(*dims)
+    p1[0, :, :] = 0.3  # a B ghost plane: kept by both
+    p2[0, :, :] = 0.3
+    n1 = O.solve(A, p1, 0.92, 6, prec)
+    n2 = O.solve_pipe(A, p2, 0.92, 6, prec, nthreads=4)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(n1, n2, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_solve_multi_gen_equals_solve_multi(prec):
+    """The memory-lean block-Jacobi driver (systems regenerated per iteration)
+    gives orc_solve_multi's phi and block norms bit for bit."""
+    g, pd = (30, 26, 20), (3, 2, 2)
+    origins, dims, nbr = O.lattice(g, pd)
+    blocks = [(O.generate(0, 500 + b, dims[b], g, origins[b]), O.field(*dims[b])) for b in range(len(dims))]
+    n1, b1 = O.solve_multi(blocks, nbr, 0.92, 5, prec, nthreads=3)
+    phis = [O.field(*d) for d in dims]
+    n2, b2 = O.solve_multi_gen(0, 500, g, pd, phis, 0.92, 5, prec, nthreads=3)
+    np.testing.assert_array_equal(b1, b2)
+    np.testing.assert_array_equal(n1, n2)
+    for (A, p), q in zip(blocks, phis):
+        assert np.array_equal(p, q)
