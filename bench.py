@@ -4,13 +4,15 @@ MLUP/s and achieved HBM GB/s vs peak).
 
 A "step" is one solve of the hot path over one synthetic system: `iters`
 SIP inner iterations (residual + forward substitution K2, backward
-substitution K3, face-halo exchange K4 for multi-block) on the
-configuration's grid.  MLUP/s = cells x iterations / time.
+substitution K3, face-halo exchange for multi-block) on the configuration's
+grid.  MLUP/s = cells x iterations / time.
 
-    python bench.py                      # N=1: config 1 (256^3, fp64 headline + fp32)
+    python bench.py                      # N=1: config 1 (256^3, fp64 headline + fp32),
+                                         #      configs 2, 3, 4 as sub-objects
+    python bench.py --gpus N             # N>1: spawns N ranks (torchrun), BASELINE config 3
+                                         #      (2x2x2 blocks of 128^3 per GPU, weak scaling)
+    python bench.py --gpus N --config 4  # strong scaling: 1024x512x512 in 128 blocks, fp32
     python bench.py --impl reference     # reference arm: CPU SIP (oracle port) on host cores
-    torchrun --nproc-per-node N bench.py --gpus N   # weak scaling: one config-1 block per GPU
-    python bench.py --config 3                       # BASELINE config 3 (8 x 128^3 per GPU)
 
 value: device-resident throughput (inputs in HBM, CUDA events on the
 library's launch stream, max over ranks).  e2e: the same metric through the
@@ -19,6 +21,9 @@ buffers: H2D of su and phi, D2H of phi and the norm history inside the
 timed region).  roofline: dominant kernel (K2 forward) -- algorithmic bytes
 per launch (14 of the 20 array touches per cell) over its
 CUDA-event duration, against MEASURED_PEAKS.json's HBM copy bandwidth.
+efficiency (N>1): Eq. 1 of the reference's perf report (perf.cpp:97-130),
+eps = T_s / (N * T_p(N)), with T_s the 1-GPU time of the whole job measured
+by rank 0 in the same run (weak scaling: N x the 1-GPU time of one GPU's share).
 """
 from __future__ import annotations
 
@@ -147,7 +152,7 @@ def cpu_reference(cfg_id: int, seconds: float = 12.0):
     work = np.zeros_like(phi)
     cells = dims[0] * dims[1] * dims[2]
     n, t = 0, 0.0
-    while t < seconds and n < c["iters"]:
+    while t < seconds and n < 20 * c["iters"]:
         t0 = time.perf_counter()
         O.sweep_pipe(A, F, phi, ncores, work)
         t += time.perf_counter() - t0
@@ -177,103 +182,115 @@ def make_solver(cfg_id, prec, rank, world, device, nccl_id=None):
     return s, g, p
 
 
-def run_gpu(args, rank, world, dist):
+def config_keys(cfg_id, world):
+    """The `config` object of both arms (identical keys, so the two lines
+    describe the same workload)."""
+    c = CONFIGS[cfg_id]
+    if cfg_id in (3, 5):
+        lx, ly, lz = GPU_LATTICE.get(world, (world, 1, 1))
+        g = (256 * lx, 256 * ly, 256 * lz)
+        p = (2 * lx, 2 * ly, 2 * lz) if cfg_id == 3 else (lx, ly, lz)
+    else:
+        g, p = c["g"], c["p"]
+    return {"workload": c["workload"], "grid": list(g), "blocks": list(p),
+            "iters_per_step": c["iters"], "alpha": 0.92,
+            "l2": "inputs larger than L2 (working set >> 126 MB)"}
+
+
+def measure(cfg_id, prec, rank, world, dist, stream, steps, warmup, e2e_reps=0):
+    """One configuration / precision on this rank's GPU(s): device-resident
+    throughput (max over ranks), the per-kernel roofline pass and, if asked,
+    the e2e call."""
     import torch
 
     import paper_1303_4538_b200 as sip
 
-    torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
-    cfg_id = args.config if args.config is not None else (1 if world == 1 else 5)
     c = CONFIGS[cfg_id]
-    # a dedicated (non-default) stream: the library launches on it and the CUDA
-    # events below are recorded on it (a NULL handle would mean "library's own
-    # stream" to sip_set_stream, invisible to events on torch's legacy stream)
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
     peak, peak_src = load_peak()
-    results = {}
-    precs = c["prec"] if args.precision == "auto" else (args.precision,)
-    for prec in precs:
-        nccl_id = None
-        if world > 1:  # a fresh ncclUniqueId per communicator
-            obj = [sip.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nccl_id = obj[0]
-        s, g, p = make_solver(cfg_id, prec, rank, world, torch.cuda.current_device(), nccl_id)
-        s.set_stream(stream.cuda_stream)
-        seed = 1303 + (1 if cfg_id == 5 else cfg_id)
-        s.generate(c["kind"], seed)
-        s.factor(0.92)
-        # resident phi0 = 0 for every local block
-        phis = [sip.field(*d) for (_, d, _) in s.blocks]
-        s.load_phi(phis)
-        cells_local = sum(d[0] * d[1] * d[2] for (_, d, _) in s.blocks)
-        cells_total = g[0] * g[1] * g[2]
-        iters = c["iters"]
+    nccl_id = None
+    if world > 1:  # a fresh ncclUniqueId per communicator
+        obj = [sip.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    s, g, p = make_solver(cfg_id, prec, rank, world, torch.cuda.current_device(), nccl_id)
+    s.set_stream(stream.cuda_stream)
+    seed = 1303 + (1 if cfg_id == 5 else cfg_id)
+    s.generate(c["kind"], seed)
+    s.factor(0.92)
+    phis = [sip.field(*d) for (_, d, _) in s.blocks]  # resident phi0 = 0
+    s.load_phi(phis)
+    cells_local = sum(d[0] * d[1] * d[2] for (_, d, _) in s.blocks)
+    cells_total = g[0] * g[1] * g[2]
+    iters = c["iters"]
 
-        def barrier():
-            if dist is not None:
-                dist.barrier()
-            torch.cuda.synchronize()
-
-        for _ in range(args.warmup):
-            s.iterate(iters)
-        barrier()
-        l0 = s.launch_count()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(torch.cuda.current_device()) as clk:
-            ev0.record(stream)
-            for _ in range(args.steps):
-                s.iterate(iters)
-            ev1.record(stream)
-            barrier()
-        ms = ev0.elapsed_time(ev1)
-        launches = s.launch_count() - l0
+    def barrier():
         if dist is not None:
-            t = torch.tensor([ms], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        ms_step = ms / args.steps
-        mlups = cells_total * iters * args.steps / (ms / 1e3) / 1e6
-        # norms of the last step (sanity: finite, decreasing overall)
-        nrm = s.read_norms(0, min(iters, 3))
+            dist.barrier()
+        torch.cuda.synchronize()
 
-        # per-kernel CUDA-event pass (same stream) for the roofline
-        s.set_profiling(True)
+    for _ in range(warmup):
         s.iterate(iters)
-        prof = s.profile()
-        s.set_profiling(False)
-        esz = 8 if prec == "f64" else 4
-        fwd_launch_ms = prof["fwd_ms"] / iters
-        bwd_launch_ms = prof["bwd_ms"] / iters
-        fwd_bytes = cells_local * TOUCH_FWD * esz
-        bwd_bytes = cells_local * TOUCH_BWD * esz
-        achieved = fwd_bytes / (fwd_launch_ms / 1e3) / 1e9
-        bwd_achieved = bwd_bytes / (bwd_launch_ms / 1e3) / 1e9
-        step_gbs = cells_local * (TOUCH_FWD + TOUCH_BWD) * esz * iters / (ms_step / 1e3) / 1e9
+    barrier()
+    l0 = s.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        for _ in range(steps):
+            s.iterate(iters)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = s.launch_count() - l0
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / steps
+    mlups = cells_total * iters * steps / (ms / 1e3) / 1e6
+    # norms of the run, read once after the timed region (sanity)
+    nrm = s.read_norms(0, min(iters, 3))
 
-        # e2e through the reference-facing call with pinned host buffers
-        e2e = None
-        if not args.no_e2e:
-            e2e = run_e2e(s, c, cfg_id, prec, args, dist, stream)
-        traffic = load_traffic(cfg_id, prec)
-        results[prec] = dict(
-            value=mlups, ms=ms_step, launches=launches, clocks=clk.summary(), e2e=e2e,
-            roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                      "frac": achieved / peak, "traffic": traffic, "kernel": "k_forward (K2)",
-                      "peak_source": peak_src, "alg_bytes_per_launch": fwd_bytes,
-                      "launch_ms": fwd_launch_ms},
-            k3={"kernel": "k_backward (K3)", "achieved": bwd_achieved, "frac": bwd_achieved / peak,
-                "launch_ms": bwd_launch_ms, "alg_bytes_per_launch": bwd_bytes},
-            step_gbs=step_gbs, step_frac=step_gbs / peak, halo_ms=prof["halo_ms"] / iters,
-            kernel_ms_per_iter=(prof["fwd_ms"] + prof["bwd_ms"] + prof["halo_ms"]) / iters,
-            first_norms=[float(x) for x in nrm], geometry=s.geometry(), cells_total=cells_total,
-            cells_local=cells_local, g=g, p=p)
-        s.close()
-    return cfg_id, results
+    # per-kernel CUDA-event pass (same stream) for the roofline
+    s.set_profiling(True)
+    s.iterate(iters)
+    prof = s.profile()
+    s.set_profiling(False)
+    esz = 8 if prec == "f64" else 4
+    fwd_launch_ms = prof["fwd_ms"] / iters
+    bwd_launch_ms = prof["bwd_ms"] / iters
+    fwd_bytes = cells_local * TOUCH_FWD * esz
+    bwd_bytes = cells_local * TOUCH_BWD * esz
+    achieved = fwd_bytes / (fwd_launch_ms / 1e3) / 1e9
+    bwd_achieved = bwd_bytes / (bwd_launch_ms / 1e3) / 1e9
+    step_gbs = cells_local * (TOUCH_FWD + TOUCH_BWD) * esz * iters / (ms_step / 1e3) / 1e9
+    e2e = run_e2e(s, c, cfg_id, prec, e2e_reps, dist, stream) if e2e_reps else None
+    r = dict(
+        value=mlups, ms=ms_step, launches=launches, clocks=clk.summary(), e2e=e2e,
+        roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                  "frac": achieved / peak, "traffic": load_traffic(cfg_id, prec),
+                  "kernel": "k_forward (K2)", "peak_source": peak_src,
+                  "alg_bytes_per_launch": fwd_bytes, "launch_ms": fwd_launch_ms},
+        k3={"kernel": "k_backward (K3)", "achieved": bwd_achieved, "frac": bwd_achieved / peak,
+            "launch_ms": bwd_launch_ms, "alg_bytes_per_launch": bwd_bytes},
+        step_gbs=step_gbs, step_frac=step_gbs / peak, halo_ms=prof["halo_ms"] / iters,
+        kernel_ms_per_iter=(prof["fwd_ms"] + prof["bwd_ms"] + prof["halo_ms"]) / iters,
+        first_norms=[float(x) for x in nrm], geometry=s.geometry(), cells_total=cells_total,
+        cells_local=cells_local, g=g, p=p)
+    s.close()
+    return r
 
 
-def run_e2e(s, c, cfg_id, prec, args, dist, stream):
+def summary(r, cfg_id, prec):
+    """Sub-object of one extra configuration in the N=1 line."""
+    return {"workload": CONFIGS[cfg_id]["workload"], "dtype": prec, "value": r["value"],
+            "unit": "MLUP/s", "ms_per_step": r["ms"], "iters_per_step": CONFIGS[cfg_id]["iters"],
+            "roofline_frac_k2": r["roofline"]["frac"], "roofline_frac_k3": r["k3"]["frac"],
+            "k2_launch_ms": r["roofline"]["launch_ms"], "k3_launch_ms": r["k3"]["launch_ms"],
+            "halo_ms_per_iter": r["halo_ms"], "achieved_frac_step": r["step_frac"],
+            "gpu_launches": r["launches"], "clocks": r["clocks"]}
+
+
+def run_e2e(s, c, cfg_id, prec, reps, dist, stream):
     import torch
 
     import paper_1303_4538_b200 as sip
@@ -299,7 +316,6 @@ def run_e2e(s, c, cfg_id, prec, args, dist, stream):
     G = sum(p[1].size for p in phis)
     h2d = 2 * G * 8
     d2h = G * 8 + iters * 8
-    reps = max(1, min(args.steps, 3))
 
     def one():
         # inputs of the step: Q and phi0 from pinned host memory (phi0 = the previous step's
@@ -393,6 +409,46 @@ def run_caller(cfg_id):
             "sip_mlups": cells * sweeps / (sip_ms * 1e-3) / 1e6, "factorizations": 1}
 
 
+def spawn(args) -> int:
+    """--gpus N without a launcher: re-run this script under torchrun, one
+    rank per GPU (fails loudly when fewer than N GPUs are visible)."""
+    import socket
+
+    import torch
+
+    n = args.gpus
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def reference_line(args, world):
+    cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+    c = CONFIGS[cfg_id]
+    vals = []
+    base = None
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        base = cpu_reference(cfg_id, seconds=max(2.0, 20.0 / max(1, args.steps)))
+        vals.append(base["value"])
+    v = statistics.median(vals)
+    base["value"] = v
+    return {"metric": "SIP inner-iteration MLUP/s", "value": v, "unit": "MLUP/s",
+            "impl": "reference", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak" if cfg_id != 4 else "strong",
+            "dtype": c["prec"][0], "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+            "config": config_keys(cfg_id, world), "vs_baseline": None, "cpu_baseline": base,
+            "e2e": {"value": v, "unit": "MLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -404,69 +460,87 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-caller", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="N=1: skip the config 2/3/4 sub-objects")
     args = ap.parse_args()
 
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        # reference arm: CPU SIP on host cores, rank 0 only (others exit 0)
+        if rank == 0:
+            print(json.dumps(reference_line(args, max(world, args.gpus))), flush=True)
+        return
+    if not launched and args.gpus > 1:
+        sys.exit(spawn(args))
+    if launched and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
+    # NCCL's own init log names the communicator size (driver check of N ranks)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist_mod.init_process_group("gloo", rank=rank, world_size=world)
         dist = dist_mod
 
-    if args.impl == "reference":
-        # reference arm: CPU SIP on host cores, rank 0 only
-        if rank == 0:
-            cfg_id = args.config if args.config is not None else (1 if world == 1 else 5)
-            c = CONFIGS[cfg_id]
-            vals = []
-            base = None
-            t_all = time.perf_counter()
-            for _ in range(args.steps):
-                base = cpu_reference(cfg_id, seconds=max(2.0, 20.0 / max(1, args.steps)))
-                vals.append(base["value"])
-            v = statistics.median(vals)
-            base["value"] = v
-            line = {"metric": "SIP inner-iteration MLUP/s", "value": v, "unit": "MLUP/s",
-                    "impl": "reference", "n_gpus": world, "steps": args.steps,
-                    "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-                    "dtype": c["prec"][0], "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-                    "config": {"workload": c["workload"], "iters_per_step": c["iters"],
-                               "cpu_sample": base["sample"]},
-                    "vs_baseline": None, "cpu_baseline": base,
-                    "e2e": {"value": v, "unit": "MLUP/s", "h2d_bytes_per_step": 0,
-                            "d2h_bytes_per_step": 0},
-                    "wall_s": time.perf_counter() - t_all}
-            print(json.dumps(line), flush=True)
-        if dist is not None:
-            dist.destroy_process_group()
-        return
+    import torch
 
     import paper_1303_4538_b200 as sip
 
     sip.lib()  # fail loudly if the native library is missing
-    cfg_id, res = run_gpu(args, rank, world, dist)
+    torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
+    # a dedicated (non-default) stream: the library launches on it and the CUDA
+    # events are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    cfg_id = args.config if args.config is not None else (1 if world == 1 else 3)
+    c = CONFIGS[cfg_id]
+    precs = c["prec"] if args.precision == "auto" else (args.precision,)
+    res = {}
+    for prec in precs:
+        res[prec] = measure(cfg_id, prec, rank, world, dist, stream, args.steps, args.warmup,
+                            0 if args.no_e2e else 10)
+    head = "f64" if "f64" in res else list(res)[0]
+    r = res[head]
+    # Eq. 1 efficiency: T_s from rank 0 alone on one GPU (the whole job for
+    # strong scaling; one GPU's share x N for weak scaling)
+    eff = None
+    if world > 1:
+        t1 = None
+        if rank == 0:
+            r1 = measure(cfg_id, head, 0, 1, None, stream, args.steps, 1)
+            t1 = r1["ms"]
+        obj = [t1]
+        dist.broadcast_object_list(obj, src=0)
+        t1 = obj[0]
+        strong = cfg_id == 4
+        t_s = t1 if strong else world * t1
+        eff = {"eq": "perf.cpp Eq. 1: eps = T_s / (N * T_p(N))", "scaling": "strong" if strong else "weak",
+               "t_s_ms": t_s, "t_p_ms": r["ms"], "n": world, "eps": t_s / (world * r["ms"]),
+               "t1_source": "rank 0 alone, " + ("whole job" if strong else "one GPU's share") + ", same run"}
     if rank == 0:
-        c = CONFIGS[cfg_id]
-        head = "f64" if "f64" in res else list(res)[0]
-        r = res[head]
         cpu = None
         if world == 1 and not args.no_cpu:
             cpu = cpu_reference(cfg_id, seconds=12.0)
         caller = None
         if world == 1 and not args.no_caller and cfg_id == 1:
             caller = run_caller(cfg_id)
+        extra = None
+        if world == 1 and cfg_id == 1 and not args.no_extra and args.config is None:
+            extra = {}
+            for xc in (2, 3, 4):
+                xp = CONFIGS[xc]["prec"][0]
+                extra[f"config{xc}"] = summary(measure(xc, xp, 0, 1, None, stream, 2, 1), xc, xp)
         line = {
             "metric": "SIP inner-iteration MLUP/s", "value": r["value"], "unit": "MLUP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": r["ms"], "higher_is_better": True,
+            "scaling": "strong" if cfg_id == 4 and world > 1 else "weak",
             "vs_baseline": None, "dtype": head, "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-            "config": {"workload": c["workload"], "grid": list(r["g"]), "blocks": list(r["p"]),
-                       "iters_per_step": c["iters"], "alpha": 0.92,
-                       "l2": "inputs larger than L2 (working set >> 126 MB)",
-                       "tile": r["geometry"], "parallelism": f"blocks over {world} GPU(s)"},
+            "config": config_keys(cfg_id, world),
+            "layout": {"bricks": r["geometry"], "parallelism": f"blocks over {world} GPU(s)"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
             "gpu_launches": r["launches"], "clocks": r["clocks"],
             "achieved_hbm_gbs_step": r["step_gbs"], "achieved_frac_step": r["step_frac"],
@@ -474,7 +548,9 @@ def main():
             "kernel_ms_per_iter": r["kernel_ms_per_iter"],
             "timed_ms_per_iter": r["ms"] / c["iters"],
             "first_norms": r["first_norms"],
+            "efficiency": eff,
             "caller": caller,
+            "configs": extra,
         }
         for prec, rr in res.items():
             if prec == head:
