@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -113,12 +114,17 @@ struct SipConfig {
   int max_iters = 50;
   double target = 0.0;  // <= 0: fixed iteration count
   bool single_precision = false;
+  int check_every = 8;  // target mode: norm-evaluation interval (sip_solve_ex)
 };
 
-/// SPEC.md:128-131
+/// iterations used, initial / final norms, per-iteration
+/// history, wall time in factorisation vs relaxation (host clock around the
+/// library calls; both calls synchronise before returning).
 struct SolveReport {
   int iterations = 0;
   std::vector<double> norms;
+  double factor_seconds = 0.0;  // 0 on the reuse path (no factorisation)
+  double relax_seconds = 0.0;   // su / fi0 upload, sweeps, fi and norms download
   double initial() const { return norms.empty() ? 0.0 : norms.front(); }
   double final_norm() const { return norms.empty() ? 0.0 : norms.back(); }
 };
@@ -152,6 +158,8 @@ class SipFactors {
   }
   sip_ctx* ctx() const { return ctx_; }
   long long stamp() const { return stamp_; }
+  /// Library-side factorisation counter of the context.
+  long long factorizations() const { return ctx_ ? ::sip_factor_count(ctx_) : 0; }
   bool single_precision() const { return single_; }
 
  private:
@@ -182,9 +190,13 @@ template <class Field>
 std::pair<Field, SolveReport> solve(const StencilSystemT<Field>& A, const Field& fi0,
                                     const SipConfig& cfg, SipFactors* F = nullptr,
                                     int device = 0) {
+  using clock = std::chrono::steady_clock;
   SipFactors own;
+  double t_factor = 0.0;
   if (!F) {
+    const auto t0 = clock::now();
     own = sip_factor(A, cfg, device);
+    t_factor = std::chrono::duration<double>(clock::now() - t0).count();
     F = &own;
   } else if (F->stamp() != A.revision) {
     throw StaleFactorsError("solve: factors stamped with revision " + std::to_string(F->stamp()) +
@@ -194,13 +206,17 @@ std::pair<Field, SolveReport> solve(const StencilSystemT<Field>& A, const Field&
   }
   Field fi = fi0;
   SolveReport rep;
+  rep.factor_seconds = t_factor;
   if (cfg.target >= 1.0) return {fi, rep};
+  const auto t0 = clock::now();
   check(::sip_set_source(F->ctx(), 0, A.q.data()), F->ctx(), "sip_set_source");
   rep.norms.assign(static_cast<size_t>(cfg.max_iters), 0.0);
   double* phis[1] = {fi.data()};
   int used = 0;
-  check(::sip_solve(F->ctx(), phis, cfg.max_iters, cfg.target, rep.norms.data(), &used), F->ctx(),
-        "sip_solve");
+  check(::sip_solve_ex(F->ctx(), phis, cfg.max_iters, cfg.target, cfg.check_every, rep.norms.data(),
+                       &used),
+        F->ctx(), "sip_solve");
+  rep.relax_seconds = std::chrono::duration<double>(clock::now() - t0).count();
   rep.norms.resize(static_cast<size_t>(used));
   rep.iterations = used;
   return {fi, rep};

@@ -124,6 +124,16 @@ int sip_factor(sip_ctx* ctx, double alpha, long long* bad_block, long long* bad_
  */
 int sip_solve(sip_ctx* ctx, double* const* phi, int max_iters, double target, double* norms_out,
               int* iters_used);
+/* sip_solve with the norm-evaluation interval of the target-reduction mode
+ * (SPEC.md DESIGN DECISIONS: "every s-th sweep").  Single rank: the stop is
+ * exact (the forward sweep's finaliser tests norm/norm[0] <= target on the
+ * device and the remaining sweeps return at once); check_every only sets how
+ * often the host polls the stop flag (<= 0: never before the end).  Several
+ * ranks: the global norm is all-gathered and tested every check_every sweeps
+ * (>= 1), so the solve stops at the first tested sweep meeting the target.
+ * sip_solve = check_every 8 (single rank) / 1 (several ranks). */
+int sip_solve_ex(sip_ctx* ctx, double* const* phi, int max_iters, double target, int check_every,
+                 double* norms_out, int* iters_used);
 
 /* Device-resident path (used for the HBM-resident throughput number). */
 int sip_load_phi(sip_ctx* ctx, double* const* phi);      /* host Field3 -> device */

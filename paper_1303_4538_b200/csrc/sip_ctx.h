@@ -116,6 +116,8 @@ struct sip_ctx {
   bool nccl_self = false;
   long long plan_gen = 0;  // bumped by install_plan (flows are bound to one plan)
   unsigned* d_norm_it = nullptr;  // device iteration counter (== n_done between calls)
+  unsigned* d_ctl = nullptr;      // [0] target reached (K2 skips), [1] K3 pending (SweepParams::ctl)
+  double solve_target = 0.0;      // > 0 while a single-rank target solve is enqueued
   // CUDA graph of one sip_iterate(iters) call (single rank, no profiling,
   // opt-in): kernels of `iters` iterations captured once and replayed
   cudaGraphExec_t graph_exec = nullptr;

@@ -193,6 +193,12 @@ struct SweepParams {
   double* norms_base;
   double* bnorms_base;
   unsigned* norm_it;
+  // device-side stop of a target-reduction solve (single rank): the K2
+  // finaliser of the first sweep with norm / norm[0] <= target sets ctl[0];
+  // a K2 launch that finds ctl[0] set returns at once.  ctl[1]: a K2 ran and
+  // its K3 is pending (K3 returns at once when it is 0).  target <= 0: never stop.
+  double target;
+  unsigned* ctl;
   unsigned long long* trace;  // optional [nbricks][4]: start ns, end ns, smid, stalls (debug)
   // debug: per-stage clock64 marks of brick trace_brick (first kTraceStages stages,
   // kTraceMarks each) after the per-brick table

@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
   int* const s_brick = reinterpret_cast<int*>(smem + C::off_misc);
   double* const s_nrm = reinterpret_cast<double*>(smem + C::off_misc + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (*(volatile unsigned*)P.ctl) return;  // target reached by an earlier sweep
   const uint32_t tag = *P.epoch;
   if (threadIdx.x == 0) {
     for (int q = 0; q < D; ++q) {
@@ -658,6 +659,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
         __syncwarp();
         if (lane == 0) mbar_arrive(rdone0 + 8 * q);
         mark(n, 3);
+        if (n == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
       }
       trace_end(P.trace, bid);
       // the residual warp's brick norm (written before its last ready arrive)
@@ -681,6 +683,11 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           P.state_other[0] = 0u;
           P.state_other[1] = 0u;
           *P.epoch = tag + 1;
+          P.ctl[1] = 1u;  // this sweep's K3 runs
+          if (P.target > 0.0) {  // same test as the host loop: n0 == 0 or n / n0 <= target
+            const double n0 = it == 0 ? tot : P.norms_base[0];
+            if (n0 == 0.0 || tot / n0 <= P.target) P.ctl[0] = 1u;
+          }
         }
       }
     } else {
@@ -746,6 +753,7 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
                  empty0 = cdone0 + 8 * D;
   int* const s_brick = reinterpret_cast<int*>(smem + C::off_misc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!*(volatile unsigned*)(P.ctl + 1)) return;  // the sweep's K2 did not run (target reached)
   const uint32_t tag = *P.epoch;
   if (threadIdx.x == 0) {
     for (int q = 0; q < D; ++q) {
@@ -890,12 +898,14 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
         __syncwarp();
         if (lane == 0) mbar_arrive(cdone0 + 8 * q);
         mark(m, 3);
+        if (m == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
       }
       trace_end(P.trace, bid);
       if (brick_done(P.state, P.nbricks) && lane == 0) {
         P.state_other[0] = 0u;
         P.state_other[1] = 0u;
         *P.epoch = tag + 1;
+        P.ctl[1] = 0u;
       }
     } else {
       // ------------------------------------------------------------- mailbox

@@ -58,7 +58,7 @@ EXPORTS = (
     "sip_ftt1_read", "sip_ftt1_write", "sip_ftt1_validate", "sip_set_halo_tables",
     "sip_plan_halo_periodic", "sip_assemble_poisson", "sip_flow_create", "sip_flow_destroy",
     "sip_flow_set", "sip_flow_get", "sip_flow_divergence", "sip_pressure_correct",
-    "sip_factor_count", "sip_num_global_blocks",
+    "sip_factor_count", "sip_num_global_blocks", "sip_solve_ex",
 )
 
 
@@ -321,11 +321,19 @@ class Solver:
         arr = (_dp * len(phis))(*[_ptr(p) for p in phis])
         return arr
 
-    def solve(self, phis: Sequence[np.ndarray], max_iters: int, target: float = 0.0):
+    def solve(self, phis: Sequence[np.ndarray], max_iters: int, target: float = 0.0,
+              check_every: Optional[int] = None):
+        """solve; check_every: norm-evaluation interval of the
+        target mode (None: sip_solve's default)."""
         norms = np.zeros(max(max_iters, 1))
         used = ctypes.c_int(0)
-        self._c(lib().sip_solve(self._ctx, self._phis(phis), max_iters, ctypes.c_double(target),
-                                norms.ctypes.data_as(_dp), ctypes.byref(used)), "sip_solve")
+        if check_every is None:
+            st = lib().sip_solve(self._ctx, self._phis(phis), max_iters, ctypes.c_double(target),
+                                 norms.ctypes.data_as(_dp), ctypes.byref(used))
+        else:
+            st = lib().sip_solve_ex(self._ctx, self._phis(phis), max_iters, ctypes.c_double(target),
+                                    int(check_every), norms.ctypes.data_as(_dp), ctypes.byref(used))
+        self._c(st, "sip_solve")
         return norms[:used.value]
 
     def load_phi(self, phis):

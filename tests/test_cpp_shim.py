@@ -80,3 +80,33 @@ def test_flow_shim_reuses_one_factorization(gpu, tmp_path):
     for s in steps:
         d0, d1 = float(s[5]), float(s[7])
         assert int(s[3]) >= 1 and d1 <= 0.1 * d0
+
+
+REF_INCLUDE = "/root/reference/proj/include"
+
+
+def build_ref(tmp_path):
+    exe = str(tmp_path / "shim_ref_example")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "shim_ref_example.cpp"), "-L", LIBDIR,
+                    "-lsip_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    return exe
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="reference headers only in the build container")
+def test_shim_with_reference_field_and_errors(tmp_path):
+    """The shim compiled against the reference's own headers: bsfv::FieldD as
+    the field type and BSFV_SIP_USE_REFERENCE_ERRORS=1, so a library failure
+    surfaces as the reference's bsfv::Error (here: no CUDA device)."""
+    exe = build_ref(tmp_path)
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except Exception:
+        gpu = False
+    r = subprocess.run([exe, "8"], capture_output=True, text=True)
+    if gpu:
+        out = r.stdout.splitlines()
+        assert r.returncode == 0 and out[-2] == "factorizations 1" and out[-1] == "stale ok", out
+    else:
+        assert r.returncode == 3 and r.stdout.startswith("bsfv::Error: sip_create: CUDA error"), r.stdout

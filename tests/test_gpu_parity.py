@@ -525,3 +525,50 @@ def test_cuda_graph_replay_matches_oracle(gpu, prec):
     np.testing.assert_allclose(ng, no, rtol=NORM_TOL)
     for b in range(2):
         assert np.array_equal(phis[b], blocks[b][1])
+
+
+@pytest.mark.parametrize("check_every", [1, 3, 8, 0])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_target_mode_stops_exactly_on_device(gpu, prec, check_every):
+    """Target reduction with the norm-evaluation interval:
+    the forward sweep's finaliser tests norm / norm[0] <= target on the
+    device, so the solve runs exactly the sweeps up to the first one meeting
+    the target whatever the host poll interval; phi bitwise = the oracle run
+    for that many sweeps."""
+    dims = (24, 20, 18)
+    A = O.generate(0, 91, dims)
+    target = 1e-5
+    s = sip.Solver(dims, prec)
+    s.set_system(0, sip.StencilSystem.from_dict(A))
+    s.factor(0.92)
+    pg = O.field(*dims)
+    ng = s.solve([pg], 300, target, check_every=check_every)
+    s.close()
+    # the oracle's stopping sweep
+    full = O.solve(A, O.field(*dims), 0.92, 300, prec)
+    want = next(i + 1 for i in range(300) if full[i] / full[0] <= target)
+    assert len(ng) == want
+    po = O.field(*dims)
+    no = O.solve(A, po, 0.92, want, prec)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL, atol=0)
+    assert np.array_equal(pg, po)
+
+
+def test_target_mode_multiblock_and_reuse(gpu):
+    """Device stop on a block lattice, then a fixed-count solve on the same
+    context (the stop flag is reset per solve); library factor counter = 1."""
+    g, pd = (40, 36, 30), (2, 2, 1)
+    s = sip.Solver(None, "f64", 0, lattice=(g, pd))
+    s.generate(0, 1306)
+    s.factor(0.92)
+    phis = [O.field(*d) for (_, d, _) in s.blocks]
+    n1 = s.solve(phis, 400, 1e-4, check_every=5)
+    assert 1 < len(n1) < 400 and n1[-1] / n1[0] <= 1e-4 and n1[-2] / n1[0] > 1e-4
+    phis = [O.field(*d) for (_, d, _) in s.blocks]
+    n2 = s.solve(phis, 7)
+    assert len(n2) == 7
+    np.testing.assert_array_equal(n2, n1[:7])
+    assert s.factor_count() == 1
+    s.factor(0.5)
+    assert s.factor_count() == 2
+    s.close()
