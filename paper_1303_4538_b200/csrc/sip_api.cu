@@ -526,7 +526,15 @@ int sipb::exchange(sip_ctx* ctx) {
 }
 
 template <typename T>
+static int launch_iterations_impl(sip_ctx* ctx, int iters);
+template <typename T>
 static int launch_iterations(sip_ctx* ctx, int iters) {
+  const int s = launch_iterations_impl<T>(ctx, iters);
+  if (s != SIP_OK) ctx->failed = true;
+  return s;
+}
+template <typename T>
+static int launch_iterations_impl(sip_ctx* ctx, int iters) {
   for (int n = 0; n < iters; ++n) {
     (void)n;
     cudaEvent_t e;
@@ -557,6 +565,10 @@ static void drop_graph(sip_ctx* ctx) {
 // replay needs no new parameters.
 template <typename T>
 int sipb::iterate_t(sip_ctx* ctx, int iters) {
+  if (ctx->failed) {
+    ctx->err = "an earlier sweep launch failed part-way: sip_load_phi (or sip_solve) resets the context";
+    return SIP_ERR_CUDA;
+  }
   CKS(ensure_norm_cap(ctx, ctx->n_done + iters));
   const int sym = 0;  // one forward kernel for general and symmetric systems
   const bool graph = ctx->use_graphs && iters > 0 && !ctx->prof && !ctx->trace && ctx->peers.empty();
@@ -898,6 +910,11 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi) {
   ctx->n_done = 0;
   CK(cudaMemsetAsync(ctx->d_norm_it, 0, sizeof(unsigned), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_ctl, 0, 4 * sizeof(unsigned), ctx->stream));
+  if (ctx->failed) {  // device sweep state back to "no sweep in flight"
+    CK(cudaMemsetAsync(ctx->st_f, 0, 32 * sizeof(unsigned), ctx->stream));
+    CK(cudaMemsetAsync(ctx->st_b, 0, 32 * sizeof(unsigned), ctx->stream));
+    ctx->failed = false;
+  }
   return s;
 }
 

@@ -118,6 +118,10 @@ struct sip_ctx {
   unsigned* d_norm_it = nullptr;  // device iteration counter (== n_done between calls)
   unsigned* d_ctl = nullptr;      // [0] target reached (K2 skips), [1] K3 pending (SweepParams::ctl)
   double solve_target = 0.0;      // > 0 while a single-rank target solve is enqueued
+  // a sweep launch failed part-way: the device counters (ticket / done state,
+  // norm slot, stop flags) may be out of step with the host; iterate refuses
+  // until sip_load_phi resets them
+  bool failed = false;
   // CUDA graph of one sip_iterate(iters) call (single rank, no profiling,
   // opt-in): kernels of `iters` iterations captured once and replayed
   cudaGraphExec_t graph_exec = nullptr;
