@@ -1324,13 +1324,13 @@ int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
   const size_t nt = ctx->hbricks.size();
   *ntiles = (long long)nt;
   if (!ctx->trace) {
-    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 2 * kTraceStages * kTraceMarks)));
+    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 5 * kTraceStages * kTraceMarks)));
     if (const char* tb = getenv("SIPB_TRACE_BRICK")) ctx->trace_brick = atoi(tb);
     return SIP_OK;
   }
   if (out) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 2 * kTraceStages * kTraceMarks),
+    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 5 * kTraceStages * kTraceMarks),
                   cudaMemcpyDeviceToHost));
   }
   return SIP_OK;

@@ -41,6 +41,53 @@ namespace sipb {
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// A value the compiler cannot re-derive: keeps the shared-window base in a
+// register (otherwise it is rematerialised with S2R SR_CgaCtaId + LEA in
+// every stage of the chain warps' loops).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+// shared loads / stores by 32-bit shared address (volatile: kept in program
+// order relative to the mbarrier waits / arrives that guard the slot)
+template <typename T>
+__device__ __forceinline__ T lds(uint32_t a);
+template <>
+__device__ __forceinline__ double lds<double>(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ float lds<float>(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// predicated forms: the load / arrive happens only when p != 0 (a branch
+// would end the basic block the chain is scheduled in)
+template <typename T>
+__device__ __forceinline__ T lds_if(uint32_t p, uint32_t a);
+template <>
+__device__ __forceinline__ double lds_if<double>(uint32_t p, uint32_t a) {
+  double v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}\n"
+               : "=d"(v) : "r"(a), "r"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ float lds_if<float>(uint32_t p, uint32_t a) {
+  float v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.f32 %0, [%1];\n}\n"
+               : "=f"(v) : "r"(a), "r"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 // Watchdog: a spin that makes no progress for kWatchdogNs aborts the kernel
 // (__trap -> the launch fails with an error instead of hanging the GPU).
 constexpr unsigned long long kWatchdogNs = 4000000000ULL;
@@ -81,6 +128,22 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "r"(bar), "r"(parity)
       : "memory");
   return ok != 0;
+}
+// non-blocking phase test (try_wait may suspend the thread for a while)
+__device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_arrive_if(uint32_t p, uint32_t bar) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(bar),
+               "r"(p)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int where) {
   if (mbar_try(bar, parity)) return;
@@ -421,12 +484,53 @@ __device__ __forceinline__ T settle(Tagged<T> v, bool need, const unsigned long 
   if (need && !v.ok(tag)) {
     Watchdog wd;
     do {
+#ifdef SIPB_BACKOFF
+      __nanosleep(SIPB_BACKOFF);
+#endif
       v.load(src);
       wd.idle(where);
     } while (!v.ok(tag));
   }
   return need ? v.value() : T(0);
 }
+
+// whole warp: like settle(), but the re-poll keeps two loads in flight
+// (the poll interval is half an L2 round trip instead of a full one)
+template <typename T>
+__device__ __forceinline__ T settle2(Tagged<T> v, bool need, const unsigned long long* src, uint32_t tag,
+                                    int where) {
+  if (need && !v.ok(tag)) {
+    Watchdog wd;
+    Tagged<T> a, b;
+    a.load(src);
+    for (;;) {
+      b.load(src);
+      if (a.ok(tag)) {
+        v = a;
+        break;
+      }
+      a.load(src);
+      if (b.ok(tag)) {
+        v = b;
+        break;
+      }
+      wd.idle(where);
+    }
+  }
+  return need ? v.value() : T(0);
+}
+// Mailbox reads issued kLook stages ahead of their use (static register
+// slots, the stage loop unrolled by kLook): the mailbox warp's throughput is
+// then no longer one L2 round trip per stage.
+#ifndef SIPB_LOOK
+#define SIPB_LOOK 1
+#endif
+constexpr int kLook = SIPB_LOOK;
+#ifdef SIPB_SETTLE2
+#define SIPB_SETTLE settle2
+#else
+#define SIPB_SETTLE settle
+#endif
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
@@ -435,7 +539,8 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   auto slot = [&](int q) { return reinterpret_cast<T*>(smem + q * C::slot_bytes); };
   T* const s_ph = reinterpret_cast<T*>(smem + C::off_ph);
-  const uint32_t full0 = saddr(smem + C::off_bar), ready0 = full0 + 8 * D, mbx0 = ready0 + 8 * D,
+  const uint32_t sb = opaque(saddr(smem));
+  const uint32_t full0 = sb + (uint32_t)C::off_bar, ready0 = full0 + 8 * D, mbx0 = ready0 + 8 * D,
                  rdone0 = mbx0 + 8 * D, empty0 = rdone0 + 8 * D;
   int* const s_brick = reinterpret_cast<int*>(smem + C::off_misc);
   double* const s_nrm = reinterpret_cast<double*>(smem + C::off_misc + 8);
@@ -447,8 +552,8 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
       mbar_init(full0 + 8 * q, 33);  // producer lane 0 expect_tx + 32 cp.async arrivals
       mbar_init(ready0 + 8 * q, 2);  // residual warp (r) + mailbox warp (cross-brick R)
       mbar_init(mbx0 + 8 * q, 1);    // (unused)
-      mbar_init(rdone0 + 8 * q, 1);  // recurrence warp: R of the stage in the slot
-      mbar_init(empty0 + 8 * q, 2);  // residual + recurrence warps: slot inputs consumed
+      mbar_init(rdone0 + 8 * q, kL);      // recurrence warp, every lane: R of the stage in the slot
+      mbar_init(empty0 + 8 * q, 1 + kL);  // residual (lane 0) + recurrence (every lane): inputs consumed
     }
     fence_mbar_init();
   }
@@ -508,8 +613,8 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
                         ((cN & (kW - 1)) < bd.wI);
         put_tagged_if(pn, P.mB + (bd.mrow + (pn ? cN : 0)) * kTagWords<T>, vN, tag);
       };
-      for (int n = 0; n < NST; ++n, ++g) {
-        const int q = (int)(g % D);
+      int q = (int)(g % D);
+      for (int n = 0; n < NST; ++n, ++g, q = q + 1 == D ? 0 : q + 1) {
         if (g >= D) {
           if (n >= D) drain(n - D, q);
           bar_wait(empty0 + 8 * q, ph_b, q, 40);
@@ -537,8 +642,8 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
     } else if (warp == 1) {
       // ------------------------------------------------------------ residual
       double nrm = 0.0;
-      for (int n = 0; n < NST; ++n, ++g) {
-        const int q = (int)(g % D);
+      int q = (int)(g % D);
+      for (int n = 0; n < NST; ++n, ++g, q = q + 1 == D ? 0 : q + 1) {
         bar_wait(full0 + 8 * q, ph_a, q, 41);
         const T* const F = slot(q) + lane;
         const T* const ed = slot(q) + C::o_ed;
@@ -597,38 +702,42 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
     } else if (warp == 2) {
       // ---------------------------------------------------------- recurrence
       trace_begin(P.trace, bid);
+#ifdef SIPB_STAGE_MARKS
       unsigned long long* const marks =
           (P.trace && bid == P.trace_brick) ? P.trace + 8ull * P.nbricks : nullptr;
       auto mark = [&](int n, int m) {
         if (marks && lane == 0 && n < kTraceStages) marks[n * kTraceMarks + m] = clock64();
       };
+#else
+      auto mark = [](int, int) {};
+#endif
       T Rprev = T(0);
       T win[kW];
 #pragma unroll
       for (int s = 0; s < kW; ++s) win[s] = T(0);
-      for (int n = 0; n < NST; ++n, ++g) {
-        const int q = (int)(g % D);
+      int q = (int)(g % D);
+      g += NST;
+      for (int n = 0; n < NST; ++n, q = q + 1 == D ? 0 : q + 1) {
         mark(n, 0);
         // ready = the residual warp's r (it waited for the TMA data of the
         // slot, so its release covers it) + the mailbox warp's values
         bar_wait(ready0 + 8 * q, ph_b, q, 43);
         mark(n, 1);
-        const T* const F = slot(q) + lane;
-        const T* const rin = slot(q) + C::o_r + lane;
-        const T* const mb = slot(q) + C::o_mb;
-        const T rW = mb[lane];
-        T t1[kStage], lw[kStage], ls[kStage], lp[kStage], eR[kStage];
+        constexpr uint32_t E = sizeof(T);
+        const uint32_t sq = sb + (uint32_t)q * (uint32_t)C::slot_bytes, sl = sq + E * lane;
+        const T rW = lds<T>(sl + E * C::o_mb);
+        T rin[kStage], lb[kStage], lw[kStage], ls[kStage], lp[kStage], eR[kStage];
 #pragma unroll
         for (int s = 0; s < kStage; ++s) {
-          const T* f = F + s * F_NA * kL;
-          t1[s] = rin[s * kL] - f[F_LB * kL] * win[s];  // R_B: previous stage's step s
-          lw[s] = f[F_LW * kL];
-          ls[s] = f[F_LS * kL];
-          lp[s] = f[F_LP * kL];
-          eR[s] = mb[kL + s];
+          const uint32_t f = sl + E * (s * F_NA * kL);
+          rin[s] = lds<T>(sl + E * (C::o_r + s * kL));
+          lb[s] = lds<T>(f + E * (F_LB * kL));
+          lw[s] = lds<T>(f + E * (F_LW * kL));
+          ls[s] = lds<T>(f + E * (F_LS * kL));
+          lp[s] = lds<T>(f + E * (F_LP * kL));
+          eR[s] = lds<T>(sq + E * (C::o_mb + kL + s));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * q);  // slot inputs now in registers
+        mbar_arrive(empty0 + 8 * q);  // slot inputs now in registers (every lane)
         // the recurrence; no masking on the chain: a valid
         // cell's W / S inputs are valid cells (or the mailbox), padding cells
         // compute exact zeros from the zero-filled packs
@@ -637,14 +746,14 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           const T RS1 = __shfl_up_sync(0xffffffffu, Rprev, 1);
           const T RW = (s == wedge_s) ? rW : Rprev;
           const T RS = lane == 0 ? eR[s] : RS1;
-          const T R = ((t1[s] - lw[s] * RW) - ls[s] * RS) * lp[s];
+          const T t1 = rin[s] - lb[s] * win[s];  // R_B: previous stage's step s
+          const T R = ((t1 - lw[s] * RW) - ls[s] * RS) * lp[s];
           win[s] = R;
           Rprev = R;
         }
         mark(n, 2);
         // (masked) R into the slot: the producer stores it and publishes the
         // E column / N row; the masked copy is also the register window
-        T* const Rout = slot(q) + C::o_R + lane;
         const bool interior = bd.wI == kW && bd.wJ == kL && n >= kL / kStage && n + kL / kStage < NST;
         if (!interior) {
 #pragma unroll
@@ -655,11 +764,12 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           }
         }
 #pragma unroll
-        for (int s = 0; s < kStage; ++s) Rout[s * kL] = win[s];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(rdone0 + 8 * q);
+        for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_R + s * kL), win[s]);
+        mbar_arrive(rdone0 + 8 * q);
         mark(n, 3);
+#ifdef SIPB_STAGE_MARKS
         if (n == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
+#endif
       }
       trace_end(P.trace, bid);
       // the residual warp's brick norm (written before its last ready arrive)
@@ -694,28 +804,81 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
       // ------------------------------------------------------------- mailbox
       // R of the W brick's E column at this lane's il == 0 step (lane jl:
       // entry k = n - jl / 8) and, lanes 16..23, of the S brick's N row at
-      // lane 0's step lane - 16; polled until this launch's tag shows, then
+      // lane 0's step lane - 16; read kLook stages ahead (only where a lane
+      // needs a value), re-polled until this launch's tag shows, then
       // deposited in the slot (0 across a block boundary)
-      for (int n = 0; n < NST; ++n, ++g) {
-        const int q = (int)(g % D);
-        if (g >= D) bar_wait(empty0 + 8 * q, ph_a, q, 46);
-        const int k = n - (lane >> 3);
-        const bool needA = bd.mWe >= 0 && lane_ok && k >= 0 && k < bd.nz;
-        const unsigned long long* aA = needA ? P.mA + (bd.mWe + (long long)k * kL + lane) * kTagWords<T> : P.mA;
-        const int c = n * kStage + (lane - 2 * kStage);
-        const bool needB =
-            lane >= 2 * kStage && lane < 3 * kStage && bd.mSr >= 0 && c < nzW && (c & (kW - 1)) < bd.wI;
-        const unsigned long long* aB = needB ? P.mB + (bd.mSr + c) * kTagWords<T> : P.mB;
-        Tagged<T> tA, tB;
-        tA.load(aA);
-        tB.load(aB);
-        const T vA = settle(tA, needA, aA, tag, 21);
-        const T vB = settle(tB, needB, aB, tag, 22);
-        T* const mb = slot(q) + C::o_mb;
-        mb[lane] = vA;
-        if (lane >= 2 * kStage && lane < 3 * kStage) mb[kL + lane - 2 * kStage] = vB;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(ready0 + 8 * q);
+      if constexpr (sizeof(T) == 8) {
+        // fp64 (HBM-bound): one read per stage, issued once the slot is free
+        // (measured 5 % faster than the read-ahead below at 256^3; fp32, which
+        // is hand-off bound, is 4 % faster with the read-ahead)
+        int q = (int)(g % D);
+        for (int n = 0; n < NST; ++n, ++g, q = q + 1 == D ? 0 : q + 1) {
+          if (g >= D) bar_wait(empty0 + 8 * q, ph_a, q, 46);
+          const int k = n - (lane >> 3);
+          const bool needA = bd.mWe >= 0 && lane_ok && k >= 0 && k < bd.nz;
+          const unsigned long long* aA = needA ? P.mA + (bd.mWe + (long long)k * kL + lane) * kTagWords<T> : P.mA;
+          const int c = n * kStage + (lane - 2 * kStage);
+          const bool needB =
+              lane >= 2 * kStage && lane < 3 * kStage && bd.mSr >= 0 && c < nzW && (c & (kW - 1)) < bd.wI;
+          const unsigned long long* aB = needB ? P.mB + (bd.mSr + c) * kTagWords<T> : P.mB;
+          Tagged<T> tA, tB;
+          tA.load(aA);
+          tB.load(aB);
+          const T vA = settle(tA, needA, aA, tag, 21);
+          const T vB = settle(tB, needB, aB, tag, 22);
+          T* const mb = slot(q) + C::o_mb;
+          mb[lane] = vA;
+          if (lane >= 2 * kStage && lane < 3 * kStage) mb[kL + lane - 2 * kStage] = vB;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(ready0 + 8 * q);
+        }
+      } else {
+        struct Req {
+          const unsigned long long *aA, *aB;
+          bool needA, needB;
+        };
+        auto req = [&](int n) {
+          const int k = n - (lane >> 3);
+          const int c = n * kStage + (lane - 2 * kStage);
+          Req r;
+          r.needA = n < NST && bd.mWe >= 0 && lane_ok && k >= 0 && k < bd.nz;
+          r.needB = n < NST && lane >= 2 * kStage && lane < 3 * kStage && bd.mSr >= 0 && c < nzW &&
+                    (c & (kW - 1)) < bd.wI;
+          r.aA = r.needA ? P.mA + (bd.mWe + (long long)k * kL + lane) * kTagWords<T> : P.mA;
+          r.aB = r.needB ? P.mB + (bd.mSr + c) * kTagWords<T> : P.mB;
+          return r;
+        };
+        Tagged<T> tA[kLook], tB[kLook];
+        auto issue = [&](int j, int n) {
+          const Req r = req(n);
+          tA[j] = Tagged<T>{};
+          tB[j] = Tagged<T>{};
+          if (r.needA) tA[j].load(r.aA);
+          if (r.needB) tB[j].load(r.aB);
+        };
+#pragma unroll
+        for (int j = 0; j < kLook; ++j) issue(j, j);
+        int q = (int)(g % D);
+        for (int n0 = 0; n0 < NST; n0 += kLook) {
+#pragma unroll
+          for (int j = 0; j < kLook; ++j) {
+            const int n = n0 + j;
+            if (n < NST) {
+              if (g >= D) bar_wait(empty0 + 8 * q, ph_a, q, 46);
+              const Req r = req(n);
+              const T vA = SIPB_SETTLE(tA[j], r.needA, r.aA, tag, 21);
+              const T vB = SIPB_SETTLE(tB[j], r.needB, r.aB, tag, 22);
+              issue(j, n + kLook);
+              T* const mb = slot(q) + C::o_mb;
+              mb[lane] = vA;
+              if (lane >= 2 * kStage && lane < 3 * kStage) mb[kL + lane - 2 * kStage] = vB;
+              __syncwarp();
+              if (lane == 0) mbar_arrive(ready0 + 8 * q);
+              ++g;
+              q = q + 1 == D ? 0 : q + 1;
+            }
+          }
+        }
       }
     }
     __syncthreads();  // brick done in all roles before the next claim
@@ -749,7 +912,8 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
   constexpr int D = C::D;
   extern __shared__ __align__(128) unsigned char smem[];
   auto slot = [&](int q) { return reinterpret_cast<T*>(smem + q * C::slot_bytes); };
-  const uint32_t full0 = saddr(smem + C::off_bar), mbx0 = full0 + 8 * D, cdone0 = mbx0 + 8 * D,
+  const uint32_t sb = opaque(saddr(smem));
+  const uint32_t full0 = sb + (uint32_t)C::off_bar, mbx0 = full0 + 8 * D, cdone0 = mbx0 + 8 * D,
                  empty0 = cdone0 + 8 * D;
   int* const s_brick = reinterpret_cast<int*>(smem + C::off_misc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -757,10 +921,10 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
   const uint32_t tag = *P.epoch;
   if (threadIdx.x == 0) {
     for (int q = 0; q < D; ++q) {
-      mbar_init(full0 + 8 * q, 2);  // producer expect_tx + mailbox warp
-      mbar_init(mbx0 + 8 * q, 1);   // (unused)
-      mbar_init(cdone0 + 8 * q, 1);
-      mbar_init(empty0 + 8 * q, 1);
+      mbar_init(full0 + 8 * q, 2);    // producer expect_tx + mailbox warp
+      mbar_init(mbx0 + 8 * q, 1);     // (unused)
+      mbar_init(cdone0 + 8 * q, kL);  // every compute lane
+      mbar_init(empty0 + 8 * q, kL);  // every compute lane
     }
     fence_mbar_init();
   }
@@ -781,6 +945,20 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
     const BrickDesc bd = P.bricks[bid];
     const int NST = bd.ns / kStage, nzW = bd.nz * kW;
     const bool lane_ok = lane < bd.wJ;
+#ifdef SIPB_STAGE_MARKS
+    // hand-off timing (globaltimer): region 3 = brick trace_brick + 1 (the E
+    // neighbour), region 4 = brick trace_brick; marks: 0 mailbox poll start,
+    // 1 mailbox value seen, 2 compute past full, 3 compute cdone, 4 published
+    unsigned long long* const hm =
+        P.trace && (bid == P.trace_brick || bid == P.trace_brick + 1)
+            ? P.trace + 4ull * P.nbricks + (bid == P.trace_brick ? 4 : 3) * kTraceStages * kTraceMarks
+            : nullptr;
+    auto hmark = [&](int m, int k) {
+      if (hm && lane == 0 && m < kTraceStages) hm[m * kTraceMarks + k] = gtime();
+    };
+#else
+    auto hmark = [](int, int) {};
+#endif
 
     if (warp == 0) {
       // ------------------------------------------------------------ producer
@@ -815,9 +993,10 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
         const bool ps = bd.mSr >= 0 && lane < kStage && bd.wJ > 0 && (unsigned)cS < (unsigned)nzW &&
                         ((cS & (kW - 1)) < bd.wI);
         put_tagged_if(ps, P.mB + (bd.mrow + (ps ? cS : 0)) * kTagWords<T>, vS, tag);
+        hmark(m, 4);
       };
-      for (int m = 0; m < NST; ++m, ++g) {
-        const int q = (int)(g % D);
+      int q = (int)(g % D);
+      for (int m = 0; m < NST; ++m, ++g, q = q + 1 == D ? 0 : q + 1) {
         if (g >= D) {
           if (m >= D) drain(m - D, q);
           bar_wait(empty0 + 8 * q, ph_b, q, 50);
@@ -836,54 +1015,50 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
       for (int m = NST > D ? NST - D : 0; m < NST; ++m) drain(m, (int)((g - NST + m) % D));
     } else if (warp == 1) {
       // ------------------------------------------------------------- compute
+      // One stage per iteration: wait for the slot (TMA data + the mailbox
+      // warp's values), inputs -> registers, release the slot, the 8-step
+      // chain, delta -> slot.  Every lane arrives on empty / cdone (count 32):
+      // each lane's release orders its own shared accesses, no warp barrier.
       trace_begin(P.trace, bid);
-      unsigned long long* const marks =
-          (P.trace && bid == P.trace_brick) ? P.trace + 8ull * P.nbricks + kTraceStages * kTraceMarks : nullptr;
-      auto mark = [&](int n, int m) {
-        if (marks && lane == 0 && n < kTraceStages) marks[n * kTraceMarks + m] = clock64();
-      };
+      constexpr uint32_t E = sizeof(T);
       T dprev = T(0);
       T win[kW];
 #pragma unroll
       for (int s = 0; s < kW; ++s) win[s] = T(0);
-      for (int m = 0; m < NST; ++m, ++g) {
-        const int n = NST - 1 - m, q = (int)(g % D);
-        mark(m, 0);
-        bar_wait(full0 + 8 * q, ph_a, q, 33);  // TMA data + the mailbox warp's values
-        mark(m, 1);
-        const T* const U = slot(q) + lane;
-        const T* const Rs = slot(q) + C::o_R + lane;
-        const T* const mb = slot(q) + C::o_mb;
-        const T dE = mb[lane];
-        // own data of the stage's steps and UT * dT (dT = previous stage's step s)
-        T rr[kStage], un[kStage], ue[kStage], utdt[kStage], eN[kStage];
+      int q = (int)(g % D);
+      g += NST;
+      for (int m = 0; m < NST; ++m, q = q + 1 == D ? 0 : q + 1) {
+        const int n = NST - 1 - m;
+        bar_wait(full0 + 8 * q, ph_a, q, 33);
+        hmark(m, 2);
+        const uint32_t sq = sb + (uint32_t)q * (uint32_t)C::slot_bytes, sl = sq + E * lane;
+        const T dE = lds<T>(sl + E * C::o_mb);
+        T rr[kStage], un[kStage], ue[kStage], ut[kStage], eN[kStage];
 #pragma unroll
         for (int s = 0; s < kStage; ++s) {
           const int o = kStage - 1 - s;  // slice tau = 8n + o
-          un[s] = U[(o * B_NA + B_UN) * kL];
-          ue[s] = U[(o * B_NA + B_UE) * kL];
-          utdt[s] = U[(o * B_NA + B_UT) * kL] * win[s];
-          rr[s] = Rs[o * kL];
-          eN[s] = mb[kL + s];
+          un[s] = lds<T>(sl + E * ((o * B_NA + B_UN) * kL));
+          ue[s] = lds<T>(sl + E * ((o * B_NA + B_UE) * kL));
+          ut[s] = lds<T>(sl + E * ((o * B_NA + B_UT) * kL));
+          rr[s] = lds<T>(sl + E * (C::o_R + o * kL));
+          eN[s] = lds<T>(sq + E * (C::o_mb + kL + s));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * q);  // slot inputs now in registers
-        mark(m, 3);
-        // delta = ((R - UN*dN) - UE*dE) - UT*dT; padding cells
-        // compute exact zeros (zero-filled packs), stored copies masked below
+        mbar_arrive(empty0 + 8 * q);  // slot inputs now in registers
+        // delta = ((R - UN*dN) - UE*dE) - UT*dT, dT = the
+        // previous stage's step s (win); padding cells compute exact zeros
+        // (zero-filled packs), stored copies masked below
 #pragma unroll
         for (int s = 0; s < kStage; ++s) {
+          const T utdt = ut[s] * win[s];
           const T dN1 = __shfl_down_sync(0xffffffffu, dprev, 1);
           const T dEv = (s == eedge_s) ? dE : dprev;
           const T dN = lane == kL - 1 ? eN[s] : dN1;
-          const T d = ((rr[s] - un[s] * dN) - ue[s] * dEv) - utdt[s];
+          const T d = ((rr[s] - un[s] * dN) - ue[s] * dEv) - utdt;
           win[s] = d;
           dprev = d;
         }
-        mark(m, 2);
         // delta into the slot (the producer applies it to phi and publishes);
         // the masked copy is also the register window
-        T* const Dout = slot(q) + C::o_pn + lane;
         const bool interior = bd.wI == kW && bd.wJ == kL && n >= kL / kStage && n + kL / kStage < NST;
         if (!interior) {
 #pragma unroll
@@ -894,11 +1069,9 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
           }
         }
 #pragma unroll
-        for (int s = 0; s < kStage; ++s) Dout[(kStage - 1 - s) * kL] = win[s];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(cdone0 + 8 * q);
-        mark(m, 3);
-        if (m == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
+        for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_pn + (kStage - 1 - s) * kL), win[s]);
+        mbar_arrive(cdone0 + 8 * q);
+        hmark(m, 3);
       }
       trace_end(P.trace, bid);
       if (brick_done(P.state, P.nbricks) && lane == 0) {
@@ -910,26 +1083,55 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
     } else {
       // ------------------------------------------------------------- mailbox
       // delta of the E brick's W column at this lane's il == kW-1 step and,
-      // lanes 24..31, of the N brick's S row at lane 31's step lane - 24
-      for (int m = 0; m < NST; ++m, ++g) {
-        const int n = NST - 1 - m, q = (int)(g % D);
-        if (g >= D) bar_wait(empty0 + 8 * q, ph_a, q, 56);
+      // lanes 24..31, of the N brick's S row at lane 31's step lane - 24;
+      // reads issued kLook stages ahead, re-polled until this launch's tag
+      struct Req {
+        const unsigned long long *aA, *aB;
+        bool needA, needB;
+      };
+      auto req = [&](int m) {
+        const int n = NST - 1 - m;
         const int k = n - ((lane + kW - 1) >> 3);
-        const bool needA = bd.mEe >= 0 && lane_ok && k >= 0 && k < bd.nz;
-        const unsigned long long* aA = needA ? P.mA + (bd.mEe + (long long)k * kL + lane) * kTagWords<T> : P.mA;
         const int c = n * kStage - 3 * kStage - (lane - 3 * kStage);
-        const bool needB = lane >= 3 * kStage && bd.mNr >= 0 && c >= 0 && c < nzW && (c & (kW - 1)) < bd.wI;
-        const unsigned long long* aB = needB ? P.mB + (bd.mNr + c) * kTagWords<T> : P.mB;
-        Tagged<T> tA, tB;
-        tA.load(aA);
-        tB.load(aB);
-        const T vA = settle(tA, needA, aA, tag, 31);
-        const T vB = settle(tB, needB, aB, tag, 32);
-        T* const mb = slot(q) + C::o_mb;
-        mb[lane] = vA;
-        if (lane >= 3 * kStage) mb[kL + lane - 3 * kStage] = vB;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full0 + 8 * q);
+        Req r;
+        r.needA = m < NST && bd.mEe >= 0 && lane_ok && k >= 0 && k < bd.nz;
+        r.needB = m < NST && lane >= 3 * kStage && bd.mNr >= 0 && c >= 0 && c < nzW && (c & (kW - 1)) < bd.wI;
+        r.aA = r.needA ? P.mA + (bd.mEe + (long long)k * kL + lane) * kTagWords<T> : P.mA;
+        r.aB = r.needB ? P.mB + (bd.mNr + c) * kTagWords<T> : P.mB;
+        return r;
+      };
+      Tagged<T> tA[kLook], tB[kLook];
+      auto issue = [&](int j, int m) {
+        const Req r = req(m);
+        tA[j] = Tagged<T>{};
+        tB[j] = Tagged<T>{};
+        if (r.needA) tA[j].load(r.aA);
+        if (r.needB) tB[j].load(r.aB);
+      };
+#pragma unroll
+      for (int j = 0; j < kLook; ++j) issue(j, j);
+      int q = (int)(g % D);
+      for (int m0 = 0; m0 < NST; m0 += kLook) {
+#pragma unroll
+        for (int j = 0; j < kLook; ++j) {
+          const int m = m0 + j;
+          if (m < NST) {
+            if (g >= D) bar_wait(empty0 + 8 * q, ph_a, q, 56);
+            hmark(m, 0);
+            const Req r = req(m);
+            const T vA = SIPB_SETTLE(tA[j], r.needA, r.aA, tag, 31);
+            const T vB = SIPB_SETTLE(tB[j], r.needB, r.aB, tag, 32);
+            hmark(m, 1);
+            issue(j, m + kLook);
+            T* const mb = slot(q) + C::o_mb;
+            mb[lane] = vA;
+            if (lane >= 3 * kStage) mb[kL + lane - 3 * kStage] = vB;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full0 + 8 * q);
+            ++g;
+            q = q + 1 == D ? 0 : q + 1;
+          }
+        }
       }
     }
     __syncthreads();

@@ -22,10 +22,10 @@ nt = ctypes.c_longlong()
 L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(3)
-buf = np.zeros(8 * nt.value + 2 * 64 * 6, dtype=np.uint64)
+buf = np.zeros(8 * nt.value + 5 * 64 * 6, dtype=np.uint64)
 L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
 tr = buf[:8 * nt.value].reshape(2, nt.value, 4)
-marks2 = buf[8 * nt.value:].reshape(2, 64, 6).astype(np.int64)
+marks2 = buf[8 * nt.value:].reshape(5, 64, 6).astype(np.int64)
 g = s.geometry()
 BX = (nx + g["brick_i"] - 1) // g["brick_i"]
 BY = (ny + g["brick_j"] - 1) // g["brick_j"]
@@ -45,15 +45,22 @@ for kind, name in ((0, "forward"), (1, "backward")):
     print("  row0 end:  ", " ".join(f"{en[x]:.0f}" for x in row))
     print("  col0 start:", " ".join(f"{st[x]:.0f}" for x in col))
     print("  col0 end:  ", " ".join(f"{en[x]:.0f}" for x in col))
+    s4 = (t[:, 3] - t0) / 1e3  # end of the brick's stage 4 (first interior stage)
+    print("  row0 stage4:", " ".join(f"{s4[x]:.0f}" for x in row))
+    print("  col0 stage4:", " ".join(f"{s4[x]:.0f}" for x in col))
     last = BX * BY - 1
     print(f"  last brick start {st[last]:.0f} end {en[last]:.0f}")
 for kk, marks in enumerate(marks2):
     if not marks[:, 0].any():
         continue
+    nz = [i for i in range(6) if marks[8, i] != 0]
+    if len(nz) < 2:
+        continue
+    marks = marks[:, nz]
     # per-stage marks of brick SIPB_TRACE_BRICK (cycles): validate, mbar wait, phase A, B, C
     d = np.diff(marks, axis=1)
     step = np.diff(marks[:, 0])
-    print("K%d stage marks (cycles, stages 8..63 median): %s  stage %.0f  (mean %s)" % (
-        2 + kk, " ".join("%.0f" % x for x in np.median(d[8:], axis=0)), np.median(step[8:]),
+    print("%s stage marks (cycles, stages 8..63 median): %s  stage %.0f  (mean %s)" % (
+        ("K2B", "K3C", "K2A", "P", "M")[kk], " ".join("%.0f" % x for x in np.median(d[8:], axis=0)), np.median(step[8:]),
         " ".join("%.0f" % x for x in np.mean(d[8:], axis=0))))
 s.close()
