@@ -1326,6 +1326,7 @@ int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
   if (!ctx->trace) {
     CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 5 * kTraceStages * kTraceMarks)));
     if (const char* tb = getenv("SIPB_TRACE_BRICK")) ctx->trace_brick = atoi(tb);
+    if (const char* tu = getenv("SIPB_TRACE_UP")) ctx->trace_brick |= atoi(tu) << 20;  // hop_trace: upstream offset
     return SIP_OK;
   }
   if (out) {

@@ -949,9 +949,11 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
     // hand-off timing (globaltimer): region 3 = brick trace_brick + 1 (the E
     // neighbour), region 4 = brick trace_brick; marks: 0 mailbox poll start,
     // 1 mailbox value seen, 2 compute past full, 3 compute cdone, 4 published
+    // (trace_brick: low 20 bits the brick, high bits the upstream offset, 0 = 1)
+    const int tb = P.trace_brick & 0xFFFFF, tup = (P.trace_brick >> 20) ? (P.trace_brick >> 20) : 1;
     unsigned long long* const hm =
-        P.trace && (bid == P.trace_brick || bid == P.trace_brick + 1)
-            ? P.trace + 4ull * P.nbricks + (bid == P.trace_brick ? 4 : 3) * kTraceStages * kTraceMarks
+        P.trace && (bid == tb || bid == tb + tup)
+            ? P.trace + 4ull * P.nbricks + (bid == tb ? 4 : 3) * kTraceStages * kTraceMarks
             : nullptr;
     auto hmark = [&](int m, int k) {
       if (hm && lane == 0 && m < kTraceStages) hm[m * kTraceMarks + k] = gtime();

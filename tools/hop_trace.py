@@ -1,4 +1,5 @@
-"""Hand-off timing between a brick and its E neighbour in one backward sweep
+"""Hand-off timing between a brick and its E neighbour (SIPB_TRACE_UP=1) or N
+neighbour (SIPB_TRACE_UP=BX) in one backward sweep
 (library built with EXTRA=-DSIPB_STAGE_MARKS; SIPB_TRACE_BRICK = the W brick).
 usage: SIPB_LIB=exp/libsip_marks.so SIPB_TRACE_BRICK=b python tools/hop_trace.py [f64|f32] [n]"""
 import ctypes
@@ -33,7 +34,7 @@ print("  up:   cdone -> published          %.3f us" % med([up[m, 4] - up[m, 3] f
 print("  down: poll start -> seen         %.3f us" % med([dn[m, 1] - dn[m, 0] for m in r]))
 print("  down: seen -> compute past full  %.3f us" % med([dn[m, 2] - dn[m, 1] for m in r]))
 print("  down: past full -> cdone         %.3f us" % med([dn[m, 3] - dn[m, 2] for m in r]))
-for d in range(0, 3):
+for d in range(0, 7):
     print(f"  seen_down(m) - published_up(m+{d}) %.3f us" % med([dn[m, 1] - up[m + d, 4] for m in r]))
 print("  cdone_down(m) - cdone_up(m)        %.3f us" % med([dn[m, 3] - up[m, 3] for m in r]))
 s.close()
