@@ -9,21 +9,23 @@
 //   K7 k_scatter / k_gather / k_phi_in   Field3 <-> brick-slice layout
 //   k_residual     residual_general / residual_symmetric
 //
-// Wavefront scheme: ONE WARP per brick of kW x kL
-// columns, persistent CTAs (one warp each) claiming bricks through an atomic
-// ticket in topological order.  Lane jl owns row j0 + jl and walks its cells
-// c = k * kW + il one per step, jl steps behind lane 0, so at slice
-// tau = c + jl:
+// Wavefront scheme (DESIGN.md sections 4-5): a brick of kW x kL columns is
+// swept by ONE recurrence warp; persistent CTAs (one brick at a time) claim
+// bricks through an atomic ticket in topological order.  Lane jl owns row
+// j0 + jl and walks its cells c = k * kW + il one per step, jl steps behind
+// lane 0, so at slice tau = c + jl:
 //   * the W neighbour (c - 1) is the lane's own previous step (register),
 //   * the S neighbour (lane jl - 1, same c) is one __shfl_up of the previous step,
 //   * the B neighbour (c - kW) is the lane's own step tau - kW (register window).
 // The recurrence therefore needs no barrier at all: its critical path per step
-// is shfl + 3 dependent floating-point operations.  The streamed packs come in
-// by TMA bulk copies (cp.async.bulk + mbarrier complete_tx) into a ring of
-// stages of kStage slices, issued by lane 0 D stages ahead.  Across bricks, the
-// producing lanes store self-validating tagged words (value + launch epoch)
-// to a mailbox; the consumer loads them one stage ahead into registers and
-// re-polls only if the epoch does not match yet.  No grid barrier, no counter.
+// is shfl + 4 dependent floating-point operations.  The other warps of the CTA
+// are specialised: a producer streams the packs by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a ring of D stages of kStage
+// slices and drains the results, a mailbox warp fetches the neighbour bricks'
+// edge values, and (K2) a residual warp computes the 8-term residuals ahead of
+// the recurrence.  Across bricks, the producer stores self-validating tagged
+// words (value + launch epoch) to a mailbox; the consumer's mailbox warp
+// re-polls only while the epoch does not match.  No grid barrier, no counter.
 //
 // Bitwise parity: every cell performs the oracle's operations in the oracle's
 // order (oracle/sip_oracle.c header); this file is compiled with
