@@ -576,6 +576,19 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
     const BrickDesc bd = P.bricks[bid];
     const int NST = bd.ns / kStage, nzW = bd.nz * kW;
     const bool lane_ok = lane < bd.wJ;
+#ifdef SIPB_STAGE_MARKS
+    // pipeline timing of brick trace_brick (clock64, one SM; tools/k2_pipe.py):
+    // region 2, per stage: 0 TMA issued, 1 residual past full, 2 residual
+    // ready, 3 mailbox ready, 4 recurrence past ready, 5 recurrence rdone
+    unsigned long long* const pmk =
+        P.trace && bid == (P.trace_brick & 0xFFFFF) ? P.trace + 8ull * P.nbricks + 2 * kTraceStages * kTraceMarks
+                                                    : nullptr;
+    auto pm = [&](int n, int k) {
+      if (pmk && (threadIdx.x & 31) == 0 && n < kTraceStages) pmk[n * kTraceMarks + k] = clock64();
+    };
+#else
+    auto pm = [](int, int) {};
+#endif
 
     if (warp == 0) {
       // ------------------------------------------------------------ producer
@@ -639,6 +652,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           put_chunk(n + 1, full);
         }
         cp_async_arrive(full);
+        pm(n, 0);
       }
       for (int n = NST > D ? NST - D : 0; n < NST; ++n) drain(n, (int)((g - NST + n) % D));
     } else if (warp == 1) {
@@ -647,6 +661,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
       int q = (int)(g % D);
       for (int n = 0; n < NST; ++n, ++g, q = q + 1 == D ? 0 : q + 1) {
         bar_wait(full0 + 8 * q, ph_a, q, 41);
+        pm(n, 1);
         const T* const F = slot(q) + lane;
         const T* const ed = slot(q) + C::o_ed;
         const T* const Pw = s_ph + pmod(n, QP) * C::kCh + lane;  // slice 8n - 8
@@ -700,6 +715,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           mbar_arrive(ready0 + 8 * q);
           mbar_arrive(empty0 + 8 * q);
         }
+        pm(n, 2);
       }
     } else if (warp == 2) {
       // ---------------------------------------------------------- recurrence
@@ -725,6 +741,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
         // slot, so its release covers it) + the mailbox warp's values
         bar_wait(ready0 + 8 * q, ph_b, q, 43);
         mark(n, 1);
+        pm(n, 4);
         constexpr uint32_t E = sizeof(T);
         const uint32_t sq = sb + (uint32_t)q * (uint32_t)C::slot_bytes, sl = sq + E * lane;
         const T rW = lds<T>(sl + E * C::o_mb);
@@ -768,6 +785,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
 #pragma unroll
         for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_R + s * kL), win[s]);
         mbar_arrive(rdone0 + 8 * q);
+        pm(n, 5);
         mark(n, 3);
 #ifdef SIPB_STAGE_MARKS
         if (n == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
@@ -833,6 +851,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
           if (lane >= 2 * kStage && lane < 3 * kStage) mb[kL + lane - 2 * kStage] = vB;
           __syncwarp();
           if (lane == 0) mbar_arrive(ready0 + 8 * q);
+          pm(n, 3);
         }
       } else {
         struct Req {
@@ -876,6 +895,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
               if (lane >= 2 * kStage && lane < 3 * kStage) mb[kL + lane - 2 * kStage] = vB;
               __syncwarp();
               if (lane == 0) mbar_arrive(ready0 + 8 * q);
+              pm(n, 3);
               ++g;
               q = q + 1 == D ? 0 : q + 1;
             }
