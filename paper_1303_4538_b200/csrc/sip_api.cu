@@ -665,7 +665,7 @@ template int sipb::iterate_t<double>(sip_ctx*, int);
 extern "C" {
 
 const char* sip_version(void) {
-  return "b200-sip 0.2 (sm_100a, 16x16-column tile wavefront K1/K2/K3 with tagged cross-tile hand-off, NCCL face halos, pressure-correction caller)";
+  return "b200-sip 0.3 (sm_100a, 8x32-column brick wavefront K1/K2/K3: warp-specialised TMA-fed rings, tagged cross-brick mailboxes, NCCL face halos, pressure-correction caller)";
 }
 
 const char* sip_status_string(int s) {

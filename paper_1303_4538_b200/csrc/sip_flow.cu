@@ -10,7 +10,7 @@
 // staging mirror).  Every step is a handful of HBM-bound stencil kernels
 // around the SIP iterations: face ghosts of u, v, w (device copies / NCCL,
 // the solver's halo plan incl. periodic wraps), divergence + source scatter,
-// SIP sweeps from p' = 0, p' gather, velocity / pressure update.
+// SIP sweeps from p' = 0, velocity / pressure update from p' in place.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -197,21 +197,75 @@ __global__ void __launch_bounds__(kFlowThreads) k_sum_partials(const double* par
   }
 }
 
-// u -= dt * dp'/dx (central), v, w likewise; p += p'.  CTA (x, k): cells
-// [256x, 256x + 256) of plane k.
-__global__ void __launch_bounds__(kFlowThreads) k_correct(int nx, int ny, double* u, double* v,
-                                                          double* w, double* p, const double* pp,
-                                                          double c2x, double c2y, double c2z,
-                                                          double dt) {
-  const int ij = blockIdx.x * kFlowThreads + threadIdx.x;
-  if (ij >= nx * ny) return;
-  const int i = ij % nx + 1, j = ij / nx + 1, k = blockIdx.y + 1;
-  const long long x = f3(nx, ny, i, j, k);
-  const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
-  u[x] = u[x] - dt * ((pp[x + 1] - pp[x - 1]) / c2x);
-  v[x] = v[x] - dt * ((pp[x + sy] - pp[x - sy]) / c2y);
-  w[x] = w[x] - dt * ((pp[x + sz] - pp[x - sz]) / c2z);
-  p[x] = p[x] + pp[x];
+// u -= dt * dp'/dx (central), v, w likewise; p += p' -- reading p' straight
+// from the solver's phi (brick layout): no gather into a Field3 mirror and no
+// wall kernel for p'.  CTA (brick, c)
+// stages p' of the brick's kW x kL columns over planes [kCorKC*c, +kCorKC)
+// plus a one-cell halo in shared memory -- the brick's own slices as
+// coalesced 32-lane rows, the halo cell by cell: the neighbour brick's cell,
+// the phi ghost (interface / periodic face, exchanged after the last sweep)
+// or, at a wall / symmetry face, the interior cell (Neumann: what
+// k_flow_walls gives the gathered p').  Values and operation order are
+// those of the Field3 formulation (oracle/flow.py), so u, v, w, p are bitwise
+// the oracle's.
+constexpr int kCorKC = 8;
+template <typename T>
+__global__ void __launch_bounds__(kFlowThreads) k_correct_b(const BlockDesc* blocks, int blk, int wall,
+                                                            const T* __restrict__ phi, double* u, double* v,
+                                                            double* w, double* p, double c2x, double c2y,
+                                                            double c2z, double dt) {
+  static_assert(kW * kL == kFlowThreads, "one thread per brick column");
+  __shared__ double sp[kCorKC + 2][kL + 2][kW + 2];
+  const BlockDesc bd = blocks[blk];
+  const int nx = bd.nx, ny = bd.ny, nz = bd.nz;
+  const int r = blockIdx.x, bi = r % bd.BX, bj = r / bd.BX;
+  const int i0 = bi * kW, j0 = bj * kL, k0 = blockIdx.y * kCorKC;
+  const int wI = min(kW, nx - i0), wJ = min(kL, ny - j0), wK = min(kCorKC, nz - k0);
+  // own slices: warp q loads slices tau = 8 k0 + q, + 8, ...; lane = jl
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const long long pslot = phi_slot(bd, r);
+  for (int tau = kW * k0 + q; tau < kW * (k0 + wK) + kL - 1; tau += kFlowThreads / 32) {
+    const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
+    if (lane < wJ && c >= 0 && k >= k0 && k < k0 + wK && ci < wI)
+      sp[k - k0 + 1][lane + 1][ci + 1] = static_cast<double>(phi[(pslot + tau) * kL + lane]);
+  }
+  // halo faces of the chunk (no edges / corners: 7-point stencil)
+  auto pv = [&](int i, int j, int k) {
+    if (i < 0 && (wall & (1 << G_W))) i = 0;
+    if (i >= nx && (wall & (1 << G_E))) i = nx - 1;
+    if (j < 0 && (wall & (1 << G_S))) j = 0;
+    if (j >= ny && (wall & (1 << G_N))) j = ny - 1;
+    if (k < 0 && (wall & (1 << G_B))) k = 0;
+    if (k >= nz && (wall & (1 << G_T))) k = nz - 1;
+    return static_cast<double>(phi[phi_index(bd, i, j, k)]);
+  };
+  const int hI = 2 * wJ * wK, hJ = 2 * wI * wK, hK = 2 * wI * wJ;
+  for (int t = threadIdx.x; t < hI + hJ + hK; t += kFlowThreads) {
+    if (t < hI) {
+      const int side = t / (wJ * wK), e = t % (wJ * wK), jl = e % wJ, kk = e / wJ;
+      const int il = side ? wI : -1;
+      sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
+    } else if (t < hI + hJ) {
+      const int x = t - hI, side = x / (wI * wK), e = x % (wI * wK), il = e % wI, kk = e / wI;
+      const int jl = side ? wJ : -1;
+      sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
+    } else {
+      const int x = t - hI - hJ, side = x / (wI * wJ), e = x % (wI * wJ), il = e % wI, jl = e / wI;
+      const int kk = side ? wK : -1;
+      sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
+    }
+  }
+  __syncthreads();
+  const int il = threadIdx.x % kW, jl = threadIdx.x / kW;
+  if (il >= wI || jl >= wJ) return;
+  for (int kk = 0; kk < wK; ++kk) {
+    const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
+    const double (*s)[kL + 2][kW + 2] = sp + kk + 1;
+    u[x] = u[x] - dt * ((s[0][jl + 1][il + 2] - s[0][jl + 1][il]) / c2x);
+    v[x] = v[x] - dt * ((s[0][jl + 2][il + 1] - s[0][jl][il + 1]) / c2y);
+    w[x] = w[x] - dt * ((s[1][jl + 1][il + 1] - s[-1][jl + 1][il + 1]) / c2z);
+    p[x] = p[x] + s[0][jl + 1][il + 1];
+  }
 }
 
 int grid_for(long long n) {
@@ -377,8 +431,8 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
   return allsum_blocks(fl, vals, l1);
 }
 
-// p' = 0 (interior and ghosts), `sweeps` SIP iterations, p' -> Field3 mirror
-// (plan ghosts from the last exchange, Neumann ghosts at walls).
+// p' = 0 (interior and ghosts), then `sweeps` SIP iterations; p' stays in the
+// solver's phi (ghosts from the last exchange) for k_correct_b.
 template <typename T>
 int flow_solve(sip_flow* fl, int sweeps) {
   sip_ctx* ctx = fl->ctx;
@@ -386,17 +440,7 @@ int flow_solve(sip_flow* fl, int sweeps) {
   CK(cudaMemsetAsync(ctx->phi, 0, (size_t)ctx->total_phi_slices * kL * sizeof(T), ctx->stream));
   ctx->n_done = 0;
   CK(cudaMemsetAsync(ctx->d_norm_it, 0, sizeof(unsigned), ctx->stream));
-  CKS(iterate_t<T>(ctx, sweeps));
-  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
-    const BlockDesc& b = ctx->hblocks[lb];
-    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
-    CKS(launch_gather<T>(static_cast<T*>(ctx->phi), ctx->d_blocks, (int)lb, b,
-                         ctx->plan_ghosts[lb].data(), st, ctx->stream));
-    ++ctx->launches;
-  }
-  double* pp[1] = {ctx->phi_stage};
-  const int none[1] = {0};
-  return flow_walls(fl, pp, 1, none);
+  return iterate_t<T>(ctx, sweeps);
 }
 
 }  // namespace
@@ -606,10 +650,15 @@ int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_oute
     for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
       const BlockDesc& b = ctx->hblocks[lb];
       const size_t o = ctx->phi_stage_off[lb];
-      const dim3 grid((unsigned)((b.nx * b.ny + kFlowThreads - 1) / kFlowThreads), (unsigned)b.nz);
-      k_correct<<<grid, kFlowThreads, 0, ctx->stream>>>(
-          b.nx, b.ny, fl->f[0] + o, fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, ctx->phi_stage + o,
-          2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
+      const dim3 grid((unsigned)b.nbricks, (unsigned)((b.nz + kCorKC - 1) / kCorKC));
+      if (ctx->precision == SIP_PREC_SINGLE)
+        k_correct_b<float><<<grid, kFlowThreads, 0, ctx->stream>>>(
+            ctx->d_blocks, (int)lb, fl->wall[lb], static_cast<const float*>(ctx->phi), fl->f[0] + o,
+            fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
+      else
+        k_correct_b<double><<<grid, kFlowThreads, 0, ctx->stream>>>(
+            ctx->d_blocks, (int)lb, fl->wall[lb], static_cast<const double*>(ctx->phi), fl->f[0] + o,
+            fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
       CK(cudaGetLastError());
       ++ctx->launches;
     }
