@@ -125,38 +125,45 @@ __global__ void k_flow_walls(BlockDesc b, int nf, double* f0, double* f1, double
 
 // Co-located central divergence of one block; Q = -(V * div) / dt straight
 // into the source array of the system's brick-slice pack (pinned cell: 0) and
-// the block's L1 partials.  CTA (brick, c) owns the brick's kW x kL columns
-// over planes [kDivKC*c, +kDivKC): phase 1 reads u, v, w (thread = (il, jl))
-// and keeps Q of the chunk in shared memory; phase 2 writes it slice by slice
-// -- a warp writes the kL lanes of one slice, so the pack writes are coalesced.
-// The partial of a CTA sums its cells in a fixed order (per column over k,
+// the block's L1 partials.  CTA (chunk, c) owns kChunkB consecutive bricks of
+// one brick row (up to 32 i x 32 j columns) over planes [kDivKC*c, +kDivKC):
+// phase 1 reads u, v, w with 32 consecutive i per warp (256 B rows) and keeps
+// Q of the chunk in shared memory; phase 2 writes it brick by brick, slice by
+// slice -- a warp writes the kL lanes of one slice (coalesced pack rows).
+// The partial of a CTA sums its cells in a fixed order (per thread over j, k;
 // fixed shuffle tree, warps in order): deterministic.
-constexpr int kDivKC = 8;
+constexpr int kChunkB = 4;  // bricks per CTA along i (caller kernels)
+constexpr int kDivKC = 4;
+__host__ __device__ inline int chunks_i(const BlockDesc& b) { return (b.BX + kChunkB - 1) / kChunkB; }
 template <typename T>
 __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* blocks, int blk,
-                                                             const double* u, const double* v,
-                                                             const double* w, double c2x, double c2y,
+                                                             const double* __restrict__ u,
+                                                             const double* __restrict__ v,
+                                                             const double* __restrict__ w, double c2x, double c2y,
                                                              double c2z, double vol, double dt, int pin,
                                                              T* fw, double* partial) {
-  static_assert(kW * kL == kFlowThreads, "one thread per brick column");
-  __shared__ double sq[kDivKC][kL][kW];
+  static_assert(kChunkB * kW == 32 && kFlowThreads % 32 == 0, "32 i per warp");
+  __shared__ double sq[kDivKC][kL][kChunkB * kW];
   __shared__ double s[kFlowThreads / 32];
   const BlockDesc bd = blocks[blk];
   const int nx = bd.nx, ny = bd.ny, nz = bd.nz;
-  const int r = blockIdx.x, bi = r % bd.BX, bj = r / bd.BX;
-  const int i0 = bi * kW, j0 = bj * kL, k0 = blockIdx.y * kDivKC;
-  const int wI = min(kW, nx - i0), wJ = min(kL, ny - j0), wK = min(kDivKC, nz - k0);
+  const int nci = chunks_i(bd), bq = blockIdx.x % nci, bj = blockIdx.x / nci;
+  const int i0 = bq * kChunkB * kW, j0 = bj * kL, k0 = blockIdx.y * kDivKC;
+  const int wI = min(kChunkB * kW, nx - i0), wJ = min(kL, ny - j0), wK = min(kDivKC, nz - k0);
   const long long sy = nx + 2, sz = (long long)(nx + 2) * (ny + 2);
-  const int il = threadIdx.x % kW, jl = threadIdx.x / kW;
+  constexpr int kRows = kFlowThreads / 32;
+  const int il = threadIdx.x & 31, jq = threadIdx.x >> 5;
   double acc = 0.0;
-  if (il < wI && jl < wJ) {
-    for (int kk = 0; kk < wK; ++kk) {
-      const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
-      const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
-                        (w[x + sz] - w[x - sz]) / c2z;
-      const bool pinned = pin && r == 0 && k0 + kk == 0 && il == 0 && jl == 0;
-      sq[kk][jl][il] = pinned ? 0.0 : -(vol * dv) / dt;
-      acc += fabs(dv) * vol;
+  if (il < wI) {
+    for (int jl = jq; jl < wJ; jl += kRows) {
+      for (int kk = 0; kk < wK; ++kk) {
+        const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
+        const double dv = ((u[x + 1] - u[x - 1]) / c2x + (v[x + sy] - v[x - sy]) / c2y) +
+                          (w[x + sz] - w[x - sz]) / c2z;
+        const bool pinned = pin && i0 + il == 0 && j0 + jl == 0 && k0 + kk == 0;
+        sq[kk][jl][il] = pinned ? 0.0 : -(vol * dv) / dt;
+        acc += fabs(dv) * vol;
+      }
     }
   }
 #pragma unroll
@@ -169,13 +176,18 @@ __global__ void __launch_bounds__(kFlowThreads) k_divergence(const BlockDesc* bl
     partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
   if (!fw) return;
-  // phase 2: warp q writes slices tau = 8 k0 + q, + 8, ...; lane = jl
+  // phase 2: per brick, warp q writes slices tau = 8 k0 + q, + 8, ...; lane = jl
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const long long slot = bd.slot0 + (long long)r * bd.ns;
-  for (int tau = kW * k0 + q; tau < kW * (k0 + wK) + kL - 1; tau += kFlowThreads / 32) {
-    const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
-    if (lane < wJ && c >= 0 && k >= k0 && k < k0 + wK && ci < wI)
-      fw[((slot + tau) * F_NA + F_Q) * kL + lane] = static_cast<T>(sq[k - k0][lane][ci]);
+  for (int bb = 0; bb < kChunkB; ++bb) {
+    const int bi = bq * kChunkB + bb;
+    if (bi >= bd.BX) break;
+    const int wIb = min(kW, nx - bi * kW);
+    const long long slot = bd.slot0 + (long long)(bi + bd.BX * bj) * bd.ns;
+    for (int tau = kW * k0 + q; tau < kW * (k0 + wK) + kL - 1; tau += kRows) {
+      const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
+      if (lane < wJ && c >= 0 && k >= k0 && k < k0 + wK && ci < wIb)
+        fw[((slot + tau) * F_NA + F_Q) * kL + lane] = static_cast<T>(sq[k - k0][lane][bb * kW + ci]);
+    }
   }
 }
 
@@ -199,72 +211,94 @@ __global__ void __launch_bounds__(kFlowThreads) k_sum_partials(const double* par
 
 // u -= dt * dp'/dx (central), v, w likewise; p += p' -- reading p' straight
 // from the solver's phi (brick layout): no gather into a Field3 mirror and no
-// wall kernel for p'.  CTA (brick, c)
-// stages p' of the brick's kW x kL columns over planes [kCorKC*c, +kCorKC)
-// plus a one-cell halo in shared memory -- the brick's own slices as
-// coalesced 32-lane rows, the halo cell by cell: the neighbour brick's cell,
-// the phi ghost (interface / periodic face, exchanged after the last sweep)
-// or, at a wall / symmetry face, the interior cell (Neumann: what
-// k_flow_walls gives the gathered p').  Values and operation order are
-// those of the Field3 formulation (oracle/flow.py), so u, v, w, p are bitwise
-// the oracle's.
-constexpr int kCorKC = 8;
+// wall kernel for p'.  CTA (chunk, c) stages p' of kChunkB bricks of one brick
+// row (up to 32 i x 32 j columns) over kCorKC planes plus a one-cell halo in
+// shared memory: the bricks' own slices incl. the planes below / above as
+// coalesced 32-lane rows, the i / j halo cell by cell -- the neighbour brick's
+// cell, the phi ghost (interface / periodic face, exchanged after the last
+// sweep) or, at a wall / symmetry face, the interior cell (Neumann: what
+// k_flow_walls gives a gathered p').  The update then runs with 32
+// consecutive i per warp.  Values and operation order are those of the
+// Field3 formulation (oracle/flow.py), so u, v, w, p are bitwise the oracle's.
 template <typename T>
-__global__ void __launch_bounds__(kFlowThreads) k_correct_b(const BlockDesc* blocks, int blk, int wall,
-                                                            const T* __restrict__ phi, double* u, double* v,
-                                                            double* w, double* p, double c2x, double c2y,
+struct CorCfg {
+  static constexpr int KC = sizeof(T) == 8 ? 3 : 4;  // planes per CTA (static smem < 48 KB)
+};
+constexpr int kCorThreads = kFlowThreads;
+template <typename T>
+__global__ void __launch_bounds__(kCorThreads) k_correct_b(const BlockDesc* blocks, int blk, int wall,
+                                                            const T* __restrict__ phi, double* __restrict__ u,
+                                                            double* __restrict__ v, double* __restrict__ w,
+                                                            double* __restrict__ p, double c2x, double c2y,
                                                             double c2z, double dt) {
-  static_assert(kW * kL == kFlowThreads, "one thread per brick column");
-  __shared__ double sp[kCorKC + 2][kL + 2][kW + 2];
+  constexpr int KC = CorCfg<T>::KC, CW = kChunkB * kW;
+  __shared__ T sp[KC + 2][kL + 2][CW + 2];
   const BlockDesc bd = blocks[blk];
   const int nx = bd.nx, ny = bd.ny, nz = bd.nz;
-  const int r = blockIdx.x, bi = r % bd.BX, bj = r / bd.BX;
-  const int i0 = bi * kW, j0 = bj * kL, k0 = blockIdx.y * kCorKC;
-  const int wI = min(kW, nx - i0), wJ = min(kL, ny - j0), wK = min(kCorKC, nz - k0);
-  // own slices: warp q loads slices tau = 8 k0 + q, + 8, ...; lane = jl
+  const int nci = chunks_i(bd), bq = blockIdx.x % nci, bj = blockIdx.x / nci;
+  const int i0 = bq * CW, j0 = bj * kL, k0 = blockIdx.y * KC;
+  const int wI = min(CW, nx - i0), wJ = min(kL, ny - j0), wK = min(KC, nz - k0);
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const long long pslot = phi_slot(bd, r);
-  for (int tau = kW * k0 + q; tau < kW * (k0 + wK) + kL - 1; tau += kFlowThreads / 32) {
-    const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
-    if (lane < wJ && c >= 0 && k >= k0 && k < k0 + wK && ci < wI)
-      sp[k - k0 + 1][lane + 1][ci + 1] = static_cast<double>(phi[(pslot + tau) * kL + lane]);
+  constexpr int kRows = kCorThreads / 32;
+  // own slices incl. planes k0 - 1 and k0 + wK (interior, or the B / T ghost
+  // plane in the porch): per brick, warp q loads slices 8 (k0 - 1) + q, + 8, ...
+  for (int bb = 0; bb < kChunkB; ++bb) {
+    const int bi = bq * kChunkB + bb;
+    if (bi >= bd.BX) break;
+    const int wIb = min(kW, nx - bi * kW);
+    const long long pslot = phi_slot(bd, bi + bd.BX * bj);
+    for (int tau = kW * (k0 - 1) + q; tau < kW * (k0 + wK + 1) + kL - 1; tau += kRows) {
+      const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);  // arithmetic shift: k = -1 below 0
+      if (lane < wJ && k >= k0 - 1 && k <= k0 + wK && ci < wIb)
+        sp[k - k0 + 1][lane + 1][bb * kW + ci + 1] = phi[(pslot + tau) * kL + lane];
+    }
   }
-  // halo faces of the chunk (no edges / corners: 7-point stencil)
+  // i / j halo faces of the chunk (no edges / corners: 7-point stencil)
   auto pv = [&](int i, int j, int k) {
     if (i < 0 && (wall & (1 << G_W))) i = 0;
     if (i >= nx && (wall & (1 << G_E))) i = nx - 1;
     if (j < 0 && (wall & (1 << G_S))) j = 0;
     if (j >= ny && (wall & (1 << G_N))) j = ny - 1;
-    if (k < 0 && (wall & (1 << G_B))) k = 0;
-    if (k >= nz && (wall & (1 << G_T))) k = nz - 1;
-    return static_cast<double>(phi[phi_index(bd, i, j, k)]);
+    return phi[phi_index(bd, i, j, k)];
   };
-  const int hI = 2 * wJ * wK, hJ = 2 * wI * wK, hK = 2 * wI * wJ;
-  for (int t = threadIdx.x; t < hI + hJ + hK; t += kFlowThreads) {
+  const int hI = 2 * wJ * wK, hJ = 2 * wI * wK;
+  for (int t = threadIdx.x; t < hI + hJ; t += kCorThreads) {
     if (t < hI) {
       const int side = t / (wJ * wK), e = t % (wJ * wK), jl = e % wJ, kk = e / wJ;
       const int il = side ? wI : -1;
       sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
-    } else if (t < hI + hJ) {
+    } else {
       const int x = t - hI, side = x / (wI * wK), e = x % (wI * wK), il = e % wI, kk = e / wI;
       const int jl = side ? wJ : -1;
-      sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
-    } else {
-      const int x = t - hI - hJ, side = x / (wI * wJ), e = x % (wI * wJ), il = e % wI, jl = e / wI;
-      const int kk = side ? wK : -1;
       sp[kk + 1][jl + 1][il + 1] = pv(i0 + il, j0 + jl, k0 + kk);
     }
   }
   __syncthreads();
-  const int il = threadIdx.x % kW, jl = threadIdx.x / kW;
-  if (il >= wI || jl >= wJ) return;
-  for (int kk = 0; kk < wK; ++kk) {
-    const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
-    const double (*s)[kL + 2][kW + 2] = sp + kk + 1;
-    u[x] = u[x] - dt * ((s[0][jl + 1][il + 2] - s[0][jl + 1][il]) / c2x);
-    v[x] = v[x] - dt * ((s[0][jl + 2][il + 1] - s[0][jl][il + 1]) / c2y);
-    w[x] = w[x] - dt * ((s[1][jl + 1][il + 1] - s[-1][jl + 1][il + 1]) / c2z);
-    p[x] = p[x] + s[0][jl + 1][il + 1];
+  // walls below / above: the ghost plane is the interior plane (Neumann)
+  const bool wb = k0 == 0 && (wall & (1 << G_B)), wt = k0 + wK == nz && (wall & (1 << G_T));
+  if (wb || wt) {
+    for (int t = threadIdx.x; t < wI * wJ; t += kCorThreads) {
+      const int il = t % wI, jl = t / wI;
+      if (wb) sp[0][jl + 1][il + 1] = sp[1][jl + 1][il + 1];
+      if (wt) sp[wK + 1][jl + 1][il + 1] = sp[wK][jl + 1][il + 1];
+    }
+    __syncthreads();
+  }
+  if (lane >= wI) return;
+  const int il = lane;
+  for (int jl = q; jl < wJ; jl += kRows) {
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      if (kk >= wK) break;
+      const long long x = f3(nx, ny, i0 + il + 1, j0 + jl + 1, k0 + kk + 1);
+      const auto& s0 = sp[kk + 1];
+      const double pc = static_cast<double>(s0[jl + 1][il + 1]);
+      u[x] = u[x] - dt * ((static_cast<double>(s0[jl + 1][il + 2]) - static_cast<double>(s0[jl + 1][il])) / c2x);
+      v[x] = v[x] - dt * ((static_cast<double>(s0[jl + 2][il + 1]) - static_cast<double>(s0[jl][il + 1])) / c2y);
+      w[x] = w[x] - dt * ((static_cast<double>(sp[kk + 2][jl + 1][il + 1]) -
+                           static_cast<double>(sp[kk][jl + 1][il + 1])) / c2z);
+      p[x] = p[x] + pc;
+    }
   }
 }
 
@@ -408,7 +442,7 @@ int flow_divergence(sip_flow* fl, double dt, bool write_q, double* l1) {
     const BlockDesc& b = ctx->hblocks[lb];
     const size_t o = ctx->phi_stage_off[lb];
     const long long n = (long long)b.nx * b.ny * b.nz;
-    const dim3 grid((unsigned)b.nbricks, (unsigned)((b.nz + kDivKC - 1) / kDivKC));
+    const dim3 grid((unsigned)(chunks_i(b) * b.BY), (unsigned)((b.nz + kDivKC - 1) / kDivKC));
     const int nch = (int)(grid.x * grid.y);
     (void)n;
     if (ctx->precision == SIP_PREC_SINGLE)
@@ -650,13 +684,14 @@ int sip_pressure_correct(sip_flow* fl, double dt, double threshold, int max_oute
     for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
       const BlockDesc& b = ctx->hblocks[lb];
       const size_t o = ctx->phi_stage_off[lb];
-      const dim3 grid((unsigned)b.nbricks, (unsigned)((b.nz + kCorKC - 1) / kCorKC));
+      const int kc = ctx->precision == SIP_PREC_SINGLE ? CorCfg<float>::KC : CorCfg<double>::KC;
+      const dim3 grid((unsigned)(chunks_i(b) * b.BY), (unsigned)((b.nz + kc - 1) / kc));
       if (ctx->precision == SIP_PREC_SINGLE)
-        k_correct_b<float><<<grid, kFlowThreads, 0, ctx->stream>>>(
+        k_correct_b<float><<<grid, kCorThreads, 0, ctx->stream>>>(
             ctx->d_blocks, (int)lb, fl->wall[lb], static_cast<const float*>(ctx->phi), fl->f[0] + o,
             fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
       else
-        k_correct_b<double><<<grid, kFlowThreads, 0, ctx->stream>>>(
+        k_correct_b<double><<<grid, kCorThreads, 0, ctx->stream>>>(
             ctx->d_blocks, (int)lb, fl->wall[lb], static_cast<const double*>(ctx->phi), fl->f[0] + o,
             fl->f[1] + o, fl->f[2] + o, fl->f[3] + o, 2.0 * hx, 2.0 * hy, 2.0 * hz, dt);
       CK(cudaGetLastError());
