@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(32) k_factor(const FactorParams<T> P) {
 #define SIPB_K2_D32 5
 #endif
 #ifndef SIPB_K3_D
-#define SIPB_K3_D 6
+#define SIPB_K3_D 4  // even: slot q is always served by compute warp q & 1
 #endif
 template <typename T>
 struct K2Cfg {
@@ -827,8 +827,10 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
 // reverse:  delta = ((R - UN*dN) - UE*dE) - UT*dT,  phi += delta.
 // dE: own previous step (or the E brick's W column, tagged), dN: lane + 1's
 // previous step (shfl_down; lane 31: the N brick's S row), dT: own step
-// tau + kW.  Three warps per brick: producer (TMA of R, phi, UN, UE, UT of a
-// stage, D stages ahead; phi stores of a finished stage), compute, mailbox.
+// tau + kW.  Five warps per brick: producer (TMA of R, phi, UN, UE, UT of a
+// stage, D stages ahead), two compute warps taking alternate stages (the
+// chain state handed over through shared memory), mailbox, and drain (phi +=
+// delta of a finished stage -> HBM, the tagged publishes).
 // =============================================================================
 template <typename T>
 struct K3Cfg {
@@ -839,12 +841,16 @@ struct K3Cfg {
   static constexpr size_t slot_bytes = (sizeof(T) * (o_mb + kL + kStage) + 127) / 128 * 128;
   static constexpr size_t off_bar = D * slot_bytes;
   static constexpr size_t off_misc = off_bar + 8 * 4 * D;  // full mbx cdone empty
-  static constexpr size_t bytes = off_misc + 16;
-  static constexpr int kThreads = 96;
+  // chain state handed between the two compute warps: [warp][kW + 1][kL]
+  // (the masked window of the stage, then the last step's delta)
+  static constexpr size_t off_hand = off_misc + 16;
+  static constexpr size_t bytes = off_hand + sizeof(T) * 2 * (kW + 1) * kL;
+  static constexpr int kThreads = 160;  // producer, compute x2, mailbox, drain
+  static_assert(D % 2 == 0, "slot parity selects the compute warp");
 };
 
 template <typename T>
-__global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(160) k_backward(const SweepParams<T> P) {
   using C = K3Cfg<T>;
   constexpr int D = C::D;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -859,9 +865,9 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
   if (threadIdx.x == 0) {
     for (int q = 0; q < D; ++q) {
       mbar_init(full0 + 8 * q, 2);    // producer expect_tx + mailbox warp
-      mbar_init(mbx0 + 8 * q, 1);     // (unused)
-      mbar_init(cdone0 + 8 * q, kL);  // every compute lane
-      mbar_init(empty0 + 8 * q, kL);  // every compute lane
+      mbar_init(mbx0 + 8 * q, kL);    // drained: every drain-warp lane (slot free for the producer)
+      mbar_init(cdone0 + 8 * q, kL);  // every lane of the slot's compute warp
+      mbar_init(empty0 + 8 * q, kL);  // every lane of the slot's compute warp
     }
     fence_mbar_init();
   }
@@ -901,14 +907,37 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
 
     if (warp == 0) {
       // ------------------------------------------------------------ producer
-      T* const P_dst = P.phi + bd.pslot * kL + lane;
-      const int wedge_o = lane & (kW - 1);  // slice offset of this lane's il == 0 step
-      // stage m (slices 8n .. 8n+7, n = NST-1-m) once the compute warp is
+      // TMA copies only: stage m's UN UE UT, R and phi once the slot's inputs
+      // were consumed (empty) and its previous stage was drained
+      int q = (int)(g % D);
+      for (int m = 0; m < NST; ++m, ++g, q = q + 1 == D ? 0 : q + 1) {
+        if (g >= D) {
+          bar_wait(empty0 + 8 * q, ph_b, q, 50);
+          bar_wait(mbx0 + 8 * q, ph_c, q, 51);
+        }
+        if (lane == 0) {
+          const int n = NST - 1 - m;  // stage m covers slices 8n .. 8n + 7
+          const uint32_t full = full0 + 8 * q;
+          const long long sl = bd.slot + (long long)n * kStage;
+          T* const d = slot(q);
+          mbar_expect_tx(full, kBwBytes + 2 * kChBytes);
+          tma_1d(saddr(d), P.bw + sl * B_NA * kL, kBwBytes, full);
+          tma_1d(saddr(d + C::o_R), P.R + sl * kL, kChBytes, full);
+          tma_1d(saddr(d + C::o_ph), P.phi + (bd.pslot + (long long)n * kStage) * kL, kChBytes, full);
+        }
+      }
+    } else if (warp == 4) {
+      // --------------------------------------------------------------- drain
+      // stage m (slices 8n .. 8n+7, n = NST-1-m) once its compute warp is
       // done: phi += delta on the valid cells (padding cells keep their
       // ghost values bit for bit) -> HBM, and the cross-brick publishes: each
       // lane's W-column delta (its il == 0 step) and, lanes 0..7, lane 0's
-      // S-row delta of slice 8n + lane
-      auto drain = [&](int m, int q) {
+      // S-row delta of slice 8n + lane; then the slot is free (drained)
+      T* const P_dst = P.phi + bd.pslot * kL + lane;
+      const int wedge_o = lane & (kW - 1);  // slice offset of this lane's il == 0 step
+      int q = (int)(g % D);
+      g += NST;
+      for (int m = 0; m < NST; ++m, q = q + 1 == D ? 0 : q + 1) {
         bar_wait(cdone0 + 8 * q, ph_c, q, 54);
         const int n = NST - 1 - m;
         const T* dsrc = slot(q) + C::o_pn;  // delta, slice-major
@@ -923,8 +952,7 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
         }
         const T vW = dsrc[wedge_o * kL + lane];
         const T vS = dsrc[(lane & (kStage - 1)) * kL];
-#pragma unroll
-        for (int o = 0; o < kStage; ++o) P_dst[((long long)n * kStage + o) * kL] = v[o];
+        // the neighbours' values first (on the wavefront's critical path)
         const int cW = n * kStage + wedge_o - lane;
         const bool pw = bd.mWe >= 0 && lane_ok && (unsigned)cW < (unsigned)nzW && ((cW & (kW - 1)) < bd.wI);
         put_tagged_if(pw, P.mA + (bd.medge + (long long)(pw ? cW >> 3 : 0) * kL + lane) * kTagWords<T>, vW, tag);
@@ -933,40 +961,29 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
                         ((cS & (kW - 1)) < bd.wI);
         put_tagged_if(ps, P.mB + (bd.mrow + (ps ? cS : 0)) * kTagWords<T>, vS, tag);
         hmark(m, 4);
-      };
-      int q = (int)(g % D);
-      for (int m = 0; m < NST; ++m, ++g, q = q + 1 == D ? 0 : q + 1) {
-        if (g >= D) {
-          if (m >= D) drain(m - D, q);
-          bar_wait(empty0 + 8 * q, ph_b, q, 50);
-        }
-        if (lane == 0) {
-          const int n = NST - 1 - m;  // stage m covers slices 8n .. 8n + 7
-          const uint32_t full = full0 + 8 * q;
-          const long long sl = bd.slot + (long long)n * kStage;
-          T* const d = slot(q);
-          mbar_expect_tx(full, kBwBytes + 2 * kChBytes);
-          tma_1d(saddr(d), P.bw + sl * B_NA * kL, kBwBytes, full);
-          tma_1d(saddr(d + C::o_R), P.R + sl * kL, kChBytes, full);
-          tma_1d(saddr(d + C::o_ph), P.phi + (bd.pslot + (long long)n * kStage) * kL, kChBytes, full);
-        }
-      }
-      for (int m = NST > D ? NST - D : 0; m < NST; ++m) drain(m, (int)((g - NST + m) % D));
-    } else if (warp == 1) {
-      // ------------------------------------------------------------- compute
-      // One stage per iteration: wait for the slot (TMA data + the mailbox
-      // warp's values), inputs -> registers, release the slot, the 8-step
-      // chain, delta -> slot.  Every lane arrives on empty / cdone (count 32):
-      // each lane's release orders its own shared accesses, no warp barrier.
-      trace_begin(P.trace, bid);
-      constexpr uint32_t E = sizeof(T);
-      T dprev = T(0);
-      T win[kW];
+        mbar_arrive(mbx0 + 8 * q);  // slot read out: the producer may refill it
 #pragma unroll
-      for (int s = 0; s < kW; ++s) win[s] = T(0);
-      int q = (int)(g % D);
+        for (int o = 0; o < kStage; ++o) P_dst[((long long)n * kStage + o) * kL] = v[o];
+      }
+    } else if (warp == 1 || warp == 3) {
+      // ------------------------------------------------------------- compute
+      // Two compute warps take alternate stages (slot parity): while one runs
+      // its stage's 8-step chain, the other loads the next stage's inputs and
+      // stores its deltas, so only the chain and the hand-over of its state
+      // (the masked window + the last delta, 9 values per lane, through
+      // shared memory and a named barrier) are serial.  Per stage: wait for
+      // the slot (TMA data + the mailbox warp's values), inputs -> registers,
+      // release the slot, the chain, delta -> slot.  Every lane arrives on
+      // empty / cdone (count 32).
+      const int cw = warp == 1 ? 0 : 1;
+      constexpr uint32_t E = sizeof(T);
+      T* const hand = reinterpret_cast<T*>(smem + C::off_hand);
+      const int q0 = (int)(g % D), qlast = (int)((g + NST - 1) % D);
+      if (cw == (q0 & 1)) trace_begin(P.trace, bid);
+      int q = q0;
       g += NST;
       for (int m = 0; m < NST; ++m, q = q + 1 == D ? 0 : q + 1) {
+        if ((q & 1) != cw) continue;
         const int n = NST - 1 - m;
         bar_wait(full0 + 8 * q, ph_a, q, 33);
         hmark(m, 2);
@@ -983,6 +1000,23 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
           eN[s] = lds<T>(sq + E * (C::o_mb + kL + s));
         }
         mbar_arrive(empty0 + 8 * q);  // slot inputs now in registers
+        // chain state: zero at the brick's first stage, else from the other warp
+        T dprev = T(0);
+        T win[kW];
+        if (m == 0) {
+#pragma unroll
+          for (int s = 0; s < kW; ++s) win[s] = T(0);
+        } else {
+          // named barrier 1 + cw: the other warp's bar.arrive + this warp's
+          // bar.sync (64 threads, membar.cta semantics); the hand-overs
+          // strictly alternate, so a barrier is never over-arrived (an
+          // mbarrier hand-over measured ~6 % slower, a polled flag ~4 %)
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + cw) : "memory");
+          const T* h = hand + cw * (kW + 1) * kL + lane;
+#pragma unroll
+          for (int s = 0; s < kW; ++s) win[s] = h[s * kL];
+          dprev = h[kW * kL];
+        }
         // delta = ((R - UN*dN) - UE*dE) - UT*dT, dT = the
         // previous stage's step s (win); padding cells compute exact zeros
         // (zero-filled packs), stored copies masked below
@@ -996,8 +1030,7 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
           win[s] = d;
           dprev = d;
         }
-        // delta into the slot (the producer applies it to phi and publishes);
-        // the masked copy is also the register window
+        // the masked copy is the next stage's window and the slot's delta
         const bool interior = bd.wI == kW && bd.wJ == kL && n >= kL / kStage && n + kL / kStage < NST;
         if (!interior) {
 #pragma unroll
@@ -1007,17 +1040,26 @@ __global__ void __launch_bounds__(96) k_backward(const SweepParams<T> P) {
             win[s] = v ? win[s] : T(0);
           }
         }
+        if (m + 1 < NST) {  // hand the chain state to the other warp first
+          T* h = hand + (cw ^ 1) * (kW + 1) * kL + lane;
+#pragma unroll
+          for (int s = 0; s < kW; ++s) h[s * kL] = win[s];
+          h[kW * kL] = dprev;
+          asm volatile("bar.arrive %0, 64;" ::"r"(1 + (cw ^ 1)) : "memory");
+        }
 #pragma unroll
         for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_pn + (kStage - 1 - s) * kL), win[s]);
         mbar_arrive(cdone0 + 8 * q);
         hmark(m, 3);
       }
-      trace_end(P.trace, bid);
-      if (brick_done(P.state, P.nbricks) && lane == 0) {
-        P.state_other[0] = 0u;
-        P.state_other[1] = 0u;
-        *P.epoch = tag + 1;
-        P.ctl[1] = 0u;
+      if (cw == (qlast & 1)) {  // the warp that ran the brick's last stage closes it
+        trace_end(P.trace, bid);
+        if (brick_done(P.state, P.nbricks) && lane == 0) {
+          P.state_other[0] = 0u;
+          P.state_other[1] = 0u;
+          *P.epoch = tag + 1;
+          P.ctl[1] = 0u;
+        }
       }
     } else {
       // ------------------------------------------------------------- mailbox
