@@ -370,18 +370,19 @@ __global__ void __launch_bounds__(32) k_factor(const FactorParams<T> P) {
 }
 
 // =============================================================================
-// K2: residual + L1 norm + forward substitution.  One CTA of four warps per
+// K2: residual + L1 norm + forward substitution.  One CTA of five warps per
 // brick, warp-specialised around a ring of D stage slots (mbarriers):
 //   warp 0 "producer":   TMA bulk copies of the stage's forward pack slices and
 //                        the next phi chunk, cp.async of the stage's W / E / S
 //                        / N neighbour phi values        -> full[q]
-//                        and the R stores of a finished stage (smem -> HBM)
 //   warp 1 "residual":   r = -(AE*phiE) - AW*phiW - AN*phiN - AS*phiS - AT*phiT
 //                        - AB*phiB + Q - AP*phiP, |r|    -> ready[q], empty[q]
-//   warp 2 "recurrence": t1 = r - LB*R_B, R = ((t1 - LW*R_W) - LS*R_S) * LP,
-//                        mailbox publishes               -> rdone[q], empty[q]
+//   warp 2 "recurrence": t1 = r - LB*R_B, R = ((t1 - LW*R_W) - LS*R_S) * LP
+//                                                        -> rdone[q], empty[q]
 //   warp 3 "mailbox":    polls the W brick's E column / S brick's N row
-//                        (tagged words) for the stage    -> mbx[q]
+//                        (tagged words) for the stage    -> ready[q]
+//   warp 4 "drain":      the E column / N row publishes and the R stores of a
+//                        finished stage (smem -> HBM)    -> drained[q]
 // The recurrence warp's per-step critical path is one shfl plus three
 // dependent fp operations; everything else runs in the other warps.  phi
 // chunks live in a mirrored ring (slices 8n-8 .. 8n+15 of stage n are
@@ -411,7 +412,7 @@ struct K2Cfg {
   static constexpr size_t off_bar = off_ph + sizeof(T) * (QP + 2) * kCh;
   static constexpr size_t off_misc = off_bar + 8 * 5 * D;  // full ready mbx rdone empty
   static constexpr size_t bytes = off_misc + 16;
-  static constexpr int kThreads = 128;
+  static constexpr int kThreads = 160;  // producer, residual, recurrence, mailbox, drain
 };
 
 // phase parity bit of slot q for one barrier kind, flipped after each wait
@@ -450,7 +451,7 @@ __device__ __forceinline__ T settle(Tagged<T> v, bool need, const unsigned long 
 constexpr int kLook = 1;
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(160) k_forward(const SweepParams<T> P) {
   using C = K2Cfg<T>;
   constexpr int D = C::D, QP = C::QP;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
     for (int q = 0; q < D; ++q) {
       mbar_init(full0 + 8 * q, 33);  // producer lane 0 expect_tx + 32 cp.async arrivals
       mbar_init(ready0 + 8 * q, 2);  // residual warp (r) + mailbox warp (cross-brick R)
-      mbar_init(mbx0 + 8 * q, 1);    // (unused)
+      mbar_init(mbx0 + 8 * q, kL);   // drained: every drain-warp lane (slot free for the producer)
       mbar_init(rdone0 + 8 * q, kL);      // recurrence warp, every lane: R of the stage in the slot
       mbar_init(empty0 + 8 * q, 1 + kL);  // residual (lane 0) + recurrence (every lane): inputs consumed
     }
@@ -513,7 +514,6 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
       const T* const phE_src = P.phi + (bd.pE - (kW - 1)) * kL + lane;
       const T* const phX_src = lane < kStage ? P.phi + (bd.pS + kL - 1 + lane) * kL + (kL - 1)
                                              : P.phi + (bd.pN - (kL - 1) + lane - kStage) * kL;
-      T* const R_dst = P.R + bd.slot * kL + lane;
       auto put_chunk = [&](int c, uint32_t bar) {
         const int r = pmod(c, QP);
         const T* src = ph_src + (long long)c * C::kCh;
@@ -522,32 +522,11 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
         if (r == 0) tma_1d(saddr(s_ph + (QP + 1) * C::kCh), src, kChBytes, bar);
       };
       auto chunk_copies = [&](int c) { const int r = pmod(c, QP); return 1 + (r == QP - 1) + (r == 0); };
-      // R of stage n (slot q) -> HBM once the recurrence warp is done with it,
-      // and the cross-brick publishes: each lane's E-column value (its
-      // il == kW-1 step) and, lanes 0..7, lane 31's N-row value of step lane
-      auto drain = [&](int n, int q) {
-        bar_wait(rdone0 + 8 * q, ph_c, q, 44);
-        const T* src = slot(q) + C::o_R;
-        T v[kStage];
-#pragma unroll
-        for (int s = 0; s < kStage; ++s) v[s] = src[s * kL + lane];
-        const T vE = src[eedge_s * kL + lane];
-        const T vN = src[(lane & (kStage - 1)) * kL + (kL - 1)];
-#pragma unroll
-        for (int s = 0; s < kStage; ++s) R_dst[((long long)n * kStage + s) * kL] = v[s];
-        const int cE = n * kStage + eedge_s - lane;
-        const bool pe = bd.mEe >= 0 && lane_ok && (unsigned)cE < (unsigned)nzW && ((cE & (kW - 1)) < bd.wI);
-        put_tagged_if(pe, P.mA + (bd.medge + (long long)(pe ? cE >> 3 : 0) * kL + lane) * kTagWords<T>, vE, tag);
-        const int cN = n * kStage + lane - (kL - 1);
-        const bool pn = bd.mNr >= 0 && lane < kStage && bd.wJ == kL && (unsigned)cN < (unsigned)nzW &&
-                        ((cN & (kW - 1)) < bd.wI);
-        put_tagged_if(pn, P.mB + (bd.mrow + (pn ? cN : 0)) * kTagWords<T>, vN, tag);
-      };
       int q = (int)(g % D);
       for (int n = 0; n < NST; ++n, ++g, q = q + 1 == D ? 0 : q + 1) {
         if (g >= D) {
-          if (n >= D) drain(n - D, q);
           bar_wait(empty0 + 8 * q, ph_b, q, 40);
+          bar_wait(mbx0 + 8 * q, ph_c, q, 45);  // the slot's previous stage drained
         }
         const uint32_t full = full0 + 8 * q;
         T* const ed = slot(q) + C::o_ed;
@@ -569,7 +548,6 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
         cp_async_arrive(full);
         pm(n, 0);
       }
-      for (int n = NST > D ? NST - D : 0; n < NST; ++n) drain(n, (int)((g - NST + n) % D));
     } else if (warp == 1) {
       // ------------------------------------------------------------ residual
       double nrm = 0.0;
@@ -734,6 +712,35 @@ __global__ void __launch_bounds__(128) k_forward(const SweepParams<T> P) {
             if (n0 == 0.0 || tot / n0 <= P.target) P.ctl[0] = 1u;
           }
         }
+      }
+    } else if (warp == 4) {
+      // --------------------------------------------------------------- drain
+      // R of stage n (slot q) -> HBM once the recurrence warp is done with it,
+      // and the cross-brick publishes: each lane's E-column value (its
+      // il == kW-1 step) and, lanes 0..7, lane 31's N-row value of step lane;
+      // then the slot is free for the producer (drained)
+      T* const R_dst = P.R + bd.slot * kL + lane;
+      int q = (int)(g % D);
+      g += NST;
+      for (int n = 0; n < NST; ++n, q = q + 1 == D ? 0 : q + 1) {
+        bar_wait(rdone0 + 8 * q, ph_c, q, 44);
+        const T* src = slot(q) + C::o_R;
+        T v[kStage];
+#pragma unroll
+        for (int s = 0; s < kStage; ++s) v[s] = src[s * kL + lane];
+        const T vE = src[eedge_s * kL + lane];
+        const T vN = src[(lane & (kStage - 1)) * kL + (kL - 1)];
+        // the neighbours' values first (on the wavefront's critical path)
+        const int cE = n * kStage + eedge_s - lane;
+        const bool pe = bd.mEe >= 0 && lane_ok && (unsigned)cE < (unsigned)nzW && ((cE & (kW - 1)) < bd.wI);
+        put_tagged_if(pe, P.mA + (bd.medge + (long long)(pe ? cE >> 3 : 0) * kL + lane) * kTagWords<T>, vE, tag);
+        const int cN = n * kStage + lane - (kL - 1);
+        const bool pn = bd.mNr >= 0 && lane < kStage && bd.wJ == kL && (unsigned)cN < (unsigned)nzW &&
+                        ((cN & (kW - 1)) < bd.wI);
+        put_tagged_if(pn, P.mB + (bd.mrow + (pn ? cN : 0)) * kTagWords<T>, vN, tag);
+        mbar_arrive(mbx0 + 8 * q);  // slot read out: the producer may refill it
+#pragma unroll
+        for (int s = 0; s < kStage; ++s) R_dst[((long long)n * kStage + s) * kL] = v[s];
       }
     } else {
       // ------------------------------------------------------------- mailbox
