@@ -53,6 +53,119 @@ int sipb::set_device(sip_ctx* ctx) {
 }
 
 // -------------------------------------------------------------- construction
+// Source plane E / N / T (K3 finishes it first) <=> ghost W / S / B written.
+static bool early_src(int kf) { return kf == G_E || kf == G_N || kf == G_T; }
+static bool early_dst(int kf) { return kf == G_W || kf == G_S || kf == G_B; }
+
+// The SIP exchange lists of the installed plan (sip_ctx::d_x / d_ux): local
+// copies and packs, early entries first; unpacks, early first.  Each peer's
+// message is [early | late] in plan order on both sides (a sender's E / N / T
+// plane lands in the receiver's W / S / B ghost), so phase 1 sends the first
+// s1 elements and phase 2 the rest, and the unsplit exchange sends it whole.
+static int install_exchange(sip_ctx* ctx) {
+  const size_t es = ctx->esize;
+  std::vector<FaceCopy> x[2], ux[2];  // [early, late]
+  int mp = 0;
+  for (const FaceCopy& f : ctx->local_copies) {
+    x[early_src(f.src_face) ? 0 : 1].push_back(f);
+    mp = std::max(mp, f.n0 * f.n1);
+  }
+  long long so = 0, ro = 0;
+  for (Peer& p : ctx->peers) {
+    p.soff = so;
+    p.roff = ro;
+    p.s1 = p.r1 = 0;
+    for (const FaceCopy& f : p.pack)
+      if (early_src(f.src_face)) p.s1 += (long long)f.n0 * f.n1;
+    for (const FaceCopy& f : p.unpack)
+      if (early_dst(f.dst_face)) p.r1 += (long long)f.n0 * f.n1;
+    long long se = so, sl = so + p.s1, re = ro, rl = ro + p.r1;
+    for (FaceCopy f : p.pack) {
+      long long& o = early_src(f.src_face) ? se : sl;
+      f.buf = o;
+      o += (long long)f.n0 * f.n1;
+      x[early_src(f.src_face) ? 0 : 1].push_back(f);
+    }
+    for (FaceCopy f : p.unpack) {
+      long long& o = early_dst(f.dst_face) ? re : rl;
+      f.buf = o;
+      o += (long long)f.n0 * f.n1;
+      ux[early_dst(f.dst_face) ? 0 : 1].push_back(f);
+    }
+    mp = std::max(mp, p.max_plane);
+    so += p.count;
+    ro += p.count;
+  }
+  // phase 1 work items: each early copy's source plane split by brick, in the
+  // order K3 finishes them -- the brick's position in K3's ticket order for
+  // a T plane (its top slices are done a few stages after it starts), one
+  // resident wave later for an E / N plane (the whole brick)
+  std::vector<int> pos(ctx->hbricks.size(), 0);
+  for (size_t t = 0; t < ctx->order_b.size(); ++t) pos[ctx->order_b[t]] = (int)t;
+  std::vector<std::pair<long long, XItem>> items;
+  for (int e = 0; e < (int)x[0].size(); ++e) {
+    const FaceCopy& f = x[0][e];
+    const BlockDesc& b = ctx->hblocks[f.src_block];
+    for (int bj = 0; bj < b.BY; ++bj)
+      for (int bi = 0; bi < b.BX; ++bi) {
+        XItem it{e, b.brick0 + bi + b.BX * bj, 1, 0, 0, 0, 0};
+        const int i0 = bi * kW, i1 = std::min(b.nx, i0 + kW), j0 = bj * kL, j1 = std::min(b.ny, j0 + kL);
+        if (f.src_face == G_E) {
+          if (bi != b.BX - 1) continue;
+          it.x0b = j0, it.x0e = j1, it.x1b = 0, it.x1e = b.nz;
+        } else if (f.src_face == G_N) {
+          if (bj != b.BY - 1) continue;
+          it.x0b = i0, it.x0e = i1, it.x1b = 0, it.x1e = b.nz;
+        } else {  // G_T
+          it.sel = 0;
+          it.x0b = i0, it.x0e = i1, it.x1b = j0, it.x1e = j1;
+        }
+        items.emplace_back(pos[it.brick] + (it.sel ? (long long)ctx->grid_b : 0), it);
+      }
+  }
+  std::stable_sort(items.begin(), items.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<XItem> hitems;
+  for (auto& pr : items) hitems.push_back(pr.second);
+  ctx->n_xitems = (int)hitems.size();
+  if (!hitems.empty()) {
+    CKS(dalloc(ctx, &ctx->d_xitems, sizeof(XItem) * hitems.size()));
+    CK(cudaMemcpy(ctx->d_xitems, hitems.data(), sizeof(XItem) * hitems.size(), cudaMemcpyHostToDevice));
+  }
+  ctx->x_early = (int)x[0].size();
+  ctx->x_late = (int)x[1].size();
+  ctx->ux_early = (int)ux[0].size();
+  ctx->ux_late = (int)ux[1].size();
+  ctx->x_max_plane = mp;
+  x[0].insert(x[0].end(), x[1].begin(), x[1].end());
+  ux[0].insert(ux[0].end(), ux[1].begin(), ux[1].end());
+  if (!x[0].empty()) {
+    CKS(dalloc(ctx, &ctx->d_x, sizeof(FaceCopy) * x[0].size()));
+    CK(cudaMemcpy(ctx->d_x, x[0].data(), sizeof(FaceCopy) * x[0].size(), cudaMemcpyHostToDevice));
+  }
+  if (!ux[0].empty()) {
+    CKS(dalloc(ctx, &ctx->d_ux, sizeof(FaceCopy) * ux[0].size()));
+    CK(cudaMemcpy(ctx->d_ux, ux[0].data(), sizeof(FaceCopy) * ux[0].size(), cudaMemcpyHostToDevice));
+  }
+  if (!ctx->peers.empty()) {
+    CKS(dalloc(ctx, &ctx->x_sbuf, (size_t)std::max(1LL, so) * es));
+    CKS(dalloc(ctx, &ctx->x_rbuf, (size_t)std::max(1LL, ro) * es));
+    for (Peer& p : ctx->peers) {
+      p.sbuf = static_cast<char*>(ctx->x_sbuf) + p.soff * es;
+      p.rbuf = static_cast<char*>(ctx->x_rbuf) + p.roff * es;
+    }
+  }
+  if (!ctx->xstream) {  // comm stream of the split exchange (highest priority)
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&ctx->xstream, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&ctx->ev_k2, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_k3, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
+  }
+  return SIP_OK;
+}
+
 // Exchange structures of a face-halo plan (this rank's entries, plan order):
 // local entries -> device face copies, send / recv entries -> per-peer NCCL
 // pack / unpack lists.  Replaces a previously installed plan.
@@ -66,10 +179,14 @@ int sipb::install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
   for (Peer& p : ctx->peers) {
     if (p.d_pack) cudaFree(p.d_pack);
     if (p.d_unpack) cudaFree(p.d_unpack);
-    if (p.sbuf) cudaFree(p.sbuf);
-    if (p.rbuf) cudaFree(p.rbuf);
   }
   ctx->peers.clear();
+  for (void* q : {(void*)ctx->d_x, (void*)ctx->d_ux, ctx->x_sbuf, ctx->x_rbuf, (void*)ctx->d_xitems})
+    if (q) cudaFree(q);
+  ctx->d_x = ctx->d_ux = nullptr;
+  ctx->d_xitems = nullptr;
+  ctx->n_xitems = 0;
+  ctx->x_sbuf = ctx->x_rbuf = nullptr;
   ctx->plan_ghosts.assign(ctx->local.size(), {-1, -1, -1, -1, -1, -1});
   // bsfv face id (E,W,N,S,T,B) -> kernel face (W,E,S,N,B,T)
   auto kface = [](int f) { static const int m[6] = {G_E, G_W, G_N, G_S, G_T, G_B}; return m[f]; };
@@ -182,10 +299,8 @@ int sipb::install_plan(sip_ctx* ctx, const std::vector<HaloEntry>& plan) {
     if (!p.unpack.empty())
       CK(cudaMemcpy(p.d_unpack, p.unpack.data(), sizeof(FaceCopy) * p.unpack.size(),
                     cudaMemcpyHostToDevice));
-    CKS(dalloc(ctx, &p.sbuf, (size_t)std::max(1LL, p.count) * es));
-    CKS(dalloc(ctx, &p.rbuf, (size_t)std::max(1LL, p.count) * es));
   }
-  return SIP_OK;
+  return install_exchange(ctx);
 }
 
 static int build(sip_ctx* ctx) {
@@ -303,6 +418,9 @@ static int build(sip_ctx* ctx) {
   CKS(dalloc(ctx, &ctx->epochs, 4 * sizeof(unsigned)));
   CKS(dalloc(ctx, &ctx->d_norm_it, sizeof(unsigned)));
   CKS(dalloc(ctx, &ctx->d_ctl, 4 * sizeof(unsigned)));
+  CKS(dalloc(ctx, &ctx->d_xflag, 2 * sizeof(unsigned) * std::max(1, nt)));
+  CKS(dalloc(ctx, &ctx->d_xseq, sizeof(unsigned)));
+  if (const char* xs = getenv("SIPB_XSPLIT")) ctx->xsplit = atoi(xs) != 0;
   // CUDA-graph replay of sip_iterate is opt-in (SIPB_GRAPH=1): the two
   // launches per iteration are already enqueued back to back
   if (const char* gr = getenv("SIPB_GRAPH")) ctx->use_graphs = atoi(gr) != 0;
@@ -446,6 +564,11 @@ static int ensure_norm_cap(sip_ctx* ctx, int need) {
   return SIP_OK;
 }
 
+// split exchange in use: enabled, and some transfer's source is final before K3 ends
+static bool use_xsplit(const sip_ctx* ctx) {
+  return ctx->xsplit && (ctx->x_early > 0 || ctx->ux_early > 0);
+}
+
 template <typename T>
 static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward) {
   SweepParams<T> p{};
@@ -470,6 +593,10 @@ static SweepParams<T> sweep_params(sip_ctx* ctx, bool forward) {
   p.norm_it = ctx->d_norm_it;
   p.target = ctx->solve_target;
   p.ctl = ctx->d_ctl;
+  if (use_xsplit(ctx)) {  // K2 bumps the stamp value, K3 stamps
+    p.xseq = ctx->d_xseq;
+    p.xflag = forward ? nullptr : ctx->d_xflag;
+  }
   p.trace = ctx->trace ? ctx->trace + (forward ? 0 : 4 * ctx->hbricks.size()) : nullptr;
   p.trace_brick = ctx->trace_brick;
   return p;
@@ -488,39 +615,98 @@ static void ev_end(sip_ctx* ctx) {
   cudaEventRecord(std::get<2>(ctx->events.back()), ctx->stream);
 }
 
+// NCCL phase of the exchange: per peer, elements [b, e) of the message
+// (0 / s1 / count); all receives and sends posted in one group, matched per
+// peer in issue order (non-blocking exchange)
+template <typename T>
+static int nccl_phase(sip_ctx* ctx, int phase, cudaStream_t st) {
+  const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+  const size_t es = sizeof(T);
+  CKN(nccl().GroupStart());
+  for (Peer& p : ctx->peers) {
+    const long long rb = phase == 2 ? p.r1 : 0, re = phase == 1 ? p.r1 : p.count;
+    const long long sb = phase == 2 ? p.s1 : 0, se = phase == 1 ? p.s1 : p.count;
+    if (re > rb)
+      CKN(nccl().Recv(static_cast<char*>(p.rbuf) + rb * es, (size_t)(re - rb), dt, p.rank, ctx->comm, st));
+    if (se > sb)
+      CKN(nccl().Send(static_cast<char*>(p.sbuf) + sb * es, (size_t)(se - sb), dt, p.rank, ctx->comm, st));
+  }
+  CKN(nccl().GroupEnd());
+  return SIP_OK;
+}
+
+// The whole exchange on ctx->stream: local copies + packs, NCCL (phase 0 =
+// whole messages), unpacks.
 template <typename T>
 int sipb::exchange(sip_ctx* ctx) {
-  if (ctx->local_copies.empty() && ctx->peers.empty()) return SIP_OK;
+  const int nx = ctx->x_early + ctx->x_late, nux = ctx->ux_early + ctx->ux_late;
+  if (nx == 0 && nux == 0) return SIP_OK;
   cudaEvent_t e;
   ev_begin(ctx, 2, &e);
   T* phi = static_cast<T*>(ctx->phi);
-  if (!ctx->local_copies.empty()) {
-    CKS(launch_face_copies<T>(ctx->d_local_copies, (int)ctx->local_copies.size(),
-                              ctx->local_max_plane, ctx->d_blocks, phi, nullptr, nullptr,
-                              ctx->stream));
+  if (nx) {
+    CKS(launch_face_copies<T>(ctx->d_x, nx, ctx->x_max_plane, ctx->d_blocks, phi, nullptr,
+                              static_cast<T*>(ctx->x_sbuf), ctx->stream));
     ++ctx->launches;
   }
   if (!ctx->peers.empty()) {
-    for (Peer& p : ctx->peers) {
-      CKS(launch_face_copies<T>(p.d_pack, (int)p.pack.size(), p.max_plane, ctx->d_blocks, phi,
-                                nullptr, static_cast<T*>(p.sbuf), ctx->stream));
-      ++ctx->launches;
-    }
-    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-    // non-blocking exchange: all receives and sends posted
-    // in one group; NCCL matches per peer in issue order
-    CKN(nccl().GroupStart());
-    for (Peer& p : ctx->peers) {
-      CKN(nccl().Recv(p.rbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
-      CKN(nccl().Send(p.sbuf, (size_t)p.count, dt, p.rank, ctx->comm, ctx->stream));
-    }
-    CKN(nccl().GroupEnd());
-    for (Peer& p : ctx->peers) {
-      CKS(launch_face_copies<T>(p.d_unpack, (int)p.unpack.size(), p.max_plane, ctx->d_blocks, phi,
-                                static_cast<T*>(p.rbuf), nullptr, ctx->stream));
+    CKS(nccl_phase<T>(ctx, 0, ctx->stream));
+    if (nux) {
+      CKS(launch_face_copies<T>(ctx->d_ux, nux, ctx->x_max_plane, ctx->d_blocks, phi,
+                                static_cast<T*>(ctx->x_rbuf), nullptr, ctx->stream));
       ++ctx->launches;
     }
   }
+  ev_end(ctx);
+  return SIP_OK;
+}
+
+// The exchange split around K3, enqueued right after K3 on
+// ctx->stream (ev_k2 recorded between K2 and K3).  Comm stream: from the end
+// of K2, the early copies / packs (waiting on K3's per-brick stamps), NCCL
+// phase 1, early unpacks -- all while K3 runs; then, after K3, the late
+// copies / packs, NCCL phase 2, late unpacks.  ctx->stream waits for it
+// before the next K2.  The profiled halo time (kind 2) is the exposed part:
+// from the end of K3 to the end of the exchange.
+template <typename T>
+static int exchange_split(sip_ctx* ctx) {
+  cudaEvent_t e;
+  ev_begin(ctx, 2, &e);
+  T* phi = static_cast<T*>(ctx->phi);
+  const cudaStream_t xs = ctx->xstream;
+  T* sbuf = static_cast<T*>(ctx->x_sbuf);
+  T* rbuf = static_cast<T*>(ctx->x_rbuf);
+  CK(cudaStreamWaitEvent(xs, ctx->ev_k2, 0));
+  if (ctx->x_early) {
+    CKS(launch_face_copies_after<T>(ctx->d_x, ctx->d_xitems, ctx->n_xitems, ctx->d_blocks, phi, sbuf,
+                                    ctx->d_xflag, ctx->d_xseq, xs));
+    ++ctx->launches;
+  }
+  if (!ctx->peers.empty()) {
+    CKS(nccl_phase<T>(ctx, 1, xs));
+    if (ctx->ux_early) {
+      CKS(launch_face_copies<T>(ctx->d_ux, ctx->ux_early, ctx->x_max_plane, ctx->d_blocks, phi, rbuf,
+                                nullptr, xs));
+      ++ctx->launches;
+    }
+  }
+  CK(cudaEventRecord(ctx->ev_k3, ctx->stream));
+  CK(cudaStreamWaitEvent(xs, ctx->ev_k3, 0));
+  if (ctx->x_late) {
+    CKS(launch_face_copies<T>(ctx->d_x + ctx->x_early, ctx->x_late, ctx->x_max_plane, ctx->d_blocks, phi,
+                              nullptr, sbuf, xs));
+    ++ctx->launches;
+  }
+  if (!ctx->peers.empty()) {
+    CKS(nccl_phase<T>(ctx, 2, xs));
+    if (ctx->ux_late) {
+      CKS(launch_face_copies<T>(ctx->d_ux + ctx->ux_early, ctx->ux_late, ctx->x_max_plane, ctx->d_blocks,
+                                phi, rbuf, nullptr, xs));
+      ++ctx->launches;
+    }
+  }
+  CK(cudaEventRecord(ctx->ev_x, xs));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_x, 0));
   ev_end(ctx);
   return SIP_OK;
 }
@@ -542,11 +728,14 @@ static int launch_iterations_impl(sip_ctx* ctx, int iters) {
     CKS(launch_forward<T>(sweep_params<T>(ctx, true), ctx->grid_f, ctx->stream));
     ++ctx->launches;
     ev_end(ctx);
+    const bool split = use_xsplit(ctx);
+    if (split) CK(cudaEventRecord(ctx->ev_k2, ctx->stream));
     ev_begin(ctx, 1, &e);
     CKS(launch_backward<T>(sweep_params<T>(ctx, false), ctx->grid_b, ctx->stream));
     ++ctx->launches;
     ev_end(ctx);
-    CKS(exchange<T>(ctx));
+    if (split) CKS(exchange_split<T>(ctx));
+    else CKS(exchange<T>(ctx));
   }
   return SIP_OK;
 }
@@ -723,8 +912,16 @@ int sip_destroy(sip_ctx* ctx) {
   for (Peer& p : ctx->peers) {
     if (p.d_pack) cudaFree(p.d_pack);
     if (p.d_unpack) cudaFree(p.d_unpack);
-    if (p.sbuf) cudaFree(p.sbuf);
-    if (p.rbuf) cudaFree(p.rbuf);
+  }
+  for (void* q : {(void*)ctx->d_x, (void*)ctx->d_ux, ctx->x_sbuf, ctx->x_rbuf, (void*)ctx->d_xflag,
+                  (void*)ctx->d_xseq, (void*)ctx->d_xitems})
+    if (q) cudaFree(q);
+  if (ctx->xstream) {
+    cudaStreamSynchronize(ctx->xstream);
+    cudaStreamDestroy(ctx->xstream);
+    cudaEventDestroy(ctx->ev_k2);
+    cudaEventDestroy(ctx->ev_k3);
+    cudaEventDestroy(ctx->ev_x);
   }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

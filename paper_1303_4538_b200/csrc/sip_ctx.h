@@ -40,9 +40,12 @@ struct Peer {
   long long count = 0;                 // elements each way
   FaceCopy* d_pack = nullptr;
   FaceCopy* d_unpack = nullptr;
-  void* sbuf = nullptr;
+  void* sbuf = nullptr;  // into sip_ctx::x_sbuf / x_rbuf at soff / roff
   void* rbuf = nullptr;
   int max_plane = 0;
+  // SIP exchange: the first s1 (r1) elements of the message are the early
+  // (E / N / T source plane) transfers, sent in phase 1
+  long long soff = 0, roff = 0, s1 = 0, r1 = 0;
 };
 }  // namespace sipb
 
@@ -97,6 +100,22 @@ struct sip_ctx {
   FaceCopy* d_local_copies = nullptr;
   int local_max_plane = 0;
   std::vector<sipb::Peer> peers;
+  // SIP face-halo exchange lists (install_plan): local copies + packs, early
+  // entries (source plane E / N / T: final while K3 still runs) first; unpacks,
+  // early (ghost W / S / B) first.  Pack / unpack offsets index x_sbuf / x_rbuf.
+  FaceCopy *d_x = nullptr, *d_ux = nullptr;
+  int x_early = 0, x_late = 0, ux_early = 0, ux_late = 0, x_max_plane = 0;
+  void *x_sbuf = nullptr, *x_rbuf = nullptr;
+  // split exchange (opt-in, env SIPB_XSPLIT=1): phase 1 on the
+  // comm stream xstream from the end of K2 (waits on K3's per-brick stamps),
+  // phase 2 after K3; the next K2 waits on ev_x
+  bool xsplit = false;
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_k2 = nullptr, ev_k3 = nullptr, ev_x = nullptr;
+  unsigned* d_xflag = nullptr;  // [2 * nbricks] K3 stamps (SweepParams::xflag)
+  unsigned* d_xseq = nullptr;   // bumped by K2's finaliser
+  XItem* d_xitems = nullptr;    // phase 1 work items (per brick of each early plane)
+  int n_xitems = 0;
   ncclComm_t comm = nullptr;
   bool prof = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo

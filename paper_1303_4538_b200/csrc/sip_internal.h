@@ -199,6 +199,12 @@ struct SweepParams {
   // its K3 is pending (K3 returns at once when it is 0).  target <= 0: never stop.
   double target;
   unsigned* ctl;
+  // split exchange: K2's finaliser bumps *xseq; K3 stamps
+  // xflag[2 * brick] (its top slices, k = nz - 1, stored) and xflag[2 * brick + 1]
+  // (all stored) with that value, so the E / N / T face copies on the comm
+  // stream can start while K3 still runs.  nullptr: no split exchange.
+  unsigned* xseq;
+  unsigned* xflag;
   unsigned long long* trace;  // optional [nbricks][4]: start ns, end ns, smid, stalls (debug)
   // debug: per-stage clock64 marks of brick trace_brick (first kTraceStages stages,
   // kTraceMarks each) after the per-brick table
@@ -246,6 +252,19 @@ template <typename T>
 int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
                        const BlockDesc* d_blocks, T* phi, const T* buf_in, T* buf_out,
                        void* stream);
+// Split exchange phase 1 work item: the part of early copy `entry`'s source
+// plane held by one brick -- plane rectangle [x0b, x0e) x [x1b, x1e) in the
+// copy's (x0, x1) coordinates -- ready once K3 stamped xflag[2 * brick + sel]
+// (sel 0: the brick's top slices, T planes; 1: the whole brick, E / N planes).
+struct XItem {
+  int entry, brick, sel;
+  int x0b, x0e, x1b, x1e;
+};
+// split exchange phase 1 (comm stream, during K3): waits on K3's per-brick stamps
+template <typename T>
+int launch_face_copies_after(const FaceCopy* d_copies, const XItem* d_items, int nitems,
+                             const BlockDesc* d_blocks, T* phi, T* buf_out, const unsigned* xflag,
+                             const unsigned* xseq, void* stream);
 template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
                     const T* phi, int symmetric, double* out, void* stream);

@@ -32,6 +32,7 @@
 // --fmad=false and IEEE division, so no contraction changes the rounding.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 
@@ -79,6 +80,11 @@ __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __noinline__ void watchdog_fire(int where) {
   printf("sip watchdog: block %d thread %d stalled at site %d\n", blockIdx.x, threadIdx.x, where);
@@ -707,6 +713,7 @@ __global__ void __launch_bounds__(160) k_forward(const SweepParams<T> P) {
           P.state_other[1] = 0u;
           *P.epoch = tag + 1;
           P.ctl[1] = 1u;  // this sweep's K3 runs
+          if (P.xseq) *P.xseq += 1u;  // K3's stamp value (split exchange)
           if (P.target > 0.0) {  // same test as the host loop: n0 == 0 or n / n0 <= target
             const double n0 = it == 0 ? tot : P.norms_base[0];
             if (n0 == 0.0 || tot / n0 <= P.target) P.ctl[0] = 1u;
@@ -857,7 +864,7 @@ struct K3Cfg {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(160) k_backward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const SweepParams<T> P) {
   using C = K3Cfg<T>;
   constexpr int D = C::D;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -869,6 +876,7 @@ __global__ void __launch_bounds__(160) k_backward(const SweepParams<T> P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!*(volatile unsigned*)(P.ctl + 1)) return;  // the sweep's K2 did not run (target reached)
   const uint32_t tag = *P.epoch;
+  const unsigned xs = P.xflag ? *(volatile unsigned*)P.xseq : 0u;
   if (threadIdx.x == 0) {
     for (int q = 0; q < D; ++q) {
       mbar_init(full0 + 8 * q, 2);    // producer expect_tx + mailbox warp
@@ -969,8 +977,28 @@ __global__ void __launch_bounds__(160) k_backward(const SweepParams<T> P) {
         put_tagged_if(ps, P.mB + (bd.mrow + (ps ? cS : 0)) * kTagWords<T>, vS, tag);
         hmark(m, 4);
         mbar_arrive(mbx0 + 8 * q);  // slot read out: the producer may refill it
+        // ghost / padding cells inside the brick's slices are written back
+        // bit for bit, except the B ghost plane (c < 0, stages n < kL / kStage,
+        // lanes with il + jl >= kW): the comm stream's face copies may write it
+        // while this sweep runs (split exchange)
+        if (n >= kL / kStage) {
 #pragma unroll
-        for (int o = 0; o < kStage; ++o) P_dst[((long long)n * kStage + o) * kL] = v[o];
+          for (int o = 0; o < kStage; ++o) P_dst[((long long)n * kStage + o) * kL] = v[o];
+        } else {
+#pragma unroll
+          for (int o = 0; o < kStage; ++o)
+            if (n * kStage + o >= lane) P_dst[((long long)n * kStage + o) * kL] = v[o];
+        }
+        if (P.xflag && (m == NST - bd.nz || m == NST - 1)) {
+          // stage NST - nz completes the brick's k = nz - 1 plane (its slices
+          // 8(nz-1) ...), stage NST - 1 the brick: stamp for the face copies
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {
+            if (m == NST - bd.nz) *(volatile unsigned*)(P.xflag + 2 * bid) = xs;
+            if (m == NST - 1) *(volatile unsigned*)(P.xflag + 2 * bid + 1) = xs;
+          }
+        }
       }
     } else if (warp == 1 || warp == 3) {
       // ------------------------------------------------------------- compute
@@ -1271,6 +1299,70 @@ __global__ void k_face_copy(const FaceCopy* copies, const BlockDesc* blocks, T* 
   }
 }
 
+// K4, split exchange phase 1: the copies whose source is an E,
+// N or T interior plane, launched on the comm stream as soon as K2 finished,
+// i.e. while K3 runs (K3 completes those planes early: it starts at the
+// block's E / N / T corner, and each brick's k = nz - 1 slices come first).
+// One work item = the part of a plane one brick holds; CTA b of G (half the
+// SMs: K3 always keeps SMs of its own) takes items b, b + G, ... (the host orders them by when K3 finishes them) and waits for
+// the brick's stamp from K3 (this iteration's value) before copying.  The
+// wait points one way only (K3 never waits on this kernel), and the CTAs are
+// small (64 threads, <= 64 registers: the 4096 registers three fp64 K3 CTAs
+// leave free), so each fits next to K3's resident CTAs on its SM: no
+// deadlock for any residency, and K3 keeps its occupancy.  Each thread keeps
+// 8 independent loads in flight.
+constexpr int kXCopyThreads = 64;
+template <typename T>
+__global__ void __launch_bounds__(kXCopyThreads, 16)
+    k_face_copy_after(const FaceCopy* copies, const XItem* items, int nitems, const BlockDesc* blocks,
+                      T* phi, T* buf_out, const unsigned* xflag, const unsigned* xseq) {
+  const unsigned want = *(const volatile unsigned*)xseq;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const XItem xi = items[it];
+    // descriptors first (independent of the stamp), then thread 0's wait
+    const FaceCopy fc = copies[xi.entry];
+    const BlockDesc sb = blocks[fc.src_block];
+    const BlockDesc db = blocks[fc.dst_block >= 0 ? fc.dst_block : fc.src_block];
+    if (threadIdx.x == 0) {
+      const unsigned* f = xflag + 2ll * xi.brick + xi.sel;
+      Watchdog wd;
+      while (ld_acquire_u32(f) != want) {
+        __nanosleep(100);
+        wd.idle(60);
+      }
+    }
+    __syncthreads();  // thread 0's acquire orders the CTA's phi reads after K3's stores
+    const int w = xi.x0e - xi.x0b, n = w * (xi.x1e - xi.x1b);
+    constexpr int U = 8;
+    for (int c0 = 0; c0 < n; c0 += U * kXCopyThreads) {
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * kXCopyThreads + threadIdx.x;
+        if (c < n) {
+          int i, j, k;
+          face_cell(sb, fc.src_face, xi.x0b + c % w, xi.x1b + c / w, false, i, j, k);
+          v[u] = phi[phi_index(sb, i, j, k)];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * kXCopyThreads + threadIdx.x;
+        if (c < n) {
+          const int x0 = xi.x0b + c % w, x1 = xi.x1b + c / w;
+          if (fc.dst_block >= 0) {
+            int i, j, k;
+            face_cell(db, fc.dst_face, x0, x1, true, i, j, k);
+            phi[phi_index(db, i, j, k)] = v[u];
+          } else {
+            buf_out[fc.buf + x0 + (long long)fc.n0 * x1] = v[u];
+          }
+        }
+      }
+    }
+  }
+}
+
 // residual_general or, with SYM, residual_symmetric
 // (Listing PAPER.md:503-518): the W / S / B couplings are
 // read as the E / N / T coefficients of the W / S / B neighbour cell (5
@@ -1495,6 +1587,28 @@ int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
   return cuda_status(cudaGetLastError());
 }
 template <typename T>
+int launch_face_copies_after(const FaceCopy* d_copies, const XItem* d_items, int nitems,
+                             const BlockDesc* d_blocks, T* phi, T* buf_out, const unsigned* xflag,
+                             const unsigned* xseq, void* stream) {
+  if (nitems <= 0) return SIP_OK;
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::max(1, nsm / 2);
+    // keep the SMs that host a copy CTA in the large-shared configuration K3
+    // needs (a CTA without shared memory would otherwise let its SM switch to
+    // a small carveout, and K3's CTAs could not join it until the copy CTA
+    // exits -- with a copy CTA on every SM, K3 would never start)
+    cudaFuncSetAttribute(k_face_copy_after<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+  }
+  k_face_copy_after<T><<<grid, kXCopyThreads, 0, (cudaStream_t)stream>>>(
+      d_copies, d_items, nitems, d_blocks, phi, buf_out, xflag, xseq);
+  return cuda_status(cudaGetLastError());
+}
+template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
                     const T* phi, int symmetric, double* out, void* stream) {
   const int g = grid_for((long long)hb.nx * hb.ny * hb.nz);
@@ -1539,6 +1653,8 @@ int launch_generate(int kind, uint64_t seed, const int g[3], const int o[3], int
                                 double*, void*);                                                  \
   template int launch_face_copies<T>(const FaceCopy*, int, int, const BlockDesc*, T*, const T*,   \
                                      T*, void*);                                                  \
+  template int launch_face_copies_after<T>(const FaceCopy*, const XItem*, int, const BlockDesc*,   \
+                                           T*, T*, const unsigned*, const unsigned*, void*);      \
   template int launch_residual<T>(const BlockDesc*, int, const BlockDesc&, const T*, const T*,    \
                                   int, double*, void*);                                           \
   template int launch_gather_any<T>(const T*, int, int, const BlockDesc*, int, const BlockDesc&,  \

@@ -54,8 +54,8 @@ def test_sip_through_nccl_matches_oracle(gpu, nccl_self, prec):
     np.testing.assert_allclose(ng, no, rtol=1e-12)
     for b in range(8):
         assert np.array_equal(phis[b], blocks[b][1]), f"block {b}"
-    # the self mode really took the pack / NCCL / unpack path: one pack and
-    # one unpack launch per exchange instead of one local-copy launch
+    # the self mode really took the pack / NCCL / unpack path: one unpack
+    # launch per exchange on top of the copy / pack launch
     os.environ["SIPB_NCCL_SELF"] = "0"
     s2 = sip.Solver(None, prec, 0, lattice=(g, pd))
     for lb in range(len(s2.blocks)):
