@@ -8,7 +8,6 @@ import paper_1303_4538_b200 as sip
 prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
 g = (256, 256, 256)
 s = sip.Solver(None, prec, 0, lattice=(g, (1, 1, 1)))
-s._nglobal = 1
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 s.set_stream(stream.cuda_stream)

@@ -6,7 +6,6 @@ import paper_1303_4538_b200 as sip
 for prec in ("f64", "f32"):
     for g in ((16, 16, 1024), (256, 256, 256)):
         s = sip.Solver(None, prec, 0, lattice=(g, (1, 1, 1)))
-        s._nglobal = 1
         st = torch.cuda.Stream(); torch.cuda.set_stream(st); s.set_stream(st.cuda_stream)
         s.generate(0, 1304); s.factor(0.92); s.load_phi([sip.field(*g)])
         s.iterate(3)

@@ -9,7 +9,6 @@ import paper_1303_4538_b200 as sip
 for prec in ("f64", "f32"):
     g = (256, 256, 256)
     s = sip.Solver(None, prec, 0, lattice=(g, (1, 1, 1)))
-    s._nglobal = 1
     st = torch.cuda.Stream(); torch.cuda.set_stream(st); s.set_stream(st.cuda_stream)
     s.generate(3, 1309)
     s.factor(0.92)
