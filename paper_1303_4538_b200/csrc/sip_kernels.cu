@@ -913,10 +913,21 @@ __global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const 
         P.trace && (bid == tb || bid == tb + tup)
             ? P.trace + 4ull * P.nbricks + (bid == tb ? 4 : 3) * kTraceStages * kTraceMarks
             : nullptr;
+#ifdef SIPB_K3_CMARKS
+    // compute-warp timeline (clock64, one SM; tools/k3_cmarks.py): 0 ready
+    // at the hand-over barrier, 3 hand-over arrived (chain done), 5 past full
+    auto hmark = [](int, int) {};
+    auto cmark = [&](int m, int k) {
+      if (hm && bid == tb && lane == 0 && m < kTraceStages) hm[m * kTraceMarks + k] = clock64();
+    };
+#else
     auto hmark = [&](int m, int k) {
       if (hm && lane == 0 && m < kTraceStages) hm[m * kTraceMarks + k] = gtime();
     };
+    auto cmark = [](int, int) {};
+#endif
 #else
+    auto cmark = [](int, int) {};
     auto hmark = [](int, int) {};
 #endif
 
@@ -1022,6 +1033,7 @@ __global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const 
         const int n = NST - 1 - m;
         bar_wait(full0 + 8 * q, ph_a, q, 33);
         hmark(m, 2);
+        cmark(m, 5);
         const uint32_t sq = sb + (uint32_t)q * (uint32_t)C::slot_bytes, sl = sq + E * lane;
         const T dE = lds<T>(sl + E * C::o_mb);
         T rr[kStage], un[kStage], ue[kStage], ut[kStage], eN[kStage];
@@ -1046,6 +1058,7 @@ __global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const 
           // bar.sync (64 threads, membar.cta semantics); the hand-overs
           // strictly alternate, so a barrier is never over-arrived (an
           // mbarrier hand-over measured ~6 % slower, a polled flag ~4 %)
+          cmark(m, 0);
           asm volatile("bar.sync %0, 64;" ::"r"(1 + cw) : "memory");
           const T* h = hand + cw * (kW + 1) * kL + lane;
 #pragma unroll
@@ -1081,6 +1094,7 @@ __global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const 
           for (int s = 0; s < kW; ++s) h[s * kL] = win[s];
           h[kW * kL] = dprev;
           asm volatile("bar.arrive %0, 64;" ::"r"(1 + (cw ^ 1)) : "memory");
+          cmark(m, 3);
         }
 #pragma unroll
         for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_pn + (kStage - 1 - s) * kL), win[s]);
