@@ -1100,6 +1100,9 @@ __global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const 
         for (int s = 0; s < kStage; ++s) sts(sl + E * (C::o_pn + (kStage - 1 - s) * kL), win[s]);
         mbar_arrive(cdone0 + 8 * q);
         hmark(m, 3);
+#ifdef SIPB_STAGE_MARKS
+        if (m == kL / kStage && P.trace && lane == 0) P.trace[4 * bid + 3] = gtime();
+#endif
       }
       if (cw == (qlast & 1)) {  // the warp that ran the brick's last stage closes it
         trace_end(P.trace, bid);
