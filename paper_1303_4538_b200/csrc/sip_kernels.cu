@@ -846,6 +846,9 @@ __global__ void __launch_bounds__(160) k_forward(const SweepParams<T> P) {
 // chain state handed over through shared memory), mailbox, and drain (phi +=
 // delta of a finished stage -> HBM, the tagged publishes).
 // =============================================================================
+#ifndef SIPB_K3_MINB
+#define SIPB_K3_MINB (sizeof(T) == 8 ? 3 : 4)  // resident CTAs per SM K3 is compiled for
+#endif
 template <typename T>
 struct K3Cfg {
   static constexpr int D = SIPB_K3_D;
@@ -864,7 +867,7 @@ struct K3Cfg {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(160, sizeof(T) == 8 ? 3 : 4) k_backward(const SweepParams<T> P) {
+__global__ void __launch_bounds__(160, SIPB_K3_MINB) k_backward(const SweepParams<T> P) {
   using C = K3Cfg<T>;
   constexpr int D = C::D;
   extern __shared__ __align__(128) unsigned char smem[];
