@@ -34,14 +34,19 @@ def _run_oracle(A, dims, prec, alpha, iters, phi0=None):
 
 
 CASES = [
-    # (dims, kind, iters) -- config 0 is (64,64,64), kind 0, 20 iterations
+    # (dims, kind, iters) -- config 0 is (64,64,64), kind 0, 20 iterations; bricks are
+    # 8 (i) x 32 (j) columns
     ((64, 64, 64), 0, 20),
-    ((37, 23, 19), 0, 6),      # ragged tiles in i and j
-    ((16, 16, 40), 0, 5),      # exactly one tile, tall
-    ((50, 33, 3), 0, 5),       # nz < tile skew
+    ((37, 23, 19), 0, 6),      # ragged bricks in i and j
+    ((16, 16, 40), 0, 5),      # tall, half a brick in j
+    ((50, 33, 3), 0, 5),       # nz < brick skew
     ((2, 3, 2), 0, 4),         # tiny
     ((1, 2, 3), 0, 3),         # degenerate columns (nx = 1)
     ((40, 24, 20), 2, 6),      # config-2 generator (anisotropic convection-diffusion)
+    ((8, 32, 16), 0, 5),       # exactly one brick: E and N ghosts in ghost bricks
+    ((24, 96, 5), 0, 4),       # exact 3 x 3 bricks
+    ((9, 33, 7), 0, 4),        # one-cell-wide second brick in i and in j
+    ((16, 64, 1), 0, 4),       # nz = 1
 ]
 
 
@@ -55,6 +60,28 @@ def test_solve_matches_oracle(gpu, dims, kind, iters, prec):
     np.testing.assert_allclose(ng, no, rtol=NORM_TOL, atol=0)
     # bitwise phi (interior and untouched ghosts)
     assert np.array_equal(pg, po), f"max |diff| {np.abs(pg - po).max()}"
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_single_cell(gpu, prec):
+    """A 1x1x1 grid.  The generator's single cell has every coupling on the
+    domain boundary, so AP = 0: both the library and the oracle reject it,
+    naming the same cell.  With AP set and the boundary coupled (Dirichlet
+    ghosts) the one-cell solve is bitwise equal to the oracle."""
+    dims = (1, 1, 1)
+    A = O.generate(0, 1303, dims)
+    with pytest.raises(sip.SingularFactorError, match="Field3 index 13"):
+        _run_gpu(A, dims, prec, 0.92, 3)
+    with pytest.raises(ValueError, match="Field3 index 13"):
+        _run_oracle(A, dims, prec, 0.92, 3)
+    for n, v in (("AW", -0.5), ("AE", -0.25), ("AS", -0.125), ("AN", -0.75), ("AB", -0.3), ("AT", -0.6)):
+        A[n][1, 1, 1] = v
+    A["AP"][1, 1, 1] = 3.5
+    phi0 = np.random.default_rng(5).uniform(-1, 1, size=(3, 3, 3))
+    pg, ng = _run_gpu(A, dims, prec, 0.92, 4, phi0)
+    po, no = _run_oracle(A, dims, prec, 0.92, 4, phi0)
+    np.testing.assert_allclose(ng, no, rtol=NORM_TOL, atol=0)
+    assert np.array_equal(pg, po)
 
 
 def test_nonzero_ghosts_and_phi0(gpu):
@@ -204,7 +231,8 @@ def test_target_reduction(gpu):
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("g,pd", [((40, 36, 30), (2, 2, 2)), ((33, 17, 20), (3, 1, 2)),
-                                  ((64, 48, 32), (2, 3, 1))])
+                                  ((64, 48, 32), (2, 3, 1)),
+                                  ((32, 128, 16), (2, 2, 2))])  # brick-exact blocks: E/N ghost bricks
 def test_multiblock_matches_oracle(gpu, g, pd, prec):
     """Block-structured lattice on one GPU: per-block factorisation, one-cell
     face halos exchanged after every inner iteration (device copies), norms
