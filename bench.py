@@ -351,23 +351,39 @@ def run_e2e(s, c, cfg_id, prec, reps, dist, stream):
     h2d = 2 * G * 8
     d2h = G * 8 + iters * 8
 
-    def one():
-        # inputs of the step: Q and phi0 from pinned host memory (phi0 = the previous step's
-        # result, a warm start: every step still runs all `iters` iterations, target 0)
-        for lb, (t, a) in enumerate(qs):
-            st = L.sip_set_source(s.handle, lb, a.ctypes.data_as(dp))
-            assert st == 0
-        st = L.sip_solve(s.handle, arr, iters, ctypes.c_double(0.0), norms.ctypes.data_as(dp),
-                         ctypes.byref(used))
-        assert st == 0, L.sip_last_error(s.handle)
+    qp = [a.ctypes.data_as(dp) for (t, a) in qs]
+    pipelined = dist is None  # sip_solve_async is single-rank
 
-    one()  # warm
+    def run(reps):
+        # every step: H2D of its inputs (Q and phi0 = the previous step's
+        # result, a warm start; every step still runs all `iters` iterations,
+        # target 0) from pinned host memory, the solve, D2H of phi and norms.
+        # Single rank: pipelined -- the next step's Q is uploaded on the copy
+        # stream while this step's solve runs (sip_set_source_async)
+        if pipelined:
+            for lb in range(len(qs)):
+                assert L.sip_set_source_async(s.handle, lb, qp[lb]) == 0
+            for r in range(reps):
+                st = L.sip_solve_async(s.handle, arr, iters, norms.ctypes.data_as(dp))
+                assert st == 0, L.sip_last_error(s.handle)
+                if r + 1 < reps:
+                    for lb in range(len(qs)):
+                        assert L.sip_set_source_async(s.handle, lb, qp[lb]) == 0
+                assert L.sip_synchronize(s.handle) == 0
+            return
+        for _ in range(reps):
+            for lb in range(len(qs)):
+                assert L.sip_set_source(s.handle, lb, qp[lb]) == 0
+            st = L.sip_solve(s.handle, arr, iters, ctypes.c_double(0.0), norms.ctypes.data_as(dp),
+                             ctypes.byref(used))
+            assert st == 0, L.sip_last_error(s.handle)
+
+    run(1)  # warm
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(reps):
-        one()
+    run(reps)
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     if dist is not None:
@@ -378,7 +394,9 @@ def run_e2e(s, c, cfg_id, prec, reps, dist, stream):
     return {"value": cells_total * iters * reps / el / 1e6, "unit": "MLUP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": el / reps * 1e3, "steps": reps,
-            "call": "sip_set_source + sip_solve (pinned host Field3 buffers, phi0 = previous result)"}
+            "call": ("sip_set_source_async (next step's Q during this step's solve) + sip_solve_async + "
+                     "sip_synchronize" if pipelined else "sip_set_source + sip_solve") +
+                    " (pinned host Field3 buffers, phi0 = previous result)"}
 
 
 def load_traffic(cfg_id, prec):

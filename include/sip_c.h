@@ -140,7 +140,26 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi);      /* host Field3 -> devic
 int sip_store_phi(sip_ctx* ctx, double* const* phi);     /* device -> host Field3 */
 int sip_iterate(sip_ctx* ctx, int iters);                 /* enqueue, no host sync */
 int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* block_norms);
+/* Waits for the context's stream; completes a pending sip_solve_async
+ * (its norms_out is filled here). */
 int sip_synchronize(sip_ctx* ctx);
+
+/*
+ * Pipelined solves (single rank).  A caller that knows the next step's source
+ * can upload it while the current solve runs:
+ *   sip_set_source_async(q_0); for each step i:
+ *     sip_solve_async(phi, iters, norms);  sip_set_source_async(q_{i+1});
+ *     sip_synchronize();   (norms of step i; one async solve pending at a time)
+ * sip_set_source_async copies q (pinned host memory for overlap) on a copy
+ * stream into one of two staging buffers per block and applies it on the
+ * context's stream after the work already enqueued there, so results are
+ * those of the sequential calls.  sip_solve_async is sip_solve with a fixed
+ * iteration count and no host synchronisation: phi (pinned for overlap) is
+ * read and written in stream order, norms_out[iters] is filled by the next
+ * sip_synchronize.
+ */
+int sip_set_source_async(sip_ctx* ctx, int local, const double* q);
+int sip_solve_async(sip_ctx* ctx, double* const* phi, int iters, double* norms_out);
 
 /* Flag (symmetric = 1) or unflag the system of local block `local` as
  * symmetric (StencilSystem invariant: ae(i) = aw(i+1),

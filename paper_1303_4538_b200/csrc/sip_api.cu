@@ -916,6 +916,16 @@ int sip_destroy(sip_ctx* ctx) {
   for (void* q : {(void*)ctx->d_x, (void*)ctx->d_ux, ctx->x_sbuf, ctx->x_rbuf, (void*)ctx->d_xflag,
                   (void*)ctx->d_xseq, (void*)ctx->d_xitems})
     if (q) cudaFree(q);
+  if (ctx->cstream) {
+    cudaStreamSynchronize(ctx->cstream);
+    cudaStreamDestroy(ctx->cstream);
+    for (auto& a : ctx->ev_qcopy)
+      for (auto e : a) cudaEventDestroy(e);
+    for (auto& a : ctx->ev_qscat)
+      for (auto e : a) cudaEventDestroy(e);
+    cudaFree(ctx->q_stage);
+  }
+  if (ctx->h_norms) cudaFreeHost(ctx->h_norms);
   if (ctx->xstream) {
     cudaStreamSynchronize(ctx->xstream);
     cudaStreamDestroy(ctx->xstream);
@@ -1227,6 +1237,90 @@ int sip_synchronize(sip_ctx* ctx) {
   if (!ctx) return SIP_ERR_MISUSE;
   CKS(set_device(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pending_norms && ctx->pending_out)
+    std::memcpy(ctx->pending_out, ctx->h_norms, sizeof(double) * ctx->pending_norms);
+  ctx->pending_norms = 0;
+  ctx->pending_out = nullptr;
+  return SIP_OK;
+}
+
+int sip_set_source_async(sip_ctx* ctx, int local, const double* q) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (local < 0 || local >= (int)ctx->local.size() || !q) {
+    ctx->err = "sip_set_source_async: bad arguments";
+    return SIP_ERR_MISUSE;
+  }
+  CKS(set_device(ctx));
+  const size_t nl = ctx->local.size();
+  if (!ctx->cstream) {
+    size_t tot = 0;
+    for (const BlockDesc& b : ctx->hblocks) tot += field3_elems(b);
+    CKS(dalloc(ctx, &ctx->q_stage, sizeof(double) * 2 * std::max<size_t>(1, tot)));
+    CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+    ctx->q_slot.assign(nl, 0);
+    ctx->ev_qcopy.resize(nl);
+    ctx->ev_qscat.resize(nl);
+    for (size_t b = 0; b < nl; ++b)
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_qcopy[b][k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_qscat[b][k], cudaEventDisableTiming));
+        CK(cudaEventRecord(ctx->ev_qscat[b][k], ctx->stream));  // slot free
+      }
+  }
+  const BlockDesc& hb = ctx->hblocks[local];
+  const size_t G = field3_elems(hb);
+  const int k = ctx->q_slot[local];
+  ctx->q_slot[local] ^= 1;
+  double* st = ctx->q_stage + 2 * ctx->phi_stage_off[local] + k * G;
+  // the copy may start at once (copy stream), once the scatter that last
+  // read this slot is done; the scatter waits for the copy and follows the
+  // work already on the context's stream
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_qscat[local][k], 0));
+  CK(cudaMemcpyAsync(st, q, G * sizeof(double), cudaMemcpyHostToDevice, ctx->cstream));
+  CK(cudaEventRecord(ctx->ev_qcopy[local][k], ctx->cstream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_qcopy[local][k], 0));
+  CKS(scatter_array(ctx, local, st, F_Q));
+  CK(cudaEventRecord(ctx->ev_qscat[local][k], ctx->stream));
+  return SIP_OK;
+}
+
+int sip_solve_async(sip_ctx* ctx, double* const* phi, int iters, double* norms_out) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  if (ctx->nranks != 1 || iters < 1 || ctx->pending_norms) {
+    ctx->err = ctx->pending_norms ? "sip_solve_async: synchronize the previous async solve first"
+                                  : "sip_solve_async: single rank, iters >= 1";
+    return SIP_ERR_MISUSE;
+  }
+  CKS(check_ready(ctx));
+  CKS(sip_load_phi(ctx, phi));
+  CKS(sip_iterate(ctx, iters));
+  if (norms_out) {
+    if (iters > ctx->h_norms_cap) {
+      if (ctx->h_norms) cudaFreeHost(ctx->h_norms);
+      ctx->h_norms = nullptr;
+      CK(cudaMallocHost(&ctx->h_norms, sizeof(double) * iters));
+      ctx->h_norms_cap = iters;
+    }
+    CK(cudaMemcpyAsync(ctx->h_norms, ctx->d_norms, sizeof(double) * iters, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    ctx->pending_norms = iters;
+    ctx->pending_out = norms_out;
+  }
+  // sip_store_phi without its final synchronisation
+  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+    const BlockDesc& hb = ctx->hblocks[lb];
+    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    const int* written = ctx->plan_ghosts[lb].data();
+    if (ctx->precision == SIP_PREC_SINGLE)
+      CKS(launch_gather<float>(static_cast<float*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
+                               ctx->stream));
+    else
+      CKS(launch_gather<double>(static_cast<double*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
+                                ctx->stream));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(phi[lb], st, field3_elems(hb) * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
   return SIP_OK;
 }
 

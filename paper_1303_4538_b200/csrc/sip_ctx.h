@@ -116,6 +116,17 @@ struct sip_ctx {
   unsigned* d_xseq = nullptr;   // bumped by K2's finaliser
   XItem* d_xitems = nullptr;    // phase 1 work items (per brick of each early plane)
   int n_xitems = 0;
+  // pipelined solves (sip_set_source_async / sip_solve_async): copy stream,
+  // two staging slots per local block (Field3 doubles), the event of each
+  // slot's H2D and of the scatter that last read it; norms of a pending
+  // async solve (pinned) and where sip_synchronize delivers them
+  cudaStream_t cstream = nullptr;
+  double* q_stage = nullptr;
+  std::vector<int> q_slot;
+  std::vector<std::array<cudaEvent_t, 2>> ev_qcopy, ev_qscat;
+  double* h_norms = nullptr;
+  int h_norms_cap = 0, pending_norms = 0;
+  double* pending_out = nullptr;
   ncclComm_t comm = nullptr;
   bool prof = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo

@@ -58,7 +58,8 @@ EXPORTS = (
     "sip_ftt1_read", "sip_ftt1_write", "sip_ftt1_validate", "sip_set_halo_tables",
     "sip_plan_halo_periodic", "sip_assemble_poisson", "sip_flow_create", "sip_flow_destroy",
     "sip_flow_set", "sip_flow_get", "sip_flow_divergence", "sip_pressure_correct",
-    "sip_factor_count", "sip_num_global_blocks", "sip_solve_ex",
+    "sip_factor_count", "sip_num_global_blocks", "sip_solve_ex", "sip_set_source_async",
+    "sip_solve_async",
 )
 
 
@@ -292,6 +293,19 @@ class Solver:
     def set_source(self, local: int, q: np.ndarray):
         self._c(lib().sip_set_source(self._ctx, local, _ptr(q)), "sip_set_source")
 
+    def set_source_async(self, local: int, q: np.ndarray):
+        """sip_set_source_async: q is copied on the copy stream (keep it alive
+        and unchanged until the next synchronize; pinned memory overlaps)."""
+        self._keep = getattr(self, "_keep", []) + [q]
+        self._c(lib().sip_set_source_async(self._ctx, local, _ptr(q)), "sip_set_source_async")
+
+    def solve_async(self, phis: Sequence[np.ndarray], iters: int, norms: np.ndarray):
+        """sip_solve_async: fixed iteration count, no host synchronisation;
+        phis and norms[iters] are complete after synchronize()."""
+        self._keep = getattr(self, "_keep", []) + [phis, norms]
+        self._c(lib().sip_solve_async(self._ctx, self._phis(phis), int(iters), norms.ctypes.data_as(_dp)),
+                "sip_solve_async")
+
     def generate(self, kind: int, seed: int):
         self._c(lib().sip_generate_system(self._ctx, kind, ctypes.c_uint64(seed)),
                 "sip_generate_system")
@@ -366,6 +380,7 @@ class Solver:
 
     def synchronize(self):
         self._c(lib().sip_synchronize(self._ctx), "sip_synchronize")
+        self._keep = []
 
     def residual(self, symmetric: bool = False):
         outs = [field(*d) for (_, d, _) in self.blocks]
