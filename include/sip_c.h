@@ -140,26 +140,31 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi);      /* host Field3 -> devic
 int sip_store_phi(sip_ctx* ctx, double* const* phi);     /* device -> host Field3 */
 int sip_iterate(sip_ctx* ctx, int iters);                 /* enqueue, no host sync */
 int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* block_norms);
-/* Waits for the context's stream; completes a pending sip_solve_async
- * (its norms_out is filled here). */
+/* Waits for the context's stream; completes the pending sip_solve_async calls
+ * (their norms_out are filled here). */
 int sip_synchronize(sip_ctx* ctx);
 
 /*
  * Pipelined solves (single rank).  A caller that knows the next step's source
- * can upload it while the current solve runs:
- *   sip_set_source_async(q_0); for each step i:
- *     sip_solve_async(phi, iters, norms);  sip_set_source_async(q_{i+1});
- *     sip_synchronize();   (norms of step i; one async solve pending at a time)
+ * can upload it while the current solve runs, and keep two solves in flight:
+ *   sip_set_source_async(q_0); sip_solve_async(phi, iters, norms_0);
+ *   for each step i:
+ *     if (i + 1 < steps) { sip_set_source_async(q_{i+1});
+ *                          sip_solve_async(phi, iters, norms_{i+1}); }
+ *     sip_wait_async();      (step i complete: phi written, norms_i filled)
  * sip_set_source_async copies q (pinned host memory for overlap) on a copy
  * stream into one of two staging buffers per block and applies it on the
- * context's stream after the work already enqueued there, so results are
- * those of the sequential calls.  sip_solve_async is sip_solve with a fixed
- * iteration count and no host synchronisation: phi (pinned for overlap) is
- * read and written in stream order, norms_out[iters] is filled by the next
- * sip_synchronize.
+ * context's stream after the work already enqueued there.  sip_solve_async
+ * is sip_solve with a fixed iteration count and no host synchronisation; at
+ * most two are pending.  When its phi buffers are the ones the previous
+ * pending solve writes its result into, the upload of phi0 follows that
+ * download chunk by chunk (both directions of the link at once).  Results are
+ * those of the sequential calls.  sip_wait_async completes the oldest pending
+ * solve, sip_synchronize all of them.
  */
 int sip_set_source_async(sip_ctx* ctx, int local, const double* q);
 int sip_solve_async(sip_ctx* ctx, double* const* phi, int iters, double* norms_out);
+int sip_wait_async(sip_ctx* ctx);
 
 /* Flag (symmetric = 1) or unflag the system of local block `local` as
  * symmetric (StencilSystem invariant: ae(i) = aw(i+1),

@@ -919,13 +919,19 @@ int sip_destroy(sip_ctx* ctx) {
   if (ctx->cstream) {
     cudaStreamSynchronize(ctx->cstream);
     cudaStreamDestroy(ctx->cstream);
-    for (auto& a : ctx->ev_qcopy)
-      for (auto e : a) cudaEventDestroy(e);
-    for (auto& a : ctx->ev_qscat)
-      for (auto e : a) cudaEventDestroy(e);
-    cudaFree(ctx->q_stage);
   }
-  if (ctx->h_norms) cudaFreeHost(ctx->h_norms);
+  for (auto& a : ctx->ev_qcopy)
+    for (auto e : a) cudaEventDestroy(e);
+  for (auto& a : ctx->ev_qscat)
+    for (auto e : a) cudaEventDestroy(e);
+  if (ctx->q_stage) cudaFree(ctx->q_stage);
+  if (ctx->phi_stage2) cudaFree(ctx->phi_stage2);
+  for (AsyncSolve& a : ctx->async) {
+    if (a.h_norms) cudaFreeHost(a.h_norms);
+    if (a.done) cudaEventDestroy(a.done);
+    if (a.h2d) cudaEventDestroy(a.h2d);
+    for (auto e : a.chunk_ev) cudaEventDestroy(e);
+  }
   if (ctx->xstream) {
     cudaStreamSynchronize(ctx->xstream);
     cudaStreamDestroy(ctx->xstream);
@@ -1093,7 +1099,9 @@ int sip_factor(sip_ctx* ctx, double alpha, long long* bad_block, long long* bad_
   return SIP_OK;
 }
 
-int sip_load_phi(sip_ctx* ctx, double* const* phi) {
+// phi0 into the device mirror `stage` (copy == false: already there) and the
+// brick layout; resets the iteration state.
+static int load_phi_into(sip_ctx* ctx, double* const* phi, double* stage, bool copy) {
   if (!ctx || !phi) return SIP_ERR_MISUSE;
   CKS(set_device(ctx));
   for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
@@ -1102,10 +1110,11 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi) {
       return SIP_ERR_MISUSE;
     }
     const BlockDesc& hb = ctx->hblocks[lb];
-    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    double* st = stage + ctx->phi_stage_off[lb];
     // Field3 -> device mirror (keeps the caller's ghost layer for the store)
-    CK(cudaMemcpyAsync(st, phi[lb], field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
-                       ctx->stream));
+    if (copy)
+      CK(cudaMemcpyAsync(st, phi[lb], field3_elems(hb) * sizeof(double), cudaMemcpyHostToDevice,
+                         ctx->stream));
     if (ctx->precision == SIP_PREC_SINGLE)
       CKS(launch_phi_in<float>(st, ctx->d_blocks, (int)lb, hb, static_cast<float*>(ctx->phi), ctx->stream));
     else
@@ -1123,6 +1132,10 @@ int sip_load_phi(sip_ctx* ctx, double* const* phi) {
     ctx->failed = false;
   }
   return s;
+}
+
+int sip_load_phi(sip_ctx* ctx, double* const* phi) {
+  return ctx ? load_phi_into(ctx, phi, ctx->phi_stage, true) : SIP_ERR_MISUSE;
 }
 
 int sip_store_phi(sip_ctx* ctx, double* const* phi) {
@@ -1233,14 +1246,35 @@ int sip_read_norms(sip_ctx* ctx, int first, int count, double* norms, double* bl
   return SIP_OK;
 }
 
+// the oldest pending sip_solve_async: wait for it, deliver its norms
+static int finish_async(sip_ctx* ctx) {
+  if (ctx->async_count == 0) return SIP_OK;
+  AsyncSolve& a = ctx->async[ctx->async_head];
+  CK(cudaEventSynchronize(a.done));
+  if (a.out) std::memcpy(a.out, a.h_norms, sizeof(double) * a.iters);
+  a.out = nullptr;
+  ctx->async_head ^= 1;
+  --ctx->async_count;
+  return SIP_OK;
+}
+
 int sip_synchronize(sip_ctx* ctx) {
   if (!ctx) return SIP_ERR_MISUSE;
   CKS(set_device(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
-  if (ctx->pending_norms && ctx->pending_out)
-    std::memcpy(ctx->pending_out, ctx->h_norms, sizeof(double) * ctx->pending_norms);
-  ctx->pending_norms = 0;
-  ctx->pending_out = nullptr;
+  while (ctx->async_count) CKS(finish_async(ctx));
+  return SIP_OK;
+}
+
+int sip_wait_async(sip_ctx* ctx) {
+  if (!ctx) return SIP_ERR_MISUSE;
+  CKS(set_device(ctx));
+  return finish_async(ctx);
+}
+
+static int ensure_cstream(sip_ctx* ctx) {
+  if (ctx->cstream) return SIP_OK;
+  CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   return SIP_OK;
 }
 
@@ -1251,12 +1285,12 @@ int sip_set_source_async(sip_ctx* ctx, int local, const double* q) {
     return SIP_ERR_MISUSE;
   }
   CKS(set_device(ctx));
+  CKS(ensure_cstream(ctx));
   const size_t nl = ctx->local.size();
-  if (!ctx->cstream) {
+  if (!ctx->q_stage) {
     size_t tot = 0;
     for (const BlockDesc& b : ctx->hblocks) tot += field3_elems(b);
     CKS(dalloc(ctx, &ctx->q_stage, sizeof(double) * 2 * std::max<size_t>(1, tot)));
-    CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
     ctx->q_slot.assign(nl, 0);
     ctx->ev_qcopy.resize(nl);
     ctx->ev_qscat.resize(nl);
@@ -1284,32 +1318,83 @@ int sip_set_source_async(sip_ctx* ctx, int local, const double* q) {
   return SIP_OK;
 }
 
+// Up to two solves in flight, each with its own device phi mirror.  When a
+// solve's phi0 buffer is the one the previous pending solve writes its result
+// into, the upload goes chunk by chunk on the copy stream, each chunk as soon
+// as that chunk of the previous result has arrived in host memory (the two
+// directions of the link overlap).
 int sip_solve_async(sip_ctx* ctx, double* const* phi, int iters, double* norms_out) {
-  if (!ctx) return SIP_ERR_MISUSE;
-  if (ctx->nranks != 1 || iters < 1 || ctx->pending_norms) {
-    ctx->err = ctx->pending_norms ? "sip_solve_async: synchronize the previous async solve first"
-                                  : "sip_solve_async: single rank, iters >= 1";
+  if (!ctx || !phi) return SIP_ERR_MISUSE;
+  if (ctx->nranks != 1 || iters < 1 || ctx->async_count == 2) {
+    ctx->err = ctx->async_count == 2 ? "sip_solve_async: two solves pending (sip_wait_async first)"
+                                     : "sip_solve_async: single rank, iters >= 1";
     return SIP_ERR_MISUSE;
   }
   CKS(check_ready(ctx));
-  CKS(sip_load_phi(ctx, phi));
-  CKS(sip_iterate(ctx, iters));
-  if (norms_out) {
-    if (iters > ctx->h_norms_cap) {
-      if (ctx->h_norms) cudaFreeHost(ctx->h_norms);
-      ctx->h_norms = nullptr;
-      CK(cudaMallocHost(&ctx->h_norms, sizeof(double) * iters));
-      ctx->h_norms_cap = iters;
-    }
-    CK(cudaMemcpyAsync(ctx->h_norms, ctx->d_norms, sizeof(double) * iters, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    ctx->pending_norms = iters;
-    ctx->pending_out = norms_out;
+  CKS(set_device(ctx));
+  CKS(ensure_cstream(ctx));
+  const size_t nl = ctx->local.size();
+  const int si = (ctx->async_head + ctx->async_count) & 1;
+  AsyncSolve& a = ctx->async[si];
+  if (!a.done) {
+    CK(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.h2d, cudaEventDisableTiming));
+    a.chunk_ev.resize(nl * kAsyncChunks);
+    for (auto& e : a.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  // sip_store_phi without its final synchronisation
-  for (size_t lb = 0; lb < ctx->local.size(); ++lb) {
+  if (si == 1 && !ctx->phi_stage2) {
+    size_t tot = 0;
+    for (const BlockDesc& b : ctx->hblocks) tot += field3_elems(b);
+    CKS(dalloc(ctx, &ctx->phi_stage2, sizeof(double) * std::max<size_t>(1, tot)));
+  }
+  double* const stage = si == 0 ? ctx->phi_stage : ctx->phi_stage2;
+  const AsyncSolve* prev = ctx->async_count ? &ctx->async[si ^ 1] : nullptr;
+  // phi0 upload: chunked after the previous result where the buffers coincide
+  bool chunked = false;
+  for (size_t lb = 0; lb < nl; ++lb) {
+    if (!phi[lb]) {
+      ctx->err = "sip_solve_async: null phi";
+      return SIP_ERR_MISUSE;
+    }
+    const size_t G = field3_elems(ctx->hblocks[lb]);
+    double* st = stage + ctx->phi_stage_off[lb];
+    if (prev && prev->phi[lb] == phi[lb]) {
+      const size_t per = (G + kAsyncChunks - 1) / kAsyncChunks;
+      for (int c = 0; c < kAsyncChunks; ++c) {
+        const size_t b = c * per, e = std::min(G, b + per);
+        if (b >= e) break;
+        CK(cudaStreamWaitEvent(ctx->cstream, prev->chunk_ev[lb * kAsyncChunks + c], 0));
+        CK(cudaMemcpyAsync(st + b, phi[lb] + b, (e - b) * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->cstream));
+      }
+      chunked = true;
+    } else {
+      CK(cudaMemcpyAsync(st, phi[lb], G * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  if (chunked) {
+    CK(cudaEventRecord(a.h2d, ctx->cstream));
+    CK(cudaStreamWaitEvent(ctx->stream, a.h2d, 0));
+  }
+  CKS(load_phi_into(ctx, phi, stage, false));
+  CKS(sip_iterate(ctx, iters));
+  a.iters = iters;
+  a.out = norms_out;
+  if (norms_out) {
+    if (iters > a.h_cap) {
+      if (a.h_norms) cudaFreeHost(a.h_norms);
+      a.h_norms = nullptr;
+      CK(cudaMallocHost(&a.h_norms, sizeof(double) * iters));
+      a.h_cap = iters;
+    }
+    CK(cudaMemcpyAsync(a.h_norms, ctx->d_norms, sizeof(double) * iters, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  // sip_store_phi into this solve's mirror, the download in chunks
+  a.phi.assign(phi, phi + nl);
+  for (size_t lb = 0; lb < nl; ++lb) {
     const BlockDesc& hb = ctx->hblocks[lb];
-    double* st = ctx->phi_stage + ctx->phi_stage_off[lb];
+    double* st = stage + ctx->phi_stage_off[lb];
     const int* written = ctx->plan_ghosts[lb].data();
     if (ctx->precision == SIP_PREC_SINGLE)
       CKS(launch_gather<float>(static_cast<float*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
@@ -1318,9 +1403,17 @@ int sip_solve_async(sip_ctx* ctx, double* const* phi, int iters, double* norms_o
       CKS(launch_gather<double>(static_cast<double*>(ctx->phi), ctx->d_blocks, (int)lb, hb, written, st,
                                 ctx->stream));
     ++ctx->launches;
-    CK(cudaMemcpyAsync(phi[lb], st, field3_elems(hb) * sizeof(double), cudaMemcpyDeviceToHost,
-                       ctx->stream));
+    const size_t G = field3_elems(hb), per = (G + kAsyncChunks - 1) / kAsyncChunks;
+    for (int c = 0; c < kAsyncChunks; ++c) {
+      const size_t b = std::min(G, c * per), e = std::min(G, b + per);
+      if (e > b)
+        CK(cudaMemcpyAsync(phi[lb] + b, st + b, (e - b) * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+      CK(cudaEventRecord(a.chunk_ev[lb * kAsyncChunks + c], ctx->stream));
+    }
   }
+  CK(cudaEventRecord(a.done, ctx->stream));
+  ++ctx->async_count;
   return SIP_OK;
 }
 

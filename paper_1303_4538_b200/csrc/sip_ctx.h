@@ -47,6 +47,20 @@ struct Peer {
   // (E / N / T source plane) transfers, sent in phase 1
   long long soff = 0, roff = 0, s1 = 0, r1 = 0;
 };
+// One pending sip_solve_async: its norms (pinned host copy, delivered to
+// `out` when it completes), the caller's phi buffers and one event per
+// downloaded chunk of each (the next solve's upload of the same buffer
+// follows them chunk by chunk).
+constexpr int kAsyncChunks = 8;
+struct AsyncSolve {
+  int iters = 0;
+  double* out = nullptr;
+  double* h_norms = nullptr;
+  int h_cap = 0;
+  std::vector<double*> phi;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t done = nullptr, h2d = nullptr;
+};
 }  // namespace sipb
 
 using namespace sipb;  // internal header: the context is built from sipb types
@@ -117,16 +131,16 @@ struct sip_ctx {
   XItem* d_xitems = nullptr;    // phase 1 work items (per brick of each early plane)
   int n_xitems = 0;
   // pipelined solves (sip_set_source_async / sip_solve_async): copy stream,
-  // two staging slots per local block (Field3 doubles), the event of each
-  // slot's H2D and of the scatter that last read it; norms of a pending
-  // async solve (pinned) and where sip_synchronize delivers them
+  // two staging slots per local block for the source (Field3 doubles), the
+  // event of each slot's H2D and of the scatter that last read it; up to two
+  // solves in flight (AsyncSolve), the second with its own phi mirror
   cudaStream_t cstream = nullptr;
   double* q_stage = nullptr;
   std::vector<int> q_slot;
   std::vector<std::array<cudaEvent_t, 2>> ev_qcopy, ev_qscat;
-  double* h_norms = nullptr;
-  int h_norms_cap = 0, pending_norms = 0;
-  double* pending_out = nullptr;
+  double* phi_stage2 = nullptr;
+  sipb::AsyncSolve async[2];
+  int async_head = 0, async_count = 0;
   ncclComm_t comm = nullptr;
   bool prof = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> events;  // kind 0 fwd, 1 bwd, 2 halo

@@ -59,7 +59,7 @@ EXPORTS = (
     "sip_plan_halo_periodic", "sip_assemble_poisson", "sip_flow_create", "sip_flow_destroy",
     "sip_flow_set", "sip_flow_get", "sip_flow_divergence", "sip_pressure_correct",
     "sip_factor_count", "sip_num_global_blocks", "sip_solve_ex", "sip_set_source_async",
-    "sip_solve_async",
+    "sip_solve_async", "sip_wait_async",
 )
 
 
@@ -305,6 +305,10 @@ class Solver:
         self._keep = getattr(self, "_keep", []) + [phis, norms]
         self._c(lib().sip_solve_async(self._ctx, self._phis(phis), int(iters), norms.ctypes.data_as(_dp)),
                 "sip_solve_async")
+
+    def wait_async(self):
+        """sip_wait_async: the oldest pending solve_async is complete."""
+        self._c(lib().sip_wait_async(self._ctx), "sip_wait_async")
 
     def generate(self, kind: int, seed: int):
         self._c(lib().sip_generate_system(self._ctx, kind, ctypes.c_uint64(seed)),

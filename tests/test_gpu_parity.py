@@ -642,3 +642,44 @@ def test_async_pipeline_equals_sequential(gpu, prec):
         assert np.array_equal(norms, seq_n[k]), k
         assert np.array_equal(phi, seq_phi[k]), k
     s.close()
+
+
+def test_two_async_solves_in_flight(gpu):
+    """The bench's e2e pattern: two solves pending, the next step's phi0 upload
+    following the previous result's download chunk by chunk (same buffers),
+    the next source uploaded during the current solve; bitwise equal to the
+    sequential calls."""
+    dims, iters, steps = (33, 40, 17), 3, 5
+    A = O.generate(0, 1303 + 71, dims)
+    qs = [A["Q"] * (1.0 + 0.125 * k) for k in range(steps)]
+
+    def make():
+        s = sip.Solver(dims, "f64")
+        s.set_system(0, sip.StencilSystem.from_dict(A))
+        s.factor(0.92)
+        return s
+
+    s = make()
+    phi = O.field(*dims)
+    seq_phi, seq_n = [], []
+    for q in qs:
+        s.set_source(0, q)
+        seq_n.append(np.asarray(s.solve([phi], iters)))
+        seq_phi.append(phi.copy())
+    s.close()
+
+    s = make()
+    phi = O.field(*dims)
+    norms = [np.zeros(iters) for _ in range(steps)]
+    s.set_source_async(0, qs[0])
+    s.solve_async([phi], iters, norms[0])
+    for k in range(steps):
+        if k + 1 < steps:
+            s.set_source_async(0, qs[k + 1])
+            s.solve_async([phi], iters, norms[k + 1])
+        s.wait_async()
+        assert np.array_equal(norms[k], seq_n[k]), k
+        if k + 1 == steps:
+            assert np.array_equal(phi, seq_phi[k])
+    s.synchronize()
+    s.close()
