@@ -399,10 +399,13 @@ __global__ void __launch_bounds__(32) k_factor(const FactorParams<T> P) {
 #define SIPB_K2_D64 3
 #endif
 #ifndef SIPB_K2_D32
-#define SIPB_K2_D32 5
+#define SIPB_K2_D32 7  // measured 293 -> 291 us at 256^3 vs 5
 #endif
 #ifndef SIPB_K3_D
 #define SIPB_K3_D 4  // even: slot q is always served by compute warp q & 1
+#endif
+#ifndef SIPB_K3_D32
+#define SIPB_K3_D32 6  // fp32 (even); measured 235 -> 232 us at 256^3 vs 4
 #endif
 template <typename T>
 struct K2Cfg {
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(160) k_forward(const SweepParams<T> P) {
 #endif
 template <typename T>
 struct K3Cfg {
-  static constexpr int D = SIPB_K3_D;
+  static constexpr int D = sizeof(T) == 8 ? SIPB_K3_D : SIPB_K3_D32;
   static constexpr int kBw = kStage * B_NA * kL, kCh = kStage * kL;
   // slot (T units): bw | R | phi (TMA) | phi new (compute -> producer) | mailbox dE[32] eN[8]
   static constexpr int o_R = kBw, o_ph = kBw + kCh, o_pn = kBw + 2 * kCh, o_mb = kBw + 3 * kCh;
