@@ -6,7 +6,7 @@
 //   K3 k_backward  backward substitution + phi update          brick wavefront
 //                  (backward3d)
 //   K4 k_face_copy face-halo copies / pack / unpack (exvec)
-//   K7 k_scatter / k_gather / k_phi_in   Field3 <-> brick-slice layout
+//   K7 k_tile_xfer / k_phi_in / k_gather  Field3 <-> brick-slice layout (interior tiled, ghost faces)
 //   k_residual     residual_general / residual_symmetric
 //
 // Wavefront scheme (DESIGN.md sections 4-5): a brick of kW x kL columns is
@@ -1191,20 +1191,59 @@ __device__ __forceinline__ void cell_ijk(const BlockDesc& bd, long long c, int& 
   k = (int)(r / (unsigned)bd.ny);
 }
 
-template <typename T>
-__global__ void k_scatter(const double* __restrict__ src, const BlockDesc* blocks, int b, T* pack,
-                          int na, int arr) {
+// Interior Field3 <-> brick layout, tiled (one CTA per brick x kXK k-levels):
+// the brick's cells of the chunk go through shared memory, so Field3 is read
+// (written) in 64 B row pieces (8 cells along i) and the brick array in 256 B
+// slice rows (32 lanes).  A slice row holds cells of different k (lane jl is
+// jl slices behind lane 0); each cell belongs to the chunk of its own k, so
+// rows at chunk boundaries are shared between two CTAs, lane by lane.
+// Brick element (slice tau, lane jl) of brick r: phi (PHI) or pack array arr.
+constexpr int kXK = 16;
+template <typename T, bool PHI>
+__device__ __forceinline__ long long brick_elem(const BlockDesc& bd, int r, int tau, int na, int arr, int jl) {
+  if (PHI) return (phi_slot(bd, r) + tau) * kL + jl;
+  return ((bd.slot0 + (long long)r * bd.ns + tau) * na + arr) * kL + jl;
+}
+template <typename T, bool PHI, bool TO_BRICK>
+__global__ void __launch_bounds__(256) k_tile_xfer(const BlockDesc* blocks, int b, const double* f3in, double* f3out,
+                                                   const T* bin, T* bout, int na, int arr) {
+  __shared__ double tile[kXK][kL][kW + 1];  // +1: no bank conflicts on the i-row accesses
   const BlockDesc bd = blocks[b];
-  const long long n = (long long)bd.nx * bd.ny * bd.nz;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-       c += (long long)gridDim.x * blockDim.x) {
-    int i, j, k;
-    cell_ijk(bd, c, i, j, k);
-    pack[pack_index(bd, na, arr, i, j, k)] = static_cast<T>(src[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)]);
+  const int r = blockIdx.x, bi = r % bd.BX, bj = r / bd.BX, k0 = blockIdx.y * kXK;
+  const int i0 = bi * kW, j0 = bj * kL, kn = min(kXK, bd.nz - k0);
+  const int t = threadIdx.x, il = t & (kW - 1), jr = t >> 3;  // 8 x 32 cells per pass
+  const bool rowok = i0 + il < bd.nx && j0 + jr < bd.ny;
+  const int w = t >> 5, lane = t & 31;
+  const bool lane_ok = j0 + lane < bd.ny;
+  if (TO_BRICK) {
+    for (int kk = 0; kk < kn; ++kk)
+      if (rowok) tile[kk][jr][il] = f3in[f3(bd.nx, bd.ny, i0 + il + 1, j0 + jr + 1, k0 + kk + 1)];
+    __syncthreads();
+    // rows tau = k0 * kW .. (k0 + kn) * kW + kL - 2: lane's cell c = tau - lane
+    for (int tau = k0 * kW + w; tau < (k0 + kn) * kW + kL - 1; tau += 8) {
+      const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
+      if (c >= k0 * kW && k < k0 + kn && lane_ok && i0 + ci < bd.nx)
+        bout[brick_elem<T, PHI>(bd, r, tau, na, arr, lane)] = static_cast<T>(tile[k - k0][lane][ci]);
+    }
+  } else {
+    for (int tau = k0 * kW + w; tau < (k0 + kn) * kW + kL - 1; tau += 8) {
+      const int c = tau - lane, k = c >> 3, ci = c & (kW - 1);
+      if (c >= k0 * kW && k < k0 + kn && lane_ok && i0 + ci < bd.nx)
+        tile[k - k0][lane][ci] = static_cast<double>(bin[brick_elem<T, PHI>(bd, r, tau, na, arr, lane)]);
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kn; ++kk)
+      if (rowok) f3out[f3(bd.nx, bd.ny, i0 + il + 1, j0 + jr + 1, k0 + kk + 1)] = tile[kk][jr][il];
   }
 }
+template <typename T, bool PHI, bool TO_BRICK>
+static void launch_tile_xfer(const BlockDesc& hb, const BlockDesc* d_blocks, int b, const double* f3in, double* f3out,
+                             const T* bin, T* bout, int na, int arr, cudaStream_t st) {
+  if (hb.nbricks == 0 || hb.nz == 0) return;
+  dim3 g(hb.nbricks, (hb.nz + kXK - 1) / kXK);
+  k_tile_xfer<T, PHI, TO_BRICK><<<g, 256, 0, st>>>(d_blocks, b, f3in, f3out, bin, bout, na, arr);
+}
 
-// plane coordinate (x0 fast, x1 slow) of face f -> 0-based cell (ghost: one outside)
 __device__ __forceinline__ void face_cell(const BlockDesc& bd, int f, int x0, int x1, bool ghost,
                                           int& i, int& j, int& k) {
   switch (f) {
@@ -1222,21 +1261,11 @@ __device__ __forceinline__ void face_dims(const BlockDesc& bd, int f, int& n0, i
   else { n0 = bd.nx; n1 = bd.ny; }
 }
 
-// Field3 -> phi: interior (blockIdx.y == 6) and the six ghost faces (blockIdx.y = face)
+// Field3 -> phi ghost faces (blockIdx.y = face; the interior: k_tile_xfer)
 template <typename T>
 __global__ void k_phi_in(const double* __restrict__ src, const BlockDesc* blocks, int b, T* phi) {
   const BlockDesc bd = blocks[b];
-  const int f = blockIdx.y;
-  if (f == 6) {
-    const long long n = (long long)bd.nx * bd.ny * bd.nz;
-    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-         c += (long long)gridDim.x * blockDim.x) {
-      int i, j, k;
-      cell_ijk(bd, c, i, j, k);
-      phi[phi_index(bd, i, j, k)] = static_cast<T>(src[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)]);
-    }
-    return;
-  }
+  const int f = blockIdx.y;  // ghost face (the interior: k_tile_xfer)
   int n0, n1;
   face_dims(bd, f, n0, n1);
   const long long n = (long long)n0 * n1;
@@ -1254,17 +1283,7 @@ template <typename T>
 __global__ void k_gather(const T* __restrict__ phi, const BlockDesc* blocks, int b, int nbrmask,
                          double* dst) {
   const BlockDesc bd = blocks[b];
-  const int f = blockIdx.y;
-  if (f == 6) {
-    const long long n = (long long)bd.nx * bd.ny * bd.nz;
-    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
-         c += (long long)gridDim.x * blockDim.x) {
-      int i, j, k;
-      cell_ijk(bd, c, i, j, k);
-      dst[f3(bd.nx, bd.ny, i + 1, j + 1, k + 1)] = static_cast<double>(phi[phi_index(bd, i, j, k)]);
-    }
-    return;
-  }
+  const int f = blockIdx.y;  // ghost face (the interior: k_tile_xfer)
   if (!((nbrmask >> f) & 1)) return;
   int n0, n1;
   face_dims(bd, f, n0, n1);
@@ -1577,14 +1596,15 @@ int max_resident_ctas(int kind, int precision, int* grid) {
 template <typename T>
 int launch_scatter(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
                    T* pack, int na, int arr, void* stream) {
-  k_scatter<T><<<grid_for((long long)hb.nx * hb.ny * hb.nz), 256, 0, (cudaStream_t)stream>>>(
-      src, d_blocks, block, pack, na, arr);
+  launch_tile_xfer<T, false, true>(hb, d_blocks, block, src, nullptr, nullptr, pack, na, arr, (cudaStream_t)stream);
   return cuda_status(cudaGetLastError());
 }
 template <typename T>
 int launch_phi_in(const double* src, const BlockDesc* d_blocks, int block, const BlockDesc& hb,
                   T* phi, void* stream) {
-  dim3 g(grid_for((long long)hb.nx * hb.ny * hb.nz) / 4 + 1, 7);
+  // interior tiled; the six ghost faces (blockIdx.y 0..5) by k_phi_in
+  launch_tile_xfer<T, true, true>(hb, d_blocks, block, src, nullptr, nullptr, phi, 1, 0, (cudaStream_t)stream);
+  dim3 g(grid_for((long long)hb.nx * hb.ny * hb.nz) / 4 + 1, 6);
   k_phi_in<T><<<g, 256, 0, (cudaStream_t)stream>>>(src, d_blocks, block, phi);
   return cuda_status(cudaGetLastError());
 }
@@ -1594,7 +1614,9 @@ int launch_gather(const T* phi, const BlockDesc* d_blocks, int block, const Bloc
   int mask = 0;
   for (int f = 0; f < 6; ++f)
     if (nbr6[f] >= 0) mask |= 1 << f;
-  dim3 g(grid_for((long long)hb.nx * hb.ny * hb.nz) / 4 + 1, 7);
+  // interior tiled; the ghost faces the plan writes (blockIdx.y 0..5) by k_gather
+  launch_tile_xfer<T, true, false>(hb, d_blocks, block, nullptr, dst, phi, nullptr, 1, 0, (cudaStream_t)stream);
+  dim3 g(grid_for((long long)hb.nx * hb.ny * hb.nz) / 4 + 1, 6);
   k_gather<T><<<g, 256, 0, (cudaStream_t)stream>>>(phi, d_blocks, block, mask, dst);
   return cuda_status(cudaGetLastError());
 }
