@@ -678,8 +678,10 @@ static int exchange_split(sip_ctx* ctx) {
   T* rbuf = static_cast<T*>(ctx->x_rbuf);
   CK(cudaStreamWaitEvent(xs, ctx->ev_k2, 0));
   if (ctx->x_early) {
+    unsigned long long* xt =
+        ctx->trace ? ctx->trace + 8 * ctx->hbricks.size() + 5 * kTraceStages * kTraceMarks : nullptr;
     CKS(launch_face_copies_after<T>(ctx->d_x, ctx->d_xitems, ctx->n_xitems, ctx->d_blocks, phi, sbuf,
-                                    ctx->d_xflag, ctx->d_xseq, xs));
+                                    ctx->d_xflag, ctx->d_xseq, xt, xs));
     ++ctx->launches;
   }
   if (!ctx->peers.empty()) {
@@ -1708,14 +1710,16 @@ int sip_debug_trace(sip_ctx* ctx, unsigned long long* out, long long* ntiles) {
   const size_t nt = ctx->hbricks.size();
   *ntiles = (long long)nt;
   if (!ctx->trace) {
-    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) * (8 * std::max<size_t>(1, nt) + 5 * kTraceStages * kTraceMarks)));
+    CKS(dalloc(ctx, &ctx->trace, sizeof(unsigned long long) *
+                                     (8 * std::max<size_t>(1, nt) + 5 * kTraceStages * kTraceMarks + 2 * kXTraceCtas)));
     if (const char* tb = getenv("SIPB_TRACE_BRICK")) ctx->trace_brick = atoi(tb);
     if (const char* tu = getenv("SIPB_TRACE_UP")) ctx->trace_brick |= atoi(tu) << 20;  // hop_trace: upstream offset
     return SIP_OK;
   }
   if (out) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->trace, sizeof(unsigned long long) * (8 * nt + 5 * kTraceStages * kTraceMarks),
+    CK(cudaMemcpy(out, ctx->trace,
+                  sizeof(unsigned long long) * (8 * nt + 5 * kTraceStages * kTraceMarks + 2 * kXTraceCtas),
                   cudaMemcpyDeviceToHost));
   }
   return SIP_OK;

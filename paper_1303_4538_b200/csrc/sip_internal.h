@@ -264,7 +264,10 @@ struct XItem {
 template <typename T>
 int launch_face_copies_after(const FaceCopy* d_copies, const XItem* d_items, int nitems,
                              const BlockDesc* d_blocks, T* phi, T* buf_out, const unsigned* xflag,
-                             const unsigned* xseq, void* stream);
+                             const unsigned* xseq, unsigned long long* xtrace, void* stream);
+// debug trace layout (sip_debug_trace): [4 nbricks] K2, [4 nbricks] K3, stage
+// marks, then kXTraceCtas x 2 of the split exchange's copy kernel
+constexpr int kXTraceCtas = 256;
 template <typename T>
 int launch_residual(const BlockDesc* d_blocks, int block, const BlockDesc& hb, const T* fw,
                     const T* phi, int symmetric, double* out, void* stream);

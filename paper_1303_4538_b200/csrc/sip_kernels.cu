@@ -1357,8 +1357,11 @@ constexpr int kXCopyThreads = 64;
 template <typename T>
 __global__ void __launch_bounds__(kXCopyThreads, 16)
     k_face_copy_after(const FaceCopy* copies, const XItem* items, int nitems, const BlockDesc* blocks,
-                      T* phi, T* buf_out, const unsigned* xflag, const unsigned* xseq) {
+                      T* phi, T* buf_out, const unsigned* xflag, const unsigned* xseq,
+                      unsigned long long* xtrace) {
   const unsigned want = *(const volatile unsigned*)xseq;
+  // debug timeline (tools/xsplit_timeline.py): this CTA's first item start, last item end
+  if (xtrace && threadIdx.x == 0 && blockIdx.x < nitems) xtrace[2 * blockIdx.x] = gtime();
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const XItem xi = items[it];
     // descriptors first (independent of the stamp), then thread 0's wait
@@ -1403,6 +1406,7 @@ __global__ void __launch_bounds__(kXCopyThreads, 16)
       }
     }
   }
+  if (xtrace && threadIdx.x == 0 && blockIdx.x < nitems) xtrace[2 * blockIdx.x + 1] = gtime();
 }
 
 // residual_general or, with SYM, residual_symmetric
@@ -1634,7 +1638,7 @@ int launch_face_copies(const FaceCopy* d_copies, int ncopies, int max_plane,
 template <typename T>
 int launch_face_copies_after(const FaceCopy* d_copies, const XItem* d_items, int nitems,
                              const BlockDesc* d_blocks, T* phi, T* buf_out, const unsigned* xflag,
-                             const unsigned* xseq, void* stream) {
+                             const unsigned* xseq, unsigned long long* xtrace, void* stream) {
   if (nitems <= 0) return SIP_OK;
   static int grid = 0;
   if (grid == 0) {
@@ -1650,7 +1654,7 @@ int launch_face_copies_after(const FaceCopy* d_copies, const XItem* d_items, int
                          (int)cudaSharedmemCarveoutMaxShared);
   }
   k_face_copy_after<T><<<grid, kXCopyThreads, 0, (cudaStream_t)stream>>>(
-      d_copies, d_items, nitems, d_blocks, phi, buf_out, xflag, xseq);
+      d_copies, d_items, nitems, d_blocks, phi, buf_out, xflag, xseq, xtrace);
   return cuda_status(cudaGetLastError());
 }
 template <typename T>
@@ -1699,7 +1703,8 @@ int launch_generate(int kind, uint64_t seed, const int g[3], const int o[3], int
   template int launch_face_copies<T>(const FaceCopy*, int, int, const BlockDesc*, T*, const T*,   \
                                      T*, void*);                                                  \
   template int launch_face_copies_after<T>(const FaceCopy*, const XItem*, int, const BlockDesc*,   \
-                                           T*, T*, const unsigned*, const unsigned*, void*);      \
+                                           T*, T*, const unsigned*, const unsigned*,              \
+                                           unsigned long long*, void*);                           \
   template int launch_residual<T>(const BlockDesc*, int, const BlockDesc&, const T*, const T*,    \
                                   int, double*, void*);                                           \
   template int launch_gather_any<T>(const T*, int, int, const BlockDesc*, int, const BlockDesc&,  \

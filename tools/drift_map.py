@@ -22,7 +22,7 @@ nt = ctypes.c_longlong()
 L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(3)
-buf = np.zeros(8 * nt.value + 5 * 64 * 6, dtype=np.uint64)
+buf = np.zeros(8 * nt.value + 5 * 64 * 6 + 2 * 256, dtype=np.uint64)
 L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
 tr = buf[:8 * nt.value].reshape(2, nt.value, 4).astype(np.int64)
 BX, BY = (n + 7) // 8, (n + 31) // 32

@@ -20,9 +20,9 @@ nt = ctypes.c_longlong()
 L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(3)
-buf = np.zeros(8 * nt.value + 5 * 64 * 6, dtype=np.uint64)
+buf = np.zeros(8 * nt.value + 5 * 64 * 6 + 2 * 256, dtype=np.uint64)
 L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
-mk = buf[8 * nt.value:].reshape(5, 64, 6).astype(np.int64)
+mk = buf[8 * nt.value:8 * nt.value + 5 * 64 * 6].reshape(5, 64, 6).astype(np.int64)
 up, dn = mk[3], mk[4]
 t0 = min(x for x in np.concatenate([up[:, :5].ravel(), dn[:, :5].ravel()]) if x > 0)
 up = np.where(up > 0, up - t0, 0) / 1e3

@@ -21,9 +21,9 @@ nt = ctypes.c_longlong()
 L = sip.lib()
 L.sip_debug_trace(s.handle, None, ctypes.byref(nt))
 s.iterate(3)
-buf = np.zeros(8 * nt.value + 5 * 64 * 6, dtype=np.uint64)
+buf = np.zeros(8 * nt.value + 5 * 64 * 6 + 2 * 256, dtype=np.uint64)
 L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
-mk = buf[8 * nt.value:].reshape(5, 64, 6).astype(np.int64)[4]
+mk = buf[8 * nt.value:8 * nt.value + 5 * 64 * 6].reshape(5, 64, 6).astype(np.int64)[4]
 arr, ready, full = mk[:, 3], mk[:, 0], mk[:, 5]
 r = range(8, 60)
 per = [arr[m + 1] - arr[m] for m in r]
