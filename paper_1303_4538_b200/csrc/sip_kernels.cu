@@ -1029,7 +1029,11 @@ __global__ void __launch_bounds__(160, SIPB_K3_MINB) k_backward(const SweepParam
       // empty / cdone (count 32).
       const int cw = warp == 1 ? 0 : 1;
       constexpr uint32_t E = sizeof(T);
-      T* const hand = reinterpret_cast<T*>(smem + C::off_hand);
+      // hand-over rows through the opaque shared base (a generic pointer here
+      // made the compiler rebuild the address with S2UR SR_CgaCtaId on the
+      // chain's critical path every stage)
+      const uint32_t hand_rx = sb + (uint32_t)C::off_hand + E * (uint32_t)(cw * (kW + 1) * kL + lane);
+      const uint32_t hand_tx = sb + (uint32_t)C::off_hand + E * (uint32_t)((cw ^ 1) * (kW + 1) * kL + lane);
       const int q0 = (int)(g % D), qlast = (int)((g + NST - 1) % D);
       if (cw == (q0 & 1)) trace_begin(P.trace, bid);
       int q = q0;
@@ -1066,11 +1070,15 @@ __global__ void __launch_bounds__(160, SIPB_K3_MINB) k_backward(const SweepParam
           // mbarrier hand-over measured ~6 % slower, a polled flag ~4 %)
           cmark(m, 0);
           asm volatile("bar.sync %0, 64;" ::"r"(1 + cw) : "memory");
-          const T* h = hand + cw * (kW + 1) * kL + lane;
+          dprev = lds<T>(hand_rx + E * (kW * kL));
 #pragma unroll
-          for (int s = 0; s < kW; ++s) win[s] = h[s * kL];
-          dprev = h[kW * kL];
+          for (int s = 0; s < kW; ++s) win[s] = lds<T>(hand_rx + E * (s * kL));
         }
+#ifdef SIPB_K3_CMARKS
+        // chain start: after dprev (the hand-over) is in a register
+        if (dprev == T(1.2345e30)) asm volatile("");
+        cmark(m, 1);
+#endif
         // delta = ((R - UN*dN) - UE*dE) - UT*dT, dT = the
         // previous stage's step s (win); padding cells compute exact zeros
         // (zero-filled packs), stored copies masked below
@@ -1084,6 +1092,10 @@ __global__ void __launch_bounds__(160, SIPB_K3_MINB) k_backward(const SweepParam
           win[s] = d;
           dprev = d;
         }
+#ifdef SIPB_K3_CMARKS
+        if (dprev == T(1.2345e30)) asm volatile("");  // chain end: the last step's delta computed
+        cmark(m, 2);
+#endif
         // the masked copy is the next stage's window and the slot's delta
         const bool interior = bd.wI == kW && bd.wJ == kL && n >= kL / kStage && n + kL / kStage < NST;
         if (!interior) {
@@ -1095,10 +1107,9 @@ __global__ void __launch_bounds__(160, SIPB_K3_MINB) k_backward(const SweepParam
           }
         }
         if (m + 1 < NST) {  // hand the chain state to the other warp first
-          T* h = hand + (cw ^ 1) * (kW + 1) * kL + lane;
+          sts(hand_tx + E * (kW * kL), dprev);
 #pragma unroll
-          for (int s = 0; s < kW; ++s) h[s * kL] = win[s];
-          h[kW * kL] = dprev;
+          for (int s = 0; s < kW; ++s) sts(hand_tx + E * (s * kL), win[s]);
           asm volatile("bar.arrive %0, 64;" ::"r"(1 + (cw ^ 1)) : "memory");
           cmark(m, 3);
         }

@@ -24,7 +24,7 @@ s.iterate(3)
 buf = np.zeros(8 * nt.value + 5 * 64 * 6 + 2 * 256, dtype=np.uint64)
 L.sip_debug_trace(s.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), ctypes.byref(nt))
 mk = buf[8 * nt.value:8 * nt.value + 5 * 64 * 6].reshape(5, 64, 6).astype(np.int64)[4]
-arr, ready, full = mk[:, 3], mk[:, 0], mk[:, 5]
+arr, ready, full, cst, cen = mk[:, 3], mk[:, 0], mk[:, 5], mk[:, 1], mk[:, 2]
 r = range(8, 60)
 per = [arr[m + 1] - arr[m] for m in r]
 late = [ready[m + 1] - arr[m] for m in r]       # > 0: receiver reached the barrier after the hand-over
@@ -34,6 +34,11 @@ med = lambda v: float(np.median(v))
 print(f"{prec} {dims}: period {med(per):.0f} cyc; receiver ready - sender arrive {med(late):.0f} cyc "
       f"(late in {sum(x > 0 for x in late)}/{len(late)} stages); release -> next arrive {med(run):.0f} cyc; "
       f"past full -> ready {med(pre):.0f} cyc")
+chain = [cen[m] - cst[m] for m in r]
+wake = [cst[m + 1] - arr[m] for m in r]          # sender's arrive -> receiver's chain start (hand-over)
+tail = [arr[m] - cen[m] for m in r]              # chain end -> hand-over stores + arrive
+print(f"  chain {med(chain):.0f} cyc; hand-over: arrive -> next chain start {med(wake):.0f} cyc, "
+      f"chain end -> arrive {med(tail):.0f} cyc")
 print("  per-stage period:", " ".join(str(x) for x in per[:24]))
 print("  late:            ", " ".join(str(x) for x in late[:24]))
 s.close()
