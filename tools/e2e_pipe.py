@@ -46,15 +46,22 @@ def one_pending(k):
         L.sip_synchronize(s.handle)
 
 
+STEP_T = []
+
+
 def two(k):
     def enq(r):
         L.sip_set_source_async(s.handle, 0, qp)
         assert L.sip_solve_async(s.handle, arr, iters, nrm[r % 2].ctypes.data_as(dp)) == 0
     enq(0)
+    t = time.perf_counter()
     for r in range(k):
         if r + 1 < k:
             enq(r + 1)
         L.sip_wait_async(s.handle)
+        t2 = time.perf_counter()
+        STEP_T.append((t2 - t) * 1e3)
+        t = t2
 
 
 def one_noq(k):
@@ -79,4 +86,6 @@ for name, f in (("sequential", seq), ("one pending", one_pending), ("two in flig
     f(steps)
     torch.cuda.synchronize()
     print(f"{prec} iters={iters}: {name:14s} {(time.perf_counter() - t0) / steps * 1e3:7.2f} ms/step")
+    if name == "two in flight":
+        print("   per step:", " ".join(f"{x:.1f}" for x in STEP_T[-steps:]))
 s.close()
