@@ -205,7 +205,9 @@ int sip_ftt1_validate(int nranks, const int* counts, const int* entries);
  * ignored: the 7-point stencil reads face ghosts only. */
 int sip_set_halo_tables(sip_ctx* ctx, int nranks, const int* counts, const int* entries);
 
-/* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */
+/* Run on a caller-provided cudaStream_t (NULL: the context's own stream).
+ * Work already enqueued on the previous stream stays ordered before anything
+ * enqueued afterwards (the new stream waits on an event of the old one). */
 int sip_set_stream(sip_ctx* ctx, void* stream);
 void* sip_get_stream(const sip_ctx* ctx);
 

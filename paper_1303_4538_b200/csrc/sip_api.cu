@@ -1590,7 +1590,18 @@ int sip_residual(sip_ctx* ctx, int symmetric, double* const* res) {
 
 int sip_set_stream(sip_ctx* ctx, void* stream) {
   if (!ctx) return SIP_ERR_MISUSE;
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  const cudaStream_t ns = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  if (ns != ctx->stream) {
+    // work already enqueued (sweeps, async solves, pending source scatters)
+    // stays ordered before anything enqueued on the new stream
+    CKS(set_device(ctx));
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, ctx->stream));
+    CK(cudaStreamWaitEvent(ns, e, 0));
+    cudaEventDestroy(e);  // released once the recorded work completes
+    ctx->stream = ns;
+  }
   return SIP_OK;
 }
 

@@ -731,3 +731,34 @@ def test_two_async_solves_multiblock(gpu):
         assert np.array_equal(phis[b], seq[-1][1][b]), b
     s.synchronize()
     s.close()
+
+
+def test_stream_switch_keeps_order(gpu):
+    """sip_iterate enqueues without a host sync; switching to a caller stream
+    in the middle of a solve keeps the earlier sweeps ordered before the
+    later ones (bitwise equal to one uninterrupted solve)."""
+    import torch
+    dims, iters = (48, 40, 30), 6
+    A = O.generate(0, 1303 + 73, dims)
+
+    def run(switch):
+        s = sip.Solver(dims, "f64")
+        s.set_system(0, sip.StencilSystem.from_dict(A))
+        s.factor(0.92)
+        phi = O.field(*dims)
+        s.load_phi([phi])
+        s.iterate(iters // 2)
+        st = torch.cuda.Stream()
+        if switch:
+            s.set_stream(st.cuda_stream)
+        s.iterate(iters - iters // 2)
+        s.synchronize()
+        n = s.read_norms(0, iters)
+        s.store_phi([phi])
+        s.close()
+        return np.asarray(n), phi
+
+    n0, p0 = run(False)
+    n1, p1 = run(True)
+    assert np.array_equal(n0, n1)
+    assert np.array_equal(p0, p1)
